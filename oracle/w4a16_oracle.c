@@ -1,0 +1,245 @@
+/* w4a16_oracle.c — CPU oracle (TEST INFRASTRUCTURE ONLY; see w4a16_oracle.h for scope and citations).
+ *
+ * Plain C, written to be checked by eye against the definitions in DESIGN.md §3 / SURVEY §8(c).
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math (fp32 steps of the pack must be IEEE, RNE, unfused).
+ */
+#include "w4a16_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* ------------------------------------------------------------------------------------------------------
+ * IEEE binary16 conversions (reading R1). half -> wider is exact; wider -> half rounds once, to nearest
+ * even, from the exact value (float -> double is exact, so float -> half is a single rounding too).
+ * ---------------------------------------------------------------------------------------------------- */
+double orc_half_to_double(uint16_t h) {
+  int sign = (h >> 15) & 1, e = (h >> 10) & 0x1F, m = h & 0x3FF;
+  double v;
+  if (e == 0) v = ldexp((double)m, -24);                       /* zero / subnormal: m * 2^-24 */
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = ldexp((double)(1024 + m), e - 25);                  /* (1 + m/1024) * 2^(e-15) */
+  return sign ? -v : v;
+}
+
+float orc_half_to_float(uint16_t h) { return (float)orc_half_to_double(h); }
+
+uint16_t orc_double_to_half(double d) {
+  uint16_t sign = signbit(d) ? 0x8000 : 0;
+  if (isnan(d)) return (uint16_t)(sign | 0x7E00);
+  double a = fabs(d);
+  if (a >= 65520.0) return (uint16_t)(sign | 0x7C00);          /* half-way between 65504 and 2^16 ties to inf */
+  if (a == 0.0) return sign;
+  int E;
+  frexp(a, &E);                                                /* a = f * 2^E, f in [0.5, 1) */
+  int e = E - 1;                                               /* a in [2^e, 2^(e+1)) */
+  if (e < -14) e = -14;                                        /* subnormal range: quantum 2^-24 */
+  double q = ldexp(a, 10 - e);                                 /* a / quantum, exact (power-of-two scaling) */
+  double r = nearbyint(q);                                     /* round to nearest, ties to even (default mode) */
+  if (r < 1024.0) return (uint16_t)(sign | (uint16_t)r);      /* subnormal (or zero) */
+  /* normal: r in [1024, 2048]; r == 2048 carries into the exponent automatically */
+  return (uint16_t)(sign | (uint16_t)(((e + 15) << 10) + ((int)r - 1024)));
+}
+
+uint16_t orc_float_to_half(float f) { return orc_double_to_half((double)f); }
+
+/* ------------------------------------------------------------------------------------------------------
+ * Packed layout (include/w4a16.h "qweight layout"): 128x128 tiles, n-tile major, then k-group;
+ * inside a tile 128 rows of 16 words; word j holds k = 8j..8j+7 of the tile, local index i in nibble
+ * slot (i%2)*4 + i/2 (so (w & 0x000F000F) yields the pair k=8j, 8j+1 as the two 16-bit halves).
+ * ---------------------------------------------------------------------------------------------------- */
+int orc_nibble_slot(int i) { return (i % 2) * 4 + i / 2; }
+
+size_t orc_word_index(int K, int N, int k, int n) {
+  (void)N;
+  size_t tile = (size_t)(n / 128) * (size_t)(K / 128) + (size_t)(k / 128);
+  return tile * 2048 + (size_t)(n % 128) * 16 + (size_t)((k % 128) / 8);
+}
+
+int orc_get_code(const uint32_t* qweight, int K, int N, int k, int n) {
+  uint32_t w = qweight[orc_word_index(K, N, k, n)];
+  return (int)((w >> (4 * orc_nibble_slot(k % 8))) & 0xF);
+}
+
+static void set_code(uint32_t* qweight, int K, int N, int k, int n, int q) {
+  size_t wi = orc_word_index(K, N, k, n);
+  int sh = 4 * orc_nibble_slot(k % 8);
+  qweight[wi] = (qweight[wi] & ~(0xFu << sh)) | ((uint32_t)q << sh);
+}
+
+static int layout_ok(int K, int N) { return K > 0 && N > 0 && K % 128 == 0 && N % 128 == 0; }
+
+/* clamp to [lo, hi]; -0.0 maps to lo (+0.0) so a zero point of 0 is stored as fp16 +0 (reading R2). */
+static float clampf(float x, float lo, float hi) {
+  if (!(x > lo)) return lo;
+  if (x > hi) return hi;
+  return x;
+}
+
+/* ------------------------------------------------------------------------------------------------------
+ * Pack (GPTQ quantizer conventions). All arithmetic is fp32 (C float,
+ * SSE, no contraction): readings R3 (0 representable), R4 (RNE), R5 (codes use the stored fp16 scale),
+ * R15 (all-zero group -> range +-1).
+ * ---------------------------------------------------------------------------------------------------- */
+int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
+             uint16_t* zeros, int32_t* status) {
+  if (!W || !qweight || !scales || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+  if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
+  if (mode == ORC_ASYM && !zeros) return -1;
+  int st = ORC_DEV_OK;
+  memset(qweight, 0, (size_t)K * N / 2);
+  for (int n = 0; n < N; ++n) {
+    for (int g = 0; g < K / group; ++g) {
+      /* 1. range, always containing 0; non-finite weights flag the status and count as 0 */
+      float wmin = 0.0f, wmax = 0.0f;
+      for (int k = g * group; k < (g + 1) * group; ++k) {
+        float w = orc_half_to_float(W[(size_t)k * N + n]);
+        if (!isfinite(w)) { st = ORC_DEV_NONFINITE; continue; }
+        if (w < wmin) wmin = w;
+        if (w > wmax) wmax = w;
+      }
+      /* 2. scale s (fp16) and integer zero z */
+      float s32, z;
+      uint16_t s;
+      if (mode == ORC_ASYM) {
+        if (wmin == wmax) { wmin = -1.0f; wmax = 1.0f; }
+        s = orc_float_to_half((wmax - wmin) / 15.0f);
+        if (orc_half_to_float(s) == 0.0f) { wmin = -1.0f; wmax = 1.0f; s = orc_float_to_half((wmax - wmin) / 15.0f); }
+        s32 = orc_half_to_float(s);
+        z = clampf(rintf(-wmin / s32), 0.0f, 15.0f);
+      } else {
+        float amax = -wmin > wmax ? -wmin : wmax;
+        if (amax == 0.0f) amax = 1.0f;
+        s = orc_float_to_half((amax + amax) / 15.0f);
+        if (orc_half_to_float(s) == 0.0f) { amax = 1.0f; s = orc_float_to_half((amax + amax) / 15.0f); }
+        s32 = orc_half_to_float(s);
+        z = 8.0f;
+      }
+      scales[(size_t)g * N + n] = s;
+      if (zeros) zeros[(size_t)g * N + n] = orc_float_to_half(z);
+      /* 3. codes q = clamp(rne(w / s) + z, 0, 15) */
+      for (int k = g * group; k < (g + 1) * group; ++k) {
+        float w = orc_half_to_float(W[(size_t)k * N + n]);
+        if (!isfinite(w)) w = 0.0f;
+        float q = clampf(rintf(w / s32) + z, 0.0f, 15.0f);
+        set_code(qweight, K, N, k, n, (int)q);
+      }
+    }
+  }
+  if (status) *status = st;
+  return 0;
+}
+
+/* w_hat = fp16_rne((q - z) * s): (q - z) is a small integer, the product is exact in double, so this is
+ * exactly one rounding. */
+static uint16_t dequant(int q, uint16_t s, uint16_t z_or_8, int mode) {
+  double z = mode == ORC_SYM ? 8.0 : orc_half_to_double(z_or_8);
+  return orc_double_to_half(((double)q - z) * orc_half_to_double(s));
+}
+
+int orc_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
+               int mode, uint16_t* W_hat) {
+  if (!qweight || !scales || !W_hat || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+  if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
+  if (mode == ORC_ASYM && !zeros) return -1;
+  for (int k = 0; k < K; ++k)
+    for (int n = 0; n < N; ++n) {
+      size_t gi = (size_t)(k / group) * N + n;
+      W_hat[(size_t)k * N + n] = dequant(orc_get_code(qweight, K, N, k, n), scales[gi], zeros ? zeros[gi] : 0, mode);
+    }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------------------
+ * GEMM reference: dequantise, then matmul, in fp64 with k in order 0..K-1.
+ * ---------------------------------------------------------------------------------------------------- */
+typedef struct {
+  const uint16_t* X; const uint32_t* qw; const uint16_t* sc; const uint16_t* ze;
+  int M, K, N, group, mode;
+  const int32_t* cols; int ncols;        /* column list (cols == NULL: all columns) */
+  double* Y; int ystride;                /* Y[m*ystride + j] */
+  int j0, j1;                            /* this worker's column positions [j0, j1) */
+} gemm_job;
+
+static void* gemm_worker(void* p) {
+  gemm_job* a = (gemm_job*)p;
+  double* wcol = (double*)malloc(sizeof(double) * (size_t)a->K);
+  double* xd = (double*)malloc(sizeof(double) * (size_t)a->K);
+  for (int j = a->j0; j < a->j1; ++j) {
+    int n = a->cols ? a->cols[j] : j;
+    for (int k = 0; k < a->K; ++k) {
+      size_t gi = (size_t)(k / a->group) * a->N + n;
+      wcol[k] = orc_half_to_double(dequant(orc_get_code(a->qw, a->K, a->N, k, n), a->sc[gi], a->ze ? a->ze[gi] : 0, a->mode));
+    }
+    for (int m = 0; m < a->M; ++m) {
+      const uint16_t* xr = a->X + (size_t)m * a->K;
+      double acc = 0.0;
+      for (int k = 0; k < a->K; ++k) acc += orc_half_to_double(xr[k]) * wcol[k];
+      a->Y[(size_t)m * a->ystride + j] = acc;
+    }
+  }
+  free(wcol); free(xd);
+  return NULL;
+}
+
+static int gemm_run(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+                    int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Y, int nthreads) {
+  if (!X || !qweight || !scales || !Y || M < 0 || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+  if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
+  if (mode == ORC_ASYM && !zeros) return -1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > ncols) nthreads = ncols > 0 ? ncols : 1;
+  gemm_job* jobs = (gemm_job*)calloc((size_t)nthreads, sizeof(gemm_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int t = 0; t < nthreads; ++t) {
+    gemm_job j = {X, qweight, scales, zeros, M, K, N, group, mode, cols, ncols, Y, ncols,
+                  (int)((long long)ncols * t / nthreads), (int)((long long)ncols * (t + 1) / nthreads)};
+    jobs[t] = j;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, gemm_worker, &jobs[t]);
+  gemm_worker(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(jobs); free(th);
+  return 0;
+}
+
+int orc_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+             int K, int N, int group, int mode, double* Y, int nthreads) {
+  return gemm_run(X, qweight, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads);
+}
+
+int orc_gemm_cols(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+                  int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols) {
+  if (!cols || ncols < 0) return -1;
+  for (int j = 0; j < ncols; ++j) if (cols[j] < 0 || cols[j] >= N) return -1;
+  return gemm_run(X, qweight, scales, zeros, M, K, N, group, mode, cols, ncols, Ycols, 1);
+}
+
+/* ------------------------------------------------------------------------------------------------------
+ * Greedy acceptance (reading R9). ok[i]: every edge on the root->i path matches the
+ * target's argmax at the parent; the accepted node is the deepest ok node (ties: smallest index); the
+ * bonus token is the target's argmax at that node.
+ * ---------------------------------------------------------------------------------------------------- */
+int orc_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n, int32_t* out) {
+  if (!tokens || !parents || !target_argmax || !out || n < 1) return -1;
+  for (int i = 0; i < n; ++i) out[3 + i] = -1;
+  int bad = parents[0] != -1;
+  for (int i = 1; i < n; ++i) if (parents[i] < 0 || parents[i] >= i) bad = 1;
+  if (bad) { out[0] = 0; out[1] = -1; out[2] = ORC_DEV_BAD_TREE; return 0; }
+  int* ok = (int*)malloc(sizeof(int) * (size_t)n);
+  int* depth = (int*)malloc(sizeof(int) * (size_t)n);
+  ok[0] = 1; depth[0] = 0;
+  for (int i = 1; i < n; ++i) {
+    int p = parents[i];
+    ok[i] = ok[p] && tokens[i] == target_argmax[p];
+    depth[i] = depth[p] + 1;
+  }
+  int best = 0;
+  for (int i = 1; i < n; ++i) if (ok[i] && depth[i] > depth[best]) best = i;
+  out[0] = depth[best];
+  out[1] = target_argmax[best];
+  out[2] = ORC_DEV_OK;
+  for (int x = best; x != 0; x = parents[x]) out[3 + depth[x] - 1] = x;
+  free(ok); free(depth);
+  return 0;
+}

@@ -1,0 +1,79 @@
+/* w4a16_oracle.h — plain, slow, obviously-correct CPU ORACLE for the W4A16 verify path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load or call this library. The product path (paper_2505_22179_b200/) never
+ * includes, links or calls it, and this code shares nothing with the CUDA path (no headers, helpers or
+ * tables); the only common code is the input generator in synth/, which holds none of the method's
+ * arithmetic.
+ *
+ * What it computes (citations: PAPER.md line numbers "P:n", SPEC.md "S:n"; readings in DESIGN.md §3):
+ *   - pack:   GPTQ-style W4 group-128 quantisation, round-to-nearest ("symmetrically quantize weights
+ *             to 4-bit with a group size of 128"; RTN stands in for GPTQ calibration as in S:95; ASYM per
+ *             BASELINE.json config 1). Arithmetic in IEEE fp32, RNE, no contraction (reading R5).
+ *   - unpack: w_hat = fp16_rne((q - z) * s)   (exact product, one rounding).
+ *   - gemm:   Y[m][n] = sum_k X[m][k] * w_hat[k][n], in fp64, sequential k (BASELINE.json north_star:
+ *             "X[M,K] fp16 x packed W[K,N] -> Y[M,N] fp16, fp32 accumulate"; the oracle uses fp64).
+ *   - accept: greedy tree acceptance (P:79-84 draft-then-verify; the rule is not stated by the paper,
+ *             SPEC S:289/S:298 greedy argmax; reading R9).
+ *
+ * Packed layout (the ABI's, re-derived here from its definition in include/w4a16.h, not shared):
+ *   qweight is uint32[K*N/8]; tile (t = n/128, g = k/128) is 2048 words at ((t*(K/128) + g) * 2048);
+ *   inside the tile, row r = n%128 has 16 words at r*16; word j = (k%128)/8 holds k = 128g+8j+i,
+ *   i in 0..7, in nibble slot (i%2)*4 + i/2.  scales/zeros: fp16 [K/group][N] row-major.
+ */
+#ifndef W4A16_ORACLE_H
+#define W4A16_ORACLE_H
+#include <stdint.h>
+#include <stddef.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_ASYM 0
+#define ORC_SYM 1
+#define ORC_DEV_OK 0
+#define ORC_DEV_NONFINITE 1
+#define ORC_DEV_BAD_TREE 2
+
+/* IEEE binary16 <-> binary32/binary64, bit-level, round-to-nearest-even (subnormals, inf, NaN). */
+float orc_half_to_float(uint16_t h);
+double orc_half_to_double(uint16_t h);
+uint16_t orc_float_to_half(float f);
+uint16_t orc_double_to_half(double d);
+
+/* Layout accessors. */
+size_t orc_word_index(int K, int N, int k, int n);
+int orc_nibble_slot(int i);
+int orc_get_code(const uint32_t* qweight, int K, int N, int k, int n);
+
+/* Quantise fp16 W[K][N] (row-major) per column n and per group of `group` consecutive k.
+ * mode ORC_ASYM (integer zero in [0,15] stored as fp16) or ORC_SYM (zero == 8, zeros may be NULL).
+ * The packed layout needs N % 128 == 0 and K % 128 == 0; group must divide K (any group for the
+ * oracle's own math, the ABI fixes 128). *status gets ORC_DEV_NONFINITE if any W is not finite.
+ * Returns 0 or -1 on bad arguments. */
+int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
+             uint16_t* zeros, int32_t* status);
+
+/* W_hat[K][N] fp16 = fp16_rne((q - z) * s). */
+int orc_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
+               int mode, uint16_t* W_hat);
+
+/* Y[M][N] (fp64) = X[M][K] (fp16) * W_hat, W_hat dequantised from the packed operands; k summed in order
+ * 0..K-1 in fp64. Columns are independent: nthreads >= 1 splits columns across pthreads, result identical. */
+int orc_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+             int K, int N, int group, int mode, double* Y, int nthreads);
+
+/* Same definition for a list of columns only (full-size sampled checks): Ycols[m*ncols + j] = Y[m][cols[j]]. */
+int orc_gemm_cols(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+                  int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols);
+
+/* Greedy acceptance over a draft tree of n nodes (node 0 = root = last committed token, parents[0] = -1,
+ * parents[i] < i). out[0] = accepted length, out[1] = bonus token, out[2] = device status,
+ * out[3 .. 3+n) = accepted path (node indices, root excluded, root->leaf), padded with -1.
+ * Returns 0, or -1 on bad arguments (n < 1 or NULL). A malformed tree gives out = {0, -1, BAD_TREE, -1...}. */
+int orc_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

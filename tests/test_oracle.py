@@ -1,0 +1,387 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names what fixes the expected value: a library routine (numpy), a closed form derived by hand,
+a golden fixture (tests/golden/, with its citation), brute force on tiny inputs, or an invariant the
+method must satisfy (losslessness vs autoregressive decoding). Chosen so that a dropped term, a wrong
+sign/index, a transposed operand or a wrong nibble slot fails at least one of them.
+"""
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RNG = np.random.default_rng(1234)
+
+
+# ---------------------------------------------------------------------------------------------------
+# fp16 conversions (reading R1) — pinned to numpy's IEEE conversions (library routine).
+# ---------------------------------------------------------------------------------------------------
+def test_half_to_float_exhaustive():
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    ref = bits.view(np.float16).astype(np.float64)
+    got = np.array([oracle.L.orc_half_to_double(int(b)) for b in bits])
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(got[~nan], ref[~nan])
+    # and the float path agrees bit-for-bit (incl. signed zeros)
+    sel = bits[::97]
+    gotf = np.array([oracle.half_to_float(int(b)) for b in sel], dtype=np.float32)
+    reff = sel.view(np.float16).astype(np.float32)
+    ok = np.isnan(reff) & np.isnan(gotf)
+    assert np.array_equal(gotf.view(np.uint32)[~ok], reff.view(np.uint32)[~ok])
+
+
+def _edge_floats():
+    e = [0.0, -0.0, 65504.0, 65519.99, 65520.0, 65536.0, -65520.0, 1e-8, 2.0 ** -24, 2.0 ** -25, 2.0 ** -25 * 1.0001,
+         3 * 2.0 ** -26, 2.0 ** -14, 2.0 ** -14 - 2.0 ** -25, 6.1e-5, np.inf, -np.inf, 1.0 + 2.0 ** -11,
+         1.0 + 3 * 2.0 ** -11, 1.0 + 2.0 ** -11 + 2.0 ** -30, 2049.0, 2051.0, 0.1, -0.1, 1.0 / 3.0]
+    # all halfway points between consecutive representable halves in [1, 2) and in the subnormal range
+    h = np.arange(0x3C00, 0x4000, 37, dtype=np.uint16).view(np.float16).astype(np.float64)
+    e += list(h + 2.0 ** -11)
+    s = np.arange(0, 1024, 13, dtype=np.uint16).view(np.float16).astype(np.float64)
+    e += list(s + 2.0 ** -25)
+    return np.array(e, dtype=np.float64)
+
+
+def test_float_to_half_rne_vs_numpy():
+    x = np.concatenate([_edge_floats(), RNG.standard_normal(100000) * 10.0 ** RNG.integers(-9, 5, 100000)])
+    x32 = x.astype(np.float32)
+    ref = x32.astype(np.float16).view(np.uint16)
+    got = np.array([oracle.float_to_half(float(v)) for v in x32], dtype=np.uint16)
+    assert np.array_equal(got, ref)
+
+
+def test_double_to_half_rne_vs_numpy():
+    x = np.concatenate([_edge_floats(), RNG.standard_normal(100000) * 10.0 ** RNG.integers(-9, 5, 100000)])
+    ref = x.astype(np.float16).view(np.uint16)
+    got = np.array([oracle.double_to_half(float(v)) for v in x], dtype=np.uint16)
+    assert np.array_equal(got, ref)
+    assert oracle.double_to_half(float("nan")) & 0x7C00 == 0x7C00
+
+
+# ---------------------------------------------------------------------------------------------------
+# Packed layout and nibble order — golden worked example (tests/golden/nibble_order.txt).
+# ---------------------------------------------------------------------------------------------------
+def hand_group(K, N):
+    """w[k][n] = (((k+n) mod 16) - 4) * 2^-(3 + n mod 4): exactly representable with s_n = 2^-(3+n%4), z = 4,
+    q = (k+n) mod 16 (derivation: wmin = -4 s, wmax = 11 s, (wmax-wmin)/15 = s exactly)."""
+    k = np.arange(K)[:, None]
+    n = np.arange(N)[None, :]
+    w = (((k + n) % 16) - 4) * 2.0 ** (-(3 + n % 4))
+    return w.astype(np.float16)
+
+
+def _read_golden(name):
+    rows = {}
+    with open(os.path.join(GOLD, name)) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            key, *vals = line.split()
+            rows.setdefault(key, []).append(vals)
+    return rows
+
+
+def test_nibble_order_golden():
+    lines = [l.split() for l in open(os.path.join(GOLD, "nibble_order.txt")) if l.strip() and not l.startswith("#")]
+    K = N = 128
+    W = hand_group(K, N)  # column 0: q = k mod 16
+    qw, sc, ze, st = oracle.pack(W)
+    for j, (codes, canon, phys) in enumerate(lines):
+        codes = [int(c) for c in codes.split(",")]
+        assert [int(oracle.get_code(qw, K, N, 8 * j + i, 0)) for i in range(8)] == codes
+        assert sum(c << (4 * i) for i, c in enumerate(codes)) == int(canon, 16)
+        word = int(qw[oracle.word_index(K, N, 8 * j, 0)])
+        assert word == int(phys, 16)
+        # the LOP3 extraction the kernels use yields the consecutive-k pair in the two halves
+        pair = word & 0x000F000F
+        assert (pair & 0xFFFF, pair >> 16) == (codes[0], codes[1])
+        pair = (word >> 8) & 0x000F000F
+        assert (pair & 0xFFFF, pair >> 16) == (codes[4], codes[5])
+
+
+def test_layout_tiles_are_n_major_contiguous():
+    K, N = 384, 256
+    assert oracle.word_index(K, N, 0, 0) == 0
+    assert oracle.word_index(K, N, 8, 0) == 1
+    assert oracle.word_index(K, N, 0, 1) == 16
+    assert oracle.word_index(K, N, 128, 0) == 2048          # next k-group, same n-tile
+    assert oracle.word_index(K, N, 0, 128) == 3 * 2048      # next n-tile after K/128 groups
+    idx = {oracle.word_index(K, N, k, n) for k in range(0, K, 8) for n in range(N)}
+    assert idx == set(range(K * N // 8))                     # a bijection onto the buffer
+
+
+# ---------------------------------------------------------------------------------------------------
+# Pack / unpack — hand-computed group, SPEC example, degenerate groups, error bound.
+# ---------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("K,N", [(128, 128), (256, 384)])
+def test_pack_hand_group_exact_roundtrip(K, N):
+    W = hand_group(K, N)
+    qw, sc, ze, st = oracle.pack(W)
+    assert st == oracle.DEV_OK
+    n = np.arange(N)
+    assert np.array_equal(sc.view(np.float16).astype(np.float64), np.broadcast_to(2.0 ** (-(3 + n % 4)), sc.shape))
+    assert np.all(ze.view(np.float16) == 4)
+    for k in range(0, K, 37):
+        for nn in range(0, N, 11):
+            assert oracle.get_code(qw, K, N, k, nn) == (k + nn) % 16
+    Wh = oracle.unpack(qw, sc, ze, K, N)
+    assert np.array_equal(Wh, W.view(np.uint16))
+
+
+def test_pack_spec_example_sym():
+    g = _read_golden("spec_sym_example.txt")
+    w = [float(x) for x in g["w"][0]]
+    K, N = 128, 128
+    W = np.zeros((K, N), dtype=np.float16)
+    W[:4, 0] = w
+    qw, sc, ze, st = oracle.pack(W, group=4, mode=oracle.SYM)
+    assert int(sc[0, 0]) == int(g["scale_bits"][0][0], 16)
+    assert [oracle.get_code(qw, K, N, k, 0) for k in range(4)] == [int(c) for c in g["codes"][0]]
+    Wh = oracle.unpack(qw, sc, ze, K, N, group=4, mode=oracle.SYM).view(np.float16)
+    assert [float(x) for x in Wh[:4, 0]] == [float(x) for x in g["w_hat"][0]]
+
+
+@pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
+def test_pack_all_zero_group(mode):
+    # reading R15 (GPTQ): an all-zero group gets the range (-1, 1): s = fp16(2/15), q = z = 8, w_hat = 0
+    W = np.zeros((128, 128), dtype=np.float16)
+    qw, sc, ze, st = oracle.pack(W, mode=mode)
+    assert np.all(sc == 0x3044)
+    assert all(oracle.get_code(qw, 128, 128, k, n) == 8 for k in range(0, 128, 7) for n in range(0, 128, 5))
+    if mode == oracle.ASYM:
+        assert np.all(ze.view(np.float16) == 8)
+    assert np.all(oracle.unpack(qw, sc, ze, 128, 128, mode=mode) == 0)
+
+
+def test_pack_nonfinite_flags_status_and_counts_as_zero():
+    W = hand_group(128, 128)
+    W2 = W.copy()
+    W2[5, 3] = np.inf
+    W2[6, 3] = np.nan
+    qw, sc, ze, st = oracle.pack(W2)
+    assert st == oracle.DEV_NONFINITE
+    W3 = W.copy()
+    W3[5, 3] = 0
+    W3[6, 3] = 0
+    qw3, sc3, ze3, st3 = oracle.pack(W3)
+    assert st3 == oracle.DEV_OK
+    assert np.array_equal(qw, qw3) and np.array_equal(sc, sc3) and np.array_equal(ze, ze3)
+
+
+def test_pack_nonneg_group_zero_point_is_plus_zero():
+    W = np.abs(hand_group(128, 128))
+    qw, sc, ze, st = oracle.pack(W)
+    assert np.all(ze == 0)          # fp16 +0, never 0x8000
+
+
+@pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
+def test_pack_error_bound_and_zero_exact(mode):
+    # |w - w_hat| <= s/2 + 15*2^-11*s (fp16 rounding of s can force one clamp) + half an fp16 ulp of w_hat
+    K, N = 512, 256
+    W = synth.host(7, 3, synth.WEIGHT, K, N).view(np.float16)
+    W[::17, ::13] = 0.0
+    qw, sc, ze, st = oracle.pack(W, mode=mode)
+    Wh = oracle.unpack(qw, sc, ze, K, N, mode=mode).view(np.float16).astype(np.float64)
+    w = W.astype(np.float64)
+    s = np.repeat(sc.view(np.float16).astype(np.float64), 128, axis=0)
+    bound = s * (0.5 + 15 * 2.0 ** -11 + 1e-6) + np.abs(Wh) * 2.0 ** -11 + 2.0 ** -25
+    assert np.all(np.abs(w - Wh) <= bound)
+    assert np.all(Wh[w == 0] == 0)  # 0 is always representable (reading R3)
+    # codes in range and zero points are integers in [0, 15]
+    if mode == oracle.ASYM:
+        z = ze.view(np.float16).astype(np.float64)
+        assert np.all((z >= 0) & (z <= 15) & (z == np.round(z)))
+
+
+def test_pack_sym_zero_is_eight_and_range_centered():
+    K, N = 256, 128
+    W = synth.host(3, 9, synth.WEIGHT, K, N)
+    qw, sc, ze, st = oracle.pack(W, mode=oracle.SYM)
+    assert ze is None
+    Wh = oracle.unpack(qw, sc, None, K, N, mode=oracle.SYM).view(np.float16).astype(np.float64)
+    s = sc.view(np.float16).astype(np.float64)
+    # every dequantised value is an integer multiple of its scale in [-8, 7]
+    r = Wh / np.repeat(s, 128, axis=0)
+    # (w_hat is (q-8)*s rounded once to fp16: within 8 * 2^-11 of an integer multiple of s)
+    assert np.all(np.abs(r - np.round(r)) <= 8 * 2.0 ** -11) and np.round(r).min() >= -8 and np.round(r).max() <= 7
+
+
+# ---------------------------------------------------------------------------------------------------
+# GEMM reference — closed forms, one-hot exactness, numpy float64 matmul.
+# ---------------------------------------------------------------------------------------------------
+def test_gemm_ones_closed_form():
+    # X = ones, hand group, K = 4096: Y[n] = s_n * sum_k ((k+n)%16 - 4) = s_n * 256 * (120 - 64) = 14336 s_n
+    K, N = 4096, 256
+    W = hand_group(K, N)
+    qw, sc, ze, st = oracle.pack(W)
+    X = np.ones((2, K), dtype=np.float16)
+    Y = oracle.gemm(X, qw, sc, ze, K, N, nthreads=4)
+    n = np.arange(N)
+    exp = 14336.0 * 2.0 ** (-(3 + n % 4))
+    assert np.array_equal(Y[0], exp) and np.array_equal(Y[1], exp)
+    assert list(exp[:4]) == [1792.0, 896.0, 448.0, 224.0]
+
+
+def test_gemm_one_hot_rows_select_dequantised_weights():
+    K, N = 512, 256
+    W = synth.host(5, 1, synth.WEIGHT, K, N)
+    qw, sc, ze, st = oracle.pack(W)
+    Wh = oracle.unpack(qw, sc, ze, K, N).view(np.float16).astype(np.float64)
+    ks = [0, 1, 7, 8, 127, 128, 300, 511]
+    X = np.zeros((len(ks), K), dtype=np.float16)
+    for m, k in enumerate(ks):
+        X[m, k] = 1.0
+    Y = oracle.gemm(X, qw, sc, ze, K, N)
+    assert np.array_equal(Y, Wh[ks])
+
+
+@pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
+def test_gemm_matches_numpy_float64(mode):
+    K, N, M = 640, 384, 5
+    W = synth.host(11, 2, synth.WEIGHT, K, N)
+    X = synth.host(11, 3, synth.ACT, M, K)
+    qw, sc, ze, st = oracle.pack(W, mode=mode)
+    Wh = oracle.unpack(qw, sc, ze, K, N, mode=mode).view(np.float16).astype(np.float64)
+    ref = X.view(np.float16).astype(np.float64) @ Wh
+    Y1 = oracle.gemm(X, qw, sc, ze, K, N, mode=mode, nthreads=1)
+    Y3 = oracle.gemm(X, qw, sc, ze, K, N, mode=mode, nthreads=3)
+    assert np.array_equal(Y1, Y3)                          # thread count never changes the result
+    assert np.allclose(Y1, ref, rtol=1e-12, atol=1e-12)
+    cols = np.array([0, 5, 127, 128, 383])
+    assert np.array_equal(oracle.gemm_cols(X, qw, sc, ze, K, N, cols, mode=mode), Y1[:, cols])
+
+
+def test_gemm_transposition_sensitive():
+    # a transposed operand (using W_hat[n][k]) or swapped X rows would change this product
+    K, N = 256, 256
+    W = synth.host(2, 2, synth.WEIGHT, K, N)
+    X = synth.host(2, 4, synth.ACT, 3, K)
+    qw, sc, ze, st = oracle.pack(W)
+    Wh = oracle.unpack(qw, sc, ze, K, N).view(np.float16).astype(np.float64)
+    Y = oracle.gemm(X, qw, sc, ze, K, N)
+    Xd = X.view(np.float16).astype(np.float64)
+    assert not np.allclose(Y, Xd @ Wh.T)
+    assert np.allclose(Y, Xd @ Wh)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Acceptance — golden worked example, SPEC examples, brute force, losslessness vs AR decoding.
+# ---------------------------------------------------------------------------------------------------
+def test_accept_golden_8node():
+    g = _read_golden("accept_8node.txt")
+    t = [int(x) for x in g["tokens"][0]]
+    p = [int(x) for x in g["parents"][0]]
+    a = [int(x) for x in g["argmax"][0]]
+    L, bonus, st, path, _ = oracle.accept(t, p, a)
+    assert (L, bonus, st) == (int(g["len"][0][0]), int(g["bonus"][0][0]), oracle.DEV_OK)
+    assert path == [int(x) for x in g["path"][0]]
+
+
+def test_accept_spec_sequence_examples():
+    d = 6
+    cont = [5, 9, 2, 7, 7, 1, 3]                       # target's greedy continuation after the root
+    toks = [42] + cont[:d]
+    par = [-1] + list(range(d))
+    argmax = cont[:d + 1]                               # argmax at node i = next greedy token
+    assert oracle.accept(toks, par, argmax)[:3] == (d, cont[d], 0)      # S:292 perfect draft: all d accepted
+    bad = list(toks)
+    bad[1] = 99
+    assert oracle.accept(bad, par, argmax)[:3] == (0, cont[0], 0)       # S:293 draft[0] wrong: 0 + bonus
+
+
+def test_accept_spec_tree_examples():
+    # S:301 single-chain tree matching the greedy continuation -> whole chain accepted
+    assert oracle.accept([0, 4, 5, 6], [-1, 0, 1, 2], [4, 5, 6, 8])[:3] == (3, 8, 0)
+    # S:302 no child of the root matches the target argmax -> 0 accepted, bonus = argmax at root
+    assert oracle.accept([0, 4, 5, 6], [-1, 0, 0, 0], [9, 1, 1, 1])[:3] == (0, 9, 0)
+
+
+def test_accept_m1_equals_autoregressive_step():
+    # verification width 1 (root only) is exactly one AR decode step: nothing accepted, bonus = argmax
+    for a in [0, 17, 128255]:
+        assert oracle.accept([3], [-1], [a])[:4] == (0, a, 0, [])
+
+
+def test_accept_bad_trees():
+    for p in ([0, 0], [-1, 1], [-1, 0, 3], [-1, -1]):
+        L, bonus, st, path, out = oracle.accept([1] * len(p), p, [1] * len(p))
+        assert (L, bonus, st) == (0, -1, oracle.DEV_BAD_TREE) and np.all(out[3:] == -1)
+
+
+def _all_trees(n):
+    """All parent vectors with parents[i] < i for n nodes."""
+    for ps in itertools.product(*[range(i) for i in range(1, n)]):
+        yield [-1] + list(ps)
+
+
+def test_accept_brute_force_small_trees():
+    # enumerate every root->node path; valid iff each edge matches; choose longest, ties smallest end node
+    rng = np.random.default_rng(7)
+    count = 0
+    for n in range(1, 8):
+        for par in _all_trees(n):
+            for _ in range(3):
+                tok = rng.integers(0, 3, n).tolist()
+                am = rng.integers(0, 3, n).tolist()
+                best = (0, 0)
+                for end in range(n):
+                    path, x = [], end
+                    while x != 0:
+                        path.append(x)
+                        x = par[x]
+                    path.reverse()
+                    prev, ok = 0, True
+                    for c in path:
+                        ok &= tok[c] == am[prev]
+                        prev = c
+                    if ok and len(path) > best[0]:
+                        best = (len(path), end)
+                L, bonus, st, got_path, _ = oracle.accept(tok, par, am)
+                assert (L, bonus) == (best[0], am[best[1]])
+                count += 1
+    assert count > 1000
+
+
+def test_accept_lossless_vs_autoregressive_decoding():
+    # A deterministic "target" f(context) -> next token. Build random trees whose node tokens are sometimes the
+    # target's greedy token; argmax[i] = f(context of i). The accepted tokens + bonus must equal the first
+    # len+1 tokens of AR greedy decoding, and no tree path may match a longer AR prefix (losslessness).
+    rng = np.random.default_rng(99)
+
+    def f(ctx):
+        h = 1469598103934665603
+        for t in ctx:
+            h = ((h ^ t) * 1099511628211) & 0xFFFFFFFFFFFF
+        return h % 5
+
+    for trial in range(400):
+        n = int(rng.integers(1, 40))
+        par = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+        prefix = [int(x) for x in rng.integers(0, 5, 3)]
+        toks, ctx = [prefix[-1]], [prefix]
+        for i in range(1, n):
+            c = ctx[par[i]]
+            t = f(c) if rng.random() < 0.6 else int(rng.integers(0, 5))
+            toks.append(t)
+            ctx.append(c + [t])
+        am = [f(c) for c in ctx]
+        L, bonus, st, path, _ = oracle.accept(toks, par, am)
+        # AR rollout from the prefix
+        ar, c = [], list(prefix)
+        for _ in range(n + 1):
+            t = f(c)
+            ar.append(t)
+            c.append(t)
+        assert [toks[i] for i in path] + [bonus] == ar[:L + 1]
+        # maximality: no node's context extends the AR prefix beyond L
+        for i in range(n):
+            d = len(ctx[i]) - len(prefix)
+            if ctx[i][len(prefix):] == ar[:d]:
+                assert d <= L
