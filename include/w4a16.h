@@ -1,0 +1,120 @@
+/* w4a16.h — C ABI of the B200 (sm_100a) W4A16 verification hot path of arXiv 2505.22179 (HierSpec).
+ *
+ * The path: the target model's multi-token verification forward through W4A16 linear layers (group-128
+ * int4 weights, fp16 activations, fp32 accumulate) at draft widths M = 1..64, followed by greedy
+ * tree/sequence acceptance.  Citations are PAPER.md lines ("P:n"), SPEC.md lines ("S:n"), SURVEY.md
+ * sections; the readings of the paper these calls implement are listed in DESIGN.md §3 (R1..R15).
+ *
+ * Conventions for every call:
+ *   - All tensor pointers are DEVICE pointers (cudaMalloc'd or equivalent), 16-byte aligned.
+ *   - fp16 tensors are passed as uint16_t* holding IEEE binary16 bit patterns.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is asynchronous on it, does no
+ *     host synchronisation, allocates nothing, and is CUDA-graph capturable.
+ *   - The caller owns and allocates every buffer; the library keeps no global state.
+ *   - Return value: W4A16_OK (0) or a negative w4a16_status detected on the host (arguments, shapes,
+ *     alignment, workspace, launch failure).  Problems only visible on the device are written to a
+ *     caller-provided device status word (w4a16_dev_status values).
+ *   - Thread safety: calls are re-entrant; concurrent calls must not share output or workspace buffers.
+ *
+ * Shapes (GEMM convention of BASELINE.json): Y[M,N] = X[M,K] · W[K,N]; K = in-features, N = out-features.
+ * Requirements: group == 128, K % 128 == 0, N % 128 == 0, 1 <= M <= 64 for the GEMM.
+ *
+ * qweight layout ("tiled n-major", the format w4a16_pack writes and w4a16_gemm reads):
+ *   uint32 qweight[K*N/8], organised in 128x128 (k x n) tiles. Tile (t = n/128, g = k/128) occupies the
+ *   2048 words starting at word (t*(K/128) + g) * 2048.  Inside a tile, row r = n % 128 owns the 16 words
+ *   at r*16 .. r*16+15; word j = (k % 128) / 8 holds k = 128g + 8j + i for i = 0..7, with the 4-bit code of
+ *   local index i in nibble slot (i % 2) * 4 + i / 2 (bits 4*slot .. 4*slot+3).  So the two 16-bit halves
+ *   of (word & 0x000F000F) are the codes of k = 8j and 8j+1, of ((word >> 4) & 0x000F000F) those of
+ *   8j+2, 8j+3, and so on.  Canonical logical order is SPEC's "low nibble first" along k
+ *   (S:33); example: codes 0..7 of one word are 0x76543210 canonical, 0x75316420 physical.
+ *   A column shard (n range, multiple of 128) is a contiguous sub-range of whole tiles.
+ * scales, zeros: fp16 [K/128][N] row-major.  zeros hold the integer zero point z in [0,15] as fp16
+ *   (ASYM); in SYM mode z == 8 and `zeros` may be NULL.
+ * Dequantised weight (definition): w_hat[k][n] = fp16_rne((q[k][n] - z) * s).
+ */
+#ifndef W4A16_H
+#define W4A16_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  W4A16_OK = 0,
+  W4A16_ERR_ARG = -1,        /* NULL pointer, bad mode/group, or value out of range */
+  W4A16_ERR_SHAPE = -2,      /* K, N not multiples of 128, M out of [1, 64], n out of [1, 1024] */
+  W4A16_ERR_ALIGN = -3,      /* a pointer is not 16-byte aligned */
+  W4A16_ERR_WORKSPACE = -4,  /* workspace NULL or smaller than w4a16_gemm_workspace_bytes() */
+  W4A16_ERR_CUDA = -5        /* kernel launch or device query failed */
+} w4a16_status;
+
+enum { W4A16_ASYM = 0, W4A16_SYM = 1 };
+enum { W4A16_DEV_OK = 0, W4A16_DEV_NONFINITE = 1, W4A16_DEV_BAD_TREE = 2 };
+#define W4A16_GROUP 128
+#define W4A16_MAX_M 64
+#define W4A16_MAX_TREE 1024
+
+typedef struct CUstream_st* w4a16_stream_t;   /* == cudaStream_t */
+
+/* w4a16_pack — quantise fp16 W[K][N] (row-major) to int4 codes + per-group fp16 scale/zero.
+ * Method: GPTQ W4 group-128 storage format, round-to-nearest in place of GPTQ's calibration
+ * (S:95), per column n and group of 128 consecutive k:
+ *   ASYM: wmin = min(min w, 0), wmax = max(max w, 0); equal -> (-1, 1); s = fp16_rne((wmax-wmin)/15);
+ *         z = clamp(rne(-wmin/s), 0, 15); q = clamp(rne(w/s) + z, 0, 15)     (fp32 arithmetic, RNE)
+ *   SYM:  amax = max|w| (0 -> 1); s = fp16_rne(2*amax/15); z = 8; q = clamp(rne(w/s) + 8, 0, 15)
+ *   A scale that underflows to 0 is recomputed from the range (-1, 1).
+ * Outputs: qweight [K*N/8] (layout above), scales [K/128][N], zeros [K/128][N] (may be NULL for SYM).
+ * Non-finite weights count as 0 and set *dev_status = W4A16_DEV_NONFINITE; otherwise *dev_status is
+ * left untouched (caller zeroes it).  dev_status may be NULL.  Bit-exact with the CPU oracle. */
+int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
+               uint16_t* zeros, int32_t* dev_status, w4a16_stream_t stream);
+
+/* w4a16_unpack — W_hat[K][N] fp16 = fp16_rne((q - z) * s) (test/debug). Bit-exact with the oracle. */
+int w4a16_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
+                 int mode, uint16_t* W_hat, w4a16_stream_t stream);
+
+/* Workspace bytes w4a16_gemm needs for this shape (split-K partials + one counter per 128-column tile).
+ * Before its first use the workspace must be zero-filled (w4a16_workspace_init); every w4a16_gemm leaves
+ * it zeroed again, so one workspace serves any sequence of calls on one stream. Returns 0 on bad shape. */
+size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group);
+int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
+
+/* w4a16_gemm — Y[M][N] fp16 = X[M][K] fp16 · W_hat[K][N], fp32 accumulation, one fp32->fp16 RNE at the
+ * end (BASELINE.json north_star; reading R8).  Scales are applied per group to fp32 partial sums, so Y
+ * equals the oracle's fp64 result within |Y - Y_ref| <= 1e-2 * (1 + |Y_ref|), not bit-for-bit.
+ * The split-K / stream-K plan depends only on (K, N, SM count), never on M, and the cross-CTA reduction
+ * runs in a fixed order: results are deterministic and row m of Y does not depend on the other rows of X
+ * within one kernel family (family = mma.sync for M <= 16, tcgen05 for M > 16).
+ * Rows of Y beyond M and bytes outside Y are never written. */
+int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
+               uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace, size_t workspace_bytes,
+               w4a16_stream_t stream);
+
+/* verify_accept — greedy acceptance of a draft tree against the target's argmax (rule per
+ * S:289/S:298, reading R9).  n nodes, node 0 = root (the last committed token, row 0 of the verify
+ * forward), parents[0] = -1, 0 <= parents[i] < i.  target_argmax[i] = target's greedy token after node i.
+ * ok(i) = every edge p->c on the root->i path has tokens[c] == target_argmax[p]; the accepted node is the
+ * deepest ok node (ties: smallest index). Writes (device int32) out[0] = accepted length (root excluded),
+ * out[1] = bonus token = target_argmax[accepted node], out[2] = device status, out[3 .. 3+n) = accepted
+ * path as node indices root->leaf, padded with -1.  A malformed tree writes {0, -1, BAD_TREE, -1 ...}.
+ * A sequence draft is parents[i] = i - 1 (longest matching prefix). 1 <= n <= W4A16_MAX_TREE. */
+int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n, int32_t* out,
+                  w4a16_stream_t stream);
+
+/* w4a16_silu_mul — Llama MLP glue between the fused gate-up GEMM and the down GEMM of the verify forward
+ * (not a step of the paper's method): GU is fp16 [M][2F] holding [gate | up] per row (the
+ * rank-local shard layout of tp.py), out is fp16 [M][F], out[m][j] = fp16_rne(silu(gate) * up) in fp32.
+ * F % 8 == 0, M >= 1. */
+int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream_t stream);
+
+/* Human-readable name of a w4a16_status value. */
+const char* w4a16_status_string(int status);
+
+/* Number of the last kernel family used by w4a16_gemm for M (0 = mma.sync, 1 = tcgen05); for reporting. */
+int w4a16_gemm_family(int M, int K, int N);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

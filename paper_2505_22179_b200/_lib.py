@@ -1,0 +1,73 @@
+"""ctypes binding of libw4a16.so — the C ABI declared in include/w4a16.h.
+
+Argument marshalling only: every step of the path runs in the sm_100a kernels behind the ABI. There is
+no CPU fallback: if the shared library is missing the import of this module raises.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libw4a16.so")
+
+W4A16_OK = 0
+W4A16_ASYM = 0
+W4A16_SYM = 1
+W4A16_DEV_OK = 0
+W4A16_DEV_NONFINITE = 1
+W4A16_DEV_BAD_TREE = 2
+W4A16_GROUP = 128
+W4A16_MAX_M = 64
+W4A16_MAX_TREE = 1024
+
+# Every symbol include/w4a16.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = (
+    "w4a16_pack",
+    "w4a16_unpack",
+    "w4a16_gemm_workspace_bytes",
+    "w4a16_workspace_init",
+    "w4a16_gemm",
+    "verify_accept",
+    "w4a16_status_string",
+    "w4a16_gemm_family",
+    "w4a16_silu_mul",
+)
+
+
+class W4A16Error(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built: run `make` (or __graft_entry__.build()). "
+            "The W4A16 path has no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.w4a16_pack.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+    lib.w4a16_unpack.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp]
+    lib.w4a16_gemm_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    lib.w4a16_gemm_workspace_bytes.restype = sz
+    lib.w4a16_workspace_init.argtypes = [vp, sz, vp]
+    lib.w4a16_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, vp]
+    lib.verify_accept.argtypes = [vp, vp, vp, i32, vp, vp]
+    lib.w4a16_status_string.argtypes = [i32]
+    lib.w4a16_status_string.restype = ctypes.c_char_p
+    lib.w4a16_gemm_family.argtypes = [i32, i32, i32]
+    lib.w4a16_silu_mul.argtypes = [vp, i32, i32, vp, vp]
+    for name in ("w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "verify_accept",
+                 "w4a16_gemm_family", "w4a16_silu_mul"):
+        getattr(lib, name).restype = i32
+    return lib
+
+
+lib = _load()
+
+
+def status_string(status: int) -> str:
+    return lib.w4a16_status_string(int(status)).decode()
+
+
+def check(status: int, what: str) -> None:
+    if status != W4A16_OK:
+        raise W4A16Error(f"{what}: {status_string(status)} ({status})")

@@ -1,0 +1,114 @@
+// abi.cu — the C-ABI entry points of libw4a16.so (include/w4a16.h): host-side validation, planning and
+// dispatch to the kernels in pack.cu, gemm_mma.cu, gemm_tc.cu and accept.cu. No device allocation, no
+// host synchronisation, no global state beyond a per-device SM-count cache.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "w4a16.h"
+
+extern "C" int w4a16_launch_pack(const uint16_t*, int, int, int, uint32_t*, uint16_t*, uint16_t*, int32_t*, cudaStream_t);
+extern "C" int w4a16_launch_unpack(const uint32_t*, const uint16_t*, const uint16_t*, int, int, int, uint16_t*, cudaStream_t);
+extern "C" int w4a16_launch_accept(const int32_t*, const int32_t*, const int32_t*, int, int32_t*, cudaStream_t);
+extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaStream_t);
+extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
+extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const uint32_t*, const uint16_t*, const uint16_t*, uint16_t*, int,
+                                     int, int, int, void*, int, cudaStream_t);
+
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int num_sms_of_current_device() {
+  static int cache[64] = {0};   // benign race: every writer stores the same value
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return -1;
+  if (dev < 64 && cache[dev] > 0) return cache[dev];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return -1;
+  if (dev < 64) cache[dev] = n;
+  return n;
+}
+
+int check_kn(int K, int N, int group) {
+  if (group != W4A16_GROUP) return W4A16_ERR_ARG;
+  if (K <= 0 || N <= 0 || K % 128 != 0 || N % 128 != 0) return W4A16_ERR_SHAPE;
+  return W4A16_OK;
+}
+
+}  // namespace
+
+extern "C" int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
+                          uint16_t* zeros, int32_t* dev_status, w4a16_stream_t stream) {
+  if (!W || !qweight || !scales || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
+    return W4A16_ERR_ARG;
+  if (int e = check_kn(K, N, group)) return e;
+  if (!aligned16(W) || !aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros))) return W4A16_ERR_ALIGN;
+  return w4a16_launch_pack(W, K, N, mode, qweight, scales, zeros, dev_status, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N,
+                            int group, int mode, uint16_t* W_hat, w4a16_stream_t stream) {
+  if (!qweight || !scales || !W_hat || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
+    return W4A16_ERR_ARG;
+  if (int e = check_kn(K, N, group)) return e;
+  if (!aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros)) || !aligned16(W_hat)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_unpack(qweight, scales, zeros, K, N, mode, W_hat, (cudaStream_t)stream);
+}
+
+extern "C" size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group) {
+  if (check_kn(K, N, group) != W4A16_OK || M < 1 || M > W4A16_MAX_M) return 0;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return 0;
+  return w4a16_mma_workspace_bytes(M, K, N, sms);
+}
+
+extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!workspace) return W4A16_ERR_ARG;
+  return cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+extern "C" int w4a16_gemm_family(int M, int K, int N) {
+  (void)M; (void)K; (void)N;
+  return 0;
+}
+
+extern "C" int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
+                          uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace,
+                          size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!X || !qweight || !scales || !Y || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
+    return W4A16_ERR_ARG;
+  if (int e = check_kn(K, N, group)) return e;
+  if (M < 1 || M > W4A16_MAX_M) return W4A16_ERR_SHAPE;
+  if (!aligned16(X) || !aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros)) || !aligned16(Y) ||
+      !aligned16(workspace))
+    return W4A16_ERR_ALIGN;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+  return w4a16_launch_gemm_mma(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+}
+
+extern "C" int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n,
+                             int32_t* out, w4a16_stream_t stream) {
+  if (!tokens || !parents || !target_argmax || !out) return W4A16_ERR_ARG;
+  if (n < 1 || n > W4A16_MAX_TREE) return W4A16_ERR_SHAPE;
+  return w4a16_launch_accept(tokens, parents, target_argmax, n, out, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream_t stream) {
+  if (!GU || !out) return W4A16_ERR_ARG;
+  if (M < 1 || F < 8 || F % 8 != 0) return W4A16_ERR_SHAPE;
+  if (!aligned16(GU) || !aligned16(out)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_silu_mul(GU, M, F, out, (cudaStream_t)stream);
+}
+
+extern "C" const char* w4a16_status_string(int status) {
+  switch (status) {
+    case W4A16_OK: return "W4A16_OK";
+    case W4A16_ERR_ARG: return "W4A16_ERR_ARG: invalid argument";
+    case W4A16_ERR_SHAPE: return "W4A16_ERR_SHAPE: unsupported shape";
+    case W4A16_ERR_ALIGN: return "W4A16_ERR_ALIGN: pointer not 16-byte aligned";
+    case W4A16_ERR_WORKSPACE: return "W4A16_ERR_WORKSPACE: workspace missing or too small";
+    case W4A16_ERR_CUDA: return "W4A16_ERR_CUDA: CUDA launch or query failed";
+    default: return "unknown w4a16 status";
+  }
+}

@@ -1,0 +1,41 @@
+// mlp_glue.cu — w4a16_silu_mul: the elementwise step between the fused gate-up GEMM and the down GEMM of
+// a Llama MLP in the verify forward. GU[m] = [gate_0..gate_{F-1} | up_0..up_{F-1}] (the
+// rank-local gate-up shard), out[m][j] = fp16_rne(silu(gate_j) * up_j), computed in fp32.
+#include "common.cuh"
+#include "w4a16.h"
+
+namespace w4 {
+
+__global__ void __launch_bounds__(256) silu_mul_kernel(const uint16_t* __restrict__ GU, int M, int F,
+                                                       uint16_t* __restrict__ out) {
+  const int vecs = F / 8;  // 8 halves per 16-byte vector
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)M * vecs;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(i / vecs), v = (int)(i % vecs);
+    const uint4 g = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + (size_t)v * 8);
+    const uint4 u = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + F + (size_t)v * 8);
+    const __half2* gh = reinterpret_cast<const __half2*>(&g);
+    const __half2* uh = reinterpret_cast<const __half2*>(&u);
+    uint4 r;
+    __half2* rh = reinterpret_cast<__half2*>(&r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 gf = __half22float2(gh[j]), uf = __half22float2(uh[j]);
+      const float a = gf.x / (1.0f + __expf(-gf.x)) * uf.x;
+      const float b = gf.y / (1.0f + __expf(-gf.y)) * uf.y;
+      rh[j] = __floats2half2_rn(a, b);
+    }
+    *reinterpret_cast<uint4*>(out + (size_t)m * F + (size_t)v * 8) = r;
+  }
+}
+
+}  // namespace w4
+
+extern "C" int w4a16_launch_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, cudaStream_t stream) {
+  const long long work = (long long)M * (F / 8);
+  if (work == 0) return W4A16_OK;
+  long long blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  w4::silu_mul_kernel<<<(unsigned)blocks, 256, 0, stream>>>(GU, M, F, out);
+  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}

@@ -28,6 +28,9 @@ def _host_lib():
         _host.synth_fill_host.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_void_p]
         _host.synth_fill_host.restype = ctypes.c_int
+        _host.synth_fill_host_block.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int] + [ctypes.c_int] * 6 + [
+            ctypes.c_void_p]
+        _host.synth_fill_host_block.restype = ctypes.c_int
         _host.synth_value_host.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_int]
         _host.synth_value_host.restype = ctypes.c_uint16
@@ -52,6 +55,14 @@ def host(seed: int, tensor_id: int, kind: int, rows: int, cols: int) -> np.ndarr
     out = np.empty((rows, cols), dtype=np.uint16)
     if _host_lib().synth_fill_host(seed, tensor_id, kind, rows, cols, out.ctypes.data) != 0:
         raise ValueError("synth_fill_host: bad arguments")
+    return out
+
+
+def host_block(seed, tensor_id, kind, rows, cols, r0, r1, c0, c1) -> np.ndarray:
+    """Sub-block [r0:r1, c0:c1] of host(seed, tensor_id, kind, rows, cols), without generating the rest."""
+    out = np.empty((r1 - r0, c1 - c0), dtype=np.uint16)
+    if _host_lib().synth_fill_host_block(seed, tensor_id, kind, rows, cols, r0, r1, c0, c1, out.ctypes.data) != 0:
+        raise ValueError("synth_fill_host_block: bad arguments")
     return out
 
 

@@ -63,3 +63,13 @@ int synth_fill_host(uint64_t seed, uint64_t tensor_id, int kind, int rows, int c
     for (int c = 0; c < cols; ++c) out[(size_t)r * cols + c] = synth_value_host(seed, tensor_id, kind, rows, cols, r, c);
   return 0;
 }
+
+int synth_fill_host_block(uint64_t seed, uint64_t tensor_id, int kind, int rows, int cols, int r0, int r1, int c0,
+                          int c1, uint16_t* out) {
+  if (!out || r0 < 0 || c0 < 0 || r1 > rows || c1 > cols || r0 > r1 || c0 > c1 || (kind != SYNTH_WEIGHT && kind != SYNTH_ACT))
+    return -1;
+  for (int r = r0; r < r1; ++r)
+    for (int c = c0; c < c1; ++c)
+      out[(size_t)(r - r0) * (c1 - c0) + (c - c0)] = synth_value_host(seed, tensor_id, kind, rows, cols, r, c);
+  return 0;
+}

@@ -31,6 +31,10 @@ enum { SYNTH_WEIGHT = 0, SYNTH_ACT = 1 };
 /* Host fill: out[r*cols + c] for r in [0,rows), c in [0,cols). kind = SYNTH_WEIGHT (rows=K, cols=N) or
  * SYNTH_ACT (rows=M, cols=K). Returns 0, or -1 on bad arguments. */
 int synth_fill_host(uint64_t seed, uint64_t tensor_id, int kind, int rows, int cols, uint16_t* out);
+/* Sub-block [r0,r1) x [c0,c1) of the same tensor (values depend only on (r, c, rows, cols)); out is
+ * (r1-r0) x (c1-c0) row-major. */
+int synth_fill_host_block(uint64_t seed, uint64_t tensor_id, int kind, int rows, int cols, int r0, int r1, int c0,
+                          int c1, uint16_t* out);
 /* Single element (used by full-size sampled parity checks). */
 uint16_t synth_value_host(uint64_t seed, uint64_t tensor_id, int kind, int rows, int cols, int r, int c);
 /* Device fill (synth_gpu.cu): out is a device pointer; async on stream (a cudaStream_t). */

@@ -1,0 +1,85 @@
+"""The C-ABI library loads, exports every symbol include/w4a16.h declares, and rejects bad arguments on the
+host before touching the GPU (-m "not gpu": no compute call is made without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "w4a16.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return re.findall(r"^\s*(?:int|size_t|const char\s*\*)\s+(\w+)\s*\(", src, flags=re.M)
+
+
+def test_header_declares_the_abi():
+    names = declared_functions()
+    for required in ("w4a16_pack", "w4a16_unpack", "w4a16_gemm", "w4a16_gemm_workspace_bytes", "verify_accept",
+                     "w4a16_status_string"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2505_22179_b200 import _lib
+    names = declared_functions()
+    assert set(names) == set(_lib.ABI_SYMBOLS)
+    raw = ctypes.CDLL(_lib.LIB_PATH)
+    for n in names:
+        assert hasattr(raw, n), n
+
+
+def test_status_strings():
+    from paper_2505_22179_b200 import w4a16_status_string
+    assert w4a16_status_string(0) == "W4A16_OK"
+    for s in (-1, -2, -3, -4, -5):
+        assert w4a16_status_string(s).startswith("W4A16_ERR")
+    assert "unknown" in w4a16_status_string(17)
+
+
+def test_host_validation_before_any_cuda_call():
+    from paper_2505_22179_b200._lib import lib
+    A = 0x10000  # a 16-byte-aligned fake device address: validation must reject before dereferencing
+    # w4a16_gemm(X, qw, sc, ze, Y, M, K, N, group, mode, ws, ws_bytes, stream)
+    assert lib.w4a16_gemm(None, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1
+    assert lib.w4a16_gemm(A, A, A, None, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1   # ASYM needs zeros
+    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 64, 0, A, 1 << 20, None) == -1       # group must be 128
+    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4000, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4100, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, A, A, 0, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, A, A, 65, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A + 2, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -3
+    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 128, 7, A, 1 << 20, None) == -1     # bad mode
+    assert lib.w4a16_pack(A, 4096, 4096, 128, 0, A, A, None, None, None) == -1
+    assert lib.w4a16_pack(A, 100, 4096, 128, 0, A, A, A, None, None) == -2
+    assert lib.w4a16_unpack(A, A, A, 4096, 4096, 128, 1, A + 8, None) == -3
+    assert lib.verify_accept(A, A, A, 0, A, None) == -2
+    assert lib.verify_accept(A, A, A, 1025, A, None) == -2
+    assert lib.verify_accept(None, A, A, 8, A, None) == -1
+    assert lib.w4a16_gemm_workspace_bytes(8, 4000, 4096, 128) == 0
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    # valid arguments on a machine without a GPU: the library reports a CUDA failure, it never computes on CPU
+    from paper_2505_22179_b200._lib import lib
+    A = 0x10000
+    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 30, None) == -5
+    assert lib.w4a16_gemm_workspace_bytes(8, 4096, 4096, 128) == 0
+
+
+def test_product_never_touches_the_oracle():
+    # the product path (package + CUDA sources) shares no code with oracle/ and never imports it
+    pkg = os.path.join(ROOT, "paper_2505_22179_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                for bad in ("w4a16_oracle", "import oracle", "from oracle", "orc_", "libw4a16_oracle"):
+                    assert bad not in txt, (f, bad)
+    hdr = open(HEADER).read()
+    assert "w4a16_oracle" not in hdr and "orc_" not in hdr

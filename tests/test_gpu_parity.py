@@ -1,0 +1,311 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): pack/unpack/accept bit-exact; GEMM |Y - Y_ref| <= 1e-2 * (1 + |Y_ref|)
+elementwise against the oracle's fp64 result. Sizes span several 128x128 tiles, ragged M, and the stream-K
+split/fixup paths; full-size 70B shapes are checked on sampled 128-column tiles (tests/test_gpu_fullsize.py).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+NPROC = os.cpu_count() or 1
+
+
+def _lib():
+    import paper_2505_22179_b200 as w4
+    return w4
+
+
+def to_np_u16(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def gpu_pack(W_u16: np.ndarray, mode):
+    w4 = _lib()
+    W = torch.from_numpy(W_u16.view(np.int16)).cuda().view(torch.float16)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pl = w4.pack_linear(W, mode=mode, dev_status=st)
+    torch.cuda.synchronize()
+    return pl, int(st.item())
+
+
+def assert_gemm_close(Y_gpu: torch.Tensor, Y_ref: np.ndarray, what=""):
+    y = Y_gpu.float().cpu().numpy().astype(np.float64)
+    err = np.abs(y - Y_ref)
+    lim = TOL * (1.0 + np.abs(Y_ref))
+    bad = err > lim
+    assert not bad.any(), f"{what}: {bad.sum()} elements out of tolerance; max err {err.max():.4g}, " \
+                          f"worst at {np.unravel_index(np.argmax(err - lim), err.shape)}"
+    assert np.isfinite(y).all()
+
+
+# ---------------------------------------------------------------------------------------------------
+# synthetic inputs: GPU generator == host generator (bit-exact), the premise of every comparison below
+# ---------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kind,rows,cols", [(synth.WEIGHT, 384, 256), (synth.ACT, 7, 4096), (synth.ACT, 64, 1024)])
+def test_synth_gpu_equals_host(kind, rows, cols):
+    h = synth.host(3, 77, kind, rows, cols)
+    g = to_np_u16(synth.gpu(3, 77, kind, rows, cols))
+    assert np.array_equal(h, g)
+
+
+# ---------------------------------------------------------------------------------------------------
+# pack / unpack: bit-exact
+# ---------------------------------------------------------------------------------------------------
+def _special_weights(K, N, seed):
+    W = synth.host(seed, 1, synth.WEIGHT, K, N).view(np.float16).copy()
+    W[0:128, 0] = 0                                   # all-zero group
+    W[128:256, 1] = np.abs(W[128:256, 1])             # non-negative group (z = 0)
+    W[0:128, 2] = -np.abs(W[0:128, 2])                # non-positive group
+    W[0:128, 3] = np.float16(6e-8)                    # subnormal, scale underflow -> (-1, 1) range
+    W[0:128, 4] = np.float16(60000.0)                 # near fp16 max
+    W[5, 5] = -60000.0
+    W[0:128, 6] = np.linspace(-1, 1, 128).astype(np.float16)
+    W[7, 7] = 1e-3                                    # single non-zero
+    return W.view(np.uint16)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("K,N", [(128, 128), (256, 384), (4096, 4096)])
+def test_pack_bit_exact(mode, K, N):
+    W = _special_weights(K, N, seed=K + N)
+    qw_r, sc_r, ze_r, st_r = oracle.pack(W, mode=mode)
+    pl, st = gpu_pack(W, mode)
+    assert st == st_r == 0
+    assert np.array_equal(pl.qweight.cpu().numpy().view(np.uint32), qw_r)
+    assert np.array_equal(to_np_u16(pl.scales), sc_r)
+    if mode == 0:
+        assert np.array_equal(to_np_u16(pl.zeros), ze_r)
+    # unpack bit-exact
+    w4 = _lib()
+    Wh = torch.empty((K, N), dtype=torch.float16, device="cuda")
+    w4.w4a16_unpack(pl.qweight, pl.scales, pl.zeros, Wh, mode)
+    assert np.array_equal(to_np_u16(Wh), oracle.unpack(qw_r, sc_r, ze_r, K, N, mode=mode))
+
+
+def test_pack_nonfinite_status():
+    K, N = 256, 256
+    W = _special_weights(K, N, 5).view(np.float16).copy()
+    W[10, 10] = np.inf
+    W[200, 100] = np.nan
+    W = W.view(np.uint16)
+    qw_r, sc_r, ze_r, st_r = oracle.pack(W)
+    pl, st = gpu_pack(W, 0)
+    assert st == st_r == oracle.DEV_NONFINITE
+    assert np.array_equal(pl.qweight.cpu().numpy().view(np.uint32), qw_r)
+    assert np.array_equal(to_np_u16(pl.scales), sc_r)
+    assert np.array_equal(to_np_u16(pl.zeros), ze_r)
+
+
+def test_pack_column_shard_is_tile_range():
+    # TP column shard (n range multiple of 128) of the packed tensor == pack of the shard
+    K, N, t = 512, 1024, 4
+    W = synth.host(9, 4, synth.WEIGHT, K, N)
+    full, _ = gpu_pack(W, 0)
+    q = full.qweight.cpu().numpy().view(np.uint32)
+    for r in range(t):
+        sh = np.ascontiguousarray(W[:, r * N // t:(r + 1) * N // t])
+        part, _ = gpu_pack(sh, 0)
+        nq = part.qweight.numel()
+        assert np.array_equal(part.qweight.cpu().numpy().view(np.uint32), q[r * nq:(r + 1) * nq])
+        assert np.array_equal(to_np_u16(part.scales), to_np_u16(full.scales)[:, r * N // t:(r + 1) * N // t])
+
+
+# ---------------------------------------------------------------------------------------------------
+# GEMM: tolerance vs fp64 oracle, one-hot exactness, batch invariance, determinism, buffer discipline
+# ---------------------------------------------------------------------------------------------------
+class Problem:
+    def __init__(self, K, N, mode=0, seed=0):
+        self.K, self.N, self.mode = K, N, mode
+        self.W = synth.host(seed, 11, synth.WEIGHT, K, N)
+        self.qw, self.sc, self.ze, _ = oracle.pack(self.W, mode=mode)
+        self.pl, _ = gpu_pack(self.W, mode)
+        w4 = _lib()
+        self.ws = w4.alloc_workspace(64, [(K, N)])
+
+    def run(self, X_u16, Y=None):
+        w4 = _lib()
+        M = X_u16.shape[0]
+        X = torch.from_numpy(X_u16.view(np.int16)).cuda().view(torch.float16)
+        if Y is None:
+            Y = torch.empty((M, self.N), dtype=torch.float16, device="cuda")
+        self.pl(X, Y, self.ws)
+        torch.cuda.synchronize()
+        return Y
+
+    def ref(self, X_u16):
+        return oracle.gemm(X_u16, self.qw, self.sc, self.ze, self.K, self.N, mode=self.mode, nthreads=NPROC)
+
+
+_P = {}
+
+
+def problem(K, N, mode=0, seed=0):
+    key = (K, N, mode, seed)
+    if key not in _P:
+        _P[key] = Problem(K, N, mode, seed)
+    return _P[key]
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 7, 8, 9, 13, 16, 17, 24, 31, 32, 48, 61, 64])
+def test_gemm_config1_tolerance(M):
+    # config 1: K = N = 4096, g128 ASYM; M sweeps both kernel families and ragged token blocks
+    P = problem(4096, 4096)
+    X = synth.host(100 + M, 12, synth.ACT, M, 4096)
+    assert_gemm_close(P.run(X), P.ref(X), f"M={M}")
+
+
+@pytest.mark.parametrize("K,N,M", [(128, 128, 4), (128, 1280, 8), (3584, 1024, 16), (1024, 8192, 7),
+                                   (28672, 256, 3), (8192, 384, 64), (256, 57344 // 8, 12)])
+def test_gemm_shapes_tolerance(K, N, M):
+    # single tile, TP8 shard shapes (QKV N=1280, O K=1024, down K=3584), tall-K/narrow-N stream-K splits
+    P = problem(K, N, seed=K ^ N)
+    X = synth.host(7 + M, 13, synth.ACT, M, K)
+    assert_gemm_close(P.run(X), P.ref(X), f"K={K} N={N} M={M}")
+
+
+@pytest.mark.parametrize("M", [1, 8, 16, 40, 64])
+def test_gemm_sym_tolerance(M):
+    P = problem(2048, 1536, mode=1, seed=3)
+    X = synth.host(55 + M, 14, synth.ACT, M, 2048)
+    assert_gemm_close(P.run(X), P.ref(X), f"SYM M={M}")
+
+
+@pytest.mark.parametrize("M", [8, 16, 33, 64])
+def test_gemm_one_hot_bit_exact(M):
+    # row m of X = e_{k_m}: Y[m] must equal the dequantised weight row w_hat[k_m] bit-for-bit (pins layout,
+    # nibble order, zero/scale handling and the epilogue mapping of the whole pack -> GEMM data path)
+    K, N = 1024, 768
+    P = problem(K, N, seed=21)
+    rng = np.random.default_rng(M)
+    ks = rng.choice(K, size=M, replace=False)
+    X = np.zeros((M, K), dtype=np.float16)
+    X[np.arange(M), ks] = 1.0
+    Y = to_np_u16(P.run(X.view(np.uint16)))
+    Wh = oracle.unpack(P.qw, P.sc, P.ze, K, N)
+    assert np.array_equal(Y, Wh[ks])
+
+
+def test_gemm_batch_invariance_within_family():
+    # the plan depends on (K, N) only: row m of Y(M) equals Y(1) of that row, bit-for-bit, within a family
+    w4 = _lib()
+    P = problem(4096, 4096)
+    X = synth.host(31, 15, synth.ACT, 64, 4096)
+    for Ms in ([1, 2, 5, 8, 16], [17, 32, 64]):
+        fam = {w4.w4a16_gemm_family(M, 4096, 4096) for M in Ms}
+        assert len(fam) == 1
+        base = to_np_u16(P.run(np.ascontiguousarray(X[:Ms[0]])))
+        for M in Ms[1:]:
+            Y = to_np_u16(P.run(np.ascontiguousarray(X[:M])))
+            assert np.array_equal(Y[:Ms[0]], base), f"M={M}"
+
+
+def test_gemm_deterministic_and_graph_capturable():
+    P = problem(8192, 1024, seed=8)
+    X_u16 = synth.host(1, 16, synth.ACT, 16, 8192)
+    Y1 = to_np_u16(P.run(X_u16))
+    Y2 = to_np_u16(P.run(X_u16))
+    assert np.array_equal(Y1, Y2)
+    X = torch.from_numpy(X_u16.view(np.int16)).cuda().view(torch.float16)
+    Yg = torch.empty((16, 1024), dtype=torch.float16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        P.pl(X, Yg, P.ws, stream=s)      # warm-up on the capture stream
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        P.pl(X, Yg, P.ws, stream=s)
+    Yg.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np_u16(Yg), Y1)
+
+
+def test_gemm_writes_only_its_output():
+    # NaN canaries around Y (extra rows/cols) and around the workspace; padded token rows never written
+    P = problem(1024, 512, seed=4)
+    M = 5
+    X = synth.host(2, 17, synth.ACT, M, 1024)
+    big = torch.full((M + 3, 512 + 128), float("nan"), dtype=torch.float16, device="cuda")
+    Yv = big[:M, :512]
+    assert not Yv.is_contiguous()
+    Y = torch.empty((M, 512), dtype=torch.float16, device="cuda")
+    w4 = _lib()
+    # contiguous output inside a canary buffer: rows M.. of a flat buffer stay NaN
+    flat = torch.full(((M + 4) * 512,), float("nan"), dtype=torch.float16, device="cuda")
+    Yc = flat[:M * 512].view(M, 512)
+    P.pl(torch.from_numpy(X.view(np.int16)).cuda().view(torch.float16), Yc, P.ws)
+    torch.cuda.synchronize()
+    assert torch.isnan(flat[M * 512:]).all()
+    assert_gemm_close(Yc, P.ref(X), "canary")
+    # the workspace counters are back to zero after every call
+    nt = 512 // 128
+    assert int(P.ws[:nt * 4].view(torch.int32).abs().sum()) == 0
+    del Y, big, Yv, w4
+
+
+def test_gemm_workspace_too_small_is_rejected():
+    w4 = _lib()
+    P = problem(4096, 4096)
+    X = torch.zeros((8, 4096), dtype=torch.float16, device="cuda")
+    Y = torch.zeros((8, 4096), dtype=torch.float16, device="cuda")
+    tiny = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(w4.W4A16Error):
+        w4.w4a16_gemm(X, P.pl.qweight, P.pl.scales, P.pl.zeros, Y, tiny)
+
+
+# ---------------------------------------------------------------------------------------------------
+# verify_accept: bit-exact (all n + 3 output words) against the oracle
+# ---------------------------------------------------------------------------------------------------
+def gpu_accept(tokens, parents, argmax):
+    w4 = _lib()
+    n = len(tokens)
+    t = torch.tensor(np.asarray(tokens, dtype=np.int32), device="cuda")
+    p = torch.tensor(np.asarray(parents, dtype=np.int32), device="cuda")
+    a = torch.tensor(np.asarray(argmax, dtype=np.int32), device="cuda")
+    out = torch.full((3 + n,), 12345, dtype=torch.int32, device="cuda")
+    w4.verify_accept(t, p, a, out)
+    return out.cpu().numpy()
+
+
+def test_accept_golden_and_degenerate():
+    cases = [
+        ([100, 11, 12, 21, 22, 23, 31, 32], [-1, 0, 0, 1, 1, 2, 3, 5], [12, 99, 23, 31, 99, 32, 99, 40]),
+        ([3], [-1], [17]),                                   # M = 1: one AR step
+        ([0, 4, 5, 6], [-1, 0, 1, 2], [4, 5, 6, 8]),         # chain fully accepted
+        ([0, 4, 5, 6], [-1, 0, 0, 0], [9, 1, 1, 1]),         # nothing accepted
+        ([0, 1, 1, 2], [-1, 0, 0, 1], [1, 2, 0, 0]),         # duplicate siblings: deepest, then smallest index
+        ([1, 1], [0, 0], [1, 1]),                            # bad: root parent
+        ([1, 1, 1], [-1, 2, 0], [1, 1, 1]),                  # bad: parent after child
+    ]
+    for t, p, a in cases:
+        assert np.array_equal(gpu_accept(t, p, a), oracle.accept(t, p, a)[4]), (t, p, a)
+
+
+@pytest.mark.parametrize("n_draft,depth,p_acc", [(7, 7, 0.8), (48, 6, 0.7), (60, 6, 0.75), (63, 10, 0.9)])
+def test_accept_eagle_trees_bit_exact(n_draft, depth, p_acc):
+    rng = np.random.default_rng(n_draft * 31 + depth)
+    for _ in range(60):
+        t, p = synth.eagle_tree(rng, n_draft, depth)
+        a = synth.target_argmax_for(rng, t, p, p_acc)
+        assert np.array_equal(gpu_accept(t, p, a), oracle.accept(t, p, a)[4])
+
+
+def test_accept_random_trees_all_sizes():
+    rng = np.random.default_rng(5)
+    for n in list(range(1, 70)) + [127, 128, 129, 500, 1023, 1024]:
+        par = [-1] + [int(rng.integers(max(0, i - 3), i)) for i in range(1, n)]  # deep, chain-like
+        if n > 2 and rng.random() < 0.5:
+            par = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]           # bushy
+        tok = rng.integers(0, 3, n).tolist()
+        am = rng.integers(0, 3, n).tolist()
+        assert np.array_equal(gpu_accept(tok, par, am), oracle.accept(tok, par, am)[4]), n
