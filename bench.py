@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the W4A16 verify hot path (BASELINE.json metric: "W4A16 verify-GEMM µs and achieved HBM
+TB/s vs draft width M=1-64").
+
+Step = one verify forward of the Llama-3-70B W4A16 linear stack (80 decoder layers: QKV, O, gate-up,
+SiLU*mul, down; attention/norms out of scope) at draft width M, then greedy acceptance of an M-node draft
+tree (BASELINE.json configs 3-5; config 4 at N GPUs = tensor-parallel over N ranks with NCCL all-reduce).
+value = algorithmic weight bytes streamed by all ranks per step / max-over-ranks step time, in TB/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--M 16] [--layers 80] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Inputs are seeded synthetic (synth/), resident in HBM before timing; per-step weights (36.4 GB at N=1)
+exceed the 126 MB L2, so no flush is needed between steps. Timing: CUDA graph replays bracketed by CUDA
+events on the launching stream, barrier + synchronize on both sides, max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W4A16 verify-GEMM µs and achieved HBM TB/s vs draft width M=1–64"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+TAU = {  # paper accepted lengths for config 5 (PAPER.md lines)
+    "eagle2_d6_n48": (49, 3.81, "P:757"),
+    "eagle2_n60_tree": (61, 3.81, "P:757 (tau of the d=6 tree; BASELINE config 5 tree of 60)"),
+    "vanilla_sp_d6": (7, 4.72, "P:714"),
+    "vanilla_sp_d7": (8, 5.09, "P:722"),
+    "hierspec_6_3": (7, 5.28, "P:768"),
+    "hierspec_7_3": (8, 5.46, "P:784"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--M", type=int, default=16, help="headline draft width (verify rows)")
+    ap.add_argument("--layers", type=int, default=None, help="decoder layers (default: the model's)")
+    ap.add_argument("--model", default="70b", choices=["70b", "8b"])
+    ap.add_argument("--mode", default="asym", choices=["asym", "sym"])
+    ap.add_argument("--sweep", default="1,2,4,7,8,16,24,32,49,61,64", help="comma list of M for the M sweep ('' = none)")
+    ap.add_argument("--sweep-steps", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--kernels", action="store_true", default=True, help="per-kernel breakdown (default on)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# --------------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands, on a bounded sample of the workload
+# --------------------------------------------------------------------------------------------------
+_SAMPLE = {}
+
+
+def oracle_sample(M, seed, repeats=1):
+    """Time oracle.gemm (+ oracle.accept) on a slice of one 70B layer: the O projection restricted to
+    1024 output columns (K=8192, N=1024) at width M. Returns (TB/s of weight bytes, seconds, sample text)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    K, N = 8192, 1024
+    key = (M, seed)
+    if key not in _SAMPLE:  # inputs are built once (untimed), like the GPU arm's resident inputs
+        W = synth.host(seed, 9001, synth.WEIGHT, K, N)
+        X = synth.host(seed, 9002, synth.ACT, M, K)
+        qw, sc, ze, _ = oracle.pack(W)
+        rng = np.random.default_rng(seed)
+        tok, par = synth.eagle_tree(rng, max(M - 1, 0), 6)
+        am = synth.target_argmax_for(rng, tok, par, 0.7)
+        _SAMPLE[key] = (X, qw, sc, ze, tok, par, am)
+    X, qw, sc, ze, tok, par, am = _SAMPLE[key]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        oracle.gemm(X, qw, sc, ze, K, N, nthreads=threads)
+        oracle.accept(tok, par, am)
+    dt = (time.perf_counter() - t0) / repeats
+    wbytes = K * N // 2 + (K // 128) * N * 4
+    sample = (f"oracle.gemm fp64 on a 70B O-projection slice K=8192 N=1024 ({wbytes / 1e6:.2f} MB of W4 weights) "
+              f"at M={M} + oracle.accept on a {M}-node tree, {threads} threads")
+    return wbytes / dt / 1e12, dt, sample, threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    M = args.M
+    for _ in range(args.warmup):
+        oracle_sample(M, args.seed)
+    times, v = [], None
+    for _ in range(args.steps):
+        v, dt, sample, threads = oracle_sample(M, args.seed)
+        times.append(dt)
+    tot = sum(times)
+    K, N = 8192, 1024
+    wbytes = K * N // 2 + (K // 128) * N * 4
+    value = wbytes * len(times) / tot / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"oracle sample of the llama3-70b W4A16 verify forward at M={M}", "M": M},
+        "cpu_baseline": {"value": value, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_22179_b200 as w4
+    import synth
+    from paper_2505_22179_b200 import tp
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    dims = tp.LLAMA3_70B if args.model == "70b" else tp.LLAMA3_8B
+    n_layers = args.layers or dims.layers
+    mode = w4.W4A16_SYM if args.mode == "sym" else w4.W4A16_ASYM
+    sweep = [int(x) for x in args.sweep.split(",") if x.strip()]
+    M_max = max([args.M] + sweep)
+    mat_id = {n: i for i, n in enumerate(tp.MATRICES)}
+
+    def make_weight(l, name, K, N, out):
+        synth.gpu(args.seed, synth.tensor_id(l, mat_id[name], rank), synth.WEIGHT, K, N, out=out)
+
+    t0 = time.perf_counter()
+    stack = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
+                           device=dev)
+    build_s = time.perf_counter() - t0
+    # activations (seeded, in HBM) and a draft tree of the headline width
+    for name, buf, tid in (("x_qkv", stack.x_qkv, 1), ("x_o", stack.x_o, 2), ("x_mlp", stack.x_mlp, 3)):
+        synth.gpu(args.seed, synth.tensor_id(0xFFF, tid, rank), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+    rng = np.random.default_rng(args.seed)
+    tok, par = synth.eagle_tree(rng, M_max - 1, 6)
+    am = synth.target_argmax_for(rng, tok, par, 0.7)
+    stack.set_tree(tok, par, am)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.Stream(dev)
+
+    def time_graph(g, steps, warmup):
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                g.replay()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                g.replay()
+            e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / steps  # ms per step
+
+    clocks = ClockSampler(local) if rank == 0 else None
+    bytes_all_ranks = stack.weight_bytes * world  # shards partition the model: == full model bytes
+    gH = stack.capture(args.M)
+    ms = time_graph(gH, args.steps, args.warmup)
+    value = bytes_all_ranks / (ms * 1e-3) / 1e12
+
+    # M sweep (same protocol)
+    m_sweep = {}
+    for M in sweep:
+        g = stack.capture(M)
+        msM = time_graph(g, args.sweep_steps, 3)
+        m_sweep[str(M)] = {"ms_per_forward": msM, "us_per_layer": 1e3 * msM / n_layers,
+                           "TBps": bytes_all_ranks / (msM * 1e-3) / 1e12}
+    peak_gbs, peak_src = hbm_peak()
+    for v in m_sweep.values():
+        v["frac_hbm"] = v["TBps"] * 1e3 / (peak_gbs * world)
+    if "1" in m_sweep and "64" in m_sweep:
+        ratio_64 = m_sweep["64"]["ms_per_forward"] / m_sweep["1"]["ms_per_forward"]
+    else:
+        ratio_64 = None
+    hier = {}
+    for k, (M, tau, cite) in TAU.items():
+        if str(M) in m_sweep:
+            hier[k] = {"M": M, "tau": tau, "cite": cite, "us_per_token": 1e3 * m_sweep[str(M)]["ms_per_forward"] / tau}
+
+    # e2e through the public API: pinned host inputs -> device -> forward -> accept result + hidden -> host
+    M = args.M
+    pin = dict(pin_memory=True)
+    host_in = {"x_qkv": stack.x_qkv.cpu().pin_memory(), "x_o": stack.x_o.cpu().pin_memory(),
+               "x_mlp": stack.x_mlp.cpu().pin_memory(), "tokens": stack.tokens.cpu().pin_memory(),
+               "parents": stack.parents.cpu().pin_memory(), "argmax": stack.argmax.cpu().pin_memory()}
+    host_out = {"accept": torch.empty(3 + M_max, dtype=torch.int32, **pin),
+                "y": torch.empty(M_max, stack.y_down.shape[1], dtype=torch.float16, **pin)}
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            stack.verify_host(M, host_in, host_out, gH)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            stack.verify_host(M, host_in, host_out, gH)
+        e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    acc = host_out["accept"][:3].tolist()
+
+    # per-kernel breakdown: each GEMM kind back-to-back over all layers (distinct weights), one graph each
+    kernels = {}
+    roofline = None
+    if args.kernels:
+        P = stack.plan
+        for name in tp.MATRICES:
+            s = P[name]
+            xin = {"qkv": stack.x_qkv, "o": stack.x_o, "gate_up": stack.x_mlp, "down": stack.act}[name][:M]
+            yout = {"qkv": stack.y_qkv, "o": stack.y_o, "gate_up": stack.y_gu, "down": stack.y_down}[name][:M]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                for L in stack.layers:
+                    L[name](xin, yout, stack.ws, stream)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                for L in stack.layers:
+                    L[name](xin, yout, stack.ws, stream)
+            msk = time_graph(g, max(3, args.steps // 2), 2) / n_layers
+            wb = stack.layers[0][name].weight_bytes
+            kernels[name] = {"K": s["K"], "N": s["N"], "us": 1e3 * msk, "weight_MB": wb / 1e6,
+                             "GBps": wb / (msk * 1e-3) / 1e9, "frac_hbm": wb / (msk * 1e-3) / 1e9 / peak_gbs}
+        gate = kernels["gate_up"]
+        roofline = {"bound": "hbm", "kernel": f"w4a16 GEMM gate-up (K={gate['K']}, N={gate['N']}, M={M})",
+                    "achieved": gate["GBps"], "peak": peak_gbs, "unit": "GB/s", "frac": gate["GBps"] / peak_gbs,
+                    "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": stack.layers[0]["gate_up"].weight_bytes + 2 * M * (gate["K"] + gate["N"]),
+                    "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA graph, "
+                            "CUDA events on the launching stream)"}
+        ncu_path = os.path.join(ROOT, "profiles", "r01_ncu_gate_up.json")
+        if os.path.exists(ncu_path):
+            try:
+                with open(ncu_path) as f:
+                    roofline["traffic"] = json.load(f).get("dram_bytes_per_launch")
+            except Exception:
+                pass
+    clk = clocks.stop() if clocks else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, sample, threads = oracle_sample(M, args.seed)
+        reps = max(1, min(500, int(10.0 / max(dt, 1e-3))))
+        v, dt, sample, threads = oracle_sample(M, args.seed, repeats=reps)
+        cpu = {"value": v, "unit": "TB/s", "cores": threads, "kind": "oracle",
+               "sample": sample + f", mean of {reps} runs ({dt:.2f} s each)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (seeded counter-based generator: N(0,0.018^2) weights with 2% x8 outlier groups, "
+                    "N(0,1.15^2) activations with 4 x16 outlier channels; EAGLE-2-shaped draft tree)",
+            "config": {"workload": f"{dims.name} W4A16 g128 {args.mode} verify forward: {n_layers} decoder layers "
+                                   f"(QKV, O, gate-up, SiLU*mul, down) + verify_accept; BASELINE configs 3-4",
+                       "M": args.M, "layers": n_layers, "tp": world, "parallelism": f"tp{world}",
+                       "weight_bytes_per_step": bytes_all_ranks,
+                       "l2": f"{bytes_all_ranks / 1e9:.1f} GB of weights per step >> 126 MB L2 (no flush needed)",
+                       "timing": "CUDA graph replay, CUDA events on the launching stream, max over ranks"},
+            "us_per_layer": 1e3 * ms / n_layers,
+            "frac_hbm": value * 1e3 / (peak_gbs * world),
+            "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
+            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
+                    "api": "VerifyStack.verify_host (pinned host buffers, graph replay, accept result read back)",
+                    "accept_result": acc},
+            "gpu_launches": stack.launches_per_forward() * args.steps,
+            "clocks": clk, "build_s": build_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -51,6 +51,7 @@ typedef enum {
 
 enum { W4A16_ASYM = 0, W4A16_SYM = 1 };
 enum { W4A16_DEV_OK = 0, W4A16_DEV_NONFINITE = 1, W4A16_DEV_BAD_TREE = 2 };
+enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 = 1 };
 #define W4A16_GROUP 128
 #define W4A16_MAX_M 64
 #define W4A16_MAX_TREE 1024
@@ -85,11 +86,18 @@ int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t
  * equals the oracle's fp64 result within |Y - Y_ref| <= 1e-2 * (1 + |Y_ref|), not bit-for-bit.
  * The split-K / stream-K plan depends only on (K, N, SM count), never on M, and the cross-CTA reduction
  * runs in a fixed order: results are deterministic and row m of Y does not depend on the other rows of X
- * within one kernel family (family = mma.sync for M <= 16, tcgen05 for M > 16).
- * Rows of Y beyond M and bytes outside Y are never written. */
+ * within one kernel family (w4a16_gemm_family). Rows of Y beyond M and bytes outside Y are
+ * never written. */
 int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
                uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace, size_t workspace_bytes,
                w4a16_stream_t stream);
+
+/* w4a16_gemm_ex — w4a16_gemm with an explicit kernel family: W4A16_FAMILY_AUTO (= w4a16_gemm),
+ * W4A16_FAMILY_MMA_SYNC (legacy mma.sync tensor path) or W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, TMEM).
+ * Both families compute the same definition; used by tests and benchmarks to compare them. */
+int w4a16_gemm_ex(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
+                  uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace, size_t workspace_bytes,
+                  int family, w4a16_stream_t stream);
 
 /* verify_accept — greedy acceptance of a draft tree against the target's argmax (rule per
  * S:289/S:298, reading R9).  n nodes, node 0 = root (the last committed token, row 0 of the verify
@@ -111,7 +119,7 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 
-/* Number of the last kernel family used by w4a16_gemm for M (0 = mma.sync, 1 = tcgen05); for reporting. */
+/* Kernel family w4a16_gemm uses for this shape (W4A16_FAMILY_MMA_SYNC or W4A16_FAMILY_TCGEN05). */
 int w4a16_gemm_family(int M, int K, int N);
 
 #ifdef __cplusplus

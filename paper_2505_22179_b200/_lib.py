@@ -18,6 +18,7 @@ W4A16_DEV_BAD_TREE = 2
 W4A16_GROUP = 128
 W4A16_MAX_M = 64
 W4A16_MAX_TREE = 1024
+W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05 = -1, 0, 1
 
 # Every symbol include/w4a16.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
@@ -26,6 +27,7 @@ ABI_SYMBOLS = (
     "w4a16_gemm_workspace_bytes",
     "w4a16_workspace_init",
     "w4a16_gemm",
+    "w4a16_gemm_ex",
     "verify_accept",
     "w4a16_status_string",
     "w4a16_gemm_family",
@@ -50,12 +52,13 @@ def _load():
     lib.w4a16_gemm_workspace_bytes.restype = sz
     lib.w4a16_workspace_init.argtypes = [vp, sz, vp]
     lib.w4a16_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, vp]
+    lib.w4a16_gemm_ex.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, i32, vp]
     lib.verify_accept.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.w4a16_status_string.argtypes = [i32]
     lib.w4a16_status_string.restype = ctypes.c_char_p
     lib.w4a16_gemm_family.argtypes = [i32, i32, i32]
     lib.w4a16_silu_mul.argtypes = [vp, i32, i32, vp, vp]
-    for name in ("w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "verify_accept",
+    for name in ("w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
                  "w4a16_gemm_family", "w4a16_silu_mul"):
         getattr(lib, name).restype = i32
     return lib

@@ -10,6 +10,9 @@ extern "C" int w4a16_launch_unpack(const uint32_t*, const uint16_t*, const uint1
 extern "C" int w4a16_launch_accept(const int32_t*, const int32_t*, const int32_t*, int, int32_t*, cudaStream_t);
 extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaStream_t);
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
+extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
+extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const uint32_t*, const uint16_t*, const uint16_t*, uint16_t*, int,
+                                    int, int, int, void*, int, cudaStream_t);
 extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const uint32_t*, const uint16_t*, const uint16_t*, uint16_t*, int,
                                      int, int, int, void*, int, cudaStream_t);
 
@@ -58,7 +61,8 @@ extern "C" size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group) {
   if (check_kn(K, N, group) != W4A16_OK || M < 1 || M > W4A16_MAX_M) return 0;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return 0;
-  return w4a16_mma_workspace_bytes(M, K, N, sms);
+  const size_t a = w4a16_mma_workspace_bytes(M, K, N, sms), b = w4a16_tc_workspace_bytes(M, K, N, sms);
+  return a > b ? a : b;
 }
 
 extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
@@ -68,12 +72,12 @@ extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a
 
 extern "C" int w4a16_gemm_family(int M, int K, int N) {
   (void)M; (void)K; (void)N;
-  return 0;
+  return W4A16_FAMILY_TCGEN05;
 }
 
-extern "C" int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
-                          uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace,
-                          size_t workspace_bytes, w4a16_stream_t stream) {
+extern "C" int w4a16_gemm_ex(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales,
+                             const uint16_t* zeros, uint16_t* Y, int M, int K, int N, int group, int mode,
+                             void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream) {
   if (!X || !qweight || !scales || !Y || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
     return W4A16_ERR_ARG;
   if (int e = check_kn(K, N, group)) return e;
@@ -83,8 +87,23 @@ extern "C" int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint
     return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
-  if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-  return w4a16_launch_gemm_mma(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+  if (family == W4A16_FAMILY_AUTO) family = w4a16_gemm_family(M, K, N);
+  if (family == W4A16_FAMILY_MMA_SYNC) {
+    if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+    return w4a16_launch_gemm_mma(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+  }
+  if (family == W4A16_FAMILY_TCGEN05) {
+    if (!workspace || workspace_bytes < w4a16_tc_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+    return w4a16_launch_gemm_tc(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+  }
+  return W4A16_ERR_ARG;
+}
+
+extern "C" int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
+                          uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace,
+                          size_t workspace_bytes, w4a16_stream_t stream) {
+  return w4a16_gemm_ex(X, qweight, scales, zeros, Y, M, K, N, group, mode, workspace, workspace_bytes,
+                       W4A16_FAMILY_AUTO, stream);
 }
 
 extern "C" int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n,

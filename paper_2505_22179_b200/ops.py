@@ -12,6 +12,7 @@ from ._lib import (  # noqa: F401
     lib, check, status_string, W4A16Error,
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
+    W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05,
 )
 
 
@@ -71,15 +72,20 @@ def alloc_workspace(M_max: int, shapes, device=None) -> torch.Tensor:
     return torch.zeros(max(need, 256), dtype=torch.uint8, device=device or "cuda")
 
 
-def w4a16_gemm(X, qweight, scales, zeros, Y, workspace, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None):
+def w4a16_gemm(X, qweight, scales, zeros, Y, workspace, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None,
+               family=W4A16_FAMILY_AUTO):
+    """Y = X . W_hat through w4a16_gemm (family AUTO) or w4a16_gemm_ex (explicit family)."""
     M, K = X.shape
     N = Y.shape[1]
     if Y.shape[0] != M:
         raise W4A16Error("Y must be [M, N]")
-    st = lib.w4a16_gemm(_ptr(X, torch.float16, "X"), _ptr(qweight, torch.int32, "qweight"),
-                        _ptr(scales, torch.float16, "scales"), _ptr(zeros, torch.float16, "zeros"),
-                        _ptr(Y, torch.float16, "Y"), M, K, N, group, mode, _ptr(workspace, None, "workspace"),
-                        workspace.numel() * workspace.element_size(), _stream(stream))
+    args = (_ptr(X, torch.float16, "X"), _ptr(qweight, torch.int32, "qweight"), _ptr(scales, torch.float16, "scales"),
+            _ptr(zeros, torch.float16, "zeros"), _ptr(Y, torch.float16, "Y"), M, K, N, group, mode,
+            _ptr(workspace, None, "workspace"), workspace.numel() * workspace.element_size())
+    if family == W4A16_FAMILY_AUTO:
+        st = lib.w4a16_gemm(*args, _stream(stream))
+    else:
+        st = lib.w4a16_gemm_ex(*args, family, _stream(stream))
     check(st, "w4a16_gemm")
 
 
@@ -121,8 +127,8 @@ class PackedLinear:
         b = self.qweight.numel() * 4 + self.scales.numel() * 2
         return b + (self.zeros.numel() * 2 if self.zeros is not None else 0)
 
-    def __call__(self, X, Y, workspace, stream=None):
-        w4a16_gemm(X, self.qweight, self.scales, self.zeros, Y, workspace, self.mode, stream=stream)
+    def __call__(self, X, Y, workspace, stream=None, family=W4A16_FAMILY_AUTO):
+        w4a16_gemm(X, self.qweight, self.scales, self.zeros, Y, workspace, self.mode, stream=stream, family=family)
         return Y
 
 

@@ -1,0 +1,206 @@
+"""Tensor-parallel W4A16 verify stack (BASELINE.json configs 4-5).
+
+One process per GPU. Megatron-style partition of each Llama decoder layer's linear layers:
+  * column-parallel (split N, no communication): QKV (head-aligned: rank r owns q heads
+    [r*nq/t, (r+1)*nq/t) and kv heads [r*nkv/t, ...)), gate-up (rank r owns the matching gate AND up
+    columns, stored locally as [gate_r | up_r] so w4a16_silu_mul pairs them);
+  * row-parallel (split K): O (rank's heads) and down (rank's FFN slice); each rank produces a partial
+    Y[M, hidden] that an all-reduce (NCCL over NVLink/NVSwitch, via torch.distributed) sums.
+Attention, norms and residual adds are outside the hot path: each layer's QKV, O and
+gate-up inputs are caller-provided activation buffers of their real shapes; gate-up -> SiLU*mul -> down is
+chained as in the model. Every compute step is a libw4a16.so kernel; torch supplies memory, streams,
+CUDA graphs and the process group.
+"""
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import torch
+import torch.distributed as dist
+
+from .ops import (W4A16_ASYM, PackedLinear, alloc_workspace, pack_linear, verify_accept, w4a16_silu_mul)
+
+
+@dataclass(frozen=True)
+class ModelDims:
+    name: str
+    hidden: int
+    ffn: int
+    n_q: int
+    n_kv: int
+    head: int
+    layers: int
+
+    @property
+    def qkv_out(self):
+        return (self.n_q + 2 * self.n_kv) * self.head
+
+
+LLAMA3_8B = ModelDims("llama3-8b", 4096, 14336, 32, 8, 128, 32)
+LLAMA3_70B = ModelDims("llama3-70b", 8192, 28672, 64, 8, 128, 80)
+MATRICES = ("qkv", "o", "gate_up", "down")
+
+
+def _split(total: int, t: int, r: int, align: int = 128):
+    if total % t or (total // t) % align:
+        raise ValueError(f"{total} does not split into {t} shards aligned to {align}")
+    s = total // t
+    return r * s, (r + 1) * s
+
+
+def shard_plan(d: ModelDims, t: int, r: int) -> dict:
+    """Per-rank GEMM shapes (K, N) and the column/row ranges of the full matrices they cover.
+
+    'cols' lists (start, stop) column ranges of the full [K, N] weight, concatenated in order;
+    'rows' is the (start, stop) row (K) range. All ranges are multiples of 128."""
+    if d.n_kv % t or d.n_q % t:
+        raise ValueError(f"tp={t} must divide the head counts")
+    hq, hk = d.n_q // t, d.n_kv // t
+    q = (r * hq * d.head, (r + 1) * hq * d.head)
+    k0 = d.n_q * d.head
+    kk = (k0 + r * hk * d.head, k0 + (r + 1) * hk * d.head)
+    v0 = k0 + d.n_kv * d.head
+    vv = (v0 + r * hk * d.head, v0 + (r + 1) * hk * d.head)
+    g = _split(d.ffn, t, r)
+    u = (d.ffn + g[0], d.ffn + g[1])
+    o_rows = _split(d.n_q * d.head, t, r)
+    return {
+        "qkv": {"K": d.hidden, "N": (hq + 2 * hk) * d.head, "rows": (0, d.hidden), "cols": [q, kk, vv],
+                "full": (d.hidden, d.qkv_out)},
+        "o": {"K": d.n_q * d.head // t, "N": d.hidden, "rows": o_rows, "cols": [(0, d.hidden)],
+              "full": (d.n_q * d.head, d.hidden)},
+        "gate_up": {"K": d.hidden, "N": 2 * d.ffn // t, "rows": (0, d.hidden), "cols": [g, u],
+                    "full": (d.hidden, 2 * d.ffn)},
+        "down": {"K": d.ffn // t, "N": d.hidden, "rows": g, "cols": [(0, d.hidden)], "full": (d.ffn, d.hidden)},
+    }
+
+
+def shard_of(W_full: torch.Tensor, spec: dict) -> torch.Tensor:
+    """The rank-local [K_r, N_r] weight of a full [K, N] weight under shard_plan (any device)."""
+    r0, r1 = spec["rows"]
+    return torch.cat([W_full[r0:r1, c0:c1] for c0, c1 in spec["cols"]], dim=1).contiguous()
+
+
+def weight_bytes(d: ModelDims, t: int, n_layers: Optional[int] = None, sym: bool = False) -> int:
+    """Algorithmic weight bytes streamed by ONE rank per verify forward (codes + scales (+ zeros))."""
+    plan = shard_plan(d, t, 0)
+    per = sum(s["K"] * s["N"] // 2 + (s["K"] // 128) * s["N"] * (2 if sym else 4) for s in plan.values())
+    return per * (n_layers if n_layers is not None else d.layers)
+
+
+class VerifyStack:
+    """The rank-local shard of an n_layers-deep W4A16 verify stack, resident in HBM.
+
+    make_weight(layer, name, K, N, out) fills `out` (fp16 [K, N] CUDA tensor) with the rank-local weight;
+    it is packed with w4a16_pack and dropped, so only the int4 shards stay resident."""
+
+    def __init__(self, dims: ModelDims, n_layers: int, M_max: int, make_weight: Callable, tp_size: int = 1,
+                 tp_rank: int = 0, group=None, mode: int = W4A16_ASYM, device=None):
+        self.d, self.n_layers, self.M_max = dims, n_layers, M_max
+        self.t, self.r, self.group, self.mode = tp_size, tp_rank, group, mode
+        self.device = torch.device(device or "cuda")
+        self.plan = shard_plan(dims, tp_size, tp_rank)
+        biggest = max(s["K"] * s["N"] for s in self.plan.values())
+        tmp = torch.empty(biggest, dtype=torch.float16, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.layers: List[dict] = []
+        for l in range(n_layers):
+            mats = {}
+            for name in MATRICES:
+                s = self.plan[name]
+                W = tmp[: s["K"] * s["N"]].view(s["K"], s["N"])
+                make_weight(l, name, s["K"], s["N"], W)
+                mats[name] = pack_linear(W, mode=mode, dev_status=self.status)
+            self.layers.append(mats)
+        del tmp
+        torch.cuda.synchronize(self.device)
+        f16 = dict(dtype=torch.float16, device=self.device)
+        P = self.plan
+        # activation inputs (caller fills) and per-layer scratch outputs
+        self.x_qkv = torch.zeros(M_max, P["qkv"]["K"], **f16)
+        self.x_o = torch.zeros(M_max, P["o"]["K"], **f16)
+        self.x_mlp = torch.zeros(M_max, P["gate_up"]["K"], **f16)
+        self.y_qkv = torch.empty(M_max, P["qkv"]["N"], **f16)
+        self.y_o = torch.empty(M_max, P["o"]["N"], **f16)
+        self.y_gu = torch.empty(M_max, P["gate_up"]["N"], **f16)
+        self.act = torch.empty(M_max, P["down"]["K"], **f16)
+        self.y_down = torch.empty(M_max, P["down"]["N"], **f16)
+        i32 = dict(dtype=torch.int32, device=self.device)
+        self.tokens = torch.zeros(M_max, **i32)
+        self.parents = torch.full((M_max,), -1, **i32)
+        self.parents[1:] = torch.arange(M_max - 1, device=self.device, dtype=torch.int32)
+        self.argmax = torch.zeros(M_max, **i32)
+        self.accept_out = torch.zeros(3 + M_max, **i32)
+        self.ws = alloc_workspace(M_max, [(s["K"], s["N"]) for s in P.values()], device=self.device)
+        self.graphs = {}
+
+    @property
+    def weight_bytes(self) -> int:
+        return sum(pl.weight_bytes for L in self.layers for pl in L.values())
+
+    def _allreduce(self, y: torch.Tensor):
+        if self.t > 1:
+            dist.all_reduce(y, group=self.group)
+
+    def forward(self, M: int, stream=None):
+        """One verify forward at width M (M = draft nodes + root), then greedy acceptance. Async."""
+        if not 1 <= M <= self.M_max:
+            raise ValueError(f"M={M} outside [1, {self.M_max}]")
+        ws = self.ws
+        for L in self.layers:
+            L["qkv"](self.x_qkv[:M], self.y_qkv[:M], ws, stream)
+            L["o"](self.x_o[:M], self.y_o[:M], ws, stream)
+            self._allreduce(self.y_o[:M])
+            L["gate_up"](self.x_mlp[:M], self.y_gu[:M], ws, stream)
+            w4a16_silu_mul(self.y_gu[:M], self.act[:M], stream)
+            L["down"](self.act[:M], self.y_down[:M], ws, stream)
+            self._allreduce(self.y_down[:M])
+        verify_accept(self.tokens[:M], self.parents[:M], self.argmax[:M], self.accept_out[:3 + M], stream)
+
+    def launches_per_forward(self) -> int:
+        """libw4a16 kernel launches per forward (4 GEMMs + SiLU*mul per layer, one acceptance)."""
+        return 5 * self.n_layers + 1
+
+    def capture(self, M: int) -> torch.cuda.CUDAGraph:
+        """Capture forward(M) as a CUDA graph (after one eager warm-up on the capture stream)."""
+        if M in self.graphs:
+            return self.graphs[M]
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward(M)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward(M)
+        torch.cuda.synchronize(self.device)
+        self.graphs[M] = g
+        return g
+
+    def set_tree(self, tokens, parents, argmax):
+        n = len(tokens)
+        self.tokens[:n].copy_(torch.as_tensor(tokens, dtype=torch.int32))
+        self.parents[:n].copy_(torch.as_tensor(parents, dtype=torch.int32))
+        self.argmax[:n].copy_(torch.as_tensor(argmax, dtype=torch.int32))
+
+    def verify_host(self, M: int, host_in: dict, host_out: dict, graph: Optional[torch.cuda.CUDAGraph] = None):
+        """End-to-end step through the public API: pinned host inputs -> device, forward (graph replay if
+        given), accepted length / path / last hidden state -> pinned host. Async on the current stream."""
+        self.x_qkv[:M].copy_(host_in["x_qkv"][:M], non_blocking=True)
+        self.x_o[:M].copy_(host_in["x_o"][:M], non_blocking=True)
+        self.x_mlp[:M].copy_(host_in["x_mlp"][:M], non_blocking=True)
+        self.tokens[:M].copy_(host_in["tokens"][:M], non_blocking=True)
+        self.parents[:M].copy_(host_in["parents"][:M], non_blocking=True)
+        self.argmax[:M].copy_(host_in["argmax"][:M], non_blocking=True)
+        if graph is not None:
+            graph.replay()
+        else:
+            self.forward(M)
+        host_out["accept"][:3 + M].copy_(self.accept_out[:3 + M], non_blocking=True)
+        host_out["y"][:M].copy_(self.y_down[:M], non_blocking=True)
+
+    def h2d_bytes(self, M: int) -> int:
+        return 2 * M * (self.x_qkv.shape[1] + self.x_o.shape[1] + self.x_mlp.shape[1]) + 3 * 4 * M
+
+    def d2h_bytes(self, M: int) -> int:
+        return 4 * (3 + M) + 2 * M * self.y_down.shape[1]

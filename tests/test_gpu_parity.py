@@ -131,13 +131,12 @@ class Problem:
         w4 = _lib()
         self.ws = w4.alloc_workspace(64, [(K, N)])
 
-    def run(self, X_u16, Y=None):
-        w4 = _lib()
+    def run(self, X_u16, Y=None, family=-1):
         M = X_u16.shape[0]
         X = torch.from_numpy(X_u16.view(np.int16)).cuda().view(torch.float16)
         if Y is None:
             Y = torch.empty((M, self.N), dtype=torch.float16, device="cuda")
-        self.pl(X, Y, self.ws)
+        self.pl(X, Y, self.ws, family=family)
         torch.cuda.synchronize()
         return Y
 
@@ -155,32 +154,39 @@ def problem(K, N, mode=0, seed=0):
     return _P[key]
 
 
+FAMILIES = [0, 1]  # W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05
+
+
+@pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [1, 2, 3, 5, 7, 8, 9, 13, 16, 17, 24, 31, 32, 48, 61, 64])
-def test_gemm_config1_tolerance(M):
-    # config 1: K = N = 4096, g128 ASYM; M sweeps both kernel families and ragged token blocks
+def test_gemm_config1_tolerance(M, family):
+    # config 1: K = N = 4096, g128 ASYM; M sweeps ragged token blocks / MMA-N padding of both families
     P = problem(4096, 4096)
     X = synth.host(100 + M, 12, synth.ACT, M, 4096)
-    assert_gemm_close(P.run(X), P.ref(X), f"M={M}")
+    assert_gemm_close(P.run(X, family=family), P.ref(X), f"M={M} family={family}")
 
 
+@pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("K,N,M", [(128, 128, 4), (128, 1280, 8), (3584, 1024, 16), (1024, 8192, 7),
                                    (28672, 256, 3), (8192, 384, 64), (256, 57344 // 8, 12)])
-def test_gemm_shapes_tolerance(K, N, M):
+def test_gemm_shapes_tolerance(K, N, M, family):
     # single tile, TP8 shard shapes (QKV N=1280, O K=1024, down K=3584), tall-K/narrow-N stream-K splits
     P = problem(K, N, seed=K ^ N)
     X = synth.host(7 + M, 13, synth.ACT, M, K)
-    assert_gemm_close(P.run(X), P.ref(X), f"K={K} N={N} M={M}")
+    assert_gemm_close(P.run(X, family=family), P.ref(X), f"K={K} N={N} M={M} family={family}")
 
 
+@pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [1, 8, 16, 40, 64])
-def test_gemm_sym_tolerance(M):
+def test_gemm_sym_tolerance(M, family):
     P = problem(2048, 1536, mode=1, seed=3)
     X = synth.host(55 + M, 14, synth.ACT, M, 2048)
-    assert_gemm_close(P.run(X), P.ref(X), f"SYM M={M}")
+    assert_gemm_close(P.run(X, family=family), P.ref(X), f"SYM M={M} family={family}")
 
 
+@pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [8, 16, 33, 64])
-def test_gemm_one_hot_bit_exact(M):
+def test_gemm_one_hot_bit_exact(M, family):
     # row m of X = e_{k_m}: Y[m] must equal the dequantised weight row w_hat[k_m] bit-for-bit (pins layout,
     # nibble order, zero/scale handling and the epilogue mapping of the whole pack -> GEMM data path)
     K, N = 1024, 768
@@ -189,23 +195,29 @@ def test_gemm_one_hot_bit_exact(M):
     ks = rng.choice(K, size=M, replace=False)
     X = np.zeros((M, K), dtype=np.float16)
     X[np.arange(M), ks] = 1.0
-    Y = to_np_u16(P.run(X.view(np.uint16)))
+    Y = to_np_u16(P.run(X.view(np.uint16), family=family))
     Wh = oracle.unpack(P.qw, P.sc, P.ze, K, N)
     assert np.array_equal(Y, Wh[ks])
 
 
-def test_gemm_batch_invariance_within_family():
+@pytest.mark.parametrize("family", FAMILIES)
+def test_gemm_batch_invariance_within_family(family):
     # the plan depends on (K, N) only: row m of Y(M) equals Y(1) of that row, bit-for-bit, within a family
-    w4 = _lib()
     P = problem(4096, 4096)
     X = synth.host(31, 15, synth.ACT, 64, 4096)
-    for Ms in ([1, 2, 5, 8, 16], [17, 32, 64]):
-        fam = {w4.w4a16_gemm_family(M, 4096, 4096) for M in Ms}
-        assert len(fam) == 1
-        base = to_np_u16(P.run(np.ascontiguousarray(X[:Ms[0]])))
-        for M in Ms[1:]:
-            Y = to_np_u16(P.run(np.ascontiguousarray(X[:M])))
-            assert np.array_equal(Y[:Ms[0]], base), f"M={M}"
+    base = to_np_u16(P.run(np.ascontiguousarray(X[:1]), family=family))
+    for M in (2, 5, 8, 16, 17, 32, 48, 64):
+        Y = to_np_u16(P.run(np.ascontiguousarray(X[:M]), family=family))
+        assert np.array_equal(Y[:1], base), f"M={M}"
+
+
+def test_gemm_families_agree_within_tolerance():
+    P = problem(4096, 4096)
+    X = synth.host(32, 15, synth.ACT, 16, 4096)
+    ref = P.ref(X)
+    Ya = P.run(X, family=0).float().cpu().numpy()
+    Yb = P.run(X, family=1).float().cpu().numpy()
+    assert np.all(np.abs(Ya - Yb) <= 2e-2 * (1 + np.abs(ref)))
 
 
 def test_gemm_deterministic_and_graph_capturable():
