@@ -19,7 +19,7 @@ $(BUILD):
 # pack.cu must not contract fp32 mul/add into FMA: its codes are bit-exact with the oracle.
 $(BUILD)/pack.o: $(CSRC)/pack.cu $(CSRC)/common.cuh include/w4a16.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) --fmad=false -c $< -o $@ 2> $(BUILD)/pack.ptxas.txt || (cat $(BUILD)/pack.ptxas.txt; false)
-$(BUILD)/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/w4a16.h | $(BUILD)
+$(BUILD)/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/tma_host.cuh include/w4a16.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
 $(LIB): $(OBJS)

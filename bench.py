@@ -129,7 +129,7 @@ def oracle_sample(M, seed, repeats=1):
     if key not in _SAMPLE:  # inputs are built once (untimed), like the GPU arm's resident inputs
         W = synth.host(seed, 9001, synth.WEIGHT, K, N)
         X = synth.host(seed, 9002, synth.ACT, M, K)
-        qw, sc, ze, _ = oracle.pack(W)
+        qw, sc, ze, _ = oracle.quantize(W)
         rng = np.random.default_rng(seed)
         tok, par = synth.eagle_tree(rng, max(M - 1, 0), 6)
         am = synth.target_argmax_for(rng, tok, par, 0.7)
@@ -138,7 +138,7 @@ def oracle_sample(M, seed, repeats=1):
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     for _ in range(repeats):
-        oracle.gemm(X, qw, sc, ze, K, N, nthreads=threads)
+        oracle.gemm(X, qw, sc, ze, nthreads=threads)
         oracle.accept(tok, par, am)
     dt = (time.perf_counter() - t0) / repeats
     wbytes = K * N // 2 + (K // 128) * N * 4
@@ -316,7 +316,21 @@ def main():
             msk = time_graph(g, max(3, args.steps // 2), 2) / n_layers
             wb = stack.layers[0][name].weight_bytes
             kernels[name] = {"K": s["K"], "N": s["N"], "us": 1e3 * msk, "weight_MB": wb / 1e6,
-                             "GBps": wb / (msk * 1e-3) / 1e9, "frac_hbm": wb / (msk * 1e-3) / 1e9 / peak_gbs}
+                             "GBps": wb / (msk * 1e-3) / 1e9, "frac_hbm": wb / (msk * 1e-3) / 1e9 / peak_gbs,
+                             "family": w4.w4a16_gemm_family(M, s["K"], s["N"])}
+            # the other kernel family on the same launches, for comparison (not part of the step)
+            alt = 1 - kernels[name]["family"]
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                for L in stack.layers:
+                    L[name](xin, yout, stack.ws, stream, family=alt)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g2, stream=stream):
+                for L in stack.layers:
+                    L[name](xin, yout, stack.ws, stream, family=alt)
+            msa = time_graph(g2, max(3, args.steps // 2), 2) / n_layers
+            kernels[name]["other_family"] = {"family": alt, "us": 1e3 * msa, "GBps": wb / (msa * 1e-3) / 1e9}
+            del g2
         gate = kernels["gate_up"]
         roofline = {"bound": "hbm", "kernel": f"w4a16 GEMM gate-up (K={gate['K']}, N={gate['N']}, M={M})",
                     "achieved": gate["GBps"], "peak": peak_gbs, "unit": "GB/s", "frac": gate["GBps"] / peak_gbs,

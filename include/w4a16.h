@@ -19,17 +19,23 @@
  * Shapes (GEMM convention of BASELINE.json): Y[M,N] = X[M,K] · W[K,N]; K = in-features, N = out-features.
  * Requirements: group == 128, K % 128 == 0, N % 128 == 0, 1 <= M <= 64 for the GEMM.
  *
- * qweight layout ("tiled n-major", the format w4a16_pack writes and w4a16_gemm reads):
- *   uint32 qweight[K*N/8], organised in 128x128 (k x n) tiles. Tile (t = n/128, g = k/128) occupies the
- *   2048 words starting at word (t*(K/128) + g) * 2048.  Inside a tile, row r = n % 128 owns the 16 words
- *   at r*16 .. r*16+15; word j = (k % 128) / 8 holds k = 128g + 8j + i for i = 0..7, with the 4-bit code of
- *   local index i in nibble slot (i % 2) * 4 + i / 2 (bits 4*slot .. 4*slot+3).  So the two 16-bit halves
- *   of (word & 0x000F000F) are the codes of k = 8j and 8j+1, of ((word >> 4) & 0x000F000F) those of
- *   8j+2, 8j+3, and so on.  Canonical logical order is SPEC's "low nibble first" along k
- *   (S:33); example: codes 0..7 of one word are 0x76543210 canonical, 0x75316420 physical.
- *   A column shard (n range, multiple of 128) is a contiguous sub-range of whole tiles.
- * scales, zeros: fp16 [K/128][N] row-major.  zeros hold the integer zero point z in [0,15] as fp16
- *   (ASYM); in SYM mode z == 8 and `zeros` may be NULL.
+ * Packed weight layout (the blob w4a16_pack writes and w4a16_gemm streams; little-endian):
+ *   a sequence of 128x128 (k x n) tiles, n-tile major: tile (t = n/128, g = k/128) occupies TB bytes at
+ *   byte (t*(K/128) + g) * TB, TB = 8704 (ASYM) or 8448 (SYM). Inside a tile:
+ *     bytes [0, 8192):     4-bit codes. Row r = n % 128 owns the 64 bytes at r*64: four 16-byte chunks, chunk
+ *                          p (k = 128g + 32p .. +31) stored at byte r*64 + 16*(p XOR ((r/2) % 4)) — the XOR
+ *                          makes the 16-byte reads of 8 consecutive rows hit 8 distinct shared-memory bank
+ *                          groups. Word w (32-bit) of a chunk holds k = 32p + 8w + i (i = 0..7) with the
+ *                          code of local index i in nibble slot (i % 2) * 4 + i / 2 (bits 4*slot..4*slot+3).
+ *                          So the two 16-bit halves of (word & 0x000F000F) are the codes of k = 8w and 8w+1,
+ *                          of ((word >> 4) & 0x000F000F) those of 8w+2, 8w+3, and so on.
+ *                          Canonical logical order is SPEC's "low nibble first" along k;
+ *                          example: codes 0..7 of one word are 0x76543210 canonical, 0x75316420 physical.
+ *     bytes [8192, 8448):  fp16 scale s of row r at 8192 + 2r.
+ *     bytes [8448, 8704):  ASYM only: fp16 zero point z (an integer in [0,15]) of row r at 8448 + 2r.
+ *   Codes, scale and zero of a 128x128 tile are adjacent, so a CTA that owns a run of tiles streams one
+ *   contiguous byte range. A column shard (n range, multiple of 128) is a contiguous
+ *   sub-range of whole tiles. SYM mode: z == 8 and no zero bytes are stored.
  * Dequantised weight (definition): w_hat[k][n] = fp16_rne((q[k][n] - z) * s).
  */
 #ifndef W4A16_H
@@ -58,6 +64,9 @@ enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 =
 
 typedef struct CUstream_st* w4a16_stream_t;   /* == cudaStream_t */
 
+/* Bytes of the packed blob for a K x N weight (0 on a bad shape/mode/group). */
+size_t w4a16_packed_bytes(int K, int N, int group, int mode);
+
 /* w4a16_pack — quantise fp16 W[K][N] (row-major) to int4 codes + per-group fp16 scale/zero.
  * Method: GPTQ W4 group-128 storage format, round-to-nearest in place of GPTQ's calibration
  * (S:95), per column n and group of 128 consecutive k:
@@ -65,15 +74,14 @@ typedef struct CUstream_st* w4a16_stream_t;   /* == cudaStream_t */
  *         z = clamp(rne(-wmin/s), 0, 15); q = clamp(rne(w/s) + z, 0, 15)     (fp32 arithmetic, RNE)
  *   SYM:  amax = max|w| (0 -> 1); s = fp16_rne(2*amax/15); z = 8; q = clamp(rne(w/s) + 8, 0, 15)
  *   A scale that underflows to 0 is recomputed from the range (-1, 1).
- * Outputs: qweight [K*N/8] (layout above), scales [K/128][N], zeros [K/128][N] (may be NULL for SYM).
+ * Output: `packed`, w4a16_packed_bytes(K, N, group, mode) bytes in the layout above.
  * Non-finite weights count as 0 and set *dev_status = W4A16_DEV_NONFINITE; otherwise *dev_status is
  * left untouched (caller zeroes it).  dev_status may be NULL.  Bit-exact with the CPU oracle. */
-int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
-               uint16_t* zeros, int32_t* dev_status, w4a16_stream_t stream);
+int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, void* packed, int32_t* dev_status,
+               w4a16_stream_t stream);
 
 /* w4a16_unpack — W_hat[K][N] fp16 = fp16_rne((q - z) * s) (test/debug). Bit-exact with the oracle. */
-int w4a16_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
-                 int mode, uint16_t* W_hat, w4a16_stream_t stream);
+int w4a16_unpack(const void* packed, int K, int N, int group, int mode, uint16_t* W_hat, w4a16_stream_t stream);
 
 /* Workspace bytes w4a16_gemm needs for this shape (split-K partials + one counter per 128-column tile).
  * Before its first use the workspace must be zero-filled (w4a16_workspace_init); every w4a16_gemm leaves
@@ -88,16 +96,14 @@ int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t
  * runs in a fixed order: results are deterministic and row m of Y does not depend on the other rows of X
  * within one kernel family (w4a16_gemm_family). Rows of Y beyond M and bytes outside Y are
  * never written. */
-int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
-               uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace, size_t workspace_bytes,
-               w4a16_stream_t stream);
+int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
+               void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
 
 /* w4a16_gemm_ex — w4a16_gemm with an explicit kernel family: W4A16_FAMILY_AUTO (= w4a16_gemm),
- * W4A16_FAMILY_MMA_SYNC (legacy mma.sync tensor path) or W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, TMEM).
- * Both families compute the same definition; used by tests and benchmarks to compare them. */
-int w4a16_gemm_ex(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
-                  uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace, size_t workspace_bytes,
-                  int family, w4a16_stream_t stream);
+ * W4A16_FAMILY_MMA_SYNC (legacy mma.sync tensor path, M <= 16 only; else W4A16_ERR_SHAPE) or
+ * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, TMEM; any M <= 64). Both compute the same definition. */
+int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
+                  void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);
 
 /* verify_accept — greedy acceptance of a draft tree against the target's argmax (rule per
  * S:289/S:298, reading R9).  n nodes, node 0 = root (the last committed token, row 0 of the verify
@@ -119,7 +125,7 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 
-/* Kernel family w4a16_gemm uses for this shape (W4A16_FAMILY_MMA_SYNC or W4A16_FAMILY_TCGEN05). */
+/* Kernel family w4a16_gemm uses for this shape: W4A16_FAMILY_MMA_SYNC for M <= 16, W4A16_FAMILY_TCGEN05 above. */
 int w4a16_gemm_family(int M, int K, int N);
 
 #ifdef __cplusplus

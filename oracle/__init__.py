@@ -28,18 +28,20 @@ def _load():
     if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
         _build()
     L = ctypes.CDLL(_SO)
-    vp, i32 = ctypes.c_void_p, ctypes.c_int
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     L.orc_half_to_float.argtypes = [ctypes.c_uint16]; L.orc_half_to_float.restype = ctypes.c_float
     L.orc_half_to_double.argtypes = [ctypes.c_uint16]; L.orc_half_to_double.restype = ctypes.c_double
     L.orc_float_to_half.argtypes = [ctypes.c_float]; L.orc_float_to_half.restype = ctypes.c_uint16
     L.orc_double_to_half.argtypes = [ctypes.c_double]; L.orc_double_to_half.restype = ctypes.c_uint16
-    L.orc_word_index.argtypes = [i32, i32, i32, i32]; L.orc_word_index.restype = ctypes.c_size_t
-    L.orc_nibble_slot.argtypes = [i32]; L.orc_nibble_slot.restype = i32
-    L.orc_get_code.argtypes = [vp, i32, i32, i32, i32]; L.orc_get_code.restype = i32
-    L.orc_pack.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp]; L.orc_pack.restype = i32
-    L.orc_unpack.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]; L.orc_unpack.restype = i32
+    L.orc_quantize.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp]; L.orc_quantize.restype = i32
+    L.orc_dequantize.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]; L.orc_dequantize.restype = i32
     L.orc_gemm.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32]; L.orc_gemm.restype = i32
     L.orc_gemm_cols.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32, vp]; L.orc_gemm_cols.restype = i32
+    L.orc_packed_bytes.argtypes = [i32, i32, i32]; L.orc_packed_bytes.restype = sz
+    L.orc_code_word_offset.argtypes = [i32, i32, i32, i32, i32]; L.orc_code_word_offset.restype = sz
+    L.orc_nibble_slot.argtypes = [i32]; L.orc_nibble_slot.restype = i32
+    L.orc_layout_pack.argtypes = [vp, vp, vp, i32, i32, i32, vp]; L.orc_layout_pack.restype = i32
+    L.orc_layout_unpack.argtypes = [vp, i32, i32, i32, vp, vp, vp]; L.orc_layout_unpack.restype = i32
     L.orc_accept.argtypes = [vp, vp, vp, i32, vp]; L.orc_accept.restype = i32
     return L
 
@@ -56,6 +58,10 @@ def _u16(a):
     return a.view(np.uint16) if a.dtype == np.float16 else a.astype(np.uint16, copy=False)
 
 
+def _c(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+
 def half_to_float(h: int) -> float:
     return L.orc_half_to_float(int(h))
 
@@ -68,63 +74,89 @@ def double_to_half(d: float) -> int:
     return L.orc_double_to_half(float(d))
 
 
-def pack(W, group=128, mode=ASYM):
-    """W: [K, N] fp16 -> (qweight uint32 [K*N/8], scales uint16 [K/g, N], zeros uint16 or None, status)."""
+def quantize(W, group=128, mode=ASYM):
+    """W [K, N] fp16 -> (codes uint8 [K, N], scales uint16 [K/g, N], zeros uint16 [K/g, N] or None, status)."""
     W = _u16(W)
     K, N = W.shape
-    qw = np.zeros(K * N // 8, dtype=np.uint32)
+    codes = np.zeros((K, N), dtype=np.uint8)
     sc = np.zeros((K // group, N), dtype=np.uint16)
     ze = np.zeros((K // group, N), dtype=np.uint16) if mode == ASYM else None
     st = np.zeros(1, dtype=np.int32)
-    rc = L.orc_pack(_p(W), K, N, group, mode, _p(qw), _p(sc), _p(ze), _p(st))
-    if rc != 0:
-        raise ValueError("orc_pack: bad arguments")
-    return qw, sc, ze, int(st[0])
+    if L.orc_quantize(_p(W), K, N, group, mode, _p(codes), _p(sc), _p(ze), _p(st)) != 0:
+        raise ValueError("orc_quantize: bad arguments")
+    return codes, sc, ze, int(st[0])
 
 
-def unpack(qw, sc, ze, K, N, group=128, mode=ASYM):
+def dequantize(codes, sc, ze, group=128, mode=ASYM):
+    codes = _c(codes, np.uint8)
+    K, N = codes.shape
     out = np.zeros((K, N), dtype=np.uint16)
-    rc = L.orc_unpack(_p(np.ascontiguousarray(qw, dtype=np.uint32)), _p(_u16(sc)), _p(None if ze is None else _u16(ze)),
-                      K, N, group, mode, _p(out))
-    if rc != 0:
-        raise ValueError("orc_unpack: bad arguments")
+    if L.orc_dequantize(_p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), K, N, group, mode, _p(out)) != 0:
+        raise ValueError("orc_dequantize: bad arguments")
     return out
 
 
-def gemm(X, qw, sc, ze, K, N, group=128, mode=ASYM, nthreads=1):
+def gemm(X, codes, sc, ze, group=128, mode=ASYM, nthreads=1):
     """fp64 Y[M, N] = X[M, K] (fp16) . W_hat."""
     X = _u16(X)
+    codes = _c(codes, np.uint8)
+    K, N = codes.shape
     M = X.shape[0]
     Y = np.zeros((M, N), dtype=np.float64)
-    rc = L.orc_gemm(_p(X), _p(np.ascontiguousarray(qw, dtype=np.uint32)), _p(_u16(sc)),
-                    _p(None if ze is None else _u16(ze)), M, K, N, group, mode, _p(Y), int(nthreads))
-    if rc != 0:
+    if L.orc_gemm(_p(X), _p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), M, K, N, group, mode, _p(Y),
+                  int(nthreads)) != 0:
         raise ValueError("orc_gemm: bad arguments")
     return Y
 
 
-def gemm_cols(X, qw, sc, ze, K, N, cols, group=128, mode=ASYM):
+def gemm_cols(X, codes, sc, ze, cols, group=128, mode=ASYM):
     X = _u16(X)
+    codes = _c(codes, np.uint8)
+    K, N = codes.shape
     M = X.shape[0]
     cols = np.ascontiguousarray(cols, dtype=np.int32)
     Y = np.zeros((M, cols.size), dtype=np.float64)
-    rc = L.orc_gemm_cols(_p(X), _p(np.ascontiguousarray(qw, dtype=np.uint32)), _p(_u16(sc)),
-                         _p(None if ze is None else _u16(ze)), M, K, N, group, mode, _p(cols), cols.size, _p(Y))
-    if rc != 0:
+    if L.orc_gemm_cols(_p(X), _p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), M, K, N, group, mode,
+                       _p(cols), cols.size, _p(Y)) != 0:
         raise ValueError("orc_gemm_cols: bad arguments")
     return Y
 
 
-def get_code(qw, K, N, k, n) -> int:
-    return L.orc_get_code(_p(np.ascontiguousarray(qw, dtype=np.uint32)), K, N, k, n)
+def packed_bytes(K, N, mode=ASYM) -> int:
+    return int(L.orc_packed_bytes(K, N, mode))
 
 
-def word_index(K, N, k, n) -> int:
-    return L.orc_word_index(K, N, k, n)
+def code_word_offset(K, N, k, n, mode=ASYM) -> int:
+    return int(L.orc_code_word_offset(K, N, mode, k, n))
 
 
 def nibble_slot(i) -> int:
     return L.orc_nibble_slot(i)
+
+
+def layout_pack(codes, sc, ze, mode=ASYM):
+    codes = _c(codes, np.uint8)
+    K, N = codes.shape
+    out = np.zeros(packed_bytes(K, N, mode), dtype=np.uint8)
+    if L.orc_layout_pack(_p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), K, N, mode, _p(out)) != 0:
+        raise ValueError("orc_layout_pack: bad arguments")
+    return out
+
+
+def layout_unpack(packed, K, N, mode=ASYM):
+    packed = _c(packed, np.uint8)
+    codes = np.zeros((K, N), dtype=np.uint8)
+    sc = np.zeros((K // 128, N), dtype=np.uint16)
+    ze = np.zeros((K // 128, N), dtype=np.uint16)
+    if L.orc_layout_unpack(_p(packed), K, N, mode, _p(codes), _p(sc), _p(ze)) != 0:
+        raise ValueError("orc_layout_unpack: bad arguments")
+    return codes, sc, (ze if mode == ASYM else None)
+
+
+def pack(W, mode=ASYM):
+    """group-128 quantise + ABI byte layout: -> (packed uint8, codes, scales, zeros, status)."""
+    codes, sc, ze, st = quantize(W, 128, mode)
+    return layout_pack(codes, sc, ze, mode), codes, sc, ze, st
 
 
 def accept(tokens, parents, argmax):

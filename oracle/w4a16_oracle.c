@@ -43,31 +43,7 @@ uint16_t orc_double_to_half(double d) {
 
 uint16_t orc_float_to_half(float f) { return orc_double_to_half((double)f); }
 
-/* ------------------------------------------------------------------------------------------------------
- * Packed layout (include/w4a16.h "qweight layout"): 128x128 tiles, n-tile major, then k-group;
- * inside a tile 128 rows of 16 words; word j holds k = 8j..8j+7 of the tile, local index i in nibble
- * slot (i%2)*4 + i/2 (so (w & 0x000F000F) yields the pair k=8j, 8j+1 as the two 16-bit halves).
- * ---------------------------------------------------------------------------------------------------- */
-int orc_nibble_slot(int i) { return (i % 2) * 4 + i / 2; }
-
-size_t orc_word_index(int K, int N, int k, int n) {
-  (void)N;
-  size_t tile = (size_t)(n / 128) * (size_t)(K / 128) + (size_t)(k / 128);
-  return tile * 2048 + (size_t)(n % 128) * 16 + (size_t)((k % 128) / 8);
-}
-
-int orc_get_code(const uint32_t* qweight, int K, int N, int k, int n) {
-  uint32_t w = qweight[orc_word_index(K, N, k, n)];
-  return (int)((w >> (4 * orc_nibble_slot(k % 8))) & 0xF);
-}
-
-static void set_code(uint32_t* qweight, int K, int N, int k, int n, int q) {
-  size_t wi = orc_word_index(K, N, k, n);
-  int sh = 4 * orc_nibble_slot(k % 8);
-  qweight[wi] = (qweight[wi] & ~(0xFu << sh)) | ((uint32_t)q << sh);
-}
-
-static int layout_ok(int K, int N) { return K > 0 && N > 0 && K % 128 == 0 && N % 128 == 0; }
+static int shape_ok(int K, int N, int group) { return K > 0 && N > 0 && group > 0 && K % group == 0; }
 
 /* clamp to [lo, hi]; -0.0 maps to lo (+0.0) so a zero point of 0 is stored as fp16 +0 (reading R2). */
 static float clampf(float x, float lo, float hi) {
@@ -77,17 +53,16 @@ static float clampf(float x, float lo, float hi) {
 }
 
 /* ------------------------------------------------------------------------------------------------------
- * Pack (GPTQ quantizer conventions). All arithmetic is fp32 (C float,
+ * Quantise (GPTQ quantizer conventions). All arithmetic is fp32 (C float,
  * SSE, no contraction): readings R3 (0 representable), R4 (RNE), R5 (codes use the stored fp16 scale),
  * R15 (all-zero group -> range +-1).
  * ---------------------------------------------------------------------------------------------------- */
-int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
-             uint16_t* zeros, int32_t* status) {
-  if (!W || !qweight || !scales || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+int orc_quantize(const uint16_t* W, int K, int N, int group, int mode, uint8_t* codes, uint16_t* scales,
+                 uint16_t* zeros, int32_t* status) {
+  if (!W || !codes || !scales || !shape_ok(K, N, group)) return -1;
   if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
   if (mode == ORC_ASYM && !zeros) return -1;
   int st = ORC_DEV_OK;
-  memset(qweight, 0, (size_t)K * N / 2);
   for (int n = 0; n < N; ++n) {
     for (int g = 0; g < K / group; ++g) {
       /* 1. range, always containing 0; non-finite weights flag the status and count as 0 */
@@ -122,7 +97,7 @@ int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qwe
         float w = orc_half_to_float(W[(size_t)k * N + n]);
         if (!isfinite(w)) w = 0.0f;
         float q = clampf(rintf(w / s32) + z, 0.0f, 15.0f);
-        set_code(qweight, K, N, k, n, (int)q);
+        codes[(size_t)k * N + n] = (uint8_t)(int)q;
       }
     }
   }
@@ -132,20 +107,20 @@ int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qwe
 
 /* w_hat = fp16_rne((q - z) * s): (q - z) is a small integer, the product is exact in double, so this is
  * exactly one rounding. */
-static uint16_t dequant(int q, uint16_t s, uint16_t z_or_8, int mode) {
-  double z = mode == ORC_SYM ? 8.0 : orc_half_to_double(z_or_8);
+static uint16_t dequant(int q, uint16_t s, const uint16_t* zeros, size_t gi, int mode) {
+  double z = mode == ORC_SYM ? 8.0 : orc_half_to_double(zeros[gi]);
   return orc_double_to_half(((double)q - z) * orc_half_to_double(s));
 }
 
-int orc_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
-               int mode, uint16_t* W_hat) {
-  if (!qweight || !scales || !W_hat || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+int orc_dequantize(const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
+                   int mode, uint16_t* W_hat) {
+  if (!codes || !scales || !W_hat || !shape_ok(K, N, group)) return -1;
   if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
   if (mode == ORC_ASYM && !zeros) return -1;
   for (int k = 0; k < K; ++k)
     for (int n = 0; n < N; ++n) {
       size_t gi = (size_t)(k / group) * N + n;
-      W_hat[(size_t)k * N + n] = dequant(orc_get_code(qweight, K, N, k, n), scales[gi], zeros ? zeros[gi] : 0, mode);
+      W_hat[(size_t)k * N + n] = dequant(codes[(size_t)k * N + n], scales[gi], zeros, gi, mode);
     }
   return 0;
 }
@@ -154,9 +129,9 @@ int orc_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* 
  * GEMM reference: dequantise, then matmul, in fp64 with k in order 0..K-1.
  * ---------------------------------------------------------------------------------------------------- */
 typedef struct {
-  const uint16_t* X; const uint32_t* qw; const uint16_t* sc; const uint16_t* ze;
+  const uint16_t* X; const uint8_t* codes; const uint16_t* sc; const uint16_t* ze;
   int M, K, N, group, mode;
-  const int32_t* cols; int ncols;        /* column list (cols == NULL: all columns) */
+  const int32_t* cols;                   /* column list (NULL: all columns) */
   double* Y; int ystride;                /* Y[m*ystride + j] */
   int j0, j1;                            /* this worker's column positions [j0, j1) */
 } gemm_job;
@@ -164,12 +139,11 @@ typedef struct {
 static void* gemm_worker(void* p) {
   gemm_job* a = (gemm_job*)p;
   double* wcol = (double*)malloc(sizeof(double) * (size_t)a->K);
-  double* xd = (double*)malloc(sizeof(double) * (size_t)a->K);
   for (int j = a->j0; j < a->j1; ++j) {
     int n = a->cols ? a->cols[j] : j;
     for (int k = 0; k < a->K; ++k) {
       size_t gi = (size_t)(k / a->group) * a->N + n;
-      wcol[k] = orc_half_to_double(dequant(orc_get_code(a->qw, a->K, a->N, k, n), a->sc[gi], a->ze ? a->ze[gi] : 0, a->mode));
+      wcol[k] = orc_half_to_double(dequant(a->codes[(size_t)k * a->N + n], a->sc[gi], a->ze, gi, a->mode));
     }
     for (int m = 0; m < a->M; ++m) {
       const uint16_t* xr = a->X + (size_t)m * a->K;
@@ -178,13 +152,13 @@ static void* gemm_worker(void* p) {
       a->Y[(size_t)m * a->ystride + j] = acc;
     }
   }
-  free(wcol); free(xd);
+  free(wcol);
   return NULL;
 }
 
-static int gemm_run(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+static int gemm_run(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
                     int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Y, int nthreads) {
-  if (!X || !qweight || !scales || !Y || M < 0 || !layout_ok(K, N) || group <= 0 || K % group != 0) return -1;
+  if (!X || !codes || !scales || !Y || M < 0 || !shape_ok(K, N, group)) return -1;
   if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
   if (mode == ORC_ASYM && !zeros) return -1;
   if (nthreads < 1) nthreads = 1;
@@ -192,7 +166,7 @@ static int gemm_run(const uint16_t* X, const uint32_t* qweight, const uint16_t* 
   gemm_job* jobs = (gemm_job*)calloc((size_t)nthreads, sizeof(gemm_job));
   pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
   for (int t = 0; t < nthreads; ++t) {
-    gemm_job j = {X, qweight, scales, zeros, M, K, N, group, mode, cols, ncols, Y, ncols,
+    gemm_job j = {X, codes, scales, zeros, M, K, N, group, mode, cols, Y, ncols,
                   (int)((long long)ncols * t / nthreads), (int)((long long)ncols * (t + 1) / nthreads)};
     jobs[t] = j;
   }
@@ -203,16 +177,83 @@ static int gemm_run(const uint16_t* X, const uint32_t* qweight, const uint16_t* 
   return 0;
 }
 
-int orc_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
-             int K, int N, int group, int mode, double* Y, int nthreads) {
-  return gemm_run(X, qweight, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads);
+int orc_gemm(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M, int K,
+             int N, int group, int mode, double* Y, int nthreads) {
+  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads);
 }
 
-int orc_gemm_cols(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+int orc_gemm_cols(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
                   int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols) {
   if (!cols || ncols < 0) return -1;
   for (int j = 0; j < ncols; ++j) if (cols[j] < 0 || cols[j] >= N) return -1;
-  return gemm_run(X, qweight, scales, zeros, M, K, N, group, mode, cols, ncols, Ycols, 1);
+  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, cols, ncols, Ycols, 1);
+}
+
+/* ------------------------------------------------------------------------------------------------------
+ * The ABI's packed blob (include/w4a16.h): 128x128 tiles, n-tile major then k-group; per tile 8192 code
+ * bytes (row r: 64 bytes at r*64 = four 16-byte chunks, chunk p = k 32p..32p+31 stored at chunk position
+ * p XOR ((r/2) % 4); word w of a chunk: k = 32p + 8w .. +7, local index i in nibble slot (i%2)*4 + i/2),
+ * then 128 fp16 scales, then (ASYM) 128 fp16 zeros. Integers are little-endian.
+ * ---------------------------------------------------------------------------------------------------- */
+static int layout_ok(int K, int N) { return K > 0 && N > 0 && K % 128 == 0 && N % 128 == 0; }
+static size_t tile_bytes(int mode) { return mode == ORC_ASYM ? 8704 : 8448; }
+static size_t tile_offset(int K, int mode, int k, int n) {
+  return ((size_t)(n / 128) * (size_t)(K / 128) + (size_t)(k / 128)) * tile_bytes(mode);
+}
+
+int orc_nibble_slot(int i) { return (i % 2) * 4 + i / 2; }
+
+size_t orc_packed_bytes(int K, int N, int mode) {
+  if (!layout_ok(K, N)) return 0;
+  return (size_t)(N / 128) * (size_t)(K / 128) * tile_bytes(mode);
+}
+
+size_t orc_code_word_offset(int K, int N, int mode, int k, int n) {
+  (void)N;
+  int r = n % 128, p = (k % 128) / 32, w = (k % 32) / 8;
+  int chunk_pos = p ^ ((r / 2) % 4);
+  return tile_offset(K, mode, k, n) + (size_t)r * 64 + (size_t)chunk_pos * 16 + (size_t)w * 4;
+}
+
+static uint32_t rd32(const uint8_t* p) { return (uint32_t)p[0] | (uint32_t)p[1] << 8 | (uint32_t)p[2] << 16 | (uint32_t)p[3] << 24; }
+static void wr32(uint8_t* p, uint32_t v) { p[0] = (uint8_t)v; p[1] = (uint8_t)(v >> 8); p[2] = (uint8_t)(v >> 16); p[3] = (uint8_t)(v >> 24); }
+static uint16_t rd16(const uint8_t* p) { return (uint16_t)(p[0] | p[1] << 8); }
+static void wr16(uint8_t* p, uint16_t v) { p[0] = (uint8_t)v; p[1] = (uint8_t)(v >> 8); }
+
+int orc_layout_pack(const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int K, int N, int mode,
+                    uint8_t* packed) {
+  if (!codes || !scales || !packed || !layout_ok(K, N) || (mode != ORC_ASYM && mode != ORC_SYM)) return -1;
+  if (mode == ORC_ASYM && !zeros) return -1;
+  memset(packed, 0, orc_packed_bytes(K, N, mode));
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k) {
+      uint8_t* w = packed + orc_code_word_offset(K, N, mode, k, n);
+      wr32(w, rd32(w) | ((uint32_t)(codes[(size_t)k * N + n] & 0xF) << (4 * orc_nibble_slot(k % 8))));
+    }
+  for (int g = 0; g < K / 128; ++g)
+    for (int n = 0; n < N; ++n) {
+      uint8_t* t = packed + tile_offset(K, mode, 128 * g, n);
+      wr16(t + 8192 + 2 * (n % 128), scales[(size_t)g * N + n]);
+      if (mode == ORC_ASYM) wr16(t + 8448 + 2 * (n % 128), zeros[(size_t)g * N + n]);
+    }
+  return 0;
+}
+
+int orc_layout_unpack(const uint8_t* packed, int K, int N, int mode, uint8_t* codes, uint16_t* scales,
+                      uint16_t* zeros) {
+  if (!packed || !codes || !scales || !layout_ok(K, N) || (mode != ORC_ASYM && mode != ORC_SYM)) return -1;
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k) {
+      uint32_t w = rd32(packed + orc_code_word_offset(K, N, mode, k, n));
+      codes[(size_t)k * N + n] = (uint8_t)((w >> (4 * orc_nibble_slot(k % 8))) & 0xF);
+    }
+  for (int g = 0; g < K / 128; ++g)
+    for (int n = 0; n < N; ++n) {
+      const uint8_t* t = packed + tile_offset(K, mode, 128 * g, n);
+      scales[(size_t)g * N + n] = rd16(t + 8192 + 2 * (n % 128));
+      if (zeros) zeros[(size_t)g * N + n] = mode == ORC_ASYM ? rd16(t + 8448 + 2 * (n % 128)) : 0x4800; /* 8.0 */
+    }
+  return 0;
 }
 
 /* ------------------------------------------------------------------------------------------------------

@@ -6,20 +6,24 @@
  * tables); the only common code is the input generator in synth/, which holds none of the method's
  * arithmetic.
  *
- * What it computes (citations: PAPER.md line numbers "P:n", SPEC.md "S:n"; readings in DESIGN.md §3):
- *   - pack:   GPTQ-style W4 group-128 quantisation, round-to-nearest ("symmetrically quantize weights
- *             to 4-bit with a group size of 128"; RTN stands in for GPTQ calibration as in S:95; ASYM per
- *             BASELINE.json config 1). Arithmetic in IEEE fp32, RNE, no contraction (reading R5).
- *   - unpack: w_hat = fp16_rne((q - z) * s)   (exact product, one rounding).
- *   - gemm:   Y[m][n] = sum_k X[m][k] * w_hat[k][n], in fp64, sequential k (BASELINE.json north_star:
- *             "X[M,K] fp16 x packed W[K,N] -> Y[M,N] fp16, fp32 accumulate"; the oracle uses fp64).
- *   - accept: greedy tree acceptance (P:79-84 draft-then-verify; the rule is not stated by the paper,
- *             SPEC S:289/S:298 greedy argmax; reading R9).
- *
- * Packed layout (the ABI's, re-derived here from its definition in include/w4a16.h, not shared):
- *   qweight is uint32[K*N/8]; tile (t = n/128, g = k/128) is 2048 words at ((t*(K/128) + g) * 2048);
- *   inside the tile, row r = n%128 has 16 words at r*16; word j = (k%128)/8 holds k = 128g+8j+i,
- *   i in 0..7, in nibble slot (i%2)*4 + i/2.  scales/zeros: fp16 [K/group][N] row-major.
+ * What it computes (citations: PAPER.md line numbers "P:n", SPEC.md "S:n"; readings R1..R15 in DESIGN.md §3):
+ *   - quantize:   GPTQ-style W4 group quantisation, round-to-nearest ("symmetrically quantize weights
+ *                 to 4-bit with a group size of 128"; RTN stands in for GPTQ calibration as in S:95; ASYM per
+ *                 BASELINE.json config 1). Arithmetic in IEEE fp32, RNE, no contraction (reading R5).
+ *   - dequantize: w_hat = fp16_rne((q - z) * s)   (exact product, one rounding).
+ *   - gemm:       Y[m][n] = sum_k X[m][k] * w_hat[k][n], in fp64, sequential k (BASELINE.json north_star:
+ *                 "X[M,K] fp16 x packed W[K,N] -> Y[M,N] fp16, fp32 accumulate"; the oracle uses fp64).
+ *   - accept:     greedy tree acceptance (P:79-84 draft-then-verify; the rule is not stated by the paper,
+ *                 SPEC S:289/S:298 greedy argmax; reading R9).
+ * The arithmetic works on plain arrays: codes uint8 [K][N], scales/zeros fp16 [K/group][N]. The byte layout
+ * of the ABI's packed blob is a separate pair of functions (layout_pack / layout_unpack), re-derived here
+ * from its definition in include/w4a16.h (not shared):
+ *   the blob is a sequence of 128x128 (k x n) tiles, tile (t = n/128, g = k/128) at byte
+ *   (t*(K/128) + g) * TB with TB = 8704 (ASYM) or 8448 (SYM). Inside a tile: bytes [0, 8192) hold codes,
+ *   row r = n%128 owns the 64 bytes at r*64, four 16-byte chunks; chunk p (k = 128g + 32p .. +31) sits at
+ *   byte r*64 + 16*(p XOR ((r/2) % 4)); inside a chunk, little-endian 32-bit word w holds k = 32p + 8w + i,
+ *   i = 0..7, in nibble slot (i%2)*4 + i/2. Bytes [8192, 8448): fp16 scale of row r at 8192 + 2r.
+ *   ASYM only: bytes [8448, 8704): fp16 zero of row r at 8448 + 2r.
  */
 #ifndef W4A16_ORACLE_H
 #define W4A16_ORACLE_H
@@ -41,31 +45,34 @@ double orc_half_to_double(uint16_t h);
 uint16_t orc_float_to_half(float f);
 uint16_t orc_double_to_half(double d);
 
-/* Layout accessors. */
-size_t orc_word_index(int K, int N, int k, int n);
-int orc_nibble_slot(int i);
-int orc_get_code(const uint32_t* qweight, int K, int N, int k, int n);
-
 /* Quantise fp16 W[K][N] (row-major) per column n and per group of `group` consecutive k.
- * mode ORC_ASYM (integer zero in [0,15] stored as fp16) or ORC_SYM (zero == 8, zeros may be NULL).
- * The packed layout needs N % 128 == 0 and K % 128 == 0; group must divide K (any group for the
- * oracle's own math, the ABI fixes 128). *status gets ORC_DEV_NONFINITE if any W is not finite.
+ * codes: uint8 [K][N] (values 0..15); scales: fp16 [K/group][N]; zeros: fp16 [K/group][N] (ASYM; in SYM mode
+ * zeros may be NULL, otherwise it is filled with 8). *status = ORC_DEV_NONFINITE if any W is not finite.
  * Returns 0 or -1 on bad arguments. */
-int orc_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
-             uint16_t* zeros, int32_t* status);
+int orc_quantize(const uint16_t* W, int K, int N, int group, int mode, uint8_t* codes, uint16_t* scales,
+                 uint16_t* zeros, int32_t* status);
 
-/* W_hat[K][N] fp16 = fp16_rne((q - z) * s). */
-int orc_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
-               int mode, uint16_t* W_hat);
+/* W_hat[K][N] fp16 = fp16_rne((q - z) * s) with z = 8 in SYM mode. */
+int orc_dequantize(const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int K, int N, int group,
+                   int mode, uint16_t* W_hat);
 
-/* Y[M][N] (fp64) = X[M][K] (fp16) * W_hat, W_hat dequantised from the packed operands; k summed in order
- * 0..K-1 in fp64. Columns are independent: nthreads >= 1 splits columns across pthreads, result identical. */
-int orc_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
-             int K, int N, int group, int mode, double* Y, int nthreads);
+/* Y[M][N] (fp64) = X[M][K] (fp16) * W_hat (dequantised from codes/scales/zeros); k summed in order 0..K-1 in
+ * fp64. Columns are independent: nthreads >= 1 splits columns across pthreads, the result is identical. */
+int orc_gemm(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M, int K,
+             int N, int group, int mode, double* Y, int nthreads);
 
-/* Same definition for a list of columns only (full-size sampled checks): Ycols[m*ncols + j] = Y[m][cols[j]]. */
-int orc_gemm_cols(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int M,
+/* Same definition for a list of columns only: Ycols[m*ncols + j] = Y[m][cols[j]]. */
+int orc_gemm_cols(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
                   int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols);
+
+/* The ABI's packed blob (group 128; K % 128 == 0, N % 128 == 0). */
+size_t orc_packed_bytes(int K, int N, int mode);
+size_t orc_code_word_offset(int K, int N, int mode, int k, int n);   /* byte offset of the word holding (k, n) */
+int orc_nibble_slot(int i);
+int orc_layout_pack(const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int K, int N, int mode,
+                    uint8_t* packed);
+int orc_layout_unpack(const uint8_t* packed, int K, int N, int mode, uint8_t* codes, uint16_t* scales,
+                      uint16_t* zeros);
 
 /* Greedy acceptance over a draft tree of n nodes (node 0 = root = last committed token, parents[0] = -1,
  * parents[i] < i). out[0] = accepted length, out[1] = bonus token, out[2] = device status,

@@ -22,6 +22,7 @@ W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05 = -1, 0, 1
 
 # Every symbol include/w4a16.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
+    "w4a16_packed_bytes",
     "w4a16_pack",
     "w4a16_unpack",
     "w4a16_gemm_workspace_bytes",
@@ -46,13 +47,15 @@ def _load():
             "The W4A16 path has no CPU fallback.")
     lib = ctypes.CDLL(LIB_PATH)
     vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
-    lib.w4a16_pack.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-    lib.w4a16_unpack.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp]
+    lib.w4a16_packed_bytes.argtypes = [i32, i32, i32, i32]
+    lib.w4a16_packed_bytes.restype = sz
+    lib.w4a16_pack.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp]
+    lib.w4a16_unpack.argtypes = [vp, i32, i32, i32, i32, vp, vp]
     lib.w4a16_gemm_workspace_bytes.argtypes = [i32, i32, i32, i32]
     lib.w4a16_gemm_workspace_bytes.restype = sz
     lib.w4a16_workspace_init.argtypes = [vp, sz, vp]
-    lib.w4a16_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, vp]
-    lib.w4a16_gemm_ex.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, i32, vp]
+    lib.w4a16_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, vp]
+    lib.w4a16_gemm_ex.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, i32, vp]
     lib.verify_accept.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.w4a16_status_string.argtypes = [i32]
     lib.w4a16_status_string.restype = ctypes.c_char_p

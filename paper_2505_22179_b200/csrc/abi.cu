@@ -5,16 +5,14 @@
 #include <cuda_runtime.h>
 #include "w4a16.h"
 
-extern "C" int w4a16_launch_pack(const uint16_t*, int, int, int, uint32_t*, uint16_t*, uint16_t*, int32_t*, cudaStream_t);
-extern "C" int w4a16_launch_unpack(const uint32_t*, const uint16_t*, const uint16_t*, int, int, int, uint16_t*, cudaStream_t);
+extern "C" int w4a16_launch_pack(const uint16_t*, int, int, int, void*, int32_t*, cudaStream_t);
+extern "C" int w4a16_launch_unpack(const void*, int, int, int, uint16_t*, cudaStream_t);
 extern "C" int w4a16_launch_accept(const int32_t*, const int32_t*, const int32_t*, int, int32_t*, cudaStream_t);
 extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaStream_t);
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
-extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const uint32_t*, const uint16_t*, const uint16_t*, uint16_t*, int,
-                                    int, int, int, void*, int, cudaStream_t);
-extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const uint32_t*, const uint16_t*, const uint16_t*, uint16_t*, int,
-                                     int, int, int, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 
 namespace {
 
@@ -39,22 +37,27 @@ int check_kn(int K, int N, int group) {
 
 }  // namespace
 
-extern "C" int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, uint32_t* qweight, uint16_t* scales,
-                          uint16_t* zeros, int32_t* dev_status, w4a16_stream_t stream) {
-  if (!W || !qweight || !scales || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
-    return W4A16_ERR_ARG;
-  if (int e = check_kn(K, N, group)) return e;
-  if (!aligned16(W) || !aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros))) return W4A16_ERR_ALIGN;
-  return w4a16_launch_pack(W, K, N, mode, qweight, scales, zeros, dev_status, (cudaStream_t)stream);
+bool mode_ok(int mode) { return mode == W4A16_ASYM || mode == W4A16_SYM; }
+
+extern "C" size_t w4a16_packed_bytes(int K, int N, int group, int mode) {
+  if (check_kn(K, N, group) != W4A16_OK || !mode_ok(mode)) return 0;
+  return (size_t)(N / 128) * (size_t)(K / 128) * (mode == W4A16_ASYM ? 8704 : 8448);
 }
 
-extern "C" int w4a16_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K, int N,
-                            int group, int mode, uint16_t* W_hat, w4a16_stream_t stream) {
-  if (!qweight || !scales || !W_hat || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
-    return W4A16_ERR_ARG;
+extern "C" int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, void* packed, int32_t* dev_status,
+                          w4a16_stream_t stream) {
+  if (!W || !packed || !mode_ok(mode)) return W4A16_ERR_ARG;
   if (int e = check_kn(K, N, group)) return e;
-  if (!aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros)) || !aligned16(W_hat)) return W4A16_ERR_ALIGN;
-  return w4a16_launch_unpack(qweight, scales, zeros, K, N, mode, W_hat, (cudaStream_t)stream);
+  if (!aligned16(W) || !aligned16(packed)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_pack(W, K, N, mode, packed, dev_status, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_unpack(const void* packed, int K, int N, int group, int mode, uint16_t* W_hat,
+                            w4a16_stream_t stream) {
+  if (!packed || !W_hat || !mode_ok(mode)) return W4A16_ERR_ARG;
+  if (int e = check_kn(K, N, group)) return e;
+  if (!aligned16(packed) || !aligned16(W_hat)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_unpack(packed, K, N, mode, W_hat, (cudaStream_t)stream);
 }
 
 extern "C" size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group) {
@@ -70,40 +73,37 @@ extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a
   return cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
+// Family choice depends on M only through the token-block count: mma.sync for M <= 16 (HMMA work per weight
+// is small, everything stays in registers), tcgen05 above (MMA cost nearly independent of M). DESIGN.md §5.
 extern "C" int w4a16_gemm_family(int M, int K, int N) {
-  (void)M; (void)K; (void)N;
-  return W4A16_FAMILY_TCGEN05;
+  (void)K; (void)N;
+  return M <= 16 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_TCGEN05;
 }
 
-extern "C" int w4a16_gemm_ex(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales,
-                             const uint16_t* zeros, uint16_t* Y, int M, int K, int N, int group, int mode,
-                             void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream) {
-  if (!X || !qweight || !scales || !Y || (mode != W4A16_ASYM && mode != W4A16_SYM) || (mode == W4A16_ASYM && !zeros))
-    return W4A16_ERR_ARG;
+extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group,
+                             int mode, void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream) {
+  if (!X || !packed || !Y || !mode_ok(mode)) return W4A16_ERR_ARG;
   if (int e = check_kn(K, N, group)) return e;
   if (M < 1 || M > W4A16_MAX_M) return W4A16_ERR_SHAPE;
-  if (!aligned16(X) || !aligned16(qweight) || !aligned16(scales) || (zeros && !aligned16(zeros)) || !aligned16(Y) ||
-      !aligned16(workspace))
-    return W4A16_ERR_ALIGN;
+  if (!aligned16(X) || !aligned16(packed) || !aligned16(Y) || !aligned16(workspace)) return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
   if (family == W4A16_FAMILY_AUTO) family = w4a16_gemm_family(M, K, N);
   if (family == W4A16_FAMILY_MMA_SYNC) {
+    if (M > 16) return W4A16_ERR_SHAPE;
     if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_mma(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+    return w4a16_launch_gemm_mma(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
   }
   if (family == W4A16_FAMILY_TCGEN05) {
     if (!workspace || workspace_bytes < w4a16_tc_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_tc(X, qweight, scales, zeros, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+    return w4a16_launch_gemm_tc(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
   }
   return W4A16_ERR_ARG;
 }
 
-extern "C" int w4a16_gemm(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros,
-                          uint16_t* Y, int M, int K, int N, int group, int mode, void* workspace,
-                          size_t workspace_bytes, w4a16_stream_t stream) {
-  return w4a16_gemm_ex(X, qweight, scales, zeros, Y, M, K, N, group, mode, workspace, workspace_bytes,
-                       W4A16_FAMILY_AUTO, stream);
+extern "C" int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
+                          void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+  return w4a16_gemm_ex(X, packed, Y, M, K, N, group, mode, workspace, workspace_bytes, W4A16_FAMILY_AUTO, stream);
 }
 
 extern "C" int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n,

@@ -2,42 +2,58 @@
 //
 //   Y[M,N] = X[M,K] · W_hat[K,N]   with W_hat = (q - z) * s per group of 128 k (include/w4a16.h)
 //
-// Design:
-//  * Work unit = one 128x128 (n x k) weight tile = 8 KiB of codes + 256 B scales + 256 B zeros. Units are
-//    numbered u = tile_n * (K/128) + group, which is exactly their order in qweight, so a CTA's range of
-//    units is one contiguous byte range of the packed weights.
-//  * Stream-K: CTA c of G owns units [c*U/G, (c+1)*U/G). A (K, N, SM-count)-only plan: no dependence on M.
-//  * Warp 8 = producer: one lane streams each unit into a STAGES-deep shared-memory ring with 1-D bulk
-//    async copies (TMA engine, mbarrier completion, L2 evict_first for the once-read weights).
-//  * Warps 0..7 = consumers: warp w owns rows 16w..16w+15 of the 128-row tile. Per unit a lane reads its
-//    two 16-byte chunks (rows g and g+8, k-chunk c), dequantises with LOP3 + HSUB2/HFMA2 to EXACT small
-//    integers (q - z) in fp16, and issues mma.sync m16n8k16 with weights as the MMA-M operand ("swap AB";
-//    tokens are MMA-N, padded to 8). A k-permutation inside each 32-wide chunk lets one lane's 32
-//    consecutive k feed 8 MMAs, so both weights and activations are read as 16-byte vectors.
-//  * The group scale is applied after the MMA, to the fp32 group sum: Y += s * sum_k X (q - z). This keeps
-//    the dequant at 9 integer/fp16 instructions per 8 weights (no HMUL2), the budget that decides whether
-//    B200's ALU can keep up with 7 TB/s of int4 weights.
-//  * Split tiles: fp32 partials to the workspace, then the last CTA to arrive (atomic counter per tile)
-//    sums the partials in CTA order (fixed, hence deterministic) and writes fp16 Y; it re-zeroes the
-//    counter, leaving the workspace ready for the next call.
+// Design. At M <= 16 the tensor work per weight is small enough for the legacy mma.sync
+// pipe (~550 TFLOP/s measured on B200), and keeping dequant + MMA inside each warp's registers avoids the
+// TMEM traffic and cross-warp hand-offs of the tcgen05 family.
+//  * Work unit = one 128x128 (n x k) weight tile (8704 / 8448 contiguous bytes of the packed blob: codes,
+//    scales, zeros). Units are numbered in blob order, so a CTA's range is one contiguous byte range.
+//  * Stream-K: CTA c of G = 2 x SMs owns units [c*U/G, (c+1)*U/G) — a (K, N, SM-count)-only plan.
+//  * Warp 8 (producer) streams stages of 2 units with ONE bulk copy each (the TMA engine costs ~100+
+//    cycles per issued copy), plus the units' activation slices with a 3-D TMA (SWIZZLE_128B, rows >= M
+//    zero-filled), into a 4-deep shared-memory ring.
+//  * Warps 0..7 = 4 row-quarters x 2 k-halves: warp (rq, kh) owns tile rows 32rq..32rq+31 (two m16 MMA
+//    tiles) and k = 64kh..64kh+63 of every unit, so each activation fragment is reused by 2 MMA row tiles
+//    and only 2 warps read each activation byte (the v1 layout re-read X 8x and was L1-bound).
+//    A lane reads one 32-bit word (8 consecutive k of one row) per row and chunk — conflict-free thanks to
+//    the XOR chunk permutation of the layout — dequantises it to EXACT (q - z) fp16 with LOP3 +
+//    HSUB2/HFMA2, and issues mma.sync m16n8k16 with weights as the MMA-M operand ("swap AB"; tokens are
+//    MMA-N). Inside each 32-k chunk a k-permutation lets one lane's 8 consecutive k feed two MMA k-steps,
+//    with the activations read as one 16-byte vector per token block.
+//  * The group scale is applied after the MMA to the fp32 group sum: Y += s * sum_k X (q - z), keeping the
+//    dequant at 9 integer/fp16 instructions per 8 weights (no HMUL2).
+//  * Tile boundary: the two k-half warps combine through shared memory; a tile split across CTAs goes to
+//    the fp32 workspace and the last CTA to arrive (atomic counter per tile) sums the partials in CTA order
+//    (fixed, hence deterministic) and writes fp16 Y, re-zeroing the counter.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "w4a16.h"
 
 namespace w4 {
+namespace ma {
 
 constexpr int kTileN = 128, kTileK = 128;
-constexpr int kUnitWBytes = kTileN * kTileK / 2;             // 8192
-constexpr int kStageBytes = kUnitWBytes + 2 * kTileN * 2;    // + scales + zeros = 8704
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;          // 288
+constexpr int kUnitWBytes = kTileN * kTileK / 2;   // 8192
+constexpr int kWarps = 8;                          // 4 row-quarters x 2 k-halves
+constexpr int kProducerWarp = kWarps;              // warp 8
+constexpr int kThreads = (kWarps + 1) * 32;        // 288
+constexpr int kR = 2;                              // units per pipeline stage
+
+template <int NTB, bool SYM>
+struct Cfg {
+  static constexpr int kMpad = 8 * NTB;                           // token rows per TMA box
+  static constexpr int kTB = SYM ? 8448 : 8704;
+  static constexpr int kXBox = kMpad * 128;                       // one 64-k SW128 box (multiple of 1024 B)
+  static constexpr int kXUnit = 2 * kXBox;
+  static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
+  static constexpr int kStages = 4;
+  static constexpr int kRedFloats = 4 * NTB * 2 * 4 * 32;         // k-half reduction scratch
+  static constexpr int kSmem = kStages * kStage + kRedFloats * 4 + 1024;
+};
 
 struct GemmParams {
-  const uint16_t* X;
-  const uint32_t* qweight;
-  const uint16_t* scales;
-  const uint16_t* zeros;
+  const uint8_t* packed;
   uint16_t* Y;
-  float* partials;   // [2G][NTB][8 warps][32 lanes] float4
+  float* partials;   // [2G][4 rq][NTB][2 mt][32 lanes] float4
   int* counters;     // [N/128]
   int M, K, N;
   int Gk;            // K / 128 groups per n-tile
@@ -50,39 +66,69 @@ __device__ __forceinline__ int unit_begin(int c, int U, int G) { return (int)(((
 __device__ __forceinline__ int cta_of_unit(int u, int U, int G) {
   return (int)((((long long)(u + 1) * G) + U - 1) / U) - 1;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 
-template <int NTB, bool SYM, int STAGES>
-__global__ void __launch_bounds__(kThreads, (NTB <= 2 ? 2 : 1)) gemm_w4a16_mma_kernel(const GemmParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES];
-  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+template <int NTB, bool SYM>
+__global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __grid_constant__ CUtensorMap xmapR,
+                                                                      const __grid_constant__ CUtensorMap xmap1,
+                                                                      const GemmParams p) {
+  using C = Cfg<NTB, SYM>;
+  constexpr int S = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int u_begin = unit_begin(cta, p.U, p.G), u_end = unit_begin(cta + 1, p.U, p.G);
+  const int n_stages = (u_end - u_begin + kR - 1) / kR;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t smem_base = smem_u32(smem);
+  float* red = reinterpret_cast<float*>(smem + S * C::kStage);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kConsumerWarps); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
-    // ---------------- producer: stream units into the ring ----------------
+  if (warp == kProducerWarp) {
+    // ---------------- producer ----------------
     if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
-      for (int u = u_begin; u < u_end; ++u) {
+      for (int i = 0; i < n_stages; ++i) {
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
         mbar_wait(&empty_bar[s], ph ^ 1);
-        const int t = u / p.Gk, g = u - t * p.Gk;
-        uint8_t* st = smem + s * kStageBytes;
-        mbar_expect_tx(&full_bar[s], SYM ? kUnitWBytes + 256 : kUnitWBytes + 512);
-        bulk_g2s(st, p.qweight + (size_t)u * (kUnitWBytes / 4), kUnitWBytes, &full_bar[s], pol);
-        bulk_g2s(st + kUnitWBytes, p.scales + (size_t)g * p.N + (size_t)t * kTileN, 256, &full_bar[s], pol);
-        if (!SYM) bulk_g2s(st + kUnitWBytes + 256, p.zeros + (size_t)g * p.N + (size_t)t * kTileN, 256, &full_bar[s], pol);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        const uint32_t st = smem_base + s * C::kStage;
+        const int g0 = u0 % p.Gk;
+        mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
+        if (nu == kR && g0 + kR <= p.Gk) {
+          tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
+        } else {
+          for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
+        }
+        bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+        if (++s == S) { s = 0; ph ^= 1; }
       }
     }
     return;
@@ -90,174 +136,210 @@ __global__ void __launch_bounds__(kThreads, (NTB <= 2 ? 2 : 1)) gemm_w4a16_mma_k
 
   // ---------------- consumers ----------------
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
-  const int r0 = warp * 16 + g8, r1 = r0 + 8; // tile rows (n) owned by this lane
-  const uint32_t smem_base = smem_u32(smem);
+  const int rq = warp & 3, kh = warp >> 2;    // row quarter, k half
+  int rows[2][2];                              // tile rows owned by this lane: [m-tile][g / g+8]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    rows[mt][0] = 32 * rq + 16 * mt + g8;
+    rows[mt][1] = rows[mt][0] + 8;
+  }
 
-  float acc[NTB][4];
+  float acc[2][NTB][4];
   int s = 0;
   uint32_t ph = 0;
-  int cur_t = -1, seg_first_unit = u_begin;
+  int cur_t = -1, seg_u0 = u_begin, boundary = 0;
   bool first_segment = true;
 
-  auto flush = [&](int t, int seg_u0, int seg_u1, bool is_first_seg) {
-    const int tile_u0 = t * p.Gk, tile_u1 = tile_u0 + p.Gk;
-    const bool whole = (seg_u0 == tile_u0 && seg_u1 == tile_u1);
-    const int n0 = t * kTileN + r0, n1 = t * kTileN + r1;
-    if (whole) {
+  auto flush = [&](int t, int sg0, int sg1, bool is_first_seg) {
+    // 1. combine the two k-halves: kh = 1 hands its partial sums to kh = 0 through shared memory
+    if (kh == 1) {
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) {
-        const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
-        if (m0 < p.M) {
-          p.Y[(size_t)m0 * p.N + n0] = __half_as_ushort(__float2half_rn(acc[tb][0]));
-          p.Y[(size_t)m0 * p.N + n1] = __half_as_ushort(__float2half_rn(acc[tb][2]));
-        }
-        if (m1 < p.M) {
-          p.Y[(size_t)m1 * p.N + n0] = __half_as_ushort(__float2half_rn(acc[tb][1]));
-          p.Y[(size_t)m1 * p.N + n1] = __half_as_ushort(__float2half_rn(acc[tb][3]));
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) red[(((rq * 2 + mt) * NTB + tb) * 4 + e) * 32 + lane] = acc[mt][tb][e];
+    }
+    named_bar_sync(1, kWarps * 32);
+    if (kh == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((rq * 2 + mt) * NTB + tb) * 4 + e) * 32 + lane];
+    }
+    named_bar_sync(1, kWarps * 32);
+    if (kh == 1) return;
+    // 2. the four kh = 0 warps own the result
+    const int tile_u0 = t * p.Gk, tile_u1 = tile_u0 + p.Gk;
+    auto store = [&](float (&v)[2][NTB][4]) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int n0 = t * kTileN + rows[mt][0], n1 = t * kTileN + rows[mt][1];
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
+          if (m0 < p.M) {
+            p.Y[(size_t)m0 * p.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][0]));
+            p.Y[(size_t)m0 * p.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][2]));
+          }
+          if (m1 < p.M) {
+            p.Y[(size_t)m1 * p.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][1]));
+            p.Y[(size_t)m1 * p.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][3]));
+          }
         }
       }
-      return;
-    }
+    };
+    if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); return; }
     // split tile: publish the fp32 partial, the last contributor reduces in CTA order.
     const int slot = 2 * cta + (is_first_seg ? 0 : 1);
     float4* part = reinterpret_cast<float4*>(p.partials);
+    auto pidx = [&](int sl, int tb, int mt) { return ((((size_t)sl * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
 #pragma unroll
-    for (int tb = 0; tb < NTB; ++tb)
-      __stcg(&part[(((size_t)slot * NTB + tb) * kConsumerWarps + warp) * 32 + lane],
-             make_float4(acc[tb][0], acc[tb][1], acc[tb][2], acc[tb][3]));
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb)
+        __stcg(&part[pidx(slot, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
     __threadfence();
-    named_bar_sync(1, kConsumerWarps * 32);
+    named_bar_sync(2, 4 * 32);
     const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
     if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[t], 1) == c_last - c_first);
-    named_bar_sync(1, kConsumerWarps * 32);
+    named_bar_sync(2, 4 * 32);
     if (!s_last) return;
     __threadfence();
-    float sum[NTB][4];
+    float sum[2][NTB][4];
 #pragma unroll
-    for (int tb = 0; tb < NTB; ++tb) sum[tb][0] = sum[tb][1] = sum[tb][2] = sum[tb][3] = 0.f;
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb) sum[mt][tb][0] = sum[mt][tb][1] = sum[mt][tb][2] = sum[mt][tb][3] = 0.f;
     for (int c = c_first; c <= c_last; ++c) {
       const int sl = 2 * c + (unit_begin(c, p.U, p.G) >= tile_u0 ? 0 : 1);
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) {
-        const float4 v = __ldcg(&part[(((size_t)sl * NTB + tb) * kConsumerWarps + warp) * 32 + lane]);
-        sum[tb][0] += v.x; sum[tb][1] += v.y; sum[tb][2] += v.z; sum[tb][3] += v.w;
-      }
-    }
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int tb = 0; tb < NTB; ++tb) {
-      const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
-      if (m0 < p.M) {
-        p.Y[(size_t)m0 * p.N + n0] = __half_as_ushort(__float2half_rn(sum[tb][0]));
-        p.Y[(size_t)m0 * p.N + n1] = __half_as_ushort(__float2half_rn(sum[tb][2]));
-      }
-      if (m1 < p.M) {
-        p.Y[(size_t)m1 * p.N + n0] = __half_as_ushort(__float2half_rn(sum[tb][1]));
-        p.Y[(size_t)m1 * p.N + n1] = __half_as_ushort(__float2half_rn(sum[tb][3]));
-      }
+        for (int tb = 0; tb < NTB; ++tb) {
+          const float4 v = __ldcg(&part[pidx(sl, tb, mt)]);
+          sum[mt][tb][0] += v.x; sum[mt][tb][1] += v.y; sum[mt][tb][2] += v.z; sum[mt][tb][3] += v.w;
+        }
     }
+    store(sum);
     if (threadIdx.x == 0) p.counters[t] = 0;   // all contributors have arrived: safe to re-arm
   };
 
-  for (int u = u_begin; u < u_end; ++u) {
-    const int t = u / p.Gk, g = u - t * p.Gk;
-    if (t != cur_t) {
-      if (cur_t >= 0) { flush(cur_t, seg_first_unit, u, first_segment); first_segment = false; }
-      cur_t = t;
-      seg_first_unit = u;
-#pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0.f;
-    }
-    // Activations for this unit: lane needs X[m][128g + 32c4 .. +31] for m = 8tb + g8 (L1/L2 resident).
-    uint4 xr[NTB][4];
-#pragma unroll
-    for (int tb = 0; tb < NTB; ++tb) {
-      const int m = tb * 8 + g8;
-      if (m < p.M) {
-        const uint16_t* xp = p.X + (size_t)m * p.K + (size_t)g * kTileK + c4 * 32;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xr[tb][j] = ldg128_nc(xp + 8 * j);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xr[tb][j] = make_uint4(0, 0, 0, 0);
-      }
-    }
-    // Weights for this unit from shared memory.
+  const uint32_t inv16 = 0x2C002C00u;   // 1/16
+  for (int i = 0; i < n_stages; ++i) {
+    const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
     mbar_wait(&full_bar[s], ph);
-    const uint32_t st = smem_base + s * kStageBytes;
-    const uint4 wa = lds128(st + r0 * 64 + c4 * 16);
-    const uint4 wb = lds128(st + r1 * 64 + c4 * 16);
-    const uint16_t* ssc = reinterpret_cast<const uint16_t*>(smem + s * kStageBytes + kUnitWBytes);
-    const float sa = __half2float(__ushort_as_half(ssc[r0])), sb = __half2float(__ushort_as_half(ssc[r1]));
-    uint32_t za_lo, zb_lo, za_hi, zb_hi;  // {1024+z} for HSUB2 and {-(64+z)} for HFMA2, per row
-    if (SYM) {
-      za_lo = zb_lo = 0x64086408u;        // 1032
-      za_hi = zb_hi = 0xD480D480u;        // -72
-    } else {
-      const uint16_t* szr = ssc + kTileN;
-      const __half za = __ushort_as_half(szr[r0]), zb = __ushort_as_half(szr[r1]);
-      za_lo = h2_bcast(__half_as_ushort(__hadd(za, __float2half_rn(1024.f))));
-      zb_lo = h2_bcast(__half_as_ushort(__hadd(zb, __float2half_rn(1024.f))));
-      za_hi = h2_bcast(__half_as_ushort(__hneg(__hadd(za, __float2half_rn(64.f)))));
-      zb_hi = h2_bcast(__half_as_ushort(__hneg(__hadd(zb, __float2half_rn(64.f)))));
+    const uint32_t st = smem_base + s * C::kStage;
+    for (int j = 0; j < nu; ++j) {
+      const int u = u0 + j;
+      if (u == boundary || cur_t < 0) {
+        if (cur_t >= 0) { flush(cur_t, seg_u0, u, first_segment); first_segment = false; }
+        cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
+        boundary = (cur_t + 1) * p.Gk;
+        seg_u0 = u;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
+      }
+      const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
+      const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
+      float sc[2][2];
+      uint32_t zlo[2][2], zhi[2][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int r = rows[mt][hf];
+          sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+          if (SYM) {
+            zlo[mt][hf] = 0x64086408u;   // 1032
+            zhi[mt][hf] = 0xD480D480u;   // -72
+          } else {
+            const __half z = __ushort_as_half(lds16(ub + 8448 + 2 * r));
+            zlo[mt][hf] = h2_bcast(__half_as_ushort(__hadd(z, __float2half_rn(1024.f))));
+            zhi[mt][hf] = h2_bcast(__half_as_ushort(__hneg(__hadd(z, __float2half_rn(64.f)))));
+          }
+        }
+      float gacc[2][NTB][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int pch = 2 * kh + cc;                          // 32-k chunk of the unit: k 32 pch .. +31
+        // activations: lane needs X[8tb + g8][32 pch + 8 c4 .. +7] (one 16-byte SW128 chunk per token row)
+        uint4 xr[NTB];
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          const int m = 8 * tb + g8;
+          const int jx = 4 * (pch & 1) + c4;                  // 16-byte chunk within the 128-byte box row
+          xr[tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int ra = rows[mt][0], rb = rows[mt][1];
+          const uint32_t wa = lds32(ub + ra * 64 + ((pch ^ ((ra >> 1) & 3)) << 4) + 4 * c4);
+          const uint32_t wb = lds32(ub + rb * 64 + ((pch ^ ((rb >> 1) & 3)) << 4) + 4 * c4);
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs) {       // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
+            const uint32_t qa = hs ? wa >> 8 : wa, qb = hs ? wb >> 8 : wb;
+            const uint32_t a0 = hsub2_u32(lop3_mask_or(qa, 0x000F000Fu), zlo[mt][0]);
+            const uint32_t a1 = hsub2_u32(lop3_mask_or(qb, 0x000F000Fu), zlo[mt][1]);
+            const uint32_t a2 = hfma2_u32(lop3_mask_or(qa, 0x00F000F0u), inv16, zhi[mt][0]);
+            const uint32_t a3 = hfma2_u32(lop3_mask_or(qb, 0x00F000F0u), inv16, zhi[mt][1]);
+            // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
+            // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) {
+              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[tb]);
+              mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
+          acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
+          acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
+          acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
+        }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
-    if (++s == STAGES) { s = 0; ph ^= 1; }
-
-    float gacc[NTB][4];
-#pragma unroll
-    for (int tb = 0; tb < NTB; ++tb) gacc[tb][0] = gacc[tb][1] = gacc[tb][2] = gacc[tb][3] = 0.f;
-    const uint32_t inv16 = 0x2C002C00u;   // 1/16
-    const uint32_t wav[4] = {wa.x, wa.y, wa.z, wa.w}, wbv[4] = {wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {          // word j: k = 32c4 + 8j .. +7 (two MMA k-steps)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {        // h = 0: k pairs (0,1),(2,3); h = 1: (4,5),(6,7)
-        const uint32_t qa = h ? wav[j] >> 8 : wav[j], qb = h ? wbv[j] >> 8 : wbv[j];
-        const uint32_t a0 = hsub2_u32(lop3_mask_or(qa, 0x000F000Fu), za_lo);
-        const uint32_t a1 = hsub2_u32(lop3_mask_or(qb, 0x000F000Fu), zb_lo);
-        const uint32_t a2 = hfma2_u32(lop3_mask_or(qa, 0x00F000F0u), inv16, za_hi);
-        const uint32_t a3 = hfma2_u32(lop3_mask_or(qb, 0x00F000F0u), inv16, zb_hi);
-        // MMA k-step (j, h) uses physical k = 32c4 + 8j + 4h + {0..3}: logical {2c,2c+1} <- {0,1},
-        // {2c+8,2c+9} <- {2,3}; activations use the same permutation.
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[tb][j]);
-          mma_16816(gacc[tb], a0, a1, a2, a3, xv[2 * h], xv[2 * h + 1]);
-        }
-      }
-    }
-#pragma unroll
-    for (int tb = 0; tb < NTB; ++tb) {
-      acc[tb][0] = fmaf(sa, gacc[tb][0], acc[tb][0]);
-      acc[tb][1] = fmaf(sa, gacc[tb][1], acc[tb][1]);
-      acc[tb][2] = fmaf(sb, gacc[tb][2], acc[tb][2]);
-      acc[tb][3] = fmaf(sb, gacc[tb][3], acc[tb][3]);
-    }
+    if (++s == S) { s = 0; ph ^= 1; }
   }
-  if (cur_t >= 0) flush(cur_t, seg_first_unit, u_end, first_segment);
+  if (cur_t >= 0) flush(cur_t, seg_u0, u_end, first_segment);
 }
 
 template <int NTB, bool SYM>
-static int launch_t(const GemmParams& p, int stages_unused, cudaStream_t stream) {
-  (void)stages_unused;
-  constexpr int STAGES = 10;
-  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, STAGES>;
-  const int smem = STAGES * kStageBytes;
+static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream) {
+  using C = Cfg<NTB, SYM>;
+  CUtensorMap mapR, map1;
+  if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * kR)) return e;
+  if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
+  auto kern = gemm_w4a16_mma_kernel<NTB, SYM>;
   static bool attr_set = false;   // benign race: idempotent attribute
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return W4A16_ERR_CUDA;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
     attr_set = true;
   }
-  kern<<<p.G, kThreads, smem, stream>>>(p);
+  kern<<<p.G, kThreads, C::kSmem, stream>>>(mapR, map1, p);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
+}  // namespace ma
 }  // namespace w4
 
 // Plan (depends on K, N and the SM count only).
 extern "C" int w4a16_mma_plan_ctas(int K, int N, int num_sms) {
-  const long long U = (long long)(N / w4::kTileN) * (K / w4::kTileK);
+  const long long U = (long long)(N / w4::ma::kTileN) * (K / w4::ma::kTileK);
   long long G = 2LL * num_sms;
   if (G > U) G = U;
   return (int)G;
@@ -266,30 +348,26 @@ extern "C" int w4a16_mma_plan_ctas(int K, int N, int num_sms) {
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
   const int ntb = (M + 7) / 8;
   const int G = w4a16_mma_plan_ctas(K, N, num_sms);
-  const size_t counters = (((size_t)(N / w4::kTileN) * 4) + 255) / 256 * 256;
-  return counters + (size_t)2 * G * ntb * w4::kConsumerWarps * 32 * 16;
+  const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
+  return counters + (size_t)2 * G * 4 * ntb * 2 * 32 * 16;
 }
 
-extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const uint32_t* qweight, const uint16_t* scales,
-                                     const uint16_t* zeros, uint16_t* Y, int M, int K, int N, int mode, void* ws,
-                                     int num_sms, cudaStream_t stream) {
-  w4::GemmParams p;
-  p.X = X; p.qweight = qweight; p.scales = scales; p.zeros = zeros; p.Y = Y;
+extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
+                                     void* ws, int num_sms, cudaStream_t stream) {
+  w4::ma::GemmParams p;
+  p.packed = reinterpret_cast<const uint8_t*>(packed);
+  p.Y = Y;
   p.M = M; p.K = K; p.N = N;
-  p.Gk = K / w4::kTileK;
-  p.U = (N / w4::kTileN) * p.Gk;
+  p.Gk = K / w4::ma::kTileK;
+  p.U = (N / w4::ma::kTileN) * p.Gk;
   p.G = w4a16_mma_plan_ctas(K, N, num_sms);
-  const size_t counters = (((size_t)(N / w4::kTileN) * 4) + 255) / 256 * 256;
+  const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
-  const int ntb = (M + 7) / 8;
   const bool sym = mode == W4A16_SYM;
-#define W4_CASE(T)                                                              \
-  case T:                                                                       \
-    return sym ? w4::launch_t<T, true>(p, 0, stream) : w4::launch_t<T, false>(p, 0, stream);
-  switch (ntb) {
-    W4_CASE(1) W4_CASE(2) W4_CASE(3) W4_CASE(4) W4_CASE(5) W4_CASE(6) W4_CASE(7) W4_CASE(8)
-    default: return W4A16_ERR_SHAPE;
+  switch ((M + 7) / 8) {
+    case 1: return sym ? w4::ma::launch_t<1, true>(X, p, stream) : w4::ma::launch_t<1, false>(X, p, stream);
+    case 2: return sym ? w4::ma::launch_t<2, true>(X, p, stream) : w4::ma::launch_t<2, false>(X, p, stream);
+    default: return W4A16_ERR_SHAPE;   // family A serves M <= 16
   }
-#undef W4_CASE
 }

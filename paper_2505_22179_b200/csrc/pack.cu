@@ -16,9 +16,10 @@ __device__ __forceinline__ float clamp_lo_hi(float x, float lo, float hi) {
 }
 
 // One thread per (column n, group g); lanes of a warp take consecutive n, so every W read is coalesced.
+__host__ __device__ __forceinline__ size_t tile_bytes(int mode) { return mode == W4A16_ASYM ? 8704 : 8448; }
+
 __global__ void __launch_bounds__(256) pack_kernel(const uint16_t* __restrict__ W, int K, int N, int mode,
-                                                   uint32_t* __restrict__ qweight, uint16_t* __restrict__ scales,
-                                                   uint16_t* __restrict__ zeros, int32_t* __restrict__ dev_status) {
+                                                   uint8_t* __restrict__ packed, int32_t* __restrict__ dev_status) {
   const int groups = K / W4A16_GROUP;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)N * groups) return;
@@ -53,11 +54,13 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint16_t* __restrict__ 
     s32 = __half2float(s);
     z = 8.0f;
   }
-  scales[(size_t)g * N + n] = __half_as_ushort(s);
-  if (zeros) zeros[(size_t)g * N + n] = __half_as_ushort(__float2half_rn(z));
+  uint8_t* tile = packed + ((size_t)(n / 128) * groups + g) * tile_bytes(mode);
+  const int r = n % 128;
+  reinterpret_cast<uint16_t*>(tile + 8192)[r] = __half_as_ushort(s);
+  if (mode == W4A16_ASYM) reinterpret_cast<uint16_t*>(tile + 8448)[r] = __half_as_ushort(__float2half_rn(z));
 
-  // 3. codes, written as the 16 words of row (n % 128) of tile (n / 128, g)
-  uint32_t* dst = qweight + ((size_t)(n / 128) * groups + g) * 2048 + (size_t)(n % 128) * 16;
+  // 3. codes: chunk p (words 4p..4p+3 = k 32p..32p+31) of row r goes to chunk position p ^ ((r/2) % 4)
+  uint32_t* dst = reinterpret_cast<uint32_t*>(tile) + (size_t)r * 16;
   for (int j = 0; j < 16; j += 4) {
     uint32_t wq[4];
 #pragma unroll
@@ -72,24 +75,24 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint16_t* __restrict__ 
       }
       wq[jj] = word;
     }
-    *reinterpret_cast<uint4*>(dst + j) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+    *reinterpret_cast<uint4*>(dst + 4 * ((j / 4) ^ ((r >> 1) & 3))) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
   }
 }
 
 // One thread per (column n, word j of k); writes W_hat[8j + i][n], i = 0..7 (coalesced along n).
 // w_hat = (q - z) * s: q - z is exact in fp16, the multiply rounds once (RNE) -> fp16_rne((q - z) * s).
-__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ qweight,
-                                                     const uint16_t* __restrict__ scales,
-                                                     const uint16_t* __restrict__ zeros, int K, int N, int mode,
+__global__ void __launch_bounds__(256) unpack_kernel(const uint8_t* __restrict__ packed, int K, int N, int mode,
                                                      uint16_t* __restrict__ W_hat) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)N * (K / 8)) return;
   const int n = (int)(idx % N), kw = (int)(idx / N);
-  const int k0 = kw * 8, g = k0 / W4A16_GROUP;
-  const uint32_t word =
-      qweight[((size_t)(n / 128) * (K / 128) + g) * 2048 + (size_t)(n % 128) * 16 + (size_t)((k0 % 128) / 8)];
-  const __half s = __ushort_as_half(scales[(size_t)g * N + n]);
-  const __half z = mode == W4A16_SYM ? __float2half_rn(8.0f) : __ushort_as_half(zeros[(size_t)g * N + n]);
+  const int k0 = kw * 8, g = k0 / W4A16_GROUP, r = n % 128;
+  const uint8_t* tile = packed + ((size_t)(n / 128) * (K / 128) + g) * tile_bytes(mode);
+  const int p = (k0 % 128) / 32, w = (k0 % 32) / 8;
+  const uint32_t word = reinterpret_cast<const uint32_t*>(tile)[(size_t)r * 16 + 4 * (p ^ ((r >> 1) & 3)) + w];
+  const __half s = __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8192)[r]);
+  const __half z = mode == W4A16_SYM ? __float2half_rn(8.0f)
+                                     : __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8448)[r]);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int q = (word >> (4 * ((i % 2) * 4 + i / 2))) & 0xF;
@@ -100,19 +103,19 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict_
 
 }  // namespace w4
 
-extern "C" int w4a16_launch_pack(const uint16_t* W, int K, int N, int mode, uint32_t* qweight, uint16_t* scales,
-                                 uint16_t* zeros, int32_t* dev_status, cudaStream_t stream) {
+extern "C" int w4a16_launch_pack(const uint16_t* W, int K, int N, int mode, void* packed, int32_t* dev_status,
+                                 cudaStream_t stream) {
   const long long threads = (long long)N * (K / W4A16_GROUP);
   if (threads == 0) return W4A16_OK;
-  w4::pack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(W, K, N, mode, qweight, scales, zeros,
-                                                                          dev_status);
+  w4::pack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(W, K, N, mode,
+                                                                          reinterpret_cast<uint8_t*>(packed), dev_status);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
-extern "C" int w4a16_launch_unpack(const uint32_t* qweight, const uint16_t* scales, const uint16_t* zeros, int K,
-                                   int N, int mode, uint16_t* W_hat, cudaStream_t stream) {
+extern "C" int w4a16_launch_unpack(const void* packed, int K, int N, int mode, uint16_t* W_hat, cudaStream_t stream) {
   const long long threads = (long long)N * (K / 8);
   if (threads == 0) return W4A16_OK;
-  w4::unpack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(qweight, scales, zeros, K, N, mode, W_hat);
+  w4::unpack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(reinterpret_cast<const uint8_t*>(packed), K,
+                                                                            N, mode, W_hat);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }

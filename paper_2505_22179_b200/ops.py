@@ -36,24 +36,26 @@ def _ptr(t: Optional[torch.Tensor], dtype=None, name="tensor") -> Optional[int]:
     return t.data_ptr()
 
 
-def packed_shapes(K: int, N: int, group: int = W4A16_GROUP):
-    """(qweight words, scales shape, zeros shape) for a K x N weight."""
-    return (K * N // 8,), (K // group, N), (K // group, N)
+def w4a16_packed_bytes(K: int, N: int, mode=W4A16_ASYM, group=W4A16_GROUP) -> int:
+    n = int(lib.w4a16_packed_bytes(K, N, group, mode))
+    if n == 0:
+        raise W4A16Error(f"bad packed shape K={K} N={N} mode={mode} group={group}")
+    return n
 
 
-def w4a16_pack(W, qweight, scales, zeros, dev_status=None, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None):
+def w4a16_pack(W, packed, dev_status=None, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None):
     K, N = W.shape
-    st = lib.w4a16_pack(_ptr(W, torch.float16, "W"), K, N, group, mode, _ptr(qweight, torch.int32, "qweight"),
-                        _ptr(scales, torch.float16, "scales"), _ptr(zeros, torch.float16, "zeros"),
+    if packed.numel() * packed.element_size() < w4a16_packed_bytes(K, N, mode, group):
+        raise W4A16Error("packed buffer too small")
+    st = lib.w4a16_pack(_ptr(W, torch.float16, "W"), K, N, group, mode, _ptr(packed, None, "packed"),
                         _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     check(st, "w4a16_pack")
 
 
-def w4a16_unpack(qweight, scales, zeros, W_hat, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None):
+def w4a16_unpack(packed, W_hat, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None):
     K, N = W_hat.shape
-    st = lib.w4a16_unpack(_ptr(qweight, torch.int32, "qweight"), _ptr(scales, torch.float16, "scales"),
-                          _ptr(zeros, torch.float16, "zeros"), K, N, group, mode,
-                          _ptr(W_hat, torch.float16, "W_hat"), _stream(stream))
+    st = lib.w4a16_unpack(_ptr(packed, None, "packed"), K, N, group, mode, _ptr(W_hat, torch.float16, "W_hat"),
+                          _stream(stream))
     check(st, "w4a16_unpack")
 
 
@@ -72,16 +74,14 @@ def alloc_workspace(M_max: int, shapes, device=None) -> torch.Tensor:
     return torch.zeros(max(need, 256), dtype=torch.uint8, device=device or "cuda")
 
 
-def w4a16_gemm(X, qweight, scales, zeros, Y, workspace, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None,
-               family=W4A16_FAMILY_AUTO):
+def w4a16_gemm(X, packed, Y, workspace, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None, family=W4A16_FAMILY_AUTO):
     """Y = X . W_hat through w4a16_gemm (family AUTO) or w4a16_gemm_ex (explicit family)."""
     M, K = X.shape
     N = Y.shape[1]
     if Y.shape[0] != M:
         raise W4A16Error("Y must be [M, N]")
-    args = (_ptr(X, torch.float16, "X"), _ptr(qweight, torch.int32, "qweight"), _ptr(scales, torch.float16, "scales"),
-            _ptr(zeros, torch.float16, "zeros"), _ptr(Y, torch.float16, "Y"), M, K, N, group, mode,
-            _ptr(workspace, None, "workspace"), workspace.numel() * workspace.element_size())
+    args = (_ptr(X, torch.float16, "X"), _ptr(packed, None, "packed"), _ptr(Y, torch.float16, "Y"), M, K, N, group,
+            mode, _ptr(workspace, None, "workspace"), workspace.numel() * workspace.element_size())
     if family == W4A16_FAMILY_AUTO:
         st = lib.w4a16_gemm(*args, _stream(stream))
     else:
@@ -113,31 +113,24 @@ def w4a16_gemm_family(M: int, K: int, N: int) -> int:
 
 @dataclass
 class PackedLinear:
-    """A W4A16 linear layer resident in HBM: Y[M, N] = X[M, K] · W_hat[K, N]."""
+    """A W4A16 linear layer resident in HBM: Y[M, N] = X[M, K] · W_hat[K, N] (packed blob, include/w4a16.h)."""
     K: int
     N: int
     mode: int
-    qweight: torch.Tensor
-    scales: torch.Tensor
-    zeros: Optional[torch.Tensor]
+    packed: torch.Tensor
 
     @property
     def weight_bytes(self) -> int:
-        """Algorithmic bytes streamed per GEMM (codes + scales (+ zeros))."""
-        b = self.qweight.numel() * 4 + self.scales.numel() * 2
-        return b + (self.zeros.numel() * 2 if self.zeros is not None else 0)
+        """Algorithmic bytes streamed per GEMM (codes + scales (+ zeros)) = the blob size."""
+        return self.packed.numel() * self.packed.element_size()
 
     def __call__(self, X, Y, workspace, stream=None, family=W4A16_FAMILY_AUTO):
-        w4a16_gemm(X, self.qweight, self.scales, self.zeros, Y, workspace, self.mode, stream=stream, family=family)
+        w4a16_gemm(X, self.packed, Y, workspace, self.mode, stream=stream, family=family)
         return Y
 
 
 def pack_linear(W: torch.Tensor, mode=W4A16_ASYM, dev_status=None, stream=None) -> PackedLinear:
     K, N = W.shape
-    qshape, sshape, zshape = packed_shapes(K, N)
-    dev = W.device
-    qweight = torch.empty(qshape, dtype=torch.int32, device=dev)
-    scales = torch.empty(sshape, dtype=torch.float16, device=dev)
-    zeros = torch.empty(zshape, dtype=torch.float16, device=dev) if mode == W4A16_ASYM else None
-    w4a16_pack(W, qweight, scales, zeros, dev_status, mode, stream=stream)
-    return PackedLinear(K, N, mode, qweight, scales, zeros)
+    packed = torch.empty(w4a16_packed_bytes(K, N, mode), dtype=torch.uint8, device=W.device)
+    w4a16_pack(W, packed, dev_status, mode, stream=stream)
+    return PackedLinear(K, N, mode, packed)

@@ -44,19 +44,23 @@ def test_status_strings():
 def test_host_validation_before_any_cuda_call():
     from paper_2505_22179_b200._lib import lib
     A = 0x10000  # a 16-byte-aligned fake device address: validation must reject before dereferencing
-    # w4a16_gemm(X, qw, sc, ze, Y, M, K, N, group, mode, ws, ws_bytes, stream)
-    assert lib.w4a16_gemm(None, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1
-    assert lib.w4a16_gemm(A, A, A, None, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1   # ASYM needs zeros
-    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 64, 0, A, 1 << 20, None) == -1       # group must be 128
-    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4000, 4096, 128, 0, A, 1 << 20, None) == -2
-    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4100, 128, 0, A, 1 << 20, None) == -2
-    assert lib.w4a16_gemm(A, A, A, A, A, 0, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
-    assert lib.w4a16_gemm(A, A, A, A, A, 65, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
-    assert lib.w4a16_gemm(A + 2, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -3
-    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 128, 7, A, 1 << 20, None) == -1     # bad mode
-    assert lib.w4a16_pack(A, 4096, 4096, 128, 0, A, A, None, None, None) == -1
-    assert lib.w4a16_pack(A, 100, 4096, 128, 0, A, A, A, None, None) == -2
-    assert lib.w4a16_unpack(A, A, A, 4096, 4096, 128, 1, A + 8, None) == -3
+    # w4a16_gemm(X, packed, Y, M, K, N, group, mode, ws, ws_bytes, stream)
+    assert lib.w4a16_gemm(None, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1
+    assert lib.w4a16_gemm(A, None, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -1
+    assert lib.w4a16_gemm(A, A, A, 8, 4096, 4096, 64, 0, A, 1 << 20, None) == -1       # group must be 128
+    assert lib.w4a16_gemm(A, A, A, 8, 4000, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, 8, 4096, 4100, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, 0, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A, A, A, 65, 4096, 4096, 128, 0, A, 1 << 20, None) == -2
+    assert lib.w4a16_gemm(A + 2, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, None) == -3
+    assert lib.w4a16_gemm(A, A, A, 8, 4096, 4096, 128, 7, A, 1 << 20, None) == -1     # bad mode
+    assert lib.w4a16_gemm_ex(A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 20, 5, None) in (-1, -5)  # bad family
+    assert lib.w4a16_pack(A, 4096, 4096, 128, 0, None, None, None) == -1
+    assert lib.w4a16_pack(A, 100, 4096, 128, 0, A, None, None) == -2
+    assert lib.w4a16_unpack(A, 4096, 4096, 128, 1, A + 8, None) == -3
+    assert lib.w4a16_packed_bytes(4096, 4096, 128, 0) == 32 * 32 * 8704
+    assert lib.w4a16_packed_bytes(4096, 4096, 128, 1) == 32 * 32 * 8448
+    assert lib.w4a16_packed_bytes(4096, 4000, 128, 0) == 0
     assert lib.verify_accept(A, A, A, 0, A, None) == -2
     assert lib.verify_accept(A, A, A, 1025, A, None) == -2
     assert lib.verify_accept(None, A, A, 8, A, None) == -1
@@ -68,7 +72,7 @@ def test_no_cpu_fallback_without_gpu():
     # valid arguments on a machine without a GPU: the library reports a CUDA failure, it never computes on CPU
     from paper_2505_22179_b200._lib import lib
     A = 0x10000
-    assert lib.w4a16_gemm(A, A, A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 30, None) == -5
+    assert lib.w4a16_gemm(A, A, A, 8, 4096, 4096, 128, 0, A, 1 << 30, None) == -5
     assert lib.w4a16_gemm_workspace_bytes(8, 4096, 4096, 128) == 0
 
 

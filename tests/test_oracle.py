@@ -92,12 +92,13 @@ def test_nibble_order_golden():
     lines = [l.split() for l in open(os.path.join(GOLD, "nibble_order.txt")) if l.strip() and not l.startswith("#")]
     K = N = 128
     W = hand_group(K, N)  # column 0: q = k mod 16
-    qw, sc, ze, st = oracle.pack(W)
+    packed, codes_all, sc, ze, st = oracle.pack(W)
     for j, (codes, canon, phys) in enumerate(lines):
         codes = [int(c) for c in codes.split(",")]
-        assert [int(oracle.get_code(qw, K, N, 8 * j + i, 0)) for i in range(8)] == codes
+        assert [int(codes_all[8 * j + i, 0]) for i in range(8)] == codes
         assert sum(c << (4 * i) for i, c in enumerate(codes)) == int(canon, 16)
-        word = int(qw[oracle.word_index(K, N, 8 * j, 0)])
+        off = oracle.code_word_offset(K, N, 8 * j, 0)
+        word = int.from_bytes(packed[off:off + 4].tobytes(), "little")
         assert word == int(phys, 16)
         # the LOP3 extraction the kernels use yields the consecutive-k pair in the two halves
         pair = word & 0x000F000F
@@ -106,15 +107,45 @@ def test_nibble_order_golden():
         assert (pair & 0xFFFF, pair >> 16) == (codes[4], codes[5])
 
 
-def test_layout_tiles_are_n_major_contiguous():
+@pytest.mark.parametrize("mode,TB", [(oracle.ASYM, 8704), (oracle.SYM, 8448)])
+def test_layout_tiles_are_n_major_contiguous(mode, TB):
     K, N = 384, 256
-    assert oracle.word_index(K, N, 0, 0) == 0
-    assert oracle.word_index(K, N, 8, 0) == 1
-    assert oracle.word_index(K, N, 0, 1) == 16
-    assert oracle.word_index(K, N, 128, 0) == 2048          # next k-group, same n-tile
-    assert oracle.word_index(K, N, 0, 128) == 3 * 2048      # next n-tile after K/128 groups
-    idx = {oracle.word_index(K, N, k, n) for k in range(0, K, 8) for n in range(N)}
-    assert idx == set(range(K * N // 8))                     # a bijection onto the buffer
+    off = lambda k, n: oracle.code_word_offset(K, N, k, n, mode)  # noqa: E731
+    assert off(0, 0) == 0 and off(8, 0) == 4 and off(0, 1) == 64
+    assert off(32, 0) == 16 and off(32, 2) == 2 * 64 + 0 and off(0, 2) == 2 * 64 + 16   # chunk XOR (r/2)%4
+    assert off(96, 7) == 7 * 64 + 16 * (3 ^ 3) and off(64, 5) == 5 * 64 + 16 * (2 ^ 2)
+    assert off(128, 0) == TB                                  # next k-group, same n-tile
+    assert off(0, 128) == 3 * TB                              # next n-tile after K/128 groups
+    assert oracle.packed_bytes(K, N, mode) == 6 * TB
+    # the 16-byte chunks a warp of 8 consecutive rows reads for one k-range hit 8 distinct bank groups
+    for p4 in range(4):
+        groups = {(off(32 * p4, r) % 128) // 16 for r in range(8)}
+        assert len(groups) == 8
+    # code words cover exactly the first 8192 bytes of every tile (a bijection)
+    words = {off(k, n) for k in range(0, K, 8) for n in range(N)}
+    expect = {t * TB + b for t in range(6) for b in range(0, 8192, 4)}
+    assert words == expect
+
+
+@pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
+def test_layout_scales_zeros_placement_and_roundtrip(mode):
+    K, N = 256, 384
+    W = synth.host(4, 5, synth.WEIGHT, K, N)
+    codes, sc, ze, st = oracle.quantize(W, 128, mode)
+    packed = oracle.layout_pack(codes, sc, ze, mode)
+    TB = 8704 if mode == oracle.ASYM else 8448
+    for g in range(K // 128):
+        for n in (0, 1, 127, 128, 200, 383):
+            t = (n // 128) * (K // 128) + g
+            b = packed[t * TB + 8192 + 2 * (n % 128): t * TB + 8194 + 2 * (n % 128)]
+            assert int.from_bytes(b.tobytes(), "little") == int(sc[g, n])
+            if mode == oracle.ASYM:
+                b = packed[t * TB + 8448 + 2 * (n % 128): t * TB + 8450 + 2 * (n % 128)]
+                assert int.from_bytes(b.tobytes(), "little") == int(ze[g, n])
+    c2, s2, z2 = oracle.layout_unpack(packed, K, N, mode)
+    assert np.array_equal(c2, codes) and np.array_equal(s2, sc)
+    if mode == oracle.ASYM:
+        assert np.array_equal(z2, ze)
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -123,15 +154,14 @@ def test_layout_tiles_are_n_major_contiguous():
 @pytest.mark.parametrize("K,N", [(128, 128), (256, 384)])
 def test_pack_hand_group_exact_roundtrip(K, N):
     W = hand_group(K, N)
-    qw, sc, ze, st = oracle.pack(W)
+    codes, sc, ze, st = oracle.quantize(W)
     assert st == oracle.DEV_OK
     n = np.arange(N)
     assert np.array_equal(sc.view(np.float16).astype(np.float64), np.broadcast_to(2.0 ** (-(3 + n % 4)), sc.shape))
     assert np.all(ze.view(np.float16) == 4)
-    for k in range(0, K, 37):
-        for nn in range(0, N, 11):
-            assert oracle.get_code(qw, K, N, k, nn) == (k + nn) % 16
-    Wh = oracle.unpack(qw, sc, ze, K, N)
+    k = np.arange(K)[:, None]
+    assert np.array_equal(codes, ((k + n[None, :]) % 16).astype(np.uint8))
+    Wh = oracle.dequantize(codes, sc, ze)
     assert np.array_equal(Wh, W.view(np.uint16))
 
 
@@ -141,10 +171,10 @@ def test_pack_spec_example_sym():
     K, N = 128, 128
     W = np.zeros((K, N), dtype=np.float16)
     W[:4, 0] = w
-    qw, sc, ze, st = oracle.pack(W, group=4, mode=oracle.SYM)
+    codes, sc, ze, st = oracle.quantize(W, group=4, mode=oracle.SYM)
     assert int(sc[0, 0]) == int(g["scale_bits"][0][0], 16)
-    assert [oracle.get_code(qw, K, N, k, 0) for k in range(4)] == [int(c) for c in g["codes"][0]]
-    Wh = oracle.unpack(qw, sc, ze, K, N, group=4, mode=oracle.SYM).view(np.float16)
+    assert [int(codes[k, 0]) for k in range(4)] == [int(c) for c in g["codes"][0]]
+    Wh = oracle.dequantize(codes, sc, ze, group=4, mode=oracle.SYM).view(np.float16)
     assert [float(x) for x in Wh[:4, 0]] == [float(x) for x in g["w_hat"][0]]
 
 
@@ -152,12 +182,12 @@ def test_pack_spec_example_sym():
 def test_pack_all_zero_group(mode):
     # reading R15 (GPTQ): an all-zero group gets the range (-1, 1): s = fp16(2/15), q = z = 8, w_hat = 0
     W = np.zeros((128, 128), dtype=np.float16)
-    qw, sc, ze, st = oracle.pack(W, mode=mode)
+    codes, sc, ze, st = oracle.quantize(W, mode=mode)
     assert np.all(sc == 0x3044)
-    assert all(oracle.get_code(qw, 128, 128, k, n) == 8 for k in range(0, 128, 7) for n in range(0, 128, 5))
+    assert np.all(codes == 8)
     if mode == oracle.ASYM:
         assert np.all(ze.view(np.float16) == 8)
-    assert np.all(oracle.unpack(qw, sc, ze, 128, 128, mode=mode) == 0)
+    assert np.all(oracle.dequantize(codes, sc, ze, mode=mode) == 0)
 
 
 def test_pack_nonfinite_flags_status_and_counts_as_zero():
@@ -165,19 +195,19 @@ def test_pack_nonfinite_flags_status_and_counts_as_zero():
     W2 = W.copy()
     W2[5, 3] = np.inf
     W2[6, 3] = np.nan
-    qw, sc, ze, st = oracle.pack(W2)
+    qw, sc, ze, st = oracle.quantize(W2)
     assert st == oracle.DEV_NONFINITE
     W3 = W.copy()
     W3[5, 3] = 0
     W3[6, 3] = 0
-    qw3, sc3, ze3, st3 = oracle.pack(W3)
+    qw3, sc3, ze3, st3 = oracle.quantize(W3)
     assert st3 == oracle.DEV_OK
     assert np.array_equal(qw, qw3) and np.array_equal(sc, sc3) and np.array_equal(ze, ze3)
 
 
 def test_pack_nonneg_group_zero_point_is_plus_zero():
     W = np.abs(hand_group(128, 128))
-    qw, sc, ze, st = oracle.pack(W)
+    qw, sc, ze, st = oracle.quantize(W)
     assert np.all(ze == 0)          # fp16 +0, never 0x8000
 
 
@@ -187,8 +217,8 @@ def test_pack_error_bound_and_zero_exact(mode):
     K, N = 512, 256
     W = synth.host(7, 3, synth.WEIGHT, K, N).view(np.float16)
     W[::17, ::13] = 0.0
-    qw, sc, ze, st = oracle.pack(W, mode=mode)
-    Wh = oracle.unpack(qw, sc, ze, K, N, mode=mode).view(np.float16).astype(np.float64)
+    qw, sc, ze, st = oracle.quantize(W, mode=mode)
+    Wh = oracle.dequantize(qw, sc, ze, mode=mode).view(np.float16).astype(np.float64)
     w = W.astype(np.float64)
     s = np.repeat(sc.view(np.float16).astype(np.float64), 128, axis=0)
     bound = s * (0.5 + 15 * 2.0 ** -11 + 1e-6) + np.abs(Wh) * 2.0 ** -11 + 2.0 ** -25
@@ -203,9 +233,9 @@ def test_pack_error_bound_and_zero_exact(mode):
 def test_pack_sym_zero_is_eight_and_range_centered():
     K, N = 256, 128
     W = synth.host(3, 9, synth.WEIGHT, K, N)
-    qw, sc, ze, st = oracle.pack(W, mode=oracle.SYM)
+    qw, sc, ze, st = oracle.quantize(W, mode=oracle.SYM)
     assert ze is None
-    Wh = oracle.unpack(qw, sc, None, K, N, mode=oracle.SYM).view(np.float16).astype(np.float64)
+    Wh = oracle.dequantize(qw, sc, None, mode=oracle.SYM).view(np.float16).astype(np.float64)
     s = sc.view(np.float16).astype(np.float64)
     # every dequantised value is an integer multiple of its scale in [-8, 7]
     r = Wh / np.repeat(s, 128, axis=0)
@@ -220,9 +250,9 @@ def test_gemm_ones_closed_form():
     # X = ones, hand group, K = 4096: Y[n] = s_n * sum_k ((k+n)%16 - 4) = s_n * 256 * (120 - 64) = 14336 s_n
     K, N = 4096, 256
     W = hand_group(K, N)
-    qw, sc, ze, st = oracle.pack(W)
+    qw, sc, ze, st = oracle.quantize(W)
     X = np.ones((2, K), dtype=np.float16)
-    Y = oracle.gemm(X, qw, sc, ze, K, N, nthreads=4)
+    Y = oracle.gemm(X, qw, sc, ze, nthreads=4)
     n = np.arange(N)
     exp = 14336.0 * 2.0 ** (-(3 + n % 4))
     assert np.array_equal(Y[0], exp) and np.array_equal(Y[1], exp)
@@ -232,13 +262,13 @@ def test_gemm_ones_closed_form():
 def test_gemm_one_hot_rows_select_dequantised_weights():
     K, N = 512, 256
     W = synth.host(5, 1, synth.WEIGHT, K, N)
-    qw, sc, ze, st = oracle.pack(W)
-    Wh = oracle.unpack(qw, sc, ze, K, N).view(np.float16).astype(np.float64)
+    qw, sc, ze, st = oracle.quantize(W)
+    Wh = oracle.dequantize(qw, sc, ze).view(np.float16).astype(np.float64)
     ks = [0, 1, 7, 8, 127, 128, 300, 511]
     X = np.zeros((len(ks), K), dtype=np.float16)
     for m, k in enumerate(ks):
         X[m, k] = 1.0
-    Y = oracle.gemm(X, qw, sc, ze, K, N)
+    Y = oracle.gemm(X, qw, sc, ze)
     assert np.array_equal(Y, Wh[ks])
 
 
@@ -247,15 +277,15 @@ def test_gemm_matches_numpy_float64(mode):
     K, N, M = 640, 384, 5
     W = synth.host(11, 2, synth.WEIGHT, K, N)
     X = synth.host(11, 3, synth.ACT, M, K)
-    qw, sc, ze, st = oracle.pack(W, mode=mode)
-    Wh = oracle.unpack(qw, sc, ze, K, N, mode=mode).view(np.float16).astype(np.float64)
+    qw, sc, ze, st = oracle.quantize(W, mode=mode)
+    Wh = oracle.dequantize(qw, sc, ze, mode=mode).view(np.float16).astype(np.float64)
     ref = X.view(np.float16).astype(np.float64) @ Wh
-    Y1 = oracle.gemm(X, qw, sc, ze, K, N, mode=mode, nthreads=1)
-    Y3 = oracle.gemm(X, qw, sc, ze, K, N, mode=mode, nthreads=3)
+    Y1 = oracle.gemm(X, qw, sc, ze, mode=mode, nthreads=1)
+    Y3 = oracle.gemm(X, qw, sc, ze, mode=mode, nthreads=3)
     assert np.array_equal(Y1, Y3)                          # thread count never changes the result
     assert np.allclose(Y1, ref, rtol=1e-12, atol=1e-12)
     cols = np.array([0, 5, 127, 128, 383])
-    assert np.array_equal(oracle.gemm_cols(X, qw, sc, ze, K, N, cols, mode=mode), Y1[:, cols])
+    assert np.array_equal(oracle.gemm_cols(X, qw, sc, ze, cols, mode=mode), Y1[:, cols])
 
 
 def test_gemm_transposition_sensitive():
@@ -263,9 +293,9 @@ def test_gemm_transposition_sensitive():
     K, N = 256, 256
     W = synth.host(2, 2, synth.WEIGHT, K, N)
     X = synth.host(2, 4, synth.ACT, 3, K)
-    qw, sc, ze, st = oracle.pack(W)
-    Wh = oracle.unpack(qw, sc, ze, K, N).view(np.float16).astype(np.float64)
-    Y = oracle.gemm(X, qw, sc, ze, K, N)
+    qw, sc, ze, st = oracle.quantize(W)
+    Wh = oracle.dequantize(qw, sc, ze).view(np.float16).astype(np.float64)
+    Y = oracle.gemm(X, qw, sc, ze)
     Xd = X.view(np.float16).astype(np.float64)
     assert not np.allclose(Y, Xd @ Wh.T)
     assert np.allclose(Y, Xd @ Wh)
