@@ -31,8 +31,9 @@
  *                          of ((word >> 4) & 0x000F000F) those of 8w+2, 8w+3, and so on.
  *                          Canonical logical order is SPEC's "low nibble first" along k;
  *                          example: codes 0..7 of one word are 0x76543210 canonical, 0x75316420 physical.
- *     bytes [8192, 8448):  fp16 scale s of row r at 8192 + 2r.
- *     bytes [8448, 8704):  ASYM only: fp16 zero point z (an integer in [0,15]) of row r at 8448 + 2r.
+ *     bytes [8192, ...):   per row r, the fp16 scale s and (ASYM) the fp16 zero point z (an integer in
+ *                          [0,15]) side by side, so one 32-bit load fetches both: ASYM {s, z} at 8192 + 4r
+ *                          (bytes [8192, 8704)); SYM s at 8192 + 2r (bytes [8192, 8448)).
  *   Codes, scale and zero of a 128x128 tile are adjacent, so a CTA that owns a run of tiles streams one
  *   contiguous byte range. A column shard (n range, multiple of 128) is a contiguous
  *   sub-range of whole tiles. SYM mode: z == 8 and no zero bytes are stored.

@@ -193,7 +193,8 @@ int orc_gemm_cols(const uint16_t* X, const uint8_t* codes, const uint16_t* scale
  * The ABI's packed blob (include/w4a16.h): 128x128 tiles, n-tile major then k-group; per tile 8192 code
  * bytes (row r: 64 bytes at r*64 = four 16-byte chunks, chunk p = k 32p..32p+31 stored at chunk position
  * p XOR ((r/2) % 4); word w of a chunk: k = 32p + 8w .. +7, local index i in nibble slot (i%2)*4 + i/2),
- * then 128 fp16 scales, then (ASYM) 128 fp16 zeros. Integers are little-endian.
+ * then per row r the fp16 scale and (ASYM) fp16 zero side by side: ASYM {s, z} at 8192 + 4r, SYM s at
+ * 8192 + 2r. Integers are little-endian.
  * ---------------------------------------------------------------------------------------------------- */
 static int layout_ok(int K, int N) { return K > 0 && N > 0 && K % 128 == 0 && N % 128 == 0; }
 static size_t tile_bytes(int mode) { return mode == ORC_ASYM ? 8704 : 8448; }
@@ -233,8 +234,12 @@ int orc_layout_pack(const uint8_t* codes, const uint16_t* scales, const uint16_t
   for (int g = 0; g < K / 128; ++g)
     for (int n = 0; n < N; ++n) {
       uint8_t* t = packed + tile_offset(K, mode, 128 * g, n);
-      wr16(t + 8192 + 2 * (n % 128), scales[(size_t)g * N + n]);
-      if (mode == ORC_ASYM) wr16(t + 8448 + 2 * (n % 128), zeros[(size_t)g * N + n]);
+      if (mode == ORC_ASYM) {
+        wr16(t + 8192 + 4 * (n % 128), scales[(size_t)g * N + n]);
+        wr16(t + 8192 + 4 * (n % 128) + 2, zeros[(size_t)g * N + n]);
+      } else {
+        wr16(t + 8192 + 2 * (n % 128), scales[(size_t)g * N + n]);
+      }
     }
   return 0;
 }
@@ -250,8 +255,13 @@ int orc_layout_unpack(const uint8_t* packed, int K, int N, int mode, uint8_t* co
   for (int g = 0; g < K / 128; ++g)
     for (int n = 0; n < N; ++n) {
       const uint8_t* t = packed + tile_offset(K, mode, 128 * g, n);
-      scales[(size_t)g * N + n] = rd16(t + 8192 + 2 * (n % 128));
-      if (zeros) zeros[(size_t)g * N + n] = mode == ORC_ASYM ? rd16(t + 8448 + 2 * (n % 128)) : 0x4800; /* 8.0 */
+      if (mode == ORC_ASYM) {
+        scales[(size_t)g * N + n] = rd16(t + 8192 + 4 * (n % 128));
+        if (zeros) zeros[(size_t)g * N + n] = rd16(t + 8192 + 4 * (n % 128) + 2);
+      } else {
+        scales[(size_t)g * N + n] = rd16(t + 8192 + 2 * (n % 128));
+        if (zeros) zeros[(size_t)g * N + n] = 0x4800; /* 8.0 */
+      }
     }
   return 0;
 }

@@ -22,8 +22,8 @@
  *   (t*(K/128) + g) * TB with TB = 8704 (ASYM) or 8448 (SYM). Inside a tile: bytes [0, 8192) hold codes,
  *   row r = n%128 owns the 64 bytes at r*64, four 16-byte chunks; chunk p (k = 128g + 32p .. +31) sits at
  *   byte r*64 + 16*(p XOR ((r/2) % 4)); inside a chunk, little-endian 32-bit word w holds k = 32p + 8w + i,
- *   i = 0..7, in nibble slot (i%2)*4 + i/2. Bytes [8192, 8448): fp16 scale of row r at 8192 + 2r.
- *   ASYM only: bytes [8448, 8704): fp16 zero of row r at 8448 + 2r.
+ *   i = 0..7, in nibble slot (i%2)*4 + i/2. Then per row r: ASYM: fp16 scale at 8192 + 4r and fp16 zero at
+ *   8192 + 4r + 2 (bytes [8192, 8704)); SYM: fp16 scale at 8192 + 2r (bytes [8192, 8448)).
  */
 #ifndef W4A16_ORACLE_H
 #define W4A16_ORACLE_H

@@ -101,6 +101,19 @@ __device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {
   return r;
 }
 __device__ __forceinline__ uint32_t h2_bcast(uint16_t h) { return (uint32_t)h | ((uint32_t)h << 16); }
+__device__ __forceinline__ __half2 u2h2(uint32_t x) { return *reinterpret_cast<const __half2*>(&x); }
+__device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+
+// Zero-point magic pair for a row: {64 + z, 1024 + z} (exact). With v = (w & 0x000F000F) | 0x64006400 the
+// exact (q - z) pair is v - zp.hi; with v = (w & 0x00F000F0) | 0x64006400 it is v / 16 - zp.lo. Written
+// with half2 intrinsics so ptxas folds the half broadcasts and the negation into operand modifiers.
+__device__ __forceinline__ __half2 zero_pair(__half z) { return __hadd2(__half2half2(z), __floats2half2_rn(64.f, 1024.f)); }
+__device__ __forceinline__ uint32_t dq_lo(uint32_t w, __half2 zp) {
+  return h22u(__hsub2(u2h2(lop3_mask_or(w, 0x000F000Fu)), __high2half2(zp)));
+}
+__device__ __forceinline__ uint32_t dq_hi(uint32_t w, __half2 zp) {
+  return h22u(__hfma2(u2h2(lop3_mask_or(w, 0x00F000F0u)), __float2half2_rn(0.0625f), __hneg2(__low2half2(zp))));
+}
 
 // D = A(16x16, row) * B(16x8, col) + C, fp16 inputs, fp32 accumulate (legacy tensor path, SASS HMMA).
 __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,

@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
     if (threadIdx.x == 0) p.counters[t] = 0;   // all contributors have arrived: safe to re-arm
   };
 
-  const uint32_t inv16 = 0x2C002C00u;   // 1/16
   for (int i = 0; i < n_stages; ++i) {
     const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
     mbar_wait(&full_bar[s], ph);
@@ -247,20 +246,19 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
       const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
       const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
       float sc[2][2];
-      uint32_t zlo[2][2], zhi[2][2];
+      __half2 zp[2][2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const int r = rows[mt][hf];
-          sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
           if (SYM) {
-            zlo[mt][hf] = 0x64086408u;   // 1032
-            zhi[mt][hf] = 0xD480D480u;   // -72
+            sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
           } else {
-            const __half z = __ushort_as_half(lds16(ub + 8448 + 2 * r));
-            zlo[mt][hf] = h2_bcast(__half_as_ushort(__hadd(z, __float2half_rn(1024.f))));
-            zhi[mt][hf] = h2_bcast(__half_as_ushort(__hneg(__hadd(z, __float2half_rn(64.f)))));
+            const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
+            sc[mt][hf] = __low2float(sz);
+            zp[mt][hf] = zero_pair(__high2half(sz));
           }
         }
       float gacc[2][NTB][4];
@@ -287,10 +285,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
 #pragma unroll
           for (int hs = 0; hs < 2; ++hs) {       // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
             const uint32_t qa = hs ? wa >> 8 : wa, qb = hs ? wb >> 8 : wb;
-            const uint32_t a0 = hsub2_u32(lop3_mask_or(qa, 0x000F000Fu), zlo[mt][0]);
-            const uint32_t a1 = hsub2_u32(lop3_mask_or(qb, 0x000F000Fu), zlo[mt][1]);
-            const uint32_t a2 = hfma2_u32(lop3_mask_or(qa, 0x00F000F0u), inv16, zhi[mt][0]);
-            const uint32_t a3 = hfma2_u32(lop3_mask_or(qb, 0x00F000F0u), inv16, zhi[mt][1]);
+            const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
+            const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
             // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
             // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
 #pragma unroll

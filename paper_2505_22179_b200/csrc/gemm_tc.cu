@@ -154,6 +154,11 @@ __device__ __forceinline__ uint16_t lds16(uint32_t addr) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B: SBO = 1024 B (8 rows x 128 B), LBO unused (1),
 // version 1 (sm_100), layout type 2. The start address (bits 0-13, >>4) is added by the caller.
 constexpr uint64_t kDescSW128 = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
@@ -340,7 +345,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       if (threadIdx.x == 0) p.counters[t] = 0;
     };
 
-    const uint32_t inv16 = 0x2C002C00u;  // 1/16
     int pend_t[kAU], pend_u0[kAU], pend_u1[kAU], pend_idx[kAU];
     for (int i = 0; i < n_stages; ++i) {
       const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
@@ -365,25 +369,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
           const uint32_t ub = st + j * C::kTB;
           // chunk h of this row (XOR-permuted layout: conflict-free across the warp's 32 rows)
           const uint4 wq = lds128(ub + row * 64 + ((h ^ ((row >> 1) & 3)) << 4));
-          const uint32_t s2 = h2_bcast(lds16(ub + 8192 + 2 * row));
-          uint32_t zlo, zhi;
+          __half2 sz, zp;   // {s, z} of this row, and its zero-point magic pair
           if (SYM) {
-            zlo = 0x64086408u;  // 1032
-            zhi = 0xD480D480u;  // -72
+            sz = __half2half2(__ushort_as_half(lds16(ub + 8192 + 2 * row)));
+            zp = __floats2half2_rn(72.f, 1032.f);   // z = 8
           } else {
-            const __half z = __ushort_as_half(lds16(ub + 8448 + 2 * row));
-            zlo = h2_bcast(__half_as_ushort(__hadd(z, __float2half_rn(1024.f))));
-            zhi = h2_bcast(__half_as_ushort(__hneg(__hadd(z, __float2half_rn(64.f)))));
+            sz = u2h2(lds32(ub + 8192 + 4 * row));
+            zp = zero_pair(__high2half(sz));
           }
+          const __half2 s2 = __low2half2(sz);
           const uint32_t wv[4] = {wq.x, wq.y, wq.z, wq.w};
           uint32_t av[16];
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const uint32_t w = wv[jj], w8 = w >> 8;
-            av[4 * jj + 0] = hmul2_u32(hsub2_u32(lop3_mask_or(w, 0x000F000Fu), zlo), s2);          // k 8jj+0, +1
-            av[4 * jj + 1] = hmul2_u32(hfma2_u32(lop3_mask_or(w, 0x00F000F0u), inv16, zhi), s2);   // k 8jj+2, +3
-            av[4 * jj + 2] = hmul2_u32(hsub2_u32(lop3_mask_or(w8, 0x000F000Fu), zlo), s2);         // k 8jj+4, +5
-            av[4 * jj + 3] = hmul2_u32(hfma2_u32(lop3_mask_or(w8, 0x00F000F0u), inv16, zhi), s2);  // k 8jj+6, +7
+            // exact (q - z) pairs, then one RNE multiply by s: exactly the oracle's w_hat = fp16((q - z) * s)
+            av[4 * jj + 0] = h22u(__hmul2(u2h2(dq_lo(w, zp)), s2));    // k 8jj+0, +1
+            av[4 * jj + 1] = h22u(__hmul2(u2h2(dq_hi(w, zp)), s2));    // k 8jj+2, +3
+            av[4 * jj + 2] = h22u(__hmul2(u2h2(dq_lo(w8, zp)), s2));   // k 8jj+4, +5
+            av[4 * jj + 3] = h22u(__hmul2(u2h2(dq_hi(w8, zp)), s2));   // k 8jj+6, +7
           }
           tmem_st_x16(tmem + lane_base + b * (kAU * 64) + (j - ja) * 64 + h * 16, av);
         }

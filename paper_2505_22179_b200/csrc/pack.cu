@@ -56,8 +56,12 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint16_t* __restrict__ 
   }
   uint8_t* tile = packed + ((size_t)(n / 128) * groups + g) * tile_bytes(mode);
   const int r = n % 128;
-  reinterpret_cast<uint16_t*>(tile + 8192)[r] = __half_as_ushort(s);
-  if (mode == W4A16_ASYM) reinterpret_cast<uint16_t*>(tile + 8448)[r] = __half_as_ushort(__float2half_rn(z));
+  if (mode == W4A16_ASYM) {
+    reinterpret_cast<uint32_t*>(tile + 8192)[r] =
+        (uint32_t)__half_as_ushort(s) | ((uint32_t)__half_as_ushort(__float2half_rn(z)) << 16);   // {s, z}
+  } else {
+    reinterpret_cast<uint16_t*>(tile + 8192)[r] = __half_as_ushort(s);
+  }
 
   // 3. codes: chunk p (words 4p..4p+3 = k 32p..32p+31) of row r goes to chunk position p ^ ((r/2) % 4)
   uint32_t* dst = reinterpret_cast<uint32_t*>(tile) + (size_t)r * 16;
@@ -90,9 +94,10 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint8_t* __restrict__
   const uint8_t* tile = packed + ((size_t)(n / 128) * (K / 128) + g) * tile_bytes(mode);
   const int p = (k0 % 128) / 32, w = (k0 % 32) / 8;
   const uint32_t word = reinterpret_cast<const uint32_t*>(tile)[(size_t)r * 16 + 4 * (p ^ ((r >> 1) & 3)) + w];
-  const __half s = __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8192)[r]);
-  const __half z = mode == W4A16_SYM ? __float2half_rn(8.0f)
-                                     : __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8448)[r]);
+  const bool asym = mode == W4A16_ASYM;
+  const __half s = __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8192)[asym ? 2 * r : r]);
+  const __half z = asym ? __ushort_as_half(reinterpret_cast<const uint16_t*>(tile + 8192)[2 * r + 1])
+                        : __float2half_rn(8.0f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int q = (word >> (4 * ((i % 2) * 4 + i / 2))) & 0xF;

@@ -137,11 +137,10 @@ def test_layout_scales_zeros_placement_and_roundtrip(mode):
     for g in range(K // 128):
         for n in (0, 1, 127, 128, 200, 383):
             t = (n // 128) * (K // 128) + g
-            b = packed[t * TB + 8192 + 2 * (n % 128): t * TB + 8194 + 2 * (n % 128)]
-            assert int.from_bytes(b.tobytes(), "little") == int(sc[g, n])
+            so = t * TB + 8192 + (4 if mode == oracle.ASYM else 2) * (n % 128)   # {s, z} side by side (ASYM)
+            assert int.from_bytes(packed[so:so + 2].tobytes(), "little") == int(sc[g, n])
             if mode == oracle.ASYM:
-                b = packed[t * TB + 8448 + 2 * (n % 128): t * TB + 8450 + 2 * (n % 128)]
-                assert int.from_bytes(b.tobytes(), "little") == int(ze[g, n])
+                assert int.from_bytes(packed[so + 2:so + 4].tobytes(), "little") == int(ze[g, n])
     c2, s2, z2 = oracle.layout_unpack(packed, K, N, mode)
     assert np.array_equal(c2, codes) and np.array_equal(s2, sc)
     if mode == oracle.ASYM:

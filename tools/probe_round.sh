@@ -1,5 +1,3 @@
 #!/bin/bash
 for m in 1 8 16; do timeout 60 python tools/probe_tc.py --family 0 --M $m --R 4 --tag famA_m$m 2>&1 | grep -v Warn; done
-for m in 16 64; do timeout 60 python tools/probe_tc.py --family 1 --M $m --R 4 --tag famB_m$m 2>&1 | grep -v Warn; done
-timeout 60 python tools/probe_tc.py --family 0 --M 16 --K 8192 --N 8192 --R 8 --tag famA_O 2>&1 | grep -v Warn
-timeout 60 python tools/probe_tc.py --family 0 --M 16 --K 28672 --N 8192 --R 4 --tag famA_down 2>&1 | grep -v Warn
+for m in 16 32 64; do timeout 60 python tools/probe_tc.py --family 1 --M $m --R 4 --tag famB_m$m 2>&1 | grep -v Warn; done
