@@ -338,11 +338,13 @@ def main():
                     "algorithmic_bytes_per_launch": stack.layers[0]["gate_up"].weight_bytes + 2 * M * (gate["K"] + gate["N"]),
                     "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA graph, "
                             "CUDA events on the launching stream)"}
-        ncu_path = os.path.join(ROOT, "profiles", "r01_ncu_gate_up.json")
-        if os.path.exists(ncu_path):
+        fam_tag = "famA" if gate["family"] == w4.W4A16_FAMILY_MMA_SYNC else "famB"
+        ncu_path = os.path.join(ROOT, "profiles", f"r01_ncu_{fam_tag}_gateup_M{M}.json")
+        if os.path.exists(ncu_path):   # committed ncu --set full capture of this kernel at this M
             try:
                 with open(ncu_path) as f:
-                    roofline["traffic"] = json.load(f).get("dram_bytes_per_launch")
+                    roofline["traffic"] = json.load(f)["derived"]["dram_traffic_bytes"]
+                roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT)
             except Exception:
                 pass
     clk = clocks.stop() if clocks else None

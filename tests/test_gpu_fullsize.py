@@ -1,0 +1,114 @@
+"""Full-size parity (BASELINE.json configs 2-4 shapes) in the launch configuration bench.py times.
+
+The GPU packs and multiplies the full Llama-3-70B / 8B layer matrices (weights generated in HBM by the same
+counter-based generator the oracle uses on the host); the oracle recomputes sampled 128-column tiles one by
+one (their weights regenerated on the host with synth.host_block), and the sampled columns must match:
+packed bytes bit-exact, Y within 1e-2 * (1 + |ref|). Also the verify stack (tp.VerifyStack at t = 1) on a
+small model: every GEMM output and the acceptance result against the oracle.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+NPROC = os.cpu_count() or 1
+
+SHAPES_70B = {"qkv": (8192, 10240), "o": (8192, 8192), "gate_up": (8192, 57344), "down": (28672, 8192)}
+SHAPES_8B = {"qkv": (4096, 6144), "gate_up": (4096, 28672), "down": (14336, 4096)}
+
+
+def _to_u16(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _check_shape(K, N, Ms, tid, mode=0):
+    import paper_2505_22179_b200 as w4
+    W = synth.gpu(11, tid, synth.WEIGHT, K, N)
+    lin = w4.pack_linear(W, mode=mode)
+    del W
+    ws = w4.alloc_workspace(max(Ms), [(K, N)])
+    tiles = sorted({0, (N // 128) // 2, N // 128 - 1})
+    TB = 8704 if mode == 0 else 8448
+    Gk = K // 128
+    packed = lin.packed
+    for t in tiles:
+        Wb = synth.host_block(11, tid, synth.WEIGHT, K, N, 0, K, 128 * t, 128 * t + 128)
+        blob_ref, codes, sc, ze, _ = oracle.pack(Wb, mode=mode)
+        got = packed[t * Gk * TB:(t + 1) * Gk * TB].cpu().numpy()
+        assert np.array_equal(got, blob_ref), f"packed tile {t} of {K}x{N} differs"
+        for M in Ms:
+            X = synth.gpu(12, tid * 100 + M, synth.ACT, M, K)
+            Y = torch.empty(M, N, dtype=torch.float16, device="cuda")
+            lin(X, Y, ws)
+            torch.cuda.synchronize()
+            Xh = synth.host(12, tid * 100 + M, synth.ACT, M, K)
+            ref = oracle.gemm(Xh, codes, sc, ze, mode=mode, nthreads=NPROC)
+            y = Y[:, 128 * t:128 * t + 128].float().cpu().numpy().astype(np.float64)
+            err = np.abs(y - ref)
+            assert np.all(err <= 1e-2 * (1 + np.abs(ref))), f"{K}x{N} M={M} tile {t}: max err {err.max()}"
+
+
+@pytest.mark.parametrize("name", list(SHAPES_70B))
+def test_llama70b_layer_shapes_sampled_tiles(name):
+    K, N = SHAPES_70B[name]
+    _check_shape(K, N, [1, 16, 61, 64], tid=700 + list(SHAPES_70B).index(name))
+
+
+@pytest.mark.parametrize("name", list(SHAPES_8B))
+def test_llama8b_layer_shapes_sampled_tiles(name):
+    K, N = SHAPES_8B[name]
+    _check_shape(K, N, [4, 32], tid=800 + list(SHAPES_8B).index(name))
+
+
+def test_llama70b_tp8_shard_shapes_sym():
+    from paper_2505_22179_b200 import tp
+    plan = tp.shard_plan(tp.LLAMA3_70B, 8, 5)
+    for i, (name, s) in enumerate(plan.items()):
+        _check_shape(s["K"], s["N"], [8, 49], tid=900 + i, mode=1)
+
+
+def test_verify_stack_one_layer_against_oracle():
+    from paper_2505_22179_b200 import tp
+    d = tp.ModelDims("tiny", hidden=1024, ffn=2048, n_q=8, n_kv=2, head=128, layers=1)
+    Wh = {}
+
+    def make_weight(l, name, K, N, out):
+        synth.gpu(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
+        Wh[name] = synth.host(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
+
+    M = 13
+    st = tp.VerifyStack(d, 1, 16, make_weight)
+    for j, buf in enumerate((st.x_qkv, st.x_o, st.x_mlp)):
+        synth.gpu(22, j, synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+    rng = np.random.default_rng(3)
+    tok, par = synth.eagle_tree(rng, M - 1, 5)
+    am = synth.target_argmax_for(rng, tok, par, 0.8)
+    st.set_tree(tok, par, am)
+    g = st.capture(M)
+    g.replay()
+    torch.cuda.synchronize()
+
+    def ref(name, X_u16):
+        c, s_, z, _ = oracle.quantize(Wh[name])
+        return oracle.gemm(X_u16, c, s_, z, nthreads=NPROC)
+
+    for name, xin, yout in (("qkv", st.x_qkv, st.y_qkv), ("o", st.x_o, st.y_o), ("gate_up", st.x_mlp, st.y_gu)):
+        r = ref(name, _to_u16(xin[:M]))
+        y = yout[:M].float().cpu().numpy()
+        assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), name
+    # SiLU*mul glue (not the paper's method): fp32 reference of the GPU's own gate-up output
+    gu = st.y_gu[:M].float().cpu().numpy()
+    F = d.ffn
+    act_ref = gu[:, :F] / (1 + np.exp(-gu[:, :F])) * gu[:, F:]
+    act = st.act[:M].float().cpu().numpy()
+    assert np.all(np.abs(act - act_ref) <= 2e-3 * (1 + np.abs(act_ref)))
+    r = ref("down", _to_u16(st.act[:M]))
+    y = st.y_down[:M].float().cpu().numpy()
+    assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r)))
+    out = st.accept_out[:3 + M].cpu().numpy()
+    assert np.array_equal(out, oracle.accept(tok, par, am)[4])
