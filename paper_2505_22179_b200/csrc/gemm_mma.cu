@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); }
     fence_mbar_init();
+    pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
   }
   __syncthreads();
 
@@ -114,20 +115,32 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
       const uint64_t pol = policy_evict_first();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int i = 0; i < n_stages; ++i) {
-        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-        mbar_wait(&empty_bar[s], ph ^ 1);
+      auto load_x = [&](int i, int s) {   // activation slices of stage i (written by the preceding kernel)
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0), g0 = u0 % p.Gk;
         const uint32_t st = smem_base + s * C::kStage;
-        const int g0 = u0 % p.Gk;
-        mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
         if (nu == kR && g0 + kR <= p.Gk) {
           tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
         } else {
           for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
         }
+      };
+      auto load_w = [&](int i, int s) {   // packed weights of stage i (never written by a preceding kernel)
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+        mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
         bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+      };
+      // Weights of the first stages stream while the preceding kernel (PDL) still drains; the activations
+      // it produces are read only after griddepcontrol.wait.
+      const int pre = min(S, n_stages);
+      for (int i = 0; i < pre; ++i) load_w(i, i);
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) load_x(i, i);
+      int s = pre % S;
+      uint32_t ph = pre == S ? 1 : 0;
+      for (int i = pre; i < n_stages; ++i) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        load_w(i, s);
+        load_x(i, s);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -135,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   }
 
   // ---------------- consumers ----------------
+  pdl_wait();   // Y / workspace writes must follow the preceding kernel (returns at once when satisfied)
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
   const int rq = warp & 3, kh = warp >> 2;    // row quarter, k half
   int rows[2][2];                              // tile rows owned by this lane: [m-tile][g / g+8]
@@ -326,8 +340,8 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
     attr_set = true;
   }
-  kern<<<p.G, kThreads, C::kSmem, stream>>>(mapR, map1, p);
-  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+  return launch_pdl(kern, dim3(p.G), dim3(kThreads), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
+                                                                                             : W4A16_ERR_CUDA;
 }
 
 }  // namespace ma

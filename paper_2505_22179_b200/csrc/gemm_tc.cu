@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     for (int b = 0; b < kNumA; ++b) { mbar_init(&afull_bar[b], kDqWarps); mbar_init(&aempty_bar[b], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&accfull_bar[a], 1); mbar_init(&accempty_bar[a], kDqWarps); }
     fence_mbar_init();
+    pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
   }
   if (warp == kMmaWarp) tmem_alloc(&s_tmem, kTmemCols);
   if (warp == kProducerWarp && lane == 0) {
@@ -203,24 +204,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int i = 0; i < n_stages; ++i) {
+      auto load_w = [&](int i, int s) {   // packed weights (never written by a preceding kernel)
         const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+        mbar_expect_tx(&full_bar[s], ((p.dbg & 4) ? 0 : nu * C::kXUnit) + nu * C::kTB);
+        bulk_g2s(smem + s * C::kStage + C::kXStage, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+      };
+      auto load_x = [&](int i, int s) {   // activations (after griddepcontrol.wait)
+        if (p.dbg & 4) return;
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0), g0 = u0 % p.Gk;
+        const uint32_t st = smem_base + s * C::kStage;
+        if (nu == kR && g0 + kR <= p.Gk) {   // the stage's units share an n-tile: one 3-D TMA
+          tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
+        } else {
+          for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
+        }
+      };
+      const int pre = min(S, n_stages);
+      for (int i = 0; i < pre; ++i) { trace(p, 0, i); load_w(i, i); }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) { load_x(i, i); trace(p, 1, i); }
+      int s = pre % S;
+      uint32_t ph = pre == S ? 1 : 0;
+      for (int i = pre; i < n_stages; ++i) {
         wait_bar(p, &empty_bar[s], ph ^ 1);
         trace(p, 0, i);
-        const uint32_t st = smem_base + s * C::kStage;
-        const int g0 = u0 % p.Gk;
-        const bool one_tma = (nu == kR) && (g0 + kR <= p.Gk);   // the stage's units share an n-tile
-        mbar_expect_tx(&full_bar[s], ((p.dbg & 4) ? 0 : nu * C::kXUnit) + nu * C::kTB);
-        if (!(p.dbg & 4)) {
-          if (one_tma) {
-            tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
-          } else {
-            for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
-          }
-        }
-        bulk_g2s(smem + s * C::kStage + C::kXStage, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+        load_w(i, s);
+        load_x(i, s);
         trace(p, 1, i);
         if (++s == S) { s = 0; ph ^= 1; }
       }
@@ -287,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     }
   } else {
     // ---------------- dequant + epilogue (warps 0..15) ----------------
+    pdl_wait();   // Y / workspace writes must follow the preceding kernel
     const int q = warp & 3;           // TMEM lane quarter = tile rows 32q..32q+31
     const int h = warp >> 2;          // k-part of each unit: k 32h .. 32h+31 (one 16-byte chunk per row)
     const int row = q * 32 + lane;
@@ -425,8 +435,8 @@ int launch(const uint16_t* X, const Params& p, cudaStream_t stream) {
       return W4A16_ERR_CUDA;
     attr = true;
   }
-  kern<<<p.G, kThreads, C::kSmem, stream>>>(mapR, map1, p);
-  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+  return launch_pdl(kern, dim3(p.G), dim3(kThreads), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
+                                                                                             : W4A16_ERR_CUDA;
 }
 
 }  // namespace tc

@@ -37,4 +37,21 @@ inline int encode_x_sw128(CUtensorMap* map, const uint16_t* X, int M, int K, int
   return W4A16_OK;
 }
 
+// Launch with programmatic stream serialization: the kernel may begin while the previous kernel in the
+// stream drains; it must call griddepcontrol.wait before touching anything that kernel writes.
+template <typename Kern, typename... Args>
+inline cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace w4
