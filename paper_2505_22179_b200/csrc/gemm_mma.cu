@@ -241,85 +241,103 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
     if (threadIdx.x == 0) p.counters[t] = 0;   // all contributors have arrived: safe to re-arm
   };
 
-  for (int i = 0; i < n_stages; ++i) {
-    const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-    mbar_wait(&full_bar[s], ph);
-    const uint32_t st = smem_base + s * C::kStage;
-    for (int j = 0; j < nu; ++j) {
-      const int u = u0 + j;
-      if (u == boundary || cur_t < 0) {
-        if (cur_t >= 0) { flush(cur_t, seg_u0, u, first_segment); first_segment = false; }
-        cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
-        boundary = (cur_t + 1) * p.Gk;
-        seg_u0 = u;
+  // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
+  // dequant + 16 MMAs, then the post-MMA group scale.
+  auto process_unit = [&](uint32_t st, int j) {
+    const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
+    const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
+    uint4 xr[2][NTB];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+    for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-          for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
+      for (int tb = 0; tb < NTB; ++tb) {
+        const int m = 8 * tb + g8;
+        const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
+        xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
       }
-      const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
-      const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
-      float sc[2][2];
-      __half2 zp[2][2];
+    uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-          const int r = rows[mt][hf];
-          if (SYM) {
-            sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
-            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
-          } else {
-            const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
-            sc[mt][hf] = __low2float(sz);
-            zp[mt][hf] = zero_pair(__high2half(sz));
-          }
+          const int r = rows[mt][hf], pch = 2 * kh + cc;
+          wq[cc][mt][hf] = lds32(ub + r * 64 + ((pch ^ ((r >> 1) & 3)) << 4) + 4 * c4);
         }
-      float gacc[2][NTB][4];
+    float sc[2][2];
+    __half2 zp[2][2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int pch = 2 * kh + cc;                          // 32-k chunk of the unit: k 32 pch .. +31
-        // activations: lane needs X[8tb + g8][32 pch + 8 c4 .. +7] (one 16-byte SW128 chunk per token row)
-        uint4 xr[NTB];
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const int m = 8 * tb + g8;
-          const int jx = 4 * (pch & 1) + c4;                  // 16-byte chunk within the 128-byte box row
-          xr[tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int ra = rows[mt][0], rb = rows[mt][1];
-          const uint32_t wa = lds32(ub + ra * 64 + ((pch ^ ((ra >> 1) & 3)) << 4) + 4 * c4);
-          const uint32_t wb = lds32(ub + rb * 64 + ((pch ^ ((rb >> 1) & 3)) << 4) + 4 * c4);
-#pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {       // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
-            const uint32_t qa = hs ? wa >> 8 : wa, qb = hs ? wb >> 8 : wb;
-            const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
-            const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
-            // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
-            // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
-#pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) {
-              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[tb]);
-              mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
-            }
-          }
+      for (int hf = 0; hf < 2; ++hf) {
+        const int r = rows[mt][hf];
+        if (SYM) {
+          sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+          zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
+        } else {
+          const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
+          sc[mt][hf] = __low2float(sz);
+          zp[mt][hf] = zero_pair(__high2half(sz));
         }
       }
+    float gacc[2][NTB][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
-          acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
-          acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
-          acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
+      for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+      for (int hs = 0; hs < 2; ++hs)            // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
+          const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
+          const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
+          const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
+          // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
+          // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
+            mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+          }
         }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb) {
+        acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
+        acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
+        acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
+        acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
+      }
+  };
+  auto begin_segment = [&](int u) {
+    if (cur_t >= 0) { flush(cur_t, seg_u0, u, first_segment); first_segment = false; }
+    cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
+    boundary = (cur_t + 1) * p.Gk;
+    seg_u0 = u;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
+  };
+
+  for (int i = 0; i < n_stages; ++i) {
+    const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+    mbar_wait(&full_bar[s], ph);
+    const uint32_t st = smem_base + s * C::kStage;
+    if (nu == kR && cur_t >= 0 && u0 + kR <= boundary) {
+      // fast path (no tile boundary inside the stage): both units back to back
+#pragma unroll
+      for (int j = 0; j < kR; ++j) process_unit(st, j);
+    } else {
+      for (int j = 0; j < nu; ++j) {
+        if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
+        process_unit(st, j);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
