@@ -318,8 +318,11 @@ def main():
             kernels[name] = {"K": s["K"], "N": s["N"], "us": 1e3 * msk, "weight_MB": wb / 1e6,
                              "GBps": wb / (msk * 1e-3) / 1e9, "frac_hbm": wb / (msk * 1e-3) / 1e9 / peak_gbs,
                              "family": w4.w4a16_gemm_family(M, s["K"], s["N"])}
-            # the other kernel family on the same launches, for comparison (not part of the step)
-            alt = 1 - kernels[name]["family"]
+            # the other engine (mma.sync <-> tcgen05) on the same launches, for comparison (not part of the step)
+            alt = (w4.W4A16_FAMILY_TCGEN05 if kernels[name]["family"] != w4.W4A16_FAMILY_TCGEN05 else
+                   w4.W4A16_FAMILY_MMA_SYNC if M <= 8 else w4.W4A16_FAMILY_MMA_SYNC_S if M <= 16 else None)
+            if alt is None:
+                continue
             g2 = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):
                 for L in stack.layers:
@@ -338,7 +341,7 @@ def main():
                     "algorithmic_bytes_per_launch": stack.layers[0]["gate_up"].weight_bytes + 2 * M * (gate["K"] + gate["N"]),
                     "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA graph, "
                             "CUDA events on the launching stream)"}
-        fam_tag = "famA" if gate["family"] == w4.W4A16_FAMILY_MMA_SYNC else "famB"
+        fam_tag = "famB" if gate["family"] == w4.W4A16_FAMILY_TCGEN05 else "famA"
         ncu_path = os.path.join(ROOT, "profiles", f"r01_ncu_{fam_tag}_gateup_M{M}.json")
         if os.path.exists(ncu_path):   # committed ncu --set full capture of this kernel at this M
             try:

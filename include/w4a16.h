@@ -58,7 +58,7 @@ typedef enum {
 
 enum { W4A16_ASYM = 0, W4A16_SYM = 1 };
 enum { W4A16_DEV_OK = 0, W4A16_DEV_NONFINITE = 1, W4A16_DEV_BAD_TREE = 2 };
-enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 = 1 };
+enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 = 1, W4A16_FAMILY_MMA_SYNC_S = 2 };
 #define W4A16_GROUP 128
 #define W4A16_MAX_M 64
 #define W4A16_MAX_TREE 1024
@@ -101,8 +101,10 @@ int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K,
                void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
 
 /* w4a16_gemm_ex — w4a16_gemm with an explicit kernel family: W4A16_FAMILY_AUTO (= w4a16_gemm),
- * W4A16_FAMILY_MMA_SYNC (legacy mma.sync tensor path, M <= 16 only; else W4A16_ERR_SHAPE) or
- * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, TMEM; any M <= 64). Both compute the same definition. */
+ * W4A16_FAMILY_MMA_SYNC (mma.sync, group scale applied to fp32 group sums; M <= 16, else W4A16_ERR_SHAPE),
+ * W4A16_FAMILY_MMA_SYNC_S (mma.sync, scale folded into the dequantised fp16 weights; M <= 16) or
+ * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, weights in TMEM; any M <= 64). All compute the same definition
+ * (within the tolerance above); results are batch-invariant within one family. */
 int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
                   void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);
 
@@ -126,7 +128,8 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 
-/* Kernel family w4a16_gemm uses for this shape: W4A16_FAMILY_MMA_SYNC for M <= 16, W4A16_FAMILY_TCGEN05 above. */
+/* Kernel family w4a16_gemm uses: W4A16_FAMILY_MMA_SYNC for M <= 8, W4A16_FAMILY_MMA_SYNC_S for 9 <= M <= 16,
+ * W4A16_FAMILY_TCGEN05 above. */
 int w4a16_gemm_family(int M, int K, int N);
 
 #ifdef __cplusplus

@@ -12,7 +12,8 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaS
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
-extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
+                                     cudaStream_t);
 
 namespace {
 
@@ -73,11 +74,14 @@ extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a
   return cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
-// Family choice depends on M only through the token-block count: mma.sync for M <= 16 (HMMA work per weight
-// is small, everything stays in registers), tcgen05 above (MMA cost nearly independent of M). DESIGN.md §5.
+// Family choice: mma.sync with the group scale applied to fp32 group sums for M <= 8,
+// mma.sync with the scale inside the dequantised weights for 9 <= M <= 16 (register-bound variant),
+// tcgen05/TMEM above (MMA cost nearly independent of M).
 extern "C" int w4a16_gemm_family(int M, int K, int N) {
   (void)K; (void)N;
-  return M <= 16 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_TCGEN05;
+  if (M <= 8) return W4A16_FAMILY_MMA_SYNC;
+  if (M <= 16) return W4A16_FAMILY_MMA_SYNC_S;
+  return W4A16_FAMILY_TCGEN05;
 }
 
 extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group,
@@ -89,10 +93,11 @@ extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y,
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
   if (family == W4A16_FAMILY_AUTO) family = w4a16_gemm_family(M, K, N);
-  if (family == W4A16_FAMILY_MMA_SYNC) {
+  if (family == W4A16_FAMILY_MMA_SYNC || family == W4A16_FAMILY_MMA_SYNC_S) {
     if (M > 16) return W4A16_ERR_SHAPE;
     if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_mma(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+    return w4a16_launch_gemm_mma(X, packed, Y, M, K, N, mode, family == W4A16_FAMILY_MMA_SYNC_S, workspace, sms,
+                                 (cudaStream_t)stream);
   }
   if (family == W4A16_FAMILY_TCGEN05) {
     if (!workspace || workspace_bytes < w4a16_tc_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;

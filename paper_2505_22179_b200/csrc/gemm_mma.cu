@@ -83,12 +83,15 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
       : "memory");
 }
 
-template <int NTB, bool SYM>
+template <int NTB, bool SYM, bool kScaleInA>
 __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __grid_constant__ CUtensorMap xmapR,
                                                                       const __grid_constant__ CUtensorMap xmap1,
                                                                       const GemmParams p) {
   using C = Cfg<NTB, SYM>;
   constexpr int S = C::kStages;
+  // kScaleInA (family W4A16_FAMILY_MMA_SYNC_S): scale inside the A fragments instead of a per-unit group
+  // accumulator — fewer registers (NTB = 2 runs at the 96-register cap of 18 warps/SM), 4 more HMUL2 per
+  // word. Post-scale (family W4A16_FAMILY_MMA_SYNC) is faster when registers allow (NTB = 1).
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
   __shared__ __align__(8) uint64_t empty_bar[S];
@@ -281,38 +284,66 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
           zp[mt][hf] = zero_pair(__high2half(sz));
         }
       }
-    float gacc[2][NTB][4];
+    if constexpr (kScaleInA) {
+      // w_hat = fp16((q - z) * s) in the A fragments (exactly the oracle's dequantised weight), accumulated
+      // straight into acc: no per-unit group accumulator (saves 16 registers at NTB = 2).
+      __half2 s2[2][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
+        for (int hf = 0; hf < 2; ++hf) s2[mt][hf] = __float2half2_rn(sc[mt][hf]);
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc)
+      for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-      for (int hs = 0; hs < 2; ++hs)            // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
+        for (int hs = 0; hs < 2; ++hs)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
-          const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-          const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
-          const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
-          // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
-          // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
+            const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
+            const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[mt][0])), s2[mt][0]));
+            const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[mt][1])), s2[mt][1]));
+            const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[mt][0])), s2[mt][0]));
+            const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[mt][1])), s2[mt][1]));
 #pragma unroll
-          for (int tb = 0; tb < NTB; ++tb) {
-            const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-            mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            for (int tb = 0; tb < NTB; ++tb) {
+              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
+              mma_16816(acc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            }
           }
+    } else {
+      float gacc[2][NTB][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int hs = 0; hs < 2; ++hs)            // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
+            const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
+            const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
+            const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
+            // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
+            // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) {
+              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
+              mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            }
+          }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
+          acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
+          acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
+          acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
         }
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) {
-        acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
-        acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
-        acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
-        acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
-      }
+    }
   };
   auto begin_segment = [&](int u) {
     if (cur_t >= 0) { flush(cur_t, seg_u0, u, first_segment); first_segment = false; }
@@ -346,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   if (cur_t >= 0) flush(cur_t, seg_u0, u_end, first_segment);
 }
 
-template <int NTB, bool SYM>
+template <int NTB, bool SYM, bool kScaleInA>
 static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream) {
   using C = Cfg<NTB, SYM>;
   CUtensorMap mapR, map1;
   if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * kR)) return e;
   if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
-  auto kern = gemm_w4a16_mma_kernel<NTB, SYM>;
+  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
   static bool attr_set = false;   // benign race: idempotent attribute
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
@@ -381,7 +412,7 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
 }
 
 extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
-                                     void* ws, int num_sms, cudaStream_t stream) {
+                                     bool scale_in_a, void* ws, int num_sms, cudaStream_t stream) {
   w4::ma::GemmParams p;
   p.packed = reinterpret_cast<const uint8_t*>(packed);
   p.Y = Y;
@@ -393,9 +424,14 @@ extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
   const bool sym = mode == W4A16_SYM;
+#define W4_MA_CASE(NTB)                                                                                \
+  case NTB:                                                                                             \
+    if (scale_in_a) return sym ? w4::ma::launch_t<NTB, true, true>(X, p, stream) : w4::ma::launch_t<NTB, false, true>(X, p, stream); \
+    return sym ? w4::ma::launch_t<NTB, true, false>(X, p, stream) : w4::ma::launch_t<NTB, false, false>(X, p, stream);
   switch ((M + 7) / 8) {
-    case 1: return sym ? w4::ma::launch_t<1, true>(X, p, stream) : w4::ma::launch_t<1, false>(X, p, stream);
-    case 2: return sym ? w4::ma::launch_t<2, true>(X, p, stream) : w4::ma::launch_t<2, false>(X, p, stream);
-    default: return W4A16_ERR_SHAPE;   // family A serves M <= 16
+    W4_MA_CASE(1)
+    W4_MA_CASE(2)
+    default: return W4A16_ERR_SHAPE;   // the mma.sync families serve M <= 16
   }
+#undef W4_MA_CASE
 }

@@ -12,7 +12,7 @@ from ._lib import (  # noqa: F401
     lib, check, status_string, W4A16Error,
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
-    W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05,
+    W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S,
 )
 
 

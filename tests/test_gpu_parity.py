@@ -149,14 +149,14 @@ def problem(K, N, mode=0, seed=0):
     return _P[key]
 
 
-FAMILIES = [0, 1]  # W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05
+FAMILIES = [0, 2, 1]  # W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05
 
 
 @pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [1, 2, 3, 5, 7, 8, 9, 13, 16, 17, 24, 31, 32, 48, 61, 64])
 def test_gemm_config1_tolerance(M, family):
     # config 1: K = N = 4096, g128 ASYM; M sweeps ragged token blocks / MMA-N padding of both families
-    if family == 0 and M > 16:
+    if family in (0, 2) and M > 16:
         pytest.skip("family A (mma.sync) serves M <= 16")
     P = problem(4096, 4096)
     X = synth.host(100 + M, 12, synth.ACT, M, 4096)
@@ -168,7 +168,7 @@ def test_gemm_config1_tolerance(M, family):
                                    (28672, 256, 3), (8192, 384, 64), (256, 57344 // 8, 12)])
 def test_gemm_shapes_tolerance(K, N, M, family):
     # single tile, TP8 shard shapes (QKV N=1280, O K=1024, down K=3584), tall-K/narrow-N stream-K splits
-    if family == 0 and M > 16:
+    if family in (0, 2) and M > 16:
         pytest.skip("family A (mma.sync) serves M <= 16")
     P = problem(K, N, seed=K ^ N)
     X = synth.host(7 + M, 13, synth.ACT, M, K)
@@ -178,7 +178,7 @@ def test_gemm_shapes_tolerance(K, N, M, family):
 @pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [1, 8, 16, 40, 64])
 def test_gemm_sym_tolerance(M, family):
-    if family == 0 and M > 16:
+    if family in (0, 2) and M > 16:
         pytest.skip("family A (mma.sync) serves M <= 16")
     P = problem(2048, 1536, mode=1, seed=3)
     X = synth.host(55 + M, 14, synth.ACT, M, 2048)
@@ -188,7 +188,7 @@ def test_gemm_sym_tolerance(M, family):
 @pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("M", [8, 13, 16, 33, 64])
 def test_gemm_one_hot_bit_exact(M, family):
-    if family == 0 and M > 16:
+    if family in (0, 2) and M > 16:
         pytest.skip("family A (mma.sync) serves M <= 16")
     # row m of X = e_{k_m}: Y[m] must equal the dequantised weight row w_hat[k_m] bit-for-bit (pins layout,
     # nibble order, zero/scale handling and the epilogue mapping of the whole pack -> GEMM data path)
@@ -209,7 +209,7 @@ def test_gemm_batch_invariance_within_family(family):
     P = problem(4096, 4096)
     X = synth.host(31, 15, synth.ACT, 64, 4096)
     base = to_np_u16(P.run(np.ascontiguousarray(X[:1]), family=family))
-    for M in ((2, 5, 8, 9, 16) if family == 0 else (2, 5, 8, 16, 17, 32, 48, 64)):
+    for M in ((2, 5, 8, 9, 16) if family in (0, 2) else (2, 5, 8, 16, 17, 32, 48, 64)):
         Y = to_np_u16(P.run(np.ascontiguousarray(X[:M]), family=family))
         assert np.array_equal(Y[:1], base), f"M={M}"
 
@@ -218,9 +218,9 @@ def test_gemm_families_agree_within_tolerance():
     P = problem(4096, 4096)
     X = synth.host(32, 15, synth.ACT, 16, 4096)
     ref = P.ref(X)
-    Ya = P.run(X, family=0).float().cpu().numpy()
-    Yb = P.run(X, family=1).float().cpu().numpy()
-    assert np.all(np.abs(Ya - Yb) <= 2e-2 * (1 + np.abs(ref)))
+    Ys = [P.run(X, family=f).float().cpu().numpy() for f in (0, 2, 1)]
+    for Ya in Ys[1:]:
+        assert np.all(np.abs(Ys[0] - Ya) <= 2e-2 * (1 + np.abs(ref)))
 
 
 def test_gemm_deterministic_and_graph_capturable():
@@ -332,5 +332,5 @@ def test_gemm_long_streams_and_many_segments():
         P = problem(K, N, seed=K + N)
         X = synth.host(K + M, 18, synth.ACT, M, K)
         ref = P.ref(X)
-        for fam in ((0, 1) if M <= 16 else (1,)):
+        for fam in ((0, 2, 1) if M <= 16 else (1,)):
             assert_gemm_close(P.run(X, family=fam), ref, f"K={K} N={N} M={M} family={fam}")
