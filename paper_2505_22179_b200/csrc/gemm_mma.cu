@@ -24,6 +24,9 @@
 //  * Tile boundary: the two k-half warps combine through shared memory; a tile split across CTAs goes to
 //    the fp32 workspace and the last CTA to arrive (atomic counter per tile) sums the partials in CTA order
 //    (fixed, hence deterministic) and writes fp16 Y, re-zeroing the counter.
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "tma_host.cuh"
 #include "w4a16.h"
@@ -33,10 +36,18 @@ namespace ma {
 
 constexpr int kTileN = 128, kTileK = 128;
 constexpr int kUnitWBytes = kTileN * kTileK / 2;   // 8192
-constexpr int kWarps = 8;                          // 4 row-quarters x 2 k-halves
-constexpr int kProducerWarp = kWarps;              // warp 8
-constexpr int kThreads = (kWarps + 1) * 32;        // 288
-constexpr int kR = 2;                              // units per pipeline stage
+#ifndef W4_MA_GROUPS
+#define W4_MA_GROUPS 1
+#endif
+constexpr int kGroups = W4_MA_GROUPS;              // consumer groups sharing one pipeline (1 CTA per SM at 2)
+constexpr int kWarps = 8 * kGroups;                // per group: 4 row-quarters x 2 k-halves
+constexpr int kProducerWarp = kWarps;
+constexpr int kXsumWarp = kWarps + 1;              // activation sums (offset-code family only)
+template <bool kScaleInA>
+constexpr int threads_for() { return (kWarps + (kScaleInA ? 1 : 2)) * 32; }
+constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
+constexpr int kCtasPerSm = kGroups == 2 ? 1 : 2;   // resident CTAs per SM
+constexpr int kSmemBudget = (kCtasPerSm == 1 ? 224 : 112) * 1024;
 
 template <int NTB, bool SYM>
 struct Cfg {
@@ -45,9 +56,12 @@ struct Cfg {
   static constexpr int kXBox = kMpad * 128;                       // one 64-k SW128 box (multiple of 1024 B)
   static constexpr int kXUnit = 2 * kXBox;
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
-  static constexpr int kStages = 4;
-  static constexpr int kRedFloats = 4 * NTB * 2 * 4 * 32;         // k-half reduction scratch
-  static constexpr int kSmem = kStages * kStage + kRedFloats * 4 + 1024;
+  static constexpr int kRedSlots = 2 * kGroups - 1;               // partial-sum sets handed to (group 0, kh 0)
+  static constexpr int kRedFloats = kRedSlots * 4 * NTB * 2 * 4 * 32;
+  static constexpr int kSumBytes = kR * 2 * NTB * 4 * 16;         // per stage: {-C, -S} float4 per (unit, kh, tb, c4)
+  static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - 1024) / (kStage + kSumBytes);
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + 1024;
 };
 
 struct GemmParams {
@@ -59,7 +73,28 @@ struct GemmParams {
   int Gk;            // K / 128 groups per n-tile
   int U;             // total units
   int G;             // CTAs
+  int dbg;           // diagnostics only (W4A16_MMA_DEBUG): bit0 skip compute, bit1 skip loads, bit2 backoff waits
 };
+
+// Diagnostics only (W4A16_MMA_DEBUG bit 16): per-CTA %globaltimer stamps (entry, first stage ready, main loop
+// done, exit) of consumer warp 0 (tools/probe_tc.py --trace-mma).
+constexpr int kTraceCtas = 1024;
+__device__ unsigned long long g_trace_ma[kTraceCtas][8];
+#ifndef W4A16_MMA_DIAG
+#define W4A16_MMA_DIAG 0   // 1: compile the per-CTA timeline trace and consumer-side diagnostics in
+#endif
+__device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
+  if (W4A16_MMA_DIAG && (p.dbg & 16) && blockIdx.x < kTraceCtas && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace_ma[blockIdx.x][ev] = t;
+    if (ev == 0) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_trace_ma[blockIdx.x][7] = smid;
+    }
+  }
+}
 
 __device__ __forceinline__ int unit_begin(int c, int U, int G) { return (int)(((long long)c * U) / G); }
 // CTA owning unit u: largest c with unit_begin(c) <= u.
@@ -84,7 +119,7 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
-__global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __grid_constant__ CUtensorMap xmapR,
+__global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a16_mma_kernel(const __grid_constant__ CUtensorMap xmapR,
                                                                       const __grid_constant__ CUtensorMap xmap1,
                                                                       const GemmParams p) {
   using C = Cfg<NTB, SYM>;
@@ -95,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
   __shared__ __align__(8) uint64_t empty_bar[S];
+  __shared__ __align__(8) uint64_t sums_bar[S];   // offset-code family: the stage's activation sums are ready
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,9 +140,10 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_base = smem_u32(smem);
   float* red = reinterpret_cast<float*>(smem + S * C::kStage);
+  const uint32_t sums_base = smem_base + S * C::kStage + C::kRedFloats * 4;   // [S][kSumBytes]
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); mbar_init(&sums_bar[s], 1); }
     fence_mbar_init();
     pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
   }
@@ -114,6 +151,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
 
   if (warp == kProducerWarp) {
     // ---------------- producer ----------------
+    // Per stage ONE bulk copy of the packed weights (the TMA engine costs ~100+ cycles per issued copy)
+    // and a 3-D TMA of the activation slices.
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
@@ -135,6 +174,15 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
       // Weights of the first stages stream while the preceding kernel (PDL) still drains; the activations
       // it produces are read only after griddepcontrol.wait.
       const int pre = min(S, n_stages);
+      if (p.dbg & 2) {   // diagnostics: no memory traffic, consumers run on stale shared memory
+        pdl_wait();
+        for (int i = 0, s = 0, ph = 0; i < n_stages; ++i) {
+          if (i >= S) mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive(&full_bar[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        return;
+      }
       for (int i = 0; i < pre; ++i) load_w(i, i);
       pdl_wait();
       for (int i = 0; i < pre; ++i) load_x(i, i);
@@ -150,10 +198,99 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
     return;
   }
 
+  if (!kScaleInA && warp == kXsumWarp) {
+    // ---------------- activation sums (offset-code family) ----------------
+    // Per unit, k-half kh and token block tb: {-C[m], -S[m]} with C = 1024 sum_lo x + 64 sum_hi x and
+    // S = sum x over the k-half (see process_unit), by one MMA per k-step with a constant A operand
+    // (rows 0-7: -1024 on lo slots, -64 on hi slots; rows 8-15: -1). The MMA sums exactly like the
+    // consumers' own MMAs, so the offsets cancel to within fp32 rounding.
+    const int g8 = lane >> 2, c4 = lane & 3;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < n_stages; ++i) {
+      const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+      mbar_wait(&full_bar[s], ph);
+      const uint32_t st = smem_base + s * C::kStage;
+      const uint32_t sb = sums_base + s * C::kSumBytes;
+      // all (unit, k-half, token-block) chains of the stage interleaved (independent accumulators)
+      auto run = [&](auto nu_c) {
+        constexpr int NU = decltype(nu_c)::value;
+        float cs[NU][2][NTB][4];
+#pragma unroll
+        for (int j = 0; j < NU; ++j)
+#pragma unroll
+          for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) cs[j][kh][tb][0] = cs[j][kh][tb][1] = cs[j][kh][tb][2] = cs[j][kh][tb][3] = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+            for (int j = 0; j < NU; ++j)
+#pragma unroll
+              for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                for (int tb = 0; tb < NTB; ++tb) {
+                  const int m = 8 * tb + g8;
+                  const uint2 xv = lds64(st + j * C::kXUnit + kh * C::kXBox + m * 128 + (((4 * cc + c4) ^ (m & 7)) << 4) + 8 * hs);
+                  mma_16816_nv(cs[j][kh][tb], 0xE400E400u, 0xBC00BC00u, 0xD400D400u, 0xBC00BC00u, xv.x, xv.y);
+                }
+        if (g8 == 0) {
+#pragma unroll
+          for (int j = 0; j < NU; ++j)
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+              for (int tb = 0; tb < NTB; ++tb)
+                sts128(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16, cs[j][kh][tb][0], cs[j][kh][tb][1], cs[j][kh][tb][2],
+                       cs[j][kh][tb][3]);
+        }
+      };
+      if (p.dbg & 32) {
+      } else if (nu == kR) {
+        run(std::integral_constant<int, kR>{});
+      } else {
+        for (int j0 = 0; j0 < nu; ++j0) {   // ragged last stage: one unit at a time
+          const uint32_t st1 = st + j0 * C::kXUnit, sb1 = sb + j0 * 2 * NTB * 4 * 16;
+          float cs[2][NTB][4];
+#pragma unroll
+          for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) cs[kh][tb][0] = cs[kh][tb][1] = cs[kh][tb][2] = cs[kh][tb][3] = 0.f;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+              for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                for (int tb = 0; tb < NTB; ++tb) {
+                  const int m = 8 * tb + g8;
+                  const uint2 xv = lds64(st1 + kh * C::kXBox + m * 128 + (((4 * cc + c4) ^ (m & 7)) << 4) + 8 * hs);
+                  mma_16816_nv(cs[kh][tb], 0xE400E400u, 0xBC00BC00u, 0xD400D400u, 0xBC00BC00u, xv.x, xv.y);
+                }
+          if (g8 == 0) {
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+              for (int tb = 0; tb < NTB; ++tb)
+                sts128(sb1 + ((kh * NTB + tb) * 4 + c4) * 16, cs[kh][tb][0], cs[kh][tb][1], cs[kh][tb][2], cs[kh][tb][3]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sums_bar[s]);
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+    return;
+  }
+
   // ---------------- consumers ----------------
+  trace_ma(p, 0);
   pdl_wait();   // Y / workspace writes must follow the preceding kernel (returns at once when satisfied)
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
-  const int rq = warp & 3, kh = warp >> 2;    // row quarter, k half
+  const int rq = warp & 3, kh = (warp >> 2) & 1, grp = warp >> 3;   // row quarter, k half, unit group
   int rows[2][2];                              // tile rows owned by this lane: [m-tile][g / g+8]
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
@@ -168,26 +305,31 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
   bool first_segment = true;
 
   auto flush = [&](int t, int sg0, int sg1, bool is_first_seg) {
-    // 1. combine the two k-halves: kh = 1 hands its partial sums to kh = 0 through shared memory
-    if (kh == 1) {
+    // 1. combine the k-halves and unit groups: every (grp, kh) != (0, 0) hands its partial sums to
+    //    (0, 0) through shared memory; (0, 0) adds them in fixed slot order
+    const int slot_id = grp * 2 + kh;   // 0 = owner
+    if (slot_id != 0) {
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) red[(((rq * 2 + mt) * NTB + tb) * 4 + e) * 32 + lane] = acc[mt][tb][e];
+          for (int e = 0; e < 4; ++e)
+            red[((((slot_id - 1) * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane] = acc[mt][tb][e];
     }
     named_bar_sync(1, kWarps * 32);
-    if (kh == 0) {
+    if (slot_id == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int sl = 0; sl < C::kRedSlots; ++sl)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb)
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((rq * 2 + mt) * NTB + tb) * 4 + e) * 32 + lane];
+          for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((sl * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane];
     }
     named_bar_sync(1, kWarps * 32);
-    if (kh == 1) return;
+    if (slot_id != 0) return;
     // 2. the four kh = 0 warps own the result
     const int tile_u0 = t * p.Gk, tile_u1 = tile_u0 + p.Gk;
     auto store = [&](float (&v)[2][NTB][4]) {
@@ -246,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
 
   // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
   // dequant + 16 MMAs, then the post-MMA group scale.
-  auto process_unit = [&](uint32_t st, int j) {
+  auto process_unit = [&](uint32_t st, uint32_t sb, int j) {
     const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
     const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
     uint4 xr[2][NTB];
@@ -268,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
           const int r = rows[mt][hf], pch = 2 * kh + cc;
           wq[cc][mt][hf] = lds32(ub + r * 64 + ((pch ^ ((r >> 1) & 3)) << 4) + 4 * c4);
         }
-    float sc[2][2];
+    float sc[2][2], zrow[2][2];
     __half2 zp[2][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -278,9 +420,11 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
         if (SYM) {
           sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
           zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
+          zrow[mt][hf] = 8.f;
         } else {
           const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
           sc[mt][hf] = __low2float(sz);
+          zrow[mt][hf] = __high2float(sz);
           zp[mt][hf] = zero_pair(__high2half(sz));
         }
       }
@@ -311,42 +455,74 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
             }
           }
     } else {
-      float gacc[2][NTB][4];
+      // Post-scale with offset codes: one LOP3 per code pair, no zero-point arithmetic.
+      //   lo slots: (w & 0x000F000F) | 0x6400 -> 1024 + q      hi slots: (w & 0x00F000F0) | 0x5400 -> 64 + q
+      // so the MMA sums sum_k (off_k + q_k) x_k. The offsets and the zero point come back out as
+      //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
+      // with C and S of this unit's k-half supplied by the activation-sum warp and folded into the
+      // initial group accumulator: gacc0 = -C - z S.
+      float cs[NTB][4];   // {-C[m0], -C[m0+1], -S[m0], -S[m0+1]} of this unit's k-half (activation-sum warp)
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb) {
+        const float4 v = lds128f(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16);
+        cs[tb][0] = v.x; cs[tb][1] = v.y; cs[tb][2] = v.z; cs[tb][3] = v.w;
+      }
+      float zf[2][2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) gacc[mt][tb][0] = gacc[mt][tb][1] = gacc[mt][tb][2] = gacc[mt][tb][3] = 0.f;
+        for (int hf = 0; hf < 2; ++hf) zf[mt][hf] = SYM ? 8.f : zrow[mt][hf];
+      // m-tiles innermost when registers allow (NTB = 1): the two accumulation chains alternate, so a
+      // dependent MMA is never issued right behind its predecessor; at NTB = 2 the token blocks alternate.
+      constexpr int kMtGroups = NTB == 1 ? 1 : 2;
+      constexpr int kMtPer = 2 / kMtGroups;
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc)
+      for (int mg = 0; mg < kMtGroups; ++mg) {
+        float gacc[kMtPer][NTB][4];
 #pragma unroll
-        for (int hs = 0; hs < 2; ++hs)            // k-step within the chunk: pairs (0,1),(2,3) or (4,5),(6,7)
+        for (int mi = 0; mi < kMtPer; ++mi)
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
-            const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-            const uint32_t a0 = dq_lo(qa, zp[mt][0]), a1 = dq_lo(qb, zp[mt][1]);
-            const uint32_t a2 = dq_hi(qa, zp[mt][0]), a3 = dq_hi(qb, zp[mt][1]);
-            // MMA k-step uses physical k = 32 pch + 8 c4 + 4 hs + {0..3}: logical {2c,2c+1} <- {0,1},
-            // {2c+8,2c+9} <- {2,3}; the activations use the same permutation.
+          for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) {
-              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-              mma_16816(gacc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            for (int e = 0; e < 4; ++e)
+              gacc[mi][tb][e] = fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+            for (int mi = 0; mi < kMtPer; ++mi) {
+              const int mt = mg * kMtPer + mi;
+              const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
+              const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
+              const uint32_t a0 = lop3_and_or(qa, 0x000F000Fu, 0x64006400u), a1 = lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
+              const uint32_t a2 = lop3_and_or(qa, 0x00F000F0u, 0x54005400u), a3 = lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
+#pragma unroll
+              for (int tb = 0; tb < NTB; ++tb) {
+                const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
+                mma_16816_nv(gacc[mi][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+              }
             }
+#pragma unroll
+        for (int mi = 0; mi < kMtPer; ++mi)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const int mt = mg * kMtPer + mi;
+            acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mi][tb][0], acc[mt][tb][0]);
+            acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mi][tb][1], acc[mt][tb][1]);
+            acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mi][tb][2], acc[mt][tb][2]);
+            acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mi][tb][3], acc[mt][tb][3]);
           }
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mt][tb][0], acc[mt][tb][0]);
-          acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mt][tb][1], acc[mt][tb][1]);
-          acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mt][tb][2], acc[mt][tb][2]);
-          acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mt][tb][3], acc[mt][tb][3]);
-        }
+      }
     }
   };
   auto begin_segment = [&](int u) {
-    if (cur_t >= 0) { flush(cur_t, seg_u0, u, first_segment); first_segment = false; }
+    if (cur_t >= 0) {
+      if (first_segment) trace_ma(p, 4);
+      flush(cur_t, seg_u0, u, first_segment);
+      if (first_segment) trace_ma(p, 5);
+      first_segment = false;
+    }
     cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
     boundary = (cur_t + 1) * p.Gk;
     seg_u0 = u;
@@ -356,25 +532,50 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_w4a16_mma_kernel(const __gri
       for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
   };
 
-  for (int i = 0; i < n_stages; ++i) {
-    const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-    mbar_wait(&full_bar[s], ph);
-    const uint32_t st = smem_base + s * C::kStage;
-    if (nu == kR && cur_t >= 0 && u0 + kR <= boundary) {
-      // fast path (no tile boundary inside the stage): both units back to back
-#pragma unroll
-      for (int j = 0; j < kR; ++j) process_unit(st, j);
-    } else {
+  const uint32_t ready_base = smem_u32(kScaleInA ? &full_bar[0] : &sums_bar[0]);
+  const uint32_t empty_base = smem_u32(&empty_bar[0]);
+  const bool skip_compute = W4A16_MMA_DIAG && (p.dbg & 1);   // diagnostics only
+  auto stage_begin = [&](int i) {
+    if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
+    else mbar_wait_a(ready_base + 8 * s, ph);
+    if (i == 0) trace_ma(p, 1);
+  };
+  auto stage_end = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(empty_base + 8 * s);
+    if (++s == S) { s = 0; ph ^= 1; }
+  };
+  const int n_full = (u_end - u_begin) / kR;   // stages holding kR units
+  int i = 0;
+  while (i < n_stages) {
+    // a stage that starts a segment, crosses a tile boundary or is the ragged last one
+    {
+      const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+      stage_begin(i);
+      const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+      // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
       for (int j = 0; j < nu; ++j) {
         if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
-        process_unit(st, j);
+        if ((j >> 1) == grp && !skip_compute) process_unit(st, sb, j);
       }
+      stage_end();
+      ++i;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
-    if (++s == S) { s = 0; ph ^= 1; }
+    // then the run of full stages inside the current tile: no per-stage bookkeeping
+    const int i_end = min(n_full, (boundary - u_begin) / kR);
+    for (; i < i_end; ++i) {
+      stage_begin(i);
+      const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+      if (!skip_compute) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) process_unit(st, sb, 2 * grp + j);
+      }
+      stage_end();
+    }
   }
+  trace_ma(p, 2);
   if (cur_t >= 0) flush(cur_t, seg_u0, u_end, first_segment);
+  trace_ma(p, 3);
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
@@ -389,17 +590,22 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
     attr_set = true;
   }
-  return launch_pdl(kern, dim3(p.G), dim3(kThreads), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
+  return launch_pdl(kern, dim3(p.G), dim3(threads_for<kScaleInA>()), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
                                                                                              : W4A16_ERR_CUDA;
 }
 
 }  // namespace ma
 }  // namespace w4
 
+extern "C" int w4a16_debug_trace_mma(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, w4::ma::g_trace_ma, bytes < sizeof(w4::ma::g_trace_ma) ? bytes : sizeof(w4::ma::g_trace_ma)) ==
+                 cudaSuccess ? 0 : -5;
+}
+
 // Plan (depends on K, N and the SM count only).
 extern "C" int w4a16_mma_plan_ctas(int K, int N, int num_sms) {
   const long long U = (long long)(N / w4::ma::kTileN) * (K / w4::ma::kTileK);
-  long long G = 2LL * num_sms;
+  long long G = (long long)w4::ma::kCtasPerSm * num_sms;
   if (G > U) G = U;
   return (int)G;
 }
@@ -423,6 +629,9 @@ extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint
   const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
+  static int dbg = -1;
+  if (dbg < 0) { const char* e = getenv("W4A16_MMA_DEBUG"); dbg = e ? atoi(e) : 0; }
+  p.dbg = dbg;
   const bool sym = mode == W4A16_SYM;
 #define W4_MA_CASE(NTB)                                                                                \
   case NTB:                                                                                             \

@@ -1,2 +1,8 @@
 #!/bin/bash
-for f in 0 2; do for m in 1 8 16; do timeout 60 python tools/probe_tc.py --family $f --M $m --R 4 --tag fam${f}_m$m 2>&1 | grep -v Warn; done; done
+for fm in "0 1" "0 8" "0 16" "2 16"; do set -- $fm
+timeout 60 python tools/probe_tc.py --family $1 --M $2 --R 4 --tag GU_fam${1}_m${2} 2>&1 | grep -v Warn
+done
+for d in 2 34; do W4A16_MMA_DEBUG=$d timeout 60 python tools/probe_tc.py --family 0 --M 8 --R 4 --tag GU_fam0_m8_d$d 2>&1 | grep -v Warn; done
+for fm in "0 8" "0 16"; do set -- $fm
+timeout 60 python tools/probe_tc.py --K 8192 --N 8192 --family $1 --M $2 --R 16 --tag O_fam${1}_m${2} 2>&1 | grep -v Warn
+done
