@@ -200,11 +200,16 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
   if (!kScaleInA && warp == kXsumWarp) {
     // ---------------- activation sums (offset-code family) ----------------
-    // Per unit, k-half kh and token block tb: {-C[m], -S[m]} with C = 1024 sum_lo x + 64 sum_hi x and
-    // S = sum x over the k-half (see process_unit), by one MMA per k-step with a constant A operand
-    // (rows 0-7: -1024 on lo slots, -64 on hi slots; rows 8-15: -1). The MMA sums exactly like the
-    // consumers' own MMAs, so the offsets cancel to within fp32 rounding.
+    // Per unit, k-half kh and token m: {-C[m], -S[m]} with C = 1024 sum_lo x + 64 sum_hi x and S = sum x
+    // over the k-half (see process_unit). One MMA per k-step with the activations as the A operand (16
+    // MMA rows = the two k-halves' 8 tokens at NTB = 1, or one k-half's 16 tokens at NTB = 2) and a
+    // constant B (column 0: -1024 on lo slots, -64 on hi slots; column 1: -1): D[row][0] = -C, D[row][1] = -S.
+    // The tensor core sums these products exactly like the consumers' own MMAs, so the offsets cancel to
+    // fp32 rounding. The activation fragments are the consumers' own B fragments, re-read as A.
     const int g8 = lane >> 2, c4 = lane & 3;
+    const uint32_t b0 = g8 == 0 ? 0xE400E400u : g8 == 1 ? 0xBC00BC00u : 0u;   // lo k slots
+    const uint32_t b1 = g8 == 0 ? 0xD400D400u : g8 == 1 ? 0xBC00BC00u : 0u;   // hi k slots
+    constexpr int kPasses = NTB == 1 ? 1 : 2;   // MMAs per k-step and unit (k-halves at NTB = 2)
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < n_stages; ++i) {
@@ -212,16 +217,13 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       mbar_wait(&full_bar[s], ph);
       const uint32_t st = smem_base + s * C::kStage;
       const uint32_t sb = sums_base + s * C::kSumBytes;
-      // all (unit, k-half, token-block) chains of the stage interleaved (independent accumulators)
-      auto run = [&](auto nu_c) {
+      auto run = [&](auto nu_c, int jbase) {
         constexpr int NU = decltype(nu_c)::value;
-        float cs[NU][2][NTB][4];
+        float d[NU][kPasses][4];
 #pragma unroll
         for (int j = 0; j < NU; ++j)
 #pragma unroll
-          for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) cs[j][kh][tb][0] = cs[j][kh][tb][1] = cs[j][kh][tb][2] = cs[j][kh][tb][3] = 0.f;
+          for (int pz = 0; pz < kPasses; ++pz) d[j][pz][0] = d[j][pz][1] = d[j][pz][2] = d[j][pz][3] = 0.f;
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -229,55 +231,35 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 #pragma unroll
             for (int j = 0; j < NU; ++j)
 #pragma unroll
-              for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-                for (int tb = 0; tb < NTB; ++tb) {
-                  const int m = 8 * tb + g8;
-                  const uint2 xv = lds64(st + j * C::kXUnit + kh * C::kXBox + m * 128 + (((4 * cc + c4) ^ (m & 7)) << 4) + 8 * hs);
-                  mma_16816_nv(cs[j][kh][tb], 0xE400E400u, 0xBC00BC00u, 0xD400D400u, 0xBC00BC00u, xv.x, xv.y);
-                }
-        if (g8 == 0) {
+              for (int pz = 0; pz < kPasses; ++pz) {
+                // A rows g8 / g8+8: (kh 0 / kh 1, token g8) at NTB = 1; (kh = pz, token g8 / 8+g8) at NTB = 2
+                const int kh0 = NTB == 1 ? 0 : pz, kh1 = NTB == 1 ? 1 : pz;
+                const int m0 = g8, m1 = NTB == 1 ? g8 : 8 + g8;
+                const uint32_t xu = st + (jbase + j) * C::kXUnit + (((4 * cc + c4) ^ (g8 & 7)) << 4) + 8 * hs;
+                const uint2 r0 = lds64(xu + kh0 * C::kXBox + m0 * 128);
+                const uint2 r1 = lds64(xu + kh1 * C::kXBox + m1 * 128);
+                mma_16816_nv(d[j][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
+              }
+        if (c4 == 0) {
 #pragma unroll
           for (int j = 0; j < NU; ++j)
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh)
+            for (int pz = 0; pz < kPasses; ++pz)
 #pragma unroll
-              for (int tb = 0; tb < NTB; ++tb)
-                sts128(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16, cs[j][kh][tb][0], cs[j][kh][tb][1], cs[j][kh][tb][2],
-                       cs[j][kh][tb][3]);
+              for (int rh = 0; rh < 2; ++rh) {   // D rows g8 (rh 0) and g8+8 (rh 1)
+                const int kh = NTB == 1 ? rh : pz;
+                const int m = NTB == 1 ? g8 : 8 * rh + g8;
+                const uint32_t slot = sb + ((((jbase + j) * 2 + kh) * NTB + (m >> 3)) * 4 + ((m & 7) >> 1)) * 16 + 4 * (m & 1);
+                sts32f(slot, d[j][pz][2 * rh]);          // -C[m]
+                sts32f(slot + 8, d[j][pz][2 * rh + 1]);  // -S[m]
+              }
         }
       };
       if (p.dbg & 32) {
       } else if (nu == kR) {
-        run(std::integral_constant<int, kR>{});
+        run(std::integral_constant<int, kR>{}, 0);
       } else {
-        for (int j0 = 0; j0 < nu; ++j0) {   // ragged last stage: one unit at a time
-          const uint32_t st1 = st + j0 * C::kXUnit, sb1 = sb + j0 * 2 * NTB * 4 * 16;
-          float cs[2][NTB][4];
-#pragma unroll
-          for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) cs[kh][tb][0] = cs[kh][tb][1] = cs[kh][tb][2] = cs[kh][tb][3] = 0.f;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-              for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-                for (int tb = 0; tb < NTB; ++tb) {
-                  const int m = 8 * tb + g8;
-                  const uint2 xv = lds64(st1 + kh * C::kXBox + m * 128 + (((4 * cc + c4) ^ (m & 7)) << 4) + 8 * hs);
-                  mma_16816_nv(cs[kh][tb], 0xE400E400u, 0xBC00BC00u, 0xD400D400u, 0xBC00BC00u, xv.x, xv.y);
-                }
-          if (g8 == 0) {
-#pragma unroll
-            for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-              for (int tb = 0; tb < NTB; ++tb)
-                sts128(sb1 + ((kh * NTB + tb) * 4 + c4) * 16, cs[kh][tb][0], cs[kh][tb][1], cs[kh][tb][2], cs[kh][tb][3]);
-          }
-        }
+        for (int j0 = 0; j0 < nu; ++j0) run(std::integral_constant<int, 1>{}, j0);   // ragged last stage
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sums_bar[s]);
