@@ -159,6 +159,16 @@ __device__ __forceinline__ void sts32f(uint32_t addr, float a) {
 __device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
+// Release-increment of a global counter (prior writes of the CTA, ordered by a preceding barrier, become
+// visible first) without waiting for the result; and the matching acquire load.
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 // (w & mask) | magic in one LOP3.
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t w, uint32_t mask, uint32_t magic) {
   uint32_t r;

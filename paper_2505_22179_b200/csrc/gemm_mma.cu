@@ -67,7 +67,7 @@ struct Cfg {
 struct GemmParams {
   const uint8_t* packed;
   uint16_t* Y;
-  float* partials;   // [2G][4 rq][NTB][2 mt][32 lanes] float4
+  float* partials;   // [G][4 rq][NTB][2 mt][32 lanes] float4 (a CTA publishes at most its first segment)
   int* counters;     // [N/128]
   int M, K, N;
   int Gk;            // K / 128 groups per n-tile
@@ -333,39 +333,40 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       }
     };
     if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); return; }
-    // split tile: publish the fp32 partial, the last contributor reduces in CTA order.
-    const int slot = 2 * cta + (is_first_seg ? 0 : 1);
-    float4* part = reinterpret_cast<float4*>(p.partials);
-    auto pidx = [&](int sl, int tb, int mt) { return ((((size_t)sl * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int tb = 0; tb < NTB; ++tb)
-        __stcg(&part[pidx(slot, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
-    __threadfence();
-    named_bar_sync(2, 4 * 32);
+    // Split tile: the tile's first CTA c_first owns it. It handles the tile's head as its
+    // LAST segment, so it finishes after every other contributor has long published its (first-segment)
+    // fp32 partial: contributors store, then release-increment the tile counter and move on (no round
+    // trip); the owner acquires the counter, adds the partials in CTA order to its own and writes Y.
+    // All G CTAs are co-resident (G = resident capacity), so the owner's wait always completes.
     const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
-    if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[t], 1) == c_last - c_first);
+    float4* part = reinterpret_cast<float4*>(p.partials);
+    auto pidx = [&](int c, int tb, int mt) { return ((((size_t)c * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
+    if (cta != c_first) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb)
+          __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
+      named_bar_sync(2, 4 * 32);
+      if (threadIdx.x == 0) red_release_gpu_add(&p.counters[t], 1);
+      return;
+    }
+    if (threadIdx.x == 0) {
+      const int want = c_last - c_first;
+      while (ld_acquire_gpu(&p.counters[t]) != want) __nanosleep(32);
+      p.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch
+    }
     named_bar_sync(2, 4 * 32);
-    if (!s_last) return;
-    __threadfence();
-    float sum[2][NTB][4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) sum[mt][tb][0] = sum[mt][tb][1] = sum[mt][tb][2] = sum[mt][tb][3] = 0.f;
-    for (int c = c_first; c <= c_last; ++c) {
-      const int sl = 2 * c + (unit_begin(c, p.U, p.G) >= tile_u0 ? 0 : 1);
+    for (int c = c_first + 1; c <= c_last; ++c) {
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
-          const float4 v = __ldcg(&part[pidx(sl, tb, mt)]);
-          sum[mt][tb][0] += v.x; sum[mt][tb][1] += v.y; sum[mt][tb][2] += v.z; sum[mt][tb][3] += v.w;
+          const float4 v = __ldcg(&part[pidx(c, tb, mt)]);
+          acc[mt][tb][0] += v.x; acc[mt][tb][1] += v.y; acc[mt][tb][2] += v.z; acc[mt][tb][3] += v.w;
         }
     }
-    store(sum);
-    if (threadIdx.x == 0) p.counters[t] = 0;   // all contributors have arrived: safe to re-arm
+    store(acc);
   };
 
   // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
@@ -596,7 +597,7 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
   const int ntb = (M + 7) / 8;
   const int G = w4a16_mma_plan_ctas(K, N, num_sms);
   const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
-  return counters + (size_t)2 * G * 4 * ntb * 2 * 32 * 16;
+  return counters + (size_t)G * 4 * ntb * 2 * 32 * 16;
 }
 
 extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
