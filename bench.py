@@ -57,6 +57,14 @@ def parse():
     return ap.parse_args()
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -178,6 +186,9 @@ def run_reference(args):
 # --------------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    if os.environ.get("BENCH_WATCHDOG"):   # diagnostics: dump the Python stack if the run stalls
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -212,6 +223,7 @@ def main():
     stack = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
                            device=dev)
     build_s = time.perf_counter() - t0
+    log(f"built {n_layers} layers ({stack.weight_bytes / 1e9:.2f} GB packed) in {build_s:.1f}s")
     # activations (seeded, in HBM) and a draft tree of the headline width
     for name, buf, tid in (("x_qkv", stack.x_qkv, 1), ("x_o", stack.x_o, 2), ("x_mlp", stack.x_mlp, 3)):
         synth.gpu(args.seed, synth.tensor_id(0xFFF, tid, rank), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
@@ -252,7 +264,9 @@ def main():
     clocks = ClockSampler(local) if rank == 0 else None
     bytes_all_ranks = stack.weight_bytes * world  # shards partition the model: == full model bytes
     gH = stack.capture(args.M)
+    log(f"captured M={args.M}")
     ms = time_graph(gH, args.steps, args.warmup)
+    log(f"headline M={args.M}: {ms:.3f} ms/step")
     value = bytes_all_ranks / (ms * 1e-3) / 1e12
 
     # M sweep (same protocol)
@@ -260,6 +274,7 @@ def main():
     for M in sweep:
         g = stack.capture(M)
         msM = time_graph(g, args.sweep_steps, 3)
+        log(f"sweep M={M}: {msM:.3f} ms/forward")
         m_sweep[str(M)] = {"ms_per_forward": msM, "us_per_layer": 1e3 * msM / n_layers,
                            "TBps": bytes_all_ranks / (msM * 1e-3) / 1e12}
     peak_gbs, peak_src = hbm_peak()
@@ -294,6 +309,7 @@ def main():
         e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    log(f"e2e: {ms_e2e:.3f} ms/step")
     acc = host_out["accept"][:3].tolist()
 
     # per-kernel breakdown: each GEMM kind back-to-back over all layers (distinct weights), one graph each
@@ -314,6 +330,7 @@ def main():
                 for L in stack.layers:
                     L[name](xin, yout, stack.ws, stream)
             msk = time_graph(g, max(3, args.steps // 2), 2) / n_layers
+            log(f"kernel {name}: {1e3 * msk:.2f} us")
             wb = stack.layers[0][name].weight_bytes
             kernels[name] = {"K": s["K"], "N": s["N"], "us": 1e3 * msk, "weight_MB": wb / 1e6,
                              "GBps": wb / (msk * 1e-3) / 1e9, "frac_hbm": wb / (msk * 1e-3) / 1e9 / peak_gbs,

@@ -62,6 +62,7 @@ enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 =
 #define W4A16_GROUP 128
 #define W4A16_MAX_M 64
 #define W4A16_MAX_TREE 1024
+#define W4A16_MAX_N 1048576   /* N limit: the workspace holds a fixed region of W4A16_MAX_N / 128 tile counters */
 
 typedef struct CUstream_st* w4a16_stream_t;   /* == cudaStream_t */
 
@@ -84,9 +85,11 @@ int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, void* packe
 /* w4a16_unpack — W_hat[K][N] fp16 = fp16_rne((q - z) * s) (test/debug). Bit-exact with the oracle. */
 int w4a16_unpack(const void* packed, int K, int N, int group, int mode, uint16_t* W_hat, w4a16_stream_t stream);
 
-/* Workspace bytes w4a16_gemm needs for this shape (split-K partials + one counter per 128-column tile).
+/* Workspace bytes w4a16_gemm needs for this shape. Layout: a fixed region of W4A16_MAX_N / 128 int32 tile
+ * counters (32 KiB, the same offset for every shape) followed by the fp32 split-K partials of this shape.
  * Before its first use the workspace must be zero-filled (w4a16_workspace_init); every w4a16_gemm leaves
- * it zeroed again, so one workspace serves any sequence of calls on one stream. Returns 0 on bad shape. */
+ * the counters zeroed again, so one workspace, sized by the maximum over the shapes it serves, can be
+ * shared by any sequence of calls of any shapes on one stream. Returns 0 on bad shape. */
 size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group);
 int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
 

@@ -32,7 +32,7 @@ int num_sms_of_current_device() {
 
 int check_kn(int K, int N, int group) {
   if (group != W4A16_GROUP) return W4A16_ERR_ARG;
-  if (K <= 0 || N <= 0 || K % 128 != 0 || N % 128 != 0) return W4A16_ERR_SHAPE;
+  if (K <= 0 || N <= 0 || K % 128 != 0 || N % 128 != 0 || N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
   return W4A16_OK;
 }
 

@@ -5,7 +5,13 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include "w4a16.h"
+
 namespace w4 {
+
+// GEMM workspace: a fixed region of tile counters (same offset for every shape, so GEMMs of different N
+// can share one workspace), then the fp32 split-K partials (include/w4a16.h).
+constexpr size_t kCounterBytes = (size_t)(W4A16_MAX_N / 128) * 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -68,7 +68,7 @@ struct GemmParams {
   const uint8_t* packed;
   uint16_t* Y;
   float* partials;   // [G][4 rq][NTB][2 mt][32 lanes] float4 (a CTA publishes at most its first segment)
-  int* counters;     // [N/128]
+  int* counters;     // [W4A16_MAX_N/128], shared by every shape (fixed offset)
   int M, K, N;
   int Gk;            // K / 128 groups per n-tile
   int U;             // total units
@@ -596,7 +596,7 @@ extern "C" int w4a16_mma_plan_ctas(int K, int N, int num_sms) {
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
   const int ntb = (M + 7) / 8;
   const int G = w4a16_mma_plan_ctas(K, N, num_sms);
-  const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
+  const size_t counters = w4::kCounterBytes;
   return counters + (size_t)G * 4 * ntb * 2 * 32 * 16;
 }
 
@@ -609,7 +609,7 @@ extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint
   p.Gk = K / w4::ma::kTileK;
   p.U = (N / w4::ma::kTileN) * p.Gk;
   p.G = w4a16_mma_plan_ctas(K, N, num_sms);
-  const size_t counters = (((size_t)(N / w4::ma::kTileN) * 4) + 255) / 256 * 256;
+  const size_t counters = w4::kCounterBytes;
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
   static int dbg = -1;

@@ -65,7 +65,7 @@ struct Params {
   const uint8_t* packed;
   uint16_t* Y;
   float* partials;   // [2G][MPAD][128] fp32
-  int* counters;     // [N/128]
+  int* counters;     // [W4A16_MAX_N/128], shared by every shape (fixed offset)
   int M, K, N, Gk, U, G;
   int dbg;           // diagnostics only (W4A16_TC_DEBUG): bit0 skip MMA, bit1 skip dequant, bit2 skip X TMA
 };
@@ -449,7 +449,7 @@ extern "C" int w4a16_tc_plan_ctas(int K, int N, int num_sms) {
 
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms) {
   const int mpad = (M + 15) / 16 * 16;
-  const size_t counters = (((size_t)(N / w4::tc::kTileN) * 4) + 255) / 256 * 256;
+  const size_t counters = w4::kCounterBytes;
   return counters + (size_t)2 * w4a16_tc_plan_ctas(K, N, num_sms) * mpad * w4::tc::kTileN * 4;
 }
 
@@ -470,7 +470,7 @@ extern "C" int w4a16_launch_gemm_tc(const uint16_t* X, const void* packed, uint1
   static int dbg = -1;
   if (dbg < 0) { const char* e = getenv("W4A16_TC_DEBUG"); dbg = e ? atoi(e) : 0; }
   p.dbg = dbg;
-  const size_t counters = (((size_t)(N / w4::tc::kTileN) * 4) + 255) / 256 * 256;
+  const size_t counters = w4::kCounterBytes;
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
   const int mpad = (M + 15) / 16 * 16;

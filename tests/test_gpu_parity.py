@@ -334,3 +334,25 @@ def test_gemm_long_streams_and_many_segments():
         ref = P.ref(X)
         for fam in ((0, 2, 1) if M <= 16 else (1,)):
             assert_gemm_close(P.run(X, family=fam), ref, f"K={K} N={N} M={M} family={fam}")
+
+
+@pytest.mark.timeout(300)
+def test_gemm_shared_workspace_across_shapes_and_families():
+    # One workspace serves GEMMs of different N (the verify stack shares one): the tile counters sit at a
+    # fixed offset, so a narrow-N GEMM's partials never land on a wide-N GEMM's counters. Regression test
+    # for a hang: a wide-N owner-reduced launch after a narrow-N split launch found stale counters.
+    w4 = _lib()
+    shapes = [(8192, 256, 7), (2048, 8192, 16), (28672, 512, 40), (1024, 14336, 3), (8192, 256, 64)]
+    probs = [problem(K, N, seed=K * 3 + N) for K, N, _ in shapes]
+    ws = w4.alloc_workspace(64, [(K, N) for K, N, _ in shapes])
+    for rep in range(2):
+        for (K, N, M), P in zip(shapes, probs):
+            X = synth.host(K + N + M, 19, synth.ACT, M, K)
+            ref = P.ref(X)
+            Xd = torch.from_numpy(X.view(np.int16)).cuda().view(torch.float16)
+            for fam in ((1, 0, 2) if M <= 16 else (1,)):
+                Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
+                P.pl(Xd, Y, ws, family=fam)
+                torch.cuda.synchronize()
+                assert_gemm_close(Y, ref, f"shared ws rep={rep} K={K} N={N} M={M} family={fam}")
+                assert int(ws[:4 * (N // 128)].view(torch.int32).abs().sum()) == 0
