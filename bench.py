@@ -352,18 +352,45 @@ def main():
             kernels[name]["other_family"] = {"family": alt, "us": 1e3 * msa, "GBps": wb / (msa * 1e-3) / 1e9}
             del g2
         gate = kernels["gate_up"]
-        roofline = {"bound": "hbm", "kernel": f"w4a16 GEMM gate-up (K={gate['K']}, N={gate['N']}, M={M})",
-                    "achieved": gate["GBps"], "peak": peak_gbs, "unit": "GB/s", "frac": gate["GBps"] / peak_gbs,
-                    "traffic": None, "peak_source": peak_src,
-                    "algorithmic_bytes_per_launch": stack.layers[0]["gate_up"].weight_bytes + 2 * M * (gate["K"] + gate["N"]),
-                    "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA graph, "
-                            "CUDA events on the launching stream)"}
-        fam_tag = "famB" if gate["family"] == w4.W4A16_FAMILY_TCGEN05 else "famA"
-        ncu_path = os.path.join(ROOT, "profiles", f"r01_ncu_{fam_tag}_gateup_M{M}.json")
+        chains = stack.chains(M) if stack.use_chains else None
+        if chains is not None:
+            # dominant kernel = the persistent chain: the whole verify forward (tp = 1) or one segment
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                for c in chains:
+                    c(stream)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gc, stream=stream):
+                for c in chains:
+                    c(stream)
+            msc = time_graph(gc, max(3, args.steps // 2), 2) / len(chains)
+            del gc
+            per_launch = stack.weight_bytes / len(chains)
+            act_bytes = sum(2 * M * (s["K"] + s["N"]) for s in P.values()) * n_layers // len(chains)
+            log(f"chain kernel: {msc:.3f} ms per launch")
+            roofline = {"bound": "hbm", "kernel": f"w4a16 chain kernel ({len(chains)} launch(es) per forward, "
+                                                  f"{stack.chains(M)[0].n} ops per launch, M={M})",
+                        "achieved": per_launch / (msc * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+                        "frac": per_launch / (msc * 1e-3) / 1e9 / peak_gbs, "traffic": None, "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": per_launch + act_bytes,
+                        "note": "achieved = packed weight bytes per launch / its average duration (CUDA events on the "
+                                "launching stream over back-to-back graph replays); activation bytes (L2-resident) "
+                                "listed but not counted"}
+            fam_tag = f"chain_M{M}"
+        else:
+            roofline = {"bound": "hbm", "kernel": f"w4a16 GEMM gate-up (K={gate['K']}, N={gate['N']}, M={M})",
+                        "achieved": gate["GBps"], "peak": peak_gbs, "unit": "GB/s", "frac": gate["GBps"] / peak_gbs,
+                        "traffic": None, "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": stack.layers[0]["gate_up"].weight_bytes + 2 * M * (gate["K"] + gate["N"]),
+                        "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA "
+                                "graph, CUDA events on the launching stream)"}
+            fam_tag = ("famB" if gate["family"] == w4.W4A16_FAMILY_TCGEN05 else "famA") + f"_gateup_M{M}"
+        ncu_path = os.path.join(ROOT, "profiles", f"r01_ncu_{fam_tag}.json")
         if os.path.exists(ncu_path):   # committed ncu --set full capture of this kernel at this M
             try:
                 with open(ncu_path) as f:
-                    roofline["traffic"] = json.load(f)["derived"]["dram_traffic_bytes"]
+                    d = json.load(f)["derived"]
+                roofline["traffic"] = d["dram_traffic_bytes"]
                 roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT)
             except Exception:
                 pass
@@ -398,7 +425,7 @@ def main():
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
                     "api": "VerifyStack.verify_host (pinned host buffers, graph replay, accept result read back)",
                     "accept_result": acc},
-            "gpu_launches": stack.launches_per_forward() * args.steps,
+            "gpu_launches": stack.launches_per_forward(args.M) * args.steps,
             "clocks": clk, "build_s": build_s,
         }
         print(json.dumps(line), flush=True)

@@ -128,6 +128,44 @@ int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* 
  * F % 8 == 0, M >= 1. */
 int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream_t stream);
 
+/* ---- Chains: a verify forward's whole sequence of ops in ONE persistent launch ----------------------
+ * A verify forward is a long sequence of small W4A16 GEMMs (4 per decoder layer, 320 for Llama-3-70B)
+ * whose weights never depend on earlier ops. Launched one by one, every GEMM pays its own pipeline fill
+ * and drain (measured ~6 us each on B200). A chain runs the sequence in one persistent
+ * kernel (one CTA group per SM): the weight stream (TMA) runs ahead across op boundaries, and an op waits
+ * only where it reads a buffer an earlier op writes (RAW), or writes a buffer an earlier op reads or
+ * writes (WAR / WAW). The dependencies are derived on the host from the ops' buffer ranges.
+ * Each GEMM op computes exactly what w4a16_gemm_ex of the same family computes (same split plan, same
+ * reduction order: bit-identical results); each SILU_MUL op exactly what w4a16_silu_mul computes.
+ * All G CTAs of a chain must be co-resident: do not run other kernels concurrently with a chain on the
+ * same device (it is launched as a cooperative kernel). */
+enum { W4A16_OP_GEMM = 0, W4A16_OP_SILU_MUL = 1 };
+typedef struct {
+  int kind;            /* W4A16_OP_GEMM or W4A16_OP_SILU_MUL */
+  const void* X;       /* GEMM: X [M][K] fp16.  SILU_MUL: GU [M][2N] fp16 ([gate | up] per row) */
+  const void* packed;  /* GEMM: packed weight blob of w4a16_pack (K x N, `mode`).  SILU_MUL: NULL */
+  void* Y;             /* GEMM: Y [M][N] fp16.  SILU_MUL: out [M][N] fp16 */
+  int K, N;            /* GEMM: as w4a16_gemm.  SILU_MUL: K = 2N, N = F (N % 8 == 0) */
+  int mode;            /* GEMM: W4A16_ASYM or W4A16_SYM; every GEMM of a chain uses the same mode */
+} w4a16_op;
+
+/* Bytes of the plan (host buffer) for n_ops ops. */
+size_t w4a16_chain_plan_bytes(int n_ops);
+/* Workspace bytes of a chain (tile counters per op, op completion counters, split partials). Zero-fill it
+ * once (w4a16_workspace_init); every chain run leaves its counters zeroed again. 0 on bad arguments. */
+size_t w4a16_chain_workspace_bytes(const w4a16_op* ops, int n_ops, int M, int family);
+/* Encode the chain (job table with TMA descriptors of every X, dependency indices) for width M into the
+ * HOST buffer `plan` (w4a16_chain_plan_bytes(n_ops) bytes). The caller copies it to device memory once
+ * (e.g. cudaMemcpy) and passes that copy to w4a16_chain_run for as long as the buffers stay where they
+ * are. family: W4A16_FAMILY_AUTO or an explicit family valid for M (chains serve the mma.sync families,
+ * M <= 16). Validates every op like w4a16_gemm / w4a16_silu_mul; in-place ops are rejected. */
+int w4a16_chain_plan(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes);
+/* Run a chain: dev_plan = device copy of the plan for (n_ops, M, family); mode = the GEMMs' mode.
+ * workspace: at least w4a16_chain_workspace_bytes(ops, n_ops, M, family) zero-initialised bytes, used by
+ * this chain's plan only. Every GEMM of a chain needs (K/128)*(N/128) >= 2 * SM count. Async on `stream`. */
+int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family, void* workspace,
+                    size_t workspace_bytes, w4a16_stream_t stream);
+
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 

@@ -34,7 +34,18 @@ ABI_SYMBOLS = (
     "w4a16_status_string",
     "w4a16_gemm_family",
     "w4a16_silu_mul",
+    "w4a16_chain_plan_bytes",
+    "w4a16_chain_workspace_bytes",
+    "w4a16_chain_plan",
+    "w4a16_chain_run",
 )
+W4A16_OP_GEMM, W4A16_OP_SILU_MUL = 0, 1
+
+
+class W4A16Op(ctypes.Structure):
+    """struct w4a16_op of include/w4a16.h."""
+    _fields_ = [("kind", ctypes.c_int), ("X", ctypes.c_void_p), ("packed", ctypes.c_void_p), ("Y", ctypes.c_void_p),
+                ("K", ctypes.c_int), ("N", ctypes.c_int), ("mode", ctypes.c_int)]
 
 
 class W4A16Error(RuntimeError):
@@ -62,7 +73,13 @@ def _load():
     lib.w4a16_status_string.restype = ctypes.c_char_p
     lib.w4a16_gemm_family.argtypes = [i32, i32, i32]
     lib.w4a16_silu_mul.argtypes = [vp, i32, i32, vp, vp]
-    for name in ("w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
+    lib.w4a16_chain_plan_bytes.argtypes = [i32]
+    lib.w4a16_chain_plan_bytes.restype = sz
+    lib.w4a16_chain_workspace_bytes.argtypes = [vp, i32, i32, i32]
+    lib.w4a16_chain_workspace_bytes.restype = sz
+    lib.w4a16_chain_plan.argtypes = [vp, i32, i32, i32, vp, sz]
+    lib.w4a16_chain_run.argtypes = [vp, i32, i32, i32, i32, vp, sz, vp]
+    for name in ("w4a16_chain_plan", "w4a16_chain_run", "w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
                  "w4a16_gemm_family", "w4a16_silu_mul"):
         getattr(lib, name).restype = i32
     return lib

@@ -12,6 +12,9 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaS
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op*, int, int, int, int);
+extern "C" int w4a16_chain_plan_sms(const w4a16_op*, int, int, int, void*, size_t, int);
+extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, cudaStream_t);
 extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
                                      cudaStream_t);
 
@@ -123,6 +126,26 @@ extern "C" int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w
   if (M < 1 || F < 8 || F % 8 != 0) return W4A16_ERR_SHAPE;
   if (!aligned16(GU) || !aligned16(out)) return W4A16_ERR_ALIGN;
   return w4a16_launch_silu_mul(GU, M, F, out, (cudaStream_t)stream);
+}
+
+extern "C" size_t w4a16_chain_workspace_bytes(const w4a16_op* ops, int n_ops, int M, int family) {
+  const int sms = num_sms_of_current_device();
+  return sms > 0 ? w4a16_chain_workspace_bytes_sms(ops, n_ops, M, family, sms) : 0;
+}
+
+extern "C" int w4a16_chain_plan(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes) {
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  return w4a16_chain_plan_sms(ops, n_ops, M, family, plan, plan_bytes, sms);
+}
+
+extern "C" int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family, void* workspace,
+                               size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!dev_plan || !workspace) return W4A16_ERR_ARG;
+  if (!aligned16(dev_plan) || !aligned16(workspace)) return W4A16_ERR_ALIGN;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  return w4a16_launch_chain_mma(dev_plan, n_ops, M, mode, family, workspace, workspace_bytes, sms, (cudaStream_t)stream);
 }
 
 extern "C" const char* w4a16_status_string(int status) {

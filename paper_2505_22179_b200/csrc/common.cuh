@@ -197,4 +197,20 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// SiLU(gate) * up on 8 fp16 pairs, fp32 arithmetic, one RNE to fp16 (w4a16_silu_mul and chain SILU ops).
+__device__ __forceinline__ uint4 silu_mul_vec(uint4 g, uint4 u) {
+  const __half2* gh = reinterpret_cast<const __half2*>(&g);
+  const __half2* uh = reinterpret_cast<const __half2*>(&u);
+  uint4 r;
+  __half2* rh = reinterpret_cast<__half2*>(&r);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 gf = __half22float2(gh[j]), uf = __half22float2(uh[j]);
+    const float a = gf.x / (1.0f + __expf(-gf.x)) * uf.x;
+    const float b = gf.y / (1.0f + __expf(-gf.y)) * uf.y;
+    rh[j] = __floats2half2_rn(a, b);
+  }
+  return r;
+}
+
 }  // namespace w4

@@ -25,6 +25,7 @@
 //    the fp32 workspace and the last CTA to arrive (atomic counter per tile) sums the partials in CTA order
 //    (fixed, hence deterministic) and writes fp16 Y, re-zeroing the counter.
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -64,17 +65,63 @@ struct Cfg {
   static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + 1024;
 };
 
+// One op of a chain: the device copy of a w4a16_chain_plan entry (include/w4a16.h). A single w4a16_gemm is
+// a one-op list whose fields come from GemmParams and the kernel's tensor-map parameters.
+enum { kOpGemm = W4A16_OP_GEMM, kOpSilu = W4A16_OP_SILU_MUL };
+struct alignas(64) ChainJob {
+  CUtensorMap xmapR;       // activation boxes of kR units (3-D SWIZZLE_128B)
+  CUtensorMap xmap1;       // activation box of one unit
+  const uint8_t* packed;   // GEMM: packed weights.  SILU: GU [M][2N]
+  uint16_t* Y;             // GEMM: Y [M][N].  SILU: out [M][N]
+  int kind, K, N, Gk, U;
+  int dep_x;               // earlier op whose completion this op's X reads wait for (-1: none)
+  int dep_y;               // earlier op whose completion this op's Y writes wait for (WAR / WAW; -1: none)
+  int cnt_off;             // this op's first tile counter
+};
+
 struct GemmParams {
   const uint8_t* packed;
   uint16_t* Y;
-  float* partials;   // [G][4 rq][NTB][2 mt][32 lanes] float4 (a CTA publishes at most its first segment)
-  int* counters;     // [W4A16_MAX_N/128], shared by every shape (fixed offset)
+  float* partials;   // [slots][G][4 rq][NTB][2 mt][32 lanes] float4 (a CTA publishes at most its first segment per op)
+  int* counters;     // tile counters: [N/128] (single GEMM) or per op at ChainJob::cnt_off (chain)
   int M, K, N;
   int Gk;            // K / 128 groups per n-tile
   int U;             // total units
   int G;             // CTAs
-  int dbg;           // diagnostics only (W4A16_MMA_DEBUG): bit0 skip compute, bit1 skip loads, bit2 backoff waits
+  int dbg;           // diagnostics only (W4A16_MMA_DEBUG): bit0 skip compute, bit2 backoff waits, bit4 trace
+  const ChainJob* jobs;   // chain: the op table (device); nullptr: single GEMM
+  int n_jobs;             // 1 for a single GEMM
+  int* done;              // chain: [n_jobs] CTAs that finished each op, then the exit counter
+  int slots;              // chain: partial-slot ring length in ops (1 for a single GEMM)
 };
+
+struct JobInfo {
+  const uint8_t* packed;
+  uint16_t* Y;
+  const CUtensorMap* mR;
+  const CUtensorMap* m1;
+  int* counters;
+  int kind, N, Gk, U, dep_x, dep_y;
+};
+__device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
+  JobInfo J;
+  if (p.jobs == nullptr) {
+    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters;
+    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1;
+  } else {
+    const ChainJob* c = p.jobs + j;
+    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + c->cnt_off;
+    J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y;
+  }
+  return J;
+}
+// Op j is complete once every CTA has counted it (CTAs walk the ops in order, so op j complete implies
+// every earlier op complete).
+__device__ __forceinline__ void wait_op(const GemmParams& p, int j) {
+  if (j < 0) return;
+  while (ld_acquire_gpu(&p.done[j]) < p.G) __nanosleep(64);
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // Diagnostics only (W4A16_MMA_DEBUG bit 16): per-CTA %globaltimer stamps (entry, first stage ready, main loop
 // done, exit) of consumer warp 0 (tools/probe_tc.py --trace-mma).
@@ -124,6 +171,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                                                                       const GemmParams p) {
   using C = Cfg<NTB, SYM>;
   constexpr int S = C::kStages;
+  static_assert(S <= 8, "producer queue holds at most 8 stages");
   // kScaleInA (family W4A16_FAMILY_MMA_SYNC_S): scale inside the A fragments instead of a per-unit group
   // accumulator — fewer registers (NTB = 2 runs at the 96-register cap of 18 warps/SM), 4 more HMUL2 per
   // word. Post-scale (family W4A16_FAMILY_MMA_SYNC) is faster when registers allow (NTB = 1).
@@ -135,8 +183,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  const int u_begin = unit_begin(cta, p.U, p.G), u_end = unit_begin(cta + 1, p.U, p.G);
-  const int n_stages = (u_end - u_begin + kR - 1) / kR;
+  const bool chain = p.jobs != nullptr;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_base = smem_u32(smem);
   float* red = reinterpret_cast<float*>(smem + S * C::kStage);
@@ -152,48 +199,72 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   if (warp == kProducerWarp) {
     // ---------------- producer ----------------
     // Per stage ONE bulk copy of the packed weights (the TMA engine costs ~100+ cycles per issued copy)
-    // and a 3-D TMA of the activation slices.
+    // and a 3-D TMA of the activation slices. Weights never depend on an earlier kernel or op, so they are
+    // issued as soon as a ring slot frees; a stage's activations wait in a queue until they may be read
+    // (after griddepcontrol.wait for a single GEMM; after the producing op's completion in a chain), so the
+    // weight stream runs ahead across op boundaries.
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
+      if (!chain) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
+      }
       const uint64_t pol = policy_evict_first();
-      auto load_x = [&](int i, int s) {   // activation slices of stage i (written by the preceding kernel)
-        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0), g0 = u0 % p.Gk;
+      int q_s[8], q_j[8], q_u0[8], q_nu[8];   // stages whose activations are not issued yet (FIFO)
+      int q_head = 0, q_n = 0, ok_upto = -1;
+      bool pdl_done = chain;                 // a chain is not launched with PDL
+      auto issue_x = [&](int s, const JobInfo& J, int u0, int nu) {
+        const int g0 = u0 % J.Gk;
         const uint32_t st = smem_base + s * C::kStage;
-        if (nu == kR && g0 + kR <= p.Gk) {
-          tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
+        if (nu == kR && g0 + kR <= J.Gk) {
+          tma_3d(st, J.mR, 0, 0, 2 * g0, &full_bar[s]);
         } else {
-          for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
+          for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, 2 * ((u0 + jj) % J.Gk), &full_bar[s]);
         }
       };
-      auto load_w = [&](int i, int s) {   // packed weights of stage i (never written by a preceding kernel)
-        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-        mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
-        bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+      auto drain = [&](bool block) {   // issue queued activation loads whose producers are done
+        while (q_n > 0) {
+          if (!pdl_done) {
+            if (!block) return;
+            pdl_wait();
+            pdl_done = true;
+          }
+          const JobInfo J = job_at(p, &xmapR, &xmap1, q_j[q_head]);
+          if (J.dep_x > ok_upto) {
+            if (ld_acquire_gpu(&p.done[J.dep_x]) < p.G) {
+              if (!block) return;
+              wait_op(p, J.dep_x);
+            }
+            ok_upto = J.dep_x;
+            fence_proxy_async_global();   // generic-proxy stores of other CTAs -> this TMA (async proxy) read
+          }
+          issue_x(q_s[q_head], J, q_u0[q_head], q_nu[q_head]);
+          q_head = (q_head + 1) & 7;
+          --q_n;
+        }
       };
-      // Weights of the first stages stream while the preceding kernel (PDL) still drains; the activations
-      // it produces are read only after griddepcontrol.wait.
-      const int pre = min(S, n_stages);
-      if (p.dbg & 2) {   // diagnostics: no memory traffic, consumers run on stale shared memory
-        pdl_wait();
-        for (int i = 0, s = 0, ph = 0; i < n_stages; ++i) {
-          if (i >= S) mbar_wait(&empty_bar[s], ph ^ 1);
-          mbar_arrive(&full_bar[s]);
+      int s = 0, issued = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < p.n_jobs; ++j) {
+        const JobInfo J = job_at(p, &xmapR, &xmap1, j);
+        if (J.kind != kOpGemm) continue;
+        const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
+        for (int u0 = u_begin; u0 < u_end; u0 += kR) {
+          const int nu = min(kR, u_end - u0);
+          if (issued >= S) {   // slot s must be released by the consumers first
+            if (!pdl_done) drain(true);
+            while (!mbar_try_wait(&empty_bar[s], ph ^ 1)) drain(false);
+          }
+          mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
+          bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+          const int e = (q_head + q_n) & 7;
+          q_s[e] = s; q_j[e] = j; q_u0[e] = u0; q_nu[e] = nu;
+          ++q_n;
+          drain(false);
+          ++issued;
           if (++s == S) { s = 0; ph ^= 1; }
         }
-        return;
       }
-      for (int i = 0; i < pre; ++i) load_w(i, i);
-      pdl_wait();
-      for (int i = 0; i < pre; ++i) load_x(i, i);
-      int s = pre % S;
-      uint32_t ph = pre == S ? 1 : 0;
-      for (int i = pre; i < n_stages; ++i) {
-        mbar_wait(&empty_bar[s], ph ^ 1);
-        load_w(i, s);
-        load_x(i, s);
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
+      drain(true);
     }
     return;
   }
@@ -212,58 +283,63 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     constexpr int kPasses = NTB == 1 ? 1 : 2;   // MMAs per k-step and unit (k-halves at NTB = 2)
     int s = 0;
     uint32_t ph = 0;
-    for (int i = 0; i < n_stages; ++i) {
-      const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-      mbar_wait(&full_bar[s], ph);
-      const uint32_t st = smem_base + s * C::kStage;
-      const uint32_t sb = sums_base + s * C::kSumBytes;
-      auto run = [&](auto nu_c, int jbase) {
-        constexpr int NU = decltype(nu_c)::value;
-        float d[NU][kPasses][4];
+    for (int j = 0; j < p.n_jobs; ++j) {
+      const JobInfo J = job_at(p, &xmapR, &xmap1, j);
+      if (J.kind != kOpGemm) continue;
+      const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
+      for (int u0 = u_begin; u0 < u_end; u0 += kR) {
+        const int nu = min(kR, u_end - u0);
+        mbar_wait(&full_bar[s], ph);
+        const uint32_t st = smem_base + s * C::kStage;
+        const uint32_t sb = sums_base + s * C::kSumBytes;
+        auto run = [&](auto nu_c, int jbase) {
+          constexpr int NU = decltype(nu_c)::value;
+          float d[NU][kPasses][4];
 #pragma unroll
-        for (int j = 0; j < NU; ++j)
+          for (int jj = 0; jj < NU; ++jj)
 #pragma unroll
-          for (int pz = 0; pz < kPasses; ++pz) d[j][pz][0] = d[j][pz][1] = d[j][pz][2] = d[j][pz][3] = 0.f;
+            for (int pz = 0; pz < kPasses; ++pz) d[jj][pz][0] = d[jj][pz][1] = d[jj][pz][2] = d[jj][pz][3] = 0.f;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc)
+          for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-          for (int hs = 0; hs < 2; ++hs)
+            for (int hs = 0; hs < 2; ++hs)
 #pragma unroll
-            for (int j = 0; j < NU; ++j)
+              for (int jj = 0; jj < NU; ++jj)
 #pragma unroll
-              for (int pz = 0; pz < kPasses; ++pz) {
-                // A rows g8 / g8+8: (kh 0 / kh 1, token g8) at NTB = 1; (kh = pz, token g8 / 8+g8) at NTB = 2
-                const int kh0 = NTB == 1 ? 0 : pz, kh1 = NTB == 1 ? 1 : pz;
-                const int m0 = g8, m1 = NTB == 1 ? g8 : 8 + g8;
-                const uint32_t xu = st + (jbase + j) * C::kXUnit + (((4 * cc + c4) ^ (g8 & 7)) << 4) + 8 * hs;
-                const uint2 r0 = lds64(xu + kh0 * C::kXBox + m0 * 128);
-                const uint2 r1 = lds64(xu + kh1 * C::kXBox + m1 * 128);
-                mma_16816_nv(d[j][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
-              }
-        if (c4 == 0) {
+                for (int pz = 0; pz < kPasses; ++pz) {
+                  // A rows g8 / g8+8: (kh 0 / kh 1, token g8) at NTB = 1; (kh = pz, token g8 / 8+g8) at NTB = 2
+                  const int kh0 = NTB == 1 ? 0 : pz, kh1 = NTB == 1 ? 1 : pz;
+                  const int m0 = g8, m1 = NTB == 1 ? g8 : 8 + g8;
+                  const uint32_t xu = st + (jbase + jj) * C::kXUnit + (((4 * cc + c4) ^ (g8 & 7)) << 4) + 8 * hs;
+                  const uint2 r0 = lds64(xu + kh0 * C::kXBox + m0 * 128);
+                  const uint2 r1 = lds64(xu + kh1 * C::kXBox + m1 * 128);
+                  mma_16816_nv(d[jj][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
+                }
+          if (c4 == 0) {
 #pragma unroll
-          for (int j = 0; j < NU; ++j)
+            for (int jj = 0; jj < NU; ++jj)
 #pragma unroll
-            for (int pz = 0; pz < kPasses; ++pz)
+              for (int pz = 0; pz < kPasses; ++pz)
 #pragma unroll
-              for (int rh = 0; rh < 2; ++rh) {   // D rows g8 (rh 0) and g8+8 (rh 1)
-                const int kh = NTB == 1 ? rh : pz;
-                const int m = NTB == 1 ? g8 : 8 * rh + g8;
-                const uint32_t slot = sb + ((((jbase + j) * 2 + kh) * NTB + (m >> 3)) * 4 + ((m & 7) >> 1)) * 16 + 4 * (m & 1);
-                sts32f(slot, d[j][pz][2 * rh]);          // -C[m]
-                sts32f(slot + 8, d[j][pz][2 * rh + 1]);  // -S[m]
-              }
+                for (int rh = 0; rh < 2; ++rh) {   // D rows g8 (rh 0) and g8+8 (rh 1)
+                  const int kh = NTB == 1 ? rh : pz;
+                  const int m = NTB == 1 ? g8 : 8 * rh + g8;
+                  const uint32_t slot = sb + ((((jbase + jj) * 2 + kh) * NTB + (m >> 3)) * 4 + ((m & 7) >> 1)) * 16 + 4 * (m & 1);
+                  sts32f(slot, d[jj][pz][2 * rh]);          // -C[m]
+                  sts32f(slot + 8, d[jj][pz][2 * rh + 1]);  // -S[m]
+                }
+          }
+        };
+        if (p.dbg & 32) {
+        } else if (nu == kR) {
+          run(std::integral_constant<int, kR>{}, 0);
+        } else {
+          for (int j0 = 0; j0 < nu; ++j0) run(std::integral_constant<int, 1>{}, j0);   // ragged last stage
         }
-      };
-      if (p.dbg & 32) {
-      } else if (nu == kR) {
-        run(std::integral_constant<int, kR>{}, 0);
-      } else {
-        for (int j0 = 0; j0 < nu; ++j0) run(std::integral_constant<int, 1>{}, j0);   // ragged last stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sums_bar[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sums_bar[s]);
-      if (++s == S) { s = 0; ph ^= 1; }
     }
     return;
   }
@@ -283,282 +359,327 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   float acc[2][NTB][4];
   int s = 0;
   uint32_t ph = 0;
-  int cur_t = -1, seg_u0 = u_begin, boundary = 0;
-  bool first_segment = true;
+  const uint32_t ready_base = smem_u32(kScaleInA ? &full_bar[0] : &sums_bar[0]);
+  const uint32_t empty_base = smem_u32(&empty_bar[0]);
+  const bool skip_compute = W4A16_MMA_DIAG && (p.dbg & 1);   // diagnostics only
 
-  auto flush = [&](int t, int sg0, int sg1, bool is_first_seg) {
-    // 1. combine the k-halves and unit groups: every (grp, kh) != (0, 0) hands its partial sums to
-    //    (0, 0) through shared memory; (0, 0) adds them in fixed slot order
-    const int slot_id = grp * 2 + kh;   // 0 = owner
-    if (slot_id != 0) {
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            red[((((slot_id - 1) * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane] = acc[mt][tb][e];
+  for (int job = 0; job < p.n_jobs; ++job) {
+    const JobInfo J = job_at(p, &xmapR, &xmap1, job);
+    if (J.kind == kOpSilu) {
+      // SiLU*mul op of a chain (same arithmetic as w4a16_silu_mul), spread over every consumer thread of
+      // every CTA once the gate-up op that writes GU (and the readers of `out`) are done.
+      if (threadIdx.x == 0) wait_op(p, max(J.dep_x, J.dep_y));
+      named_bar_sync(1, kWarps * 32);
+      const int F = J.N, vecs = F / 8;
+      const long long total = (long long)p.M * vecs;
+      const uint16_t* GU = reinterpret_cast<const uint16_t*>(J.packed);
+      for (long long i = (long long)cta * (kWarps * 32) + threadIdx.x; i < total; i += (long long)p.G * (kWarps * 32)) {
+        const int m = (int)(i / vecs), v = (int)(i % vecs);
+        const uint4 g = __ldcg(reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + (size_t)v * 8));
+        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + F + (size_t)v * 8));
+        *reinterpret_cast<uint4*>(J.Y + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
+      }
+      named_bar_sync(1, kWarps * 32);
+      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+      continue;
     }
-    named_bar_sync(1, kWarps * 32);
-    if (slot_id == 0) {
-#pragma unroll
-      for (int sl = 0; sl < C::kRedSlots; ++sl)
+    const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
+    const int n_stages = (u_end - u_begin + kR - 1) / kR;
+    int cur_t = -1, seg_u0 = u_begin, boundary = 0;
+    bool first_segment = true;
+    // Y writes (and this op's partial slot) wait for the earlier ops that read / write the same buffers.
+    const int wdep = chain ? max(J.dep_y, job - p.slots) : -1;
+    bool y_ready = wdep < 0;
+    float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (4 * NTB * 2 * 32);
+
+    auto flush = [&](int t, int sg0, int sg1) {
+      if (!y_ready) {
+        if (threadIdx.x == 0) wait_op(p, wdep);   // released to the other warps by the barrier below
+        y_ready = true;
+      }
+      // 1. combine the k-halves and unit groups: every (grp, kh) != (0, 0) hands its partial sums to
+      //    (0, 0) through shared memory; (0, 0) adds them in fixed slot order
+      const int slot_id = grp * 2 + kh;   // 0 = owner
+      if (slot_id != 0) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
           for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((sl * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane];
-    }
-    named_bar_sync(1, kWarps * 32);
-    if (slot_id != 0) return;
-    // 2. the four kh = 0 warps own the result
-    const int tile_u0 = t * p.Gk, tile_u1 = tile_u0 + p.Gk;
-    auto store = [&](float (&v)[2][NTB][4]) {
+            for (int e = 0; e < 4; ++e)
+              red[((((slot_id - 1) * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane] = acc[mt][tb][e];
+      }
+      named_bar_sync(1, kWarps * 32);
+      if (slot_id == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int n0 = t * kTileN + rows[mt][0], n1 = t * kTileN + rows[mt][1];
+        for (int sl = 0; sl < C::kRedSlots; ++sl)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
-          if (m0 < p.M) {
-            p.Y[(size_t)m0 * p.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][0]));
-            p.Y[(size_t)m0 * p.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][2]));
-          }
-          if (m1 < p.M) {
-            p.Y[(size_t)m1 * p.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][1]));
-            p.Y[(size_t)m1 * p.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][3]));
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((sl * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane];
+      }
+      named_bar_sync(1, kWarps * 32);
+      if (slot_id != 0) return;
+      // 2. the four kh = 0 warps own the result
+      const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
+      auto store = [&](float (&v)[2][NTB][4]) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int n0 = t * kTileN + rows[mt][0], n1 = t * kTileN + rows[mt][1];
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
+            if (m0 < p.M) {
+              J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][0]));
+              J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][2]));
+            }
+            if (m1 < p.M) {
+              J.Y[(size_t)m1 * J.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][1]));
+              J.Y[(size_t)m1 * J.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][3]));
+            }
           }
         }
+      };
+      if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); return; }
+      // Split tile: the tile's first CTA c_first owns it. It handles the tile's head as its
+      // LAST segment of the op, so it finishes after every other contributor has long published its
+      // (first-segment) fp32 partial: contributors store, then release-increment the tile counter and move
+      // on (no round trip); the owner acquires the counter, adds the partials in CTA order to its own and
+      // writes Y. All G CTAs are co-resident (G = resident capacity), so the owner's wait always completes.
+      const int c_first = cta_of_unit(tile_u0, J.U, p.G), c_last = cta_of_unit(tile_u1 - 1, J.U, p.G);
+      auto pidx = [&](int c, int tb, int mt) { return ((((size_t)c * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
+      if (cta != c_first) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb)
+            __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
+        named_bar_sync(2, 4 * 32);
+        if (threadIdx.x == 0) red_release_gpu_add(&J.counters[t], 1);
+        return;
       }
-    };
-    if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); return; }
-    // Split tile: the tile's first CTA c_first owns it. It handles the tile's head as its
-    // LAST segment, so it finishes after every other contributor has long published its (first-segment)
-    // fp32 partial: contributors store, then release-increment the tile counter and move on (no round
-    // trip); the owner acquires the counter, adds the partials in CTA order to its own and writes Y.
-    // All G CTAs are co-resident (G = resident capacity), so the owner's wait always completes.
-    const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
-    float4* part = reinterpret_cast<float4*>(p.partials);
-    auto pidx = [&](int c, int tb, int mt) { return ((((size_t)c * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
-    if (cta != c_first) {
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb)
-          __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
+      if (threadIdx.x == 0) {
+        const int want = c_last - c_first;
+        while (ld_acquire_gpu(&J.counters[t]) != want) __nanosleep(32);
+        J.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch
+      }
       named_bar_sync(2, 4 * 32);
-      if (threadIdx.x == 0) red_release_gpu_add(&p.counters[t], 1);
-      return;
-    }
-    if (threadIdx.x == 0) {
-      const int want = c_last - c_first;
-      while (ld_acquire_gpu(&p.counters[t]) != want) __nanosleep(32);
-      p.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch
-    }
-    named_bar_sync(2, 4 * 32);
-    for (int c = c_first + 1; c <= c_last; ++c) {
+      for (int c = c_first + 1; c <= c_last; ++c) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const float4 v = __ldcg(&part[pidx(c, tb, mt)]);
+            acc[mt][tb][0] += v.x; acc[mt][tb][1] += v.y; acc[mt][tb][2] += v.z; acc[mt][tb][3] += v.w;
+          }
+      }
+      store(acc);
+    };
+
+    // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
+    // dequant + 16 MMAs, then the post-MMA group scale.
+    auto process_unit = [&](uint32_t st, uint32_t sb, int j) {
+      const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
+      const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
+      uint4 xr[2][NTB];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
-          const float4 v = __ldcg(&part[pidx(c, tb, mt)]);
-          acc[mt][tb][0] += v.x; acc[mt][tb][1] += v.y; acc[mt][tb][2] += v.z; acc[mt][tb][3] += v.w;
+          const int m = 8 * tb + g8;
+          const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
+          xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
-    }
-    store(acc);
-  };
-
-  // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
-  // dequant + 16 MMAs, then the post-MMA group scale.
-  auto process_unit = [&](uint32_t st, uint32_t sb, int j) {
-    const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
-    const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
-    uint4 xr[2][NTB];
+      uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc)
+      for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) {
-        const int m = 8 * tb + g8;
-        const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
-        xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
-      }
-    uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc)
+          for (int hf = 0; hf < 2; ++hf) {
+            const int r = rows[mt][hf], pch = 2 * kh + cc;
+            wq[cc][mt][hf] = lds32(ub + r * 64 + ((pch ^ ((r >> 1) & 3)) << 4) + 4 * c4);
+          }
+      float sc[2][2], zrow[2][2];
+      __half2 zp[2][2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-          const int r = rows[mt][hf], pch = 2 * kh + cc;
-          wq[cc][mt][hf] = lds32(ub + r * 64 + ((pch ^ ((r >> 1) & 3)) << 4) + 4 * c4);
-        }
-    float sc[2][2], zrow[2][2];
-    __half2 zp[2][2];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        const int r = rows[mt][hf];
-        if (SYM) {
-          sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
-          zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
-          zrow[mt][hf] = 8.f;
-        } else {
-          const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
-          sc[mt][hf] = __low2float(sz);
-          zrow[mt][hf] = __high2float(sz);
-          zp[mt][hf] = zero_pair(__high2half(sz));
-        }
-      }
-    if constexpr (kScaleInA) {
-      // w_hat = fp16((q - z) * s) in the A fragments (exactly the oracle's dequantised weight), accumulated
-      // straight into acc: no per-unit group accumulator (saves 16 registers at NTB = 2).
-      __half2 s2[2][2];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) s2[mt][hf] = __float2half2_rn(sc[mt][hf]);
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-        for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
-            const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-            const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[mt][0])), s2[mt][0]));
-            const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[mt][1])), s2[mt][1]));
-            const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[mt][0])), s2[mt][0]));
-            const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[mt][1])), s2[mt][1]));
-#pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) {
-              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-              mma_16816(acc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
-            }
+          const int r = rows[mt][hf];
+          if (SYM) {
+            sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
+            zrow[mt][hf] = 8.f;
+          } else {
+            const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
+            sc[mt][hf] = __low2float(sz);
+            zrow[mt][hf] = __high2float(sz);
+            zp[mt][hf] = zero_pair(__high2half(sz));
           }
-    } else {
-      // Post-scale with offset codes: one LOP3 per code pair, no zero-point arithmetic.
-      //   lo slots: (w & 0x000F000F) | 0x6400 -> 1024 + q      hi slots: (w & 0x00F000F0) | 0x5400 -> 64 + q
-      // so the MMA sums sum_k (off_k + q_k) x_k. The offsets and the zero point come back out as
-      //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
-      // with C and S of this unit's k-half supplied by the activation-sum warp and folded into the
-      // initial group accumulator: gacc0 = -C - z S.
-      float cs[NTB][4];   // {-C[m0], -C[m0+1], -S[m0], -S[m0+1]} of this unit's k-half (activation-sum warp)
+        }
+      if constexpr (kScaleInA) {
+        // w_hat = fp16((q - z) * s) in the A fragments (exactly the oracle's dequantised weight), accumulated
+        // straight into acc: no per-unit group accumulator (saves 16 registers at NTB = 2).
+        __half2 s2[2][2];
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) {
-        const float4 v = lds128f(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16);
-        cs[tb][0] = v.x; cs[tb][1] = v.y; cs[tb][2] = v.z; cs[tb][3] = v.w;
-      }
-      float zf[2][2];
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) zf[mt][hf] = SYM ? 8.f : zrow[mt][hf];
-      // m-tiles innermost when registers allow (NTB = 1): the two accumulation chains alternate, so a
-      // dependent MMA is never issued right behind its predecessor; at NTB = 2 the token blocks alternate.
-      constexpr int kMtGroups = NTB == 1 ? 1 : 2;
-      constexpr int kMtPer = 2 / kMtGroups;
-#pragma unroll
-      for (int mg = 0; mg < kMtGroups; ++mg) {
-        float gacc[kMtPer][NTB][4];
-#pragma unroll
-        for (int mi = 0; mi < kMtPer; ++mi)
-#pragma unroll
-          for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              gacc[mi][tb][e] = fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
+          for (int hf = 0; hf < 2; ++hf) s2[mt][hf] = __float2half2_rn(sc[mt][hf]);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
           for (int hs = 0; hs < 2; ++hs)
 #pragma unroll
-            for (int mi = 0; mi < kMtPer; ++mi) {
-              const int mt = mg * kMtPer + mi;
+            for (int mt = 0; mt < 2; ++mt) {
               const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
               const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-              const uint32_t a0 = lop3_and_or(qa, 0x000F000Fu, 0x64006400u), a1 = lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
-              const uint32_t a2 = lop3_and_or(qa, 0x00F000F0u, 0x54005400u), a3 = lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
+              const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[mt][0])), s2[mt][0]));
+              const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[mt][1])), s2[mt][1]));
+              const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[mt][0])), s2[mt][0]));
+              const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[mt][1])), s2[mt][1]));
 #pragma unroll
               for (int tb = 0; tb < NTB; ++tb) {
                 const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-                mma_16816_nv(gacc[mi][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+                mma_16816(acc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
               }
             }
+      } else {
+        // Post-scale with offset codes: one LOP3 per code pair, no zero-point arithmetic.
+        //   lo slots: (w & 0x000F000F) | 0x6400 -> 1024 + q      hi slots: (w & 0x00F000F0) | 0x5400 -> 64 + q
+        // so the MMA sums sum_k (off_k + q_k) x_k. The offsets and the zero point come back out as
+        //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
+        // with C and S of this unit's k-half supplied by the activation-sum warp and folded into the
+        // initial group accumulator: gacc0 = -C - z S.
+        float cs[NTB][4];   // {-C[m0], -C[m0+1], -S[m0], -S[m0+1]} of this unit's k-half (activation-sum warp)
 #pragma unroll
-        for (int mi = 0; mi < kMtPer; ++mi)
+        for (int tb = 0; tb < NTB; ++tb) {
+          const float4 v = lds128f(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16);
+          cs[tb][0] = v.x; cs[tb][1] = v.y; cs[tb][2] = v.z; cs[tb][3] = v.w;
+        }
+        float zf[2][2];
 #pragma unroll
-          for (int tb = 0; tb < NTB; ++tb) {
-            const int mt = mg * kMtPer + mi;
-            acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mi][tb][0], acc[mt][tb][0]);
-            acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mi][tb][1], acc[mt][tb][1]);
-            acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mi][tb][2], acc[mt][tb][2]);
-            acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mi][tb][3], acc[mt][tb][3]);
-          }
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) zf[mt][hf] = SYM ? 8.f : zrow[mt][hf];
+        // m-tiles innermost when registers allow (NTB = 1): the two accumulation chains alternate, so a
+        // dependent MMA is never issued right behind its predecessor; at NTB = 2 the token blocks alternate.
+        constexpr int kMtGroups = NTB == 1 ? 1 : 2;
+        constexpr int kMtPer = 2 / kMtGroups;
+#pragma unroll
+        for (int mg = 0; mg < kMtGroups; ++mg) {
+          float gacc[kMtPer][NTB][4];
+#pragma unroll
+          for (int mi = 0; mi < kMtPer; ++mi)
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                gacc[mi][tb][e] = fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+              for (int mi = 0; mi < kMtPer; ++mi) {
+                const int mt = mg * kMtPer + mi;
+                const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
+                const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
+                const uint32_t a0 = lop3_and_or(qa, 0x000F000Fu, 0x64006400u), a1 = lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
+                const uint32_t a2 = lop3_and_or(qa, 0x00F000F0u, 0x54005400u), a3 = lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
+#pragma unroll
+                for (int tb = 0; tb < NTB; ++tb) {
+                  const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
+                  mma_16816_nv(gacc[mi][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+                }
+              }
+#pragma unroll
+          for (int mi = 0; mi < kMtPer; ++mi)
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) {
+              const int mt = mg * kMtPer + mi;
+              acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mi][tb][0], acc[mt][tb][0]);
+              acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mi][tb][1], acc[mt][tb][1]);
+              acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mi][tb][2], acc[mt][tb][2]);
+              acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mi][tb][3], acc[mt][tb][3]);
+            }
+        }
+      }
+    };
+    auto begin_segment = [&](int u) {
+      if (cur_t >= 0) {
+        if (first_segment) trace_ma(p, 4);
+        flush(cur_t, seg_u0, u);
+        if (first_segment) trace_ma(p, 5);
+        first_segment = false;
+      }
+      cur_t = cur_t < 0 ? u / J.Gk : cur_t + 1;
+      boundary = (cur_t + 1) * J.Gk;
+      seg_u0 = u;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
+    };
+    auto stage_begin = [&](int i) {
+      if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
+      else mbar_wait_a(ready_base + 8 * s, ph);
+      if (i == 0) trace_ma(p, 1);
+    };
+    auto stage_end = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(empty_base + 8 * s);
+      if (++s == S) { s = 0; ph ^= 1; }
+    };
+    const int n_full = (u_end - u_begin) / kR;   // stages holding kR units
+    int i = 0;
+    while (i < n_stages) {
+      // a stage that starts a segment, crosses a tile boundary or is the ragged last one
+      {
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+        stage_begin(i);
+        const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+        // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
+        for (int j = 0; j < nu; ++j) {
+          if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
+          if ((j >> 1) == grp && !skip_compute) process_unit(st, sb, j);
+        }
+        stage_end();
+        ++i;
+      }
+      // then the run of full stages inside the current tile: no per-stage bookkeeping
+      const int i_end = min(n_full, (boundary - u_begin) / kR);
+      for (; i < i_end; ++i) {
+        stage_begin(i);
+        const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+        if (!skip_compute) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) process_unit(st, sb, 2 * grp + j);
+        }
+        stage_end();
       }
     }
-  };
-  auto begin_segment = [&](int u) {
-    if (cur_t >= 0) {
-      if (first_segment) trace_ma(p, 4);
-      flush(cur_t, seg_u0, u, first_segment);
-      if (first_segment) trace_ma(p, 5);
-      first_segment = false;
-    }
-    cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
-    boundary = (cur_t + 1) * p.Gk;
-    seg_u0 = u;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
-  };
-
-  const uint32_t ready_base = smem_u32(kScaleInA ? &full_bar[0] : &sums_bar[0]);
-  const uint32_t empty_base = smem_u32(&empty_bar[0]);
-  const bool skip_compute = W4A16_MMA_DIAG && (p.dbg & 1);   // diagnostics only
-  auto stage_begin = [&](int i) {
-    if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
-    else mbar_wait_a(ready_base + 8 * s, ph);
-    if (i == 0) trace_ma(p, 1);
-  };
-  auto stage_end = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive_a(empty_base + 8 * s);
-    if (++s == S) { s = 0; ph ^= 1; }
-  };
-  const int n_full = (u_end - u_begin) / kR;   // stages holding kR units
-  int i = 0;
-  while (i < n_stages) {
-    // a stage that starts a segment, crosses a tile boundary or is the ragged last one
-    {
-      const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
-      stage_begin(i);
-      const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
-      // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
-      for (int j = 0; j < nu; ++j) {
-        if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
-        if ((j >> 1) == grp && !skip_compute) process_unit(st, sb, j);
-      }
-      stage_end();
-      ++i;
-    }
-    // then the run of full stages inside the current tile: no per-stage bookkeeping
-    const int i_end = min(n_full, (boundary - u_begin) / kR);
-    for (; i < i_end; ++i) {
-      stage_begin(i);
-      const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
-      if (!skip_compute) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) process_unit(st, sb, 2 * grp + j);
-      }
-      stage_end();
+    trace_ma(p, 2);
+    if (cur_t >= 0) flush(cur_t, seg_u0, u_end);
+    trace_ma(p, 3);
+    if (chain) {   // this CTA's share of the op is written: count it
+      named_bar_sync(1, kWarps * 32);
+      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
     }
   }
-  trace_ma(p, 2);
-  if (cur_t >= 0) flush(cur_t, seg_u0, u_end, first_segment);
-  trace_ma(p, 3);
+  if (chain && threadIdx.x == 0) {
+    // The last CTA out re-arms the op counters for the next run of the chain (every CTA has finished
+    // every access to them once it has counted itself out; the fences order its op counts first).
+    __threadfence();
+    if (atomicAdd(&p.done[p.n_jobs], 1) == p.G - 1) {
+      __threadfence();
+      for (int j = 0; j < p.n_jobs; ++j) p.done[j] = 0;
+      p.done[p.n_jobs] = 0;
+      __threadfence();
+    }
+  }
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
@@ -576,6 +697,37 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
   return launch_pdl(kern, dim3(p.G), dim3(threads_for<kScaleInA>()), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
                                                                                              : W4A16_ERR_CUDA;
 }
+
+template <int NTB, bool SYM, bool kScaleInA>
+static int launch_chain_t(const GemmParams& p, cudaStream_t stream) {
+  using C = Cfg<NTB, SYM>;
+  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
+  static bool attr_set = false;   // benign race: idempotent attribute
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
+    attr_set = true;
+  }
+  CUtensorMap unused;
+  memset(&unused, 0, sizeof(unused));
+  // Cooperative: the owner-reduced tile fixup and the op dependencies need all G CTAs co-resident.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.G);
+  cfg.blockDim = dim3(threads_for<kScaleInA>());
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, unused, unused, p) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+constexpr int kChainSlots = 8;   // partial-slot ring of a chain, in ops
+
+inline int ntb_of(int M) { return (M + 7) / 8; }
+inline size_t chain_partial_bytes(int M, int G) { return (size_t)kChainSlots * G * 4 * ntb_of(M) * 2 * 32 * 16; }
+inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 1) * 4 + 255) / 256 * 256; }
 
 }  // namespace ma
 }  // namespace w4
@@ -600,6 +752,140 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
   return counters + (size_t)G * 4 * ntb * 2 * 32 * 16;
 }
 
+// ---- chains (include/w4a16.h) ----
+namespace {
+int chain_family(int M, int family) {
+  if (family == W4A16_FAMILY_AUTO) family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_MMA_SYNC_S;
+  if (M < 1 || M > 16) return W4A16_ERR_SHAPE;   // chains serve the mma.sync families (M <= 16)
+  if (family != W4A16_FAMILY_MMA_SYNC && family != W4A16_FAMILY_MMA_SYNC_S) return W4A16_ERR_ARG;
+  return family;
+}
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+struct Span { uintptr_t a, b; };
+bool overlaps(Span x, Span y) { return x.a < y.b && y.a < x.b; }
+Span x_span(const w4a16_op& o, int M) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(o.X);
+  return {a, a + (size_t)M * (size_t)o.K * 2};
+}
+Span y_span(const w4a16_op& o, int M) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(o.Y);
+  return {a, a + (size_t)M * (size_t)o.N * 2};
+}
+// Validate the ops; on success return the number of tile counters and the common mode.
+int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, int* mode) {
+  if (!ops || n_ops < 1) return W4A16_ERR_ARG;
+  long long t = 0;
+  *mode = -1;
+  for (int j = 0; j < n_ops; ++j) {
+    const w4a16_op& o = ops[j];
+    if (!o.X || !o.Y) return W4A16_ERR_ARG;
+    if (!al16(o.X) || !al16(o.Y)) return W4A16_ERR_ALIGN;
+    if (o.kind == W4A16_OP_GEMM) {
+      if (!o.packed || (o.mode != W4A16_ASYM && o.mode != W4A16_SYM)) return W4A16_ERR_ARG;
+      if (*mode >= 0 && o.mode != *mode) return W4A16_ERR_ARG;
+      *mode = o.mode;
+      if (!al16(o.packed)) return W4A16_ERR_ALIGN;
+      if (o.K <= 0 || o.N <= 0 || o.K % 128 || o.N % 128 || o.N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
+      if ((long long)(o.K / 128) * (o.N / 128) < G) return W4A16_ERR_SHAPE;   // every CTA owns >= 1 unit
+      t += o.N / 128;
+    } else if (o.kind == W4A16_OP_SILU_MUL) {
+      if (o.N < 8 || o.N % 8 || o.K != 2 * o.N) return W4A16_ERR_SHAPE;
+    } else {
+      return W4A16_ERR_ARG;
+    }
+    if (overlaps(x_span(o, M), y_span(o, M))) return W4A16_ERR_ARG;   // in-place ops are not supported
+  }
+  if (*mode < 0) *mode = W4A16_ASYM;
+  *tiles = t;
+  return W4A16_OK;
+}
+int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }
+}  // namespace
+
+extern "C" size_t w4a16_chain_plan_bytes(int n_ops) { return n_ops > 0 ? (size_t)n_ops * sizeof(w4::ma::ChainJob) : 0; }
+
+extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op* ops, int n_ops, int M, int family, int sms) {
+  if (chain_family(M, family) < 0 || sms <= 0) return 0;
+  long long tiles = 0;
+  int mode = 0;
+  const int G = chain_ctas(sms);
+  if (check_ops(ops, n_ops, M, G, &tiles, &mode) != W4A16_OK) return 0;
+  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
+}
+
+extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes,
+                                    int sms) {
+  if (!plan) return W4A16_ERR_ARG;
+  const int fam = chain_family(M, family);
+  if (fam < 0) return fam;
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  if (plan_bytes < w4a16_chain_plan_bytes(n_ops)) return W4A16_ERR_ARG;
+  long long tiles = 0;
+  int mode = 0;
+  if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
+  const int mpad = 8 * w4::ma::ntb_of(M);
+  w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
+  int cnt = 0;
+  for (int j = 0; j < n_ops; ++j) {
+    const w4a16_op& o = ops[j];
+    w4::ma::ChainJob& J = jobs[j];
+    memset(&J, 0, sizeof(J));
+    J.kind = o.kind;
+    J.packed = reinterpret_cast<const uint8_t*>(o.kind == W4A16_OP_GEMM ? o.packed : o.X);
+    J.Y = reinterpret_cast<uint16_t*>(o.Y);
+    J.K = o.K;
+    J.N = o.N;
+    if (o.kind == W4A16_OP_GEMM) {
+      J.Gk = o.K / 128;
+      J.U = (o.N / 128) * J.Gk;
+      J.cnt_off = cnt;
+      cnt += o.N / 128;
+      const uint16_t* X = reinterpret_cast<const uint16_t*>(o.X);
+      if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, 2 * w4::ma::kR)) return e;
+      if (int e = w4::encode_x_sw128(&J.xmap1, X, M, o.K, mpad, 2)) return e;
+    }
+    // dependencies from buffer overlaps: RAW for X; WAR / WAW for Y. Completion of op i implies the
+    // completion of every op before it, so the latest conflicting op is enough.
+    J.dep_x = -1;
+    J.dep_y = -1;
+    for (int i = j - 1; i >= 0 && (J.dep_x < 0 || J.dep_y < 0); --i) {
+      if (J.dep_x < 0 && overlaps(y_span(ops[i], M), x_span(o, M))) J.dep_x = i;
+      if (J.dep_y < 0 && (overlaps(y_span(ops[i], M), y_span(o, M)) || overlaps(x_span(ops[i], M), y_span(o, M)))) J.dep_y = i;
+    }
+  }
+  return W4A16_OK;
+}
+
+extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, int mode, int family, void* ws,
+                                      size_t ws_bytes, int sms, cudaStream_t stream) {
+  const int fam = chain_family(M, family);
+  if (fam < 0) return fam;
+  if (!dev_plan || !ws || n_ops < 1 || (mode != W4A16_ASYM && mode != W4A16_SYM)) return W4A16_ERR_ARG;
+  w4::ma::GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.G = chain_ctas(sms);
+  p.M = M;
+  const size_t pb = w4::ma::chain_partial_bytes(M, p.G), db = w4::ma::chain_done_bytes(n_ops);
+  if (ws_bytes < pb + db) return W4A16_ERR_WORKSPACE;
+  p.partials = reinterpret_cast<float*>(ws);
+  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb);
+  p.counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb + db);
+  p.jobs = reinterpret_cast<const w4::ma::ChainJob*>(dev_plan);
+  p.n_jobs = n_ops;
+  p.slots = w4::ma::kChainSlots;
+  const bool sym = mode == W4A16_SYM, s = fam == W4A16_FAMILY_MMA_SYNC_S;
+  switch (w4::ma::ntb_of(M)) {
+    case 1:
+      if (s) return sym ? w4::ma::launch_chain_t<1, true, true>(p, stream) : w4::ma::launch_chain_t<1, false, true>(p, stream);
+      return sym ? w4::ma::launch_chain_t<1, true, false>(p, stream) : w4::ma::launch_chain_t<1, false, false>(p, stream);
+    case 2:
+      if (s) return sym ? w4::ma::launch_chain_t<2, true, true>(p, stream) : w4::ma::launch_chain_t<2, false, true>(p, stream);
+      return sym ? w4::ma::launch_chain_t<2, true, false>(p, stream) : w4::ma::launch_chain_t<2, false, false>(p, stream);
+    default:
+      return W4A16_ERR_SHAPE;
+  }
+}
+
 extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
                                      bool scale_in_a, void* ws, int num_sms, cudaStream_t stream) {
   w4::ma::GemmParams p;
@@ -615,6 +901,10 @@ extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint
   static int dbg = -1;
   if (dbg < 0) { const char* e = getenv("W4A16_MMA_DEBUG"); dbg = e ? atoi(e) : 0; }
   p.dbg = dbg;
+  p.jobs = nullptr;
+  p.n_jobs = 1;
+  p.done = nullptr;
+  p.slots = 1;
   const bool sym = mode == W4A16_SYM;
 #define W4_MA_CASE(NTB)                                                                                \
   case NTB:                                                                                             \

@@ -14,18 +14,7 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const uint16_t* __restric
     const int m = (int)(i / vecs), v = (int)(i % vecs);
     const uint4 g = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + (size_t)v * 8);
     const uint4 u = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + F + (size_t)v * 8);
-    const __half2* gh = reinterpret_cast<const __half2*>(&g);
-    const __half2* uh = reinterpret_cast<const __half2*>(&u);
-    uint4 r;
-    __half2* rh = reinterpret_cast<__half2*>(&r);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 gf = __half22float2(gh[j]), uf = __half22float2(uh[j]);
-      const float a = gf.x / (1.0f + __expf(-gf.x)) * uf.x;
-      const float b = gf.y / (1.0f + __expf(-gf.y)) * uf.y;
-      rh[j] = __floats2half2_rn(a, b);
-    }
-    *reinterpret_cast<uint4*>(out + (size_t)m * F + (size_t)v * 8) = r;
+    *reinterpret_cast<uint4*>(out + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
   }
 }
 

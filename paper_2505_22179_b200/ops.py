@@ -3,6 +3,7 @@
 Each function checks dtypes/devices, passes raw device pointers and the current CUDA stream to
 libw4a16.so, and raises W4A16Error on a non-zero status. Nothing here computes any part of the path.
 """
+import ctypes
 from dataclasses import dataclass
 from typing import Optional
 
@@ -13,6 +14,7 @@ from ._lib import (  # noqa: F401
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
     W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S,
+    W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16Op,
 )
 
 
@@ -134,3 +136,51 @@ def pack_linear(W: torch.Tensor, mode=W4A16_ASYM, dev_status=None, stream=None) 
     packed = torch.empty(w4a16_packed_bytes(K, N, mode), dtype=torch.uint8, device=W.device)
     w4a16_pack(W, packed, dev_status, mode, stream=stream)
     return PackedLinear(K, N, mode, packed)
+
+
+class Chain:
+    """A sequence of ops run as ONE persistent launch (include/w4a16.h: w4a16_chain_plan / w4a16_chain_run).
+
+    ops: ("gemm", X [M,K] fp16, PackedLinear, Y [M,N] fp16) or ("silu_mul", GU [M,2F] fp16, out [M,F] fp16).
+    The plan (TMA descriptors, dependencies) is encoded once by the library into host memory and copied to
+    the device here; the tensors must stay where they are while the chain is in use (references are kept)."""
+
+    def __init__(self, ops, M: int, family=W4A16_FAMILY_AUTO, device=None):
+        self.M, self.family = M, family
+        self._keep = []
+        arr = (W4A16Op * len(ops))()
+        mode = W4A16_ASYM
+        for i, op in enumerate(ops):
+            if op[0] == "gemm":
+                _, X, pl, Y = op
+                if X.shape[0] != M or Y.shape[0] != M or X.shape[1] != pl.K or Y.shape[1] != pl.N:
+                    raise W4A16Error(f"chain op {i}: shapes do not match M={M}, K={pl.K}, N={pl.N}")
+                arr[i] = W4A16Op(W4A16_OP_GEMM, _ptr(X, torch.float16, "X"), _ptr(pl.packed, None, "packed"),
+                                 _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode)
+                mode = pl.mode
+                self._keep += [X, pl.packed, Y]
+            elif op[0] == "silu_mul":
+                _, GU, out = op
+                F = out.shape[1]
+                if GU.shape != (M, 2 * F) or out.shape[0] != M:
+                    raise W4A16Error(f"chain op {i}: silu_mul shapes")
+                arr[i] = W4A16Op(W4A16_OP_SILU_MUL, _ptr(GU, torch.float16, "GU"), None, _ptr(out, torch.float16, "out"),
+                                 2 * F, F, 0)
+                self._keep += [GU, out]
+            else:
+                raise W4A16Error(f"unknown chain op {op[0]!r}")
+        self.n, self.mode = len(ops), mode
+        nbytes = int(lib.w4a16_chain_plan_bytes(self.n))
+        host = (ctypes.c_uint8 * nbytes)()
+        check(lib.w4a16_chain_plan(ctypes.addressof(arr), self.n, M, family, ctypes.addressof(host), nbytes),
+              "w4a16_chain_plan")
+        dev = torch.device(device) if device is not None else self._keep[0].device
+        self.plan = torch.frombuffer(bytearray(host), dtype=torch.uint8).to(dev)
+        wsb = int(lib.w4a16_chain_workspace_bytes(ctypes.addressof(arr), self.n, M, family))
+        if wsb == 0:
+            raise W4A16Error("w4a16_chain_workspace_bytes: bad chain")
+        self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+
+    def __call__(self, stream=None):
+        check(lib.w4a16_chain_run(self.plan.data_ptr(), self.n, self.M, self.mode, self.family, self.ws.data_ptr(),
+                                  self.ws.numel(), _stream(stream)), "w4a16_chain_run")

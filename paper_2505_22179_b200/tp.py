@@ -17,7 +17,8 @@ from typing import Callable, List, Optional
 import torch
 import torch.distributed as dist
 
-from .ops import (W4A16_ASYM, PackedLinear, alloc_workspace, pack_linear, verify_accept, w4a16_silu_mul)
+from .ops import (W4A16_ASYM, Chain, PackedLinear, W4A16Error, alloc_workspace, pack_linear, verify_accept,
+                  w4a16_silu_mul)
 
 
 @dataclass(frozen=True)
@@ -132,6 +133,8 @@ class VerifyStack:
         self.accept_out = torch.zeros(3 + M_max, **i32)
         self.ws = alloc_workspace(M_max, [(s["K"], s["N"]) for s in P.values()], device=self.device)
         self.graphs = {}
+        self.use_chains = True
+        self._chains = {}
 
     @property
     def weight_bytes(self) -> int:
@@ -141,10 +144,41 @@ class VerifyStack:
         if self.t > 1:
             dist.all_reduce(y, group=self.group)
 
+    def _layer_ops(self, L, M):
+        """The layer's ops between its all-reduces: [QKV, O] and [gate-up, SiLU*mul, down]."""
+        return ([("gemm", self.x_qkv[:M], L["qkv"], self.y_qkv[:M]), ("gemm", self.x_o[:M], L["o"], self.y_o[:M])],
+                [("gemm", self.x_mlp[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
+                 ("gemm", self.act[:M], L["down"], self.y_down[:M])])
+
+    def chains(self, M: int):
+        """Persistent chains for width M (include/w4a16.h w4a16_chain_*): the whole stack in ONE launch at
+        tp = 1; at tp > 1 one launch per segment between all-reduces. None where chains do not apply
+        (M > 16, or a shard too small to give every CTA a unit): then every op is launched on its own."""
+        if M not in self._chains:
+            try:
+                segs = [self._layer_ops(L, M) for L in self.layers]
+                if self.t == 1:
+                    self._chains[M] = [Chain([op for a, b in segs for op in a + b], M, device=self.device)]
+                else:
+                    self._chains[M] = [Chain(seg, M, device=self.device) for a, b in segs for seg in (a, b)]
+            except W4A16Error:
+                self._chains[M] = None
+        return self._chains[M]
+
     def forward(self, M: int, stream=None):
         """One verify forward at width M (M = draft nodes + root), then greedy acceptance. Async."""
         if not 1 <= M <= self.M_max:
             raise ValueError(f"M={M} outside [1, {self.M_max}]")
+        ch = self.chains(M) if self.use_chains else None
+        if ch is not None:
+            if self.t == 1:
+                ch[0](stream)
+            else:
+                for i, c in enumerate(ch):
+                    c(stream)
+                    self._allreduce(self.y_o[:M] if i % 2 == 0 else self.y_down[:M])
+            verify_accept(self.tokens[:M], self.parents[:M], self.argmax[:M], self.accept_out[:3 + M], stream)
+            return
         ws = self.ws
         for L in self.layers:
             L["qkv"](self.x_qkv[:M], self.y_qkv[:M], ws, stream)
@@ -156,8 +190,11 @@ class VerifyStack:
             self._allreduce(self.y_down[:M])
         verify_accept(self.tokens[:M], self.parents[:M], self.argmax[:M], self.accept_out[:3 + M], stream)
 
-    def launches_per_forward(self) -> int:
-        """libw4a16 kernel launches per forward (4 GEMMs + SiLU*mul per layer, one acceptance)."""
+    def launches_per_forward(self, M: int = None) -> int:
+        """libw4a16 kernel launches per forward: one chain (tp = 1) or two per layer (tp > 1) plus the
+        acceptance; without chains 4 GEMMs + SiLU*mul per layer plus the acceptance."""
+        if M is not None and self.use_chains and self.chains(M) is not None:
+            return len(self.chains(M)) + 1
         return 5 * self.n_layers + 1
 
     def capture(self, M: int) -> torch.cuda.CUDAGraph:

@@ -72,9 +72,14 @@ def test_llama70b_tp8_shard_shapes_sym():
         _check_shape(s["K"], s["N"], [8, 49], tid=900 + i, mode=1)
 
 
-def test_verify_stack_one_layer_against_oracle():
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("dims,layers,chains", [((1024, 2048, 8, 2), 1, True), ((2560, 4096, 20, 4), 2, True),
+                                                ((2560, 4096, 20, 4), 2, False)])
+def test_verify_stack_against_oracle(dims, layers, chains):
+    # tiny model: per-op launches (too few units for a chain); small model: the whole stack as one
+    # persistent chain, and the same stack op by op. Buffers hold the last layer's values.
     from paper_2505_22179_b200 import tp
-    d = tp.ModelDims("tiny", hidden=1024, ffn=2048, n_q=8, n_kv=2, head=128, layers=1)
+    d = tp.ModelDims("tiny", hidden=dims[0], ffn=dims[1], n_q=dims[2], n_kv=dims[3], head=128, layers=layers)
     Wh = {}
 
     def make_weight(l, name, K, N, out):
@@ -82,7 +87,8 @@ def test_verify_stack_one_layer_against_oracle():
         Wh[name] = synth.host(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
 
     M = 13
-    st = tp.VerifyStack(d, 1, 16, make_weight)
+    st = tp.VerifyStack(d, layers, 16, make_weight)
+    st.use_chains = chains
     for j, buf in enumerate((st.x_qkv, st.x_o, st.x_mlp)):
         synth.gpu(22, j, synth.ACT, buf.shape[0], buf.shape[1], out=buf)
     rng = np.random.default_rng(3)
@@ -92,6 +98,8 @@ def test_verify_stack_one_layer_against_oracle():
     g = st.capture(M)
     g.replay()
     torch.cuda.synchronize()
+    if chains and dims[0] == 2560:
+        assert st.chains(M) is not None
 
     def ref(name, X_u16):
         c, s_, z, _ = oracle.quantize(Wh[name])
