@@ -22,6 +22,16 @@ $(BUILD)/pack.o: $(CSRC)/pack.cu $(CSRC)/common.cuh include/w4a16.h | $(BUILD)
 $(BUILD)/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/tma_host.cuh include/w4a16.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
+# Diagnostics build (make diag): the same library with W4A16_MMA_DIAG=1 (skip-compute / skip-load / trace
+# switches of gemm_mma.cu, selected at run time by W4A16_MMA_DEBUG); loaded instead of libw4a16.so when
+# W4A16_LIB=diag. Never used by tests, smoke or bench.
+DIAG_LIB := paper_2505_22179_b200/libw4a16_diag.so
+$(BUILD)/gemm_mma_diag.o: $(CSRC)/gemm_mma.cu $(CSRC)/common.cuh $(CSRC)/tma_host.cuh include/w4a16.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DW4A16_MMA_DIAG=1 -c $< -o $@ 2> $(BUILD)/gemm_mma_diag.ptxas.txt || (cat $(BUILD)/gemm_mma_diag.ptxas.txt; false)
+$(DIAG_LIB): $(filter-out $(BUILD)/gemm_mma.o,$(OBJS)) $(BUILD)/gemm_mma_diag.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
+diag: $(DIAG_LIB)
+
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
@@ -36,4 +46,4 @@ oracle/libw4a16_oracle.so: oracle/w4a16_oracle.c oracle/w4a16_oracle.h
 clean:
 	rm -rf build $(LIB) synth/*.so oracle/*.so
 
-.PHONY: all clean
+.PHONY: all clean diag

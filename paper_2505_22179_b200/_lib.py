@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libw4a16.so")
+LIB_PATH = os.path.join(_HERE, "libw4a16_diag.so" if os.environ.get("W4A16_LIB") == "diag" else "libw4a16.so")
 
 W4A16_OK = 0
 W4A16_ASYM = 0

@@ -47,8 +47,11 @@ constexpr int kXsumWarp = kWarps + 1;              // activation sums (offset-co
 template <bool kScaleInA>
 constexpr int threads_for() { return (kWarps + (kScaleInA ? 1 : 2)) * 32; }
 constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
-constexpr int kCtasPerSm = kGroups == 2 ? 1 : 2;   // resident CTAs per SM
-constexpr int kSmemBudget = (kCtasPerSm == 1 ? 224 : 112) * 1024;
+#ifndef W4_MA_CTAS
+#define W4_MA_CTAS 2
+#endif
+constexpr int kCtasPerSm = kGroups == 2 ? 1 : W4_MA_CTAS;   // resident CTAs per SM
+constexpr int kSmemBudget = (kCtasPerSm == 1 ? 224 : kCtasPerSm == 2 ? 112 : 74) * 1024;
 
 template <int NTB, bool SYM>
 struct Cfg {
@@ -88,7 +91,7 @@ struct GemmParams {
   int Gk;            // K / 128 groups per n-tile
   int U;             // total units
   int G;             // CTAs
-  int dbg;           // diagnostics only (W4A16_MMA_DEBUG): bit0 skip compute, bit2 backoff waits, bit4 trace
+  int dbg;           // diagnostics only (W4A16_MMA_DEBUG, W4A16_MMA_DIAG builds): bit0 skip compute, bit1 skip loads, bit2 backoff waits, bit4 trace
   const ChainJob* jobs;   // chain: the op table (device); nullptr: single GEMM
   int n_jobs;             // 1 for a single GEMM
   int* done;              // chain: [n_jobs] CTAs that finished each op, then the exit counter
@@ -253,6 +256,12 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           if (issued >= S) {   // slot s must be released by the consumers first
             if (!pdl_done) drain(true);
             while (!mbar_try_wait(&empty_bar[s], ph ^ 1)) drain(false);
+          }
+          if (W4A16_MMA_DIAG && (p.dbg & 2)) {   // diagnostics: no memory traffic, stale shared memory
+            mbar_arrive(&full_bar[s]);
+            ++issued;
+            if (++s == S) { s = 0; ph ^= 1; }
+            continue;
           }
           mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
           bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
