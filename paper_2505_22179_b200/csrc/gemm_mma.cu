@@ -146,6 +146,11 @@ __device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
   }
 }
 
+// MMA column j (fragment group g8 = j) carries token pi(j) of its 8-token block: with it, the 8 lanes of each
+// quarter-warp phase of an activation LDS.128 read rows {r, r + 4}, whose SWIZZLE_128B chunk positions differ
+// in the high bit, instead of rows {r, r + 1}, which collide on the same four bank groups (2-way conflict).
+__device__ __forceinline__ int tok_pi(int j) { return (j >> 1) | ((j & 1) << 2); }
+
 __device__ __forceinline__ int unit_begin(int c, int U, int G) { return (int)(((long long)c * U) / G); }
 // CTA owning unit u: largest c with unit_begin(c) <= u.
 __device__ __forceinline__ int cta_of_unit(int u, int U, int G) {
@@ -318,8 +323,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                 for (int pz = 0; pz < kPasses; ++pz) {
                   // A rows g8 / g8+8: (kh 0 / kh 1, token g8) at NTB = 1; (kh = pz, token g8 / 8+g8) at NTB = 2
                   const int kh0 = NTB == 1 ? 0 : pz, kh1 = NTB == 1 ? 1 : pz;
-                  const int m0 = g8, m1 = NTB == 1 ? g8 : 8 + g8;
-                  const uint32_t xu = st + (jbase + jj) * C::kXUnit + (((4 * cc + c4) ^ (g8 & 7)) << 4) + 8 * hs;
+                  const int m0 = tok_pi(g8), m1 = NTB == 1 ? m0 : 8 + m0;
+                  const uint32_t xu = st + (jbase + jj) * C::kXUnit + (((4 * cc + c4) ^ tok_pi(g8)) << 4) + 8 * hs;
                   const uint2 r0 = lds64(xu + kh0 * C::kXBox + m0 * 128);
                   const uint2 r1 = lds64(xu + kh1 * C::kXBox + m1 * 128);
                   mma_16816_nv(d[jj][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
@@ -332,8 +337,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 #pragma unroll
                 for (int rh = 0; rh < 2; ++rh) {   // D rows g8 (rh 0) and g8+8 (rh 1)
                   const int kh = NTB == 1 ? rh : pz;
-                  const int m = NTB == 1 ? g8 : 8 * rh + g8;
-                  const uint32_t slot = sb + ((((jbase + jj) * 2 + kh) * NTB + (m >> 3)) * 4 + ((m & 7) >> 1)) * 16 + 4 * (m & 1);
+                  const int m = NTB == 1 ? tok_pi(g8) : 8 * rh + tok_pi(g8);
+                  // consumer lane c4 holds MMA columns 2c4, 2c4 + 1 = tokens c4, c4 + 4 of the block
+                  const uint32_t slot = sb + ((((jbase + jj) * 2 + kh) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
                   sts32f(slot, d[jj][pz][2 * rh]);          // -C[m]
                   sts32f(slot + 8, d[jj][pz][2 * rh + 1]);  // -S[m]
                 }
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           const int n0 = t * kTileN + rows[mt][0], n1 = t * kTileN + rows[mt][1];
 #pragma unroll
           for (int tb = 0; tb < NTB; ++tb) {
-            const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
+            const int m0 = tb * 8 + c4, m1 = m0 + 4;   // MMA columns 2c4, 2c4 + 1 = tokens tok_pi(2c4), tok_pi(2c4 + 1)
             if (m0 < p.M) {
               J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][0]));
               J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][2]));
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
-          const int m = 8 * tb + g8;
+          const int m = 8 * tb + tok_pi(g8);                    // MMA column g8 carries token tok_pi(g8)
           const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
           xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
@@ -562,7 +568,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
         // with C and S of this unit's k-half supplied by the activation-sum warp and folded into the
         // initial group accumulator: gacc0 = -C - z S.
-        float cs[NTB][4];   // {-C[m0], -C[m0+1], -S[m0], -S[m0+1]} of this unit's k-half (activation-sum warp)
+        float cs[NTB][4];   // {-C[m0], -C[m1], -S[m0], -S[m1]}, m0 = 8tb + c4, m1 = m0 + 4 (activation-sum warp)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
           const float4 v = lds128f(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16);
