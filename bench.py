@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--kernels", action="store_true", default=True, help="per-kernel breakdown (default on)")
+    ap.add_argument("--no-kernels", dest="kernels", action="store_false", help="skip the per-kernel breakdown")
     return ap.parse_args()
 
 
