@@ -43,6 +43,7 @@ def _load():
     L.orc_layout_pack.argtypes = [vp, vp, vp, i32, i32, i32, vp]; L.orc_layout_pack.restype = i32
     L.orc_layout_unpack.argtypes = [vp, i32, i32, i32, vp, vp, vp]; L.orc_layout_unpack.restype = i32
     L.orc_accept.argtypes = [vp, vp, vp, i32, vp]; L.orc_accept.restype = i32
+    L.orc_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, i32]; L.orc_lmhead_argmax.restype = i32
     return L
 
 
@@ -170,3 +171,19 @@ def accept(tokens, parents, argmax):
     if rc != 0:
         raise ValueError("orc_accept: bad arguments")
     return int(out[0]), int(out[1]), int(out[2]), [int(x) for x in out[3:3 + out[0]]], out
+
+
+def lmhead_argmax(H, W, nthreads=1, want_logits=False):
+    """Greedy token per row: (argmax int32 [M], max logit fp64 [M][, logits fp64 [M][V]]) of H[M,K] . W[V,K]^T
+    (fp16 inputs, fp64 logits, ties -> lowest id)."""
+    H, W = _u16(H), _u16(W)
+    M, K = H.shape
+    V = W.shape[0]
+    if W.shape[1] != K:
+        raise ValueError("lmhead_argmax: K mismatch")
+    idx = np.zeros(M, dtype=np.int32)
+    val = np.zeros(M, dtype=np.float64)
+    lg = np.zeros((M, V), dtype=np.float64) if want_logits else None
+    if L.orc_lmhead_argmax(_p(H), _p(W), M, K, V, _p(idx), _p(val), _p(lg), int(nthreads)) != 0:
+        raise ValueError("orc_lmhead_argmax: bad arguments")
+    return (idx, val, lg) if want_logits else (idx, val)

@@ -294,3 +294,56 @@ int orc_accept(const int32_t* tokens, const int32_t* parents, const int32_t* tar
   free(ok); free(depth);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------------------
+ * LM head + greedy argmax (reading R12: FP16 LM head; ties to the lowest id).
+ * Straight from the definition: every logit in fp64 (products of fp16 values are exact in fp64), then a
+ * left-to-right scan keeping the first maximum.
+ * ---------------------------------------------------------------------------------------------------- */
+typedef struct {
+  const uint16_t* H; const uint16_t* W; int M, K, V;
+  double* L;                              /* logits [M][V] */
+  int v0, v1;
+} lm_job;
+
+static void* lm_worker(void* p) {
+  lm_job* a = (lm_job*)p;
+  for (int v = a->v0; v < a->v1; ++v) {
+    const uint16_t* wr = a->W + (size_t)v * a->K;
+    for (int m = 0; m < a->M; ++m) {
+      const uint16_t* hr = a->H + (size_t)m * a->K;
+      double acc = 0.0;
+      for (int k = 0; k < a->K; ++k) acc += orc_half_to_double(hr[k]) * orc_half_to_double(wr[k]);
+      a->L[(size_t)m * a->V + v] = acc;
+    }
+  }
+  return NULL;
+}
+
+int orc_lmhead_argmax(const uint16_t* H, const uint16_t* W, int M, int K, int V, int32_t* out_idx, double* out_val,
+                      double* logits, int nthreads) {
+  if (!H || !W || !out_idx || M < 1 || K < 1 || V < 1) return -1;
+  double* L = logits ? logits : (double*)malloc(sizeof(double) * (size_t)M * (size_t)V);
+  if (!L) return -1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > V) nthreads = V;
+  lm_job* jobs = (lm_job*)calloc((size_t)nthreads, sizeof(lm_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int t = 0; t < nthreads; ++t) {
+    lm_job j = {H, W, M, K, V, L, (int)((long long)V * t / nthreads), (int)((long long)V * (t + 1) / nthreads)};
+    jobs[t] = j;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, lm_worker, &jobs[t]);
+  lm_worker(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  for (int m = 0; m < M; ++m) {
+    const double* row = L + (size_t)m * V;
+    int best = 0;
+    for (int v = 1; v < V; ++v) if (row[v] > row[best]) best = v;   /* strict: the first maximum wins */
+    out_idx[m] = best;
+    if (out_val) out_val[m] = row[best];
+  }
+  free(jobs); free(th);
+  if (!logits) free(L);
+  return 0;
+}

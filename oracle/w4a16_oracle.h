@@ -15,6 +15,9 @@
  *                 "X[M,K] fp16 x packed W[K,N] -> Y[M,N] fp16, fp32 accumulate"; the oracle uses fp64).
  *   - accept:     greedy tree acceptance (P:79-84 draft-then-verify; the rule is not stated by the paper,
  *                 SPEC S:289/S:298 greedy argmax; reading R9).
+ *   - lmhead_argmax: the target's greedy token per verify row: logits[m][v] =
+ *                 sum_k H[m][k] * W[v][k] in fp64 (FP16 LM head, reading R12), argmax over v with ties to the
+ *                 lowest id — the target_argmax input of accept.
  * The arithmetic works on plain arrays: codes uint8 [K][N], scales/zeros fp16 [K/group][N]. The byte layout
  * of the ABI's packed blob is a separate pair of functions (layout_pack / layout_unpack), re-derived here
  * from its definition in include/w4a16.h (not shared):
@@ -79,6 +82,13 @@ int orc_layout_unpack(const uint8_t* packed, int K, int N, int mode, uint8_t* co
  * out[3 .. 3+n) = accepted path (node indices, root excluded, root->leaf), padded with -1.
  * Returns 0, or -1 on bad arguments (n < 1 or NULL). A malformed tree gives out = {0, -1, BAD_TREE, -1...}. */
 int orc_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n, int32_t* out);
+
+/* LM head + greedy argmax: H fp16 [M][K], W fp16 [V][K] (row v = token v's output
+ * embedding, the nn.Linear weight layout). logits[m][v] = sum_k H[m][k] * W[v][k] in fp64, k in order.
+ * out_idx[m] = the smallest v with the largest logit, out_val[m] = that logit; logits (may be NULL)
+ * receives all M x V values. nthreads splits the vocabulary; the result does not depend on it. */
+int orc_lmhead_argmax(const uint16_t* H, const uint16_t* W, int M, int K, int V, int32_t* out_idx, double* out_val,
+                      double* logits, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -414,3 +414,54 @@ def test_accept_lossless_vs_autoregressive_decoding():
             d = len(ctx[i]) - len(prefix)
             if ctx[i][len(prefix):] == ar[:d]:
                 assert d <= L
+
+
+# ---------------------------------------------------------------------------------------------------
+# LM head + greedy argmax: pins against numpy, closed forms, ties, planted winners
+# ---------------------------------------------------------------------------------------------------
+def test_lmhead_argmax_matches_numpy_float64():
+    # library routine: float64 matmul of the same fp16 values, argmax (first maximum); K != V catches a
+    # transposed operand
+    rng = np.random.default_rng(11)
+    for M, K, V in ((1, 128, 77), (5, 384, 1000), (13, 256, 333)):
+        H = rng.standard_normal((M, K)).astype(np.float16)
+        W = (0.05 * rng.standard_normal((V, K))).astype(np.float16)
+        idx, val, lg = oracle.lmhead_argmax(H, W, nthreads=3, want_logits=True)
+        ref = H.astype(np.float64) @ W.astype(np.float64).T
+        assert np.allclose(lg, ref, rtol=0, atol=1e-9)
+        assert np.array_equal(idx, np.argmax(ref, axis=1))
+        assert np.allclose(val, ref.max(axis=1), rtol=0, atol=1e-9)
+
+
+def test_lmhead_argmax_closed_form_and_ties():
+    K, V = 256, 64
+    H = np.ones((2, K), dtype=np.float16)
+    c = np.array([(v * 37) % 64 - 20 for v in range(V)], dtype=np.float64) / 64.0   # exact fp16 values
+    W = np.repeat(c[:, None], K, axis=1).astype(np.float16)
+    idx, val = oracle.lmhead_argmax(H, W)
+    assert np.all(val == K * c.max())                       # logit = K * c_v exactly
+    assert np.all(idx == int(np.argmax(c)))
+    # exact ties -> lowest id: duplicate the winning row at a lower and a higher id
+    W2 = W.copy()
+    w = int(np.argmax(c))
+    W2[w + 5] = W2[w]
+    W2[3] = W2[w]
+    idx2, _ = oracle.lmhead_argmax(H, W2)
+    assert np.all(idx2 == min(3, w))
+    # all-zero head: every logit 0, the lowest id wins
+    idx3, val3 = oracle.lmhead_argmax(H, np.zeros((V, K), dtype=np.float16))
+    assert np.all(idx3 == 0) and np.all(val3 == 0)
+
+
+def test_lmhead_argmax_planted_winner_and_thread_invariance():
+    rng = np.random.default_rng(12)
+    M, K, V = 6, 512, 900
+    H = rng.standard_normal((M, K)).astype(np.float16)
+    W = (0.02 * rng.standard_normal((V, K))).astype(np.float16)
+    plant = rng.choice(V, size=M, replace=False)
+    for m, v in enumerate(plant):
+        W[v] = (H[m].astype(np.float32) * 0.5).astype(np.float16)    # logit ~ 0.5 |h|^2 >> the rest
+    idx1, val1 = oracle.lmhead_argmax(H, W, nthreads=1)
+    idx7, val7 = oracle.lmhead_argmax(H, W, nthreads=7)
+    assert np.array_equal(idx1, plant)
+    assert np.array_equal(idx1, idx7) and np.array_equal(val1, val7)
