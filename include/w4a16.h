@@ -122,6 +122,19 @@ int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int
 int verify_accept(const int32_t* tokens, const int32_t* parents, const int32_t* target_argmax, int n, int32_t* out,
                   w4a16_stream_t stream);
 
+/* w4a16_lmhead_argmax — the target's greedy token for every verify row (the argmax the
+ * greedy acceptance rule compares drafts with): out_argmax[m] = the smallest v maximising
+ * logit[m][v] = sum_k H[m][k] * W_lm[v][k], out_max[m] = that logit (may be NULL). FP16 LM head (the paper
+ * keeps the drafter FP16; reading R12), fp32 accumulation, ties -> lowest id; the logits are
+ * reduced in the GEMM epilogue and never written. H: fp16 [M][K] (the verify rows' final hidden states);
+ * W_lm: fp16 [V][K] row-major (the nn.Linear weight layout: row v = token v); out_argmax: int32 [M], the
+ * target_argmax input of verify_accept. 1 <= M <= 64, K % 128 == 0, V % 128 == 0. workspace: zero-filled
+ * once, w4a16_lmhead_workspace_bytes() bytes; every call leaves it re-armed. Because fp32 sums decide the
+ * argmax, a row whose top two logits are closer than the accumulation error may pick either. */
+size_t w4a16_lmhead_workspace_bytes(int M, int K, int V);
+int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int M, int K, int V, int32_t* out_argmax,
+                        float* out_max, void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
+
 /* w4a16_silu_mul — Llama MLP glue between the fused gate-up GEMM and the down GEMM of the verify forward
  * (not a step of the paper's method): GU is fp16 [M][2F] holding [gate | up] per row (the
  * rank-local shard layout of tp.py), out is fp16 [M][F], out[m][j] = fp16_rne(silu(gate) * up) in fp32.

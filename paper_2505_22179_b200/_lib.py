@@ -38,6 +38,8 @@ ABI_SYMBOLS = (
     "w4a16_chain_workspace_bytes",
     "w4a16_chain_plan",
     "w4a16_chain_run",
+    "w4a16_lmhead_workspace_bytes",
+    "w4a16_lmhead_argmax",
 )
 W4A16_OP_GEMM, W4A16_OP_SILU_MUL = 0, 1
 
@@ -73,6 +75,10 @@ def _load():
     lib.w4a16_status_string.restype = ctypes.c_char_p
     lib.w4a16_gemm_family.argtypes = [i32, i32, i32]
     lib.w4a16_silu_mul.argtypes = [vp, i32, i32, vp, vp]
+    lib.w4a16_lmhead_workspace_bytes.argtypes = [i32, i32, i32]
+    lib.w4a16_lmhead_workspace_bytes.restype = sz
+    lib.w4a16_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
+    lib.w4a16_lmhead_argmax.restype = i32
     lib.w4a16_chain_plan_bytes.argtypes = [i32]
     lib.w4a16_chain_plan_bytes.restype = sz
     lib.w4a16_chain_workspace_bytes.argtypes = [vp, i32, i32, i32]

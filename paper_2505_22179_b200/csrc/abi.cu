@@ -12,6 +12,9 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaS
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" size_t w4a16_lmhead_workspace_bytes_sms(int num_sms);
+extern "C" int w4a16_launch_lmhead_argmax(const uint16_t*, const uint16_t*, int, int, int, int32_t*, float*, void*, int,
+                                          cudaStream_t);
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op*, int, int, int, int);
 extern "C" int w4a16_chain_plan_sms(const w4a16_op*, int, int, int, void*, size_t, int);
 extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, cudaStream_t);
@@ -146,6 +149,25 @@ extern "C" int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode,
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
   return w4a16_launch_chain_mma(dev_plan, n_ops, M, mode, family, workspace, workspace_bytes, sms, (cudaStream_t)stream);
+}
+
+extern "C" size_t w4a16_lmhead_workspace_bytes(int M, int K, int V) {
+  if (M < 1 || M > W4A16_MAX_M || K <= 0 || K % 128 || V <= 0 || V % 128) return 0;
+  const int sms = num_sms_of_current_device();
+  return sms > 0 ? w4a16_lmhead_workspace_bytes_sms(sms) : 0;
+}
+
+extern "C" int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int M, int K, int V, int32_t* out_argmax,
+                                   float* out_max, void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!H || !W_lm || !out_argmax || !workspace) return W4A16_ERR_ARG;
+  if (M < 1 || M > W4A16_MAX_M || K <= 0 || K % 128 || V <= 0 || V % 128) return W4A16_ERR_SHAPE;
+  if (!aligned16(H) || !aligned16(W_lm) || !aligned16(workspace) || (reinterpret_cast<uintptr_t>(out_argmax) & 3) ||
+      (reinterpret_cast<uintptr_t>(out_max) & 3))
+    return W4A16_ERR_ALIGN;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  if (workspace_bytes < w4a16_lmhead_workspace_bytes_sms(sms)) return W4A16_ERR_WORKSPACE;
+  return w4a16_launch_lmhead_argmax(H, W_lm, M, K, V, out_argmax, out_max, workspace, sms, (cudaStream_t)stream);
 }
 
 extern "C" const char* w4a16_status_string(int status) {

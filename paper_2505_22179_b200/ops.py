@@ -99,6 +99,29 @@ def verify_accept(tokens, parents, target_argmax, out, stream=None):
     check(st, "verify_accept")
 
 
+def w4a16_lmhead_workspace_bytes(M: int, K: int, V: int) -> int:
+    return int(lib.w4a16_lmhead_workspace_bytes(M, K, V))
+
+
+def w4a16_lmhead_argmax(H, W_lm, out_argmax, workspace, out_max=None, stream=None):
+    """out_argmax[m] (int32) = argmax_v H[m] . W_lm[v] (ties -> lowest id); out_max[m] (fp32) = that logit."""
+    M, K = H.shape
+    V = W_lm.shape[0]
+    if W_lm.shape[1] != K or out_argmax.numel() < M:
+        raise W4A16Error("w4a16_lmhead_argmax: shapes")
+    check(lib.w4a16_lmhead_argmax(_ptr(H, torch.float16, "H"), _ptr(W_lm, torch.float16, "W_lm"), M, K, V,
+                                  _ptr(out_argmax, torch.int32, "out_argmax"), _ptr(out_max, torch.float32, "out_max"),
+                                  _ptr(workspace, None, "workspace"), workspace.numel() * workspace.element_size(),
+                                  _stream(stream)), "w4a16_lmhead_argmax")
+
+
+def alloc_lmhead_workspace(M_max: int, K: int, V: int, device=None) -> torch.Tensor:
+    n = w4a16_lmhead_workspace_bytes(M_max, K, V)
+    if n == 0:
+        raise W4A16Error("w4a16_lmhead_workspace_bytes: bad shape")
+    return torch.zeros(n, dtype=torch.uint8, device=device or "cuda")
+
+
 def w4a16_silu_mul(GU, out, stream=None):
     M, F2 = GU.shape
     check(lib.w4a16_silu_mul(_ptr(GU, torch.float16, "GU"), M, F2 // 2, _ptr(out, torch.float16, "out"),
