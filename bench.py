@@ -7,7 +7,7 @@ SiLU*mul, down; attention/norms out of scope) at draft width M, then greedy acce
 tree (BASELINE.json configs 3-5; config 4 at N GPUs = tensor-parallel over N ranks with NCCL all-reduce).
 value = algorithmic weight bytes streamed by all ranks per step / max-over-ranks step time, in TB/s.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--M 16] [--layers 80] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--M 8] [--layers 80] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 Inputs are seeded synthetic (synth/), resident in HBM before timing; per-step weights (36.4 GB at N=1)
@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--M", type=int, default=16, help="headline draft width (verify rows)")
+    ap.add_argument("--M", type=int, default=8, help="headline draft width (verify rows): 8 = HierSpec's 70B sequence "
+                    "verification d = 7 (P:784), M = d + 1 (reading R10)")
     ap.add_argument("--layers", type=int, default=None, help="decoder layers (default: the model's)")
     ap.add_argument("--model", default="70b", choices=["70b", "8b"])
     ap.add_argument("--mode", default="asym", choices=["asym", "sym"])
@@ -54,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-kernels", dest="kernels", action="store_false", help="skip the per-kernel breakdown")
+    ap.add_argument("--no-lm-head", dest="lm_head", action="store_false",
+                    help="skip the LM head + argmax measurement (SURVEY 8(f) f3)")
     return ap.parse_args()
 
 
@@ -394,6 +397,33 @@ def main():
                 roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT)
             except Exception:
                 pass
+    # FP16 LM head [M, hidden] x [hidden, vocab] with the greedy argmax fused (the target_argmax
+    # that verify_accept consumes), measured on its own: its weights (2.1 GB fp16) are not W4A16 bytes.
+    lm = None
+    if args.lm_head and rank == 0:
+        V = 128256
+        Kh = dims.hidden
+        R = 3   # distinct heads back to back (3 x 2.1 GB >> L2)
+        heads = [synth.gpu(args.seed, synth.tensor_id(0xFFE, r, 0), synth.WEIGHT, V, Kh) for r in range(R)]
+        hid = stack.y_down[:M] if stack.y_down.shape[1] == Kh else torch.zeros(M, Kh, dtype=torch.float16, device=dev)
+        am = torch.empty(M, dtype=torch.int32, device=dev)
+        mx = torch.empty(M, dtype=torch.float32, device=dev)
+        lws = w4.alloc_lmhead_workspace(M, Kh, V, device=dev)
+        with torch.cuda.stream(stream):
+            for h in heads:
+                w4.w4a16_lmhead_argmax(hid, h, am, lws, out_max=mx, stream=stream)
+        torch.cuda.synchronize()
+        gl = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gl, stream=stream):
+            for h in heads:
+                w4.w4a16_lmhead_argmax(hid, h, am, lws, out_max=mx, stream=stream)
+        msl = time_graph(gl, 5, 2) / R
+        hb = V * Kh * 2
+        lm = {"row": "f3", "what": f"FP16 LM head {Kh}x{V} + fused greedy argmax at M={M} (w4a16_lmhead_argmax)",
+              "us": 1e3 * msl, "GBps": hb / (msl * 1e-3) / 1e9, "frac_hbm": hb / (msl * 1e-3) / 1e9 / peak_gbs,
+              "weight_bytes": hb, "bound": "hbm"}
+        log(f"lm head + argmax: {1e3 * msl:.1f} us ({lm['frac_hbm']:.2f} of HBM)")
+        del heads, gl
     clk = clocks.stop() if clocks else None
 
     cpu = None
@@ -420,7 +450,7 @@ def main():
             "us_per_layer": 1e3 * ms / n_layers,
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
-            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu,
+            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm,
             "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
                     "api": "VerifyStack.verify_host (pinned host buffers, graph replay, accept result read back)",
