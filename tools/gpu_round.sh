@@ -9,7 +9,7 @@ timeout 1200 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu_$TAG.log 2>&1
 BENCH_WATCHDOG=700 timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"; tail -3 $OUT/bench_$TAG.err
 # launch list of the bench command (4 layers): every launch with its device time (cold, serialised)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --layers 4 --steps 3 --warmup 3 --sweep "" --no-cpu-baseline --no-kernels > $OUT/bench_ncu_$TAG.log 2>&1; echo "ncu list rc=$?"
+    python bench.py --layers 4 --steps 3 --warmup 3 --sweep "" --no-cpu-baseline --no-kernels --no-lm-head > $OUT/bench_ncu_$TAG.log 2>&1; echo "ncu list rc=$?"
 # full capture of the dominant kernel: the persistent chain (8-layer stack, headline M=16)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a16_mma -s 1 -c 1 -f -o $OUT/prof_chain_$TAG \
     python bench.py --layers 8 --steps 1 --warmup 3 --sweep "" --no-cpu-baseline > $OUT/ncu_chain_$TAG.log 2>&1; echo "ncu chain rc=$?"
