@@ -38,7 +38,7 @@ namespace ma {
 constexpr int kTileN = 128, kTileK = 128;
 constexpr int kUnitWBytes = kTileN * kTileK / 2;   // 8192
 #ifndef W4_MA_GROUPS
-#define W4_MA_GROUPS 1
+#define W4_MA_GROUPS 2
 #endif
 constexpr int kGroups = W4_MA_GROUPS;              // consumer groups sharing one pipeline (1 CTA per SM at 2)
 constexpr int kWarps = 8 * kGroups;                // per group: 4 row-quarters x 2 k-halves
@@ -133,6 +133,21 @@ __device__ unsigned long long g_trace_ma[kTraceCtas][8];
 #ifndef W4A16_MMA_DIAG
 #define W4A16_MMA_DIAG 0   // 1: compile the per-CTA timeline trace and consumer-side diagnostics in
 #endif
+// Diagnostics only (W4A16_MMA_DIAG builds, W4A16_MMA_DEBUG bit 64): per CTA and chain op, %globaltimer when
+// consumer warp 0 starts the op, has its first stage, finished its last stage, and has counted the op done.
+constexpr int kOpTraceCtas = 296, kOpTraceOps = 512;
+#if W4A16_MMA_DIAG
+__device__ unsigned long long g_op_trace[kOpTraceCtas][kOpTraceOps][4];
+#endif
+__device__ __forceinline__ void trace_op(const GemmParams& p, int job, int ev) {
+#if W4A16_MMA_DIAG
+  if ((p.dbg & 64) && threadIdx.x == 0 && blockIdx.x < kOpTraceCtas && job < kOpTraceOps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_op_trace[blockIdx.x][job][ev] = t;
+  }
+#endif
+}
 __device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
   if (W4A16_MMA_DIAG && (p.dbg & 16) && blockIdx.x < kTraceCtas && threadIdx.x == 0) {
     unsigned long long t;
@@ -379,12 +394,14 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   const bool skip_compute = W4A16_MMA_DIAG && (p.dbg & 1);   // diagnostics only
 
   for (int job = 0; job < p.n_jobs; ++job) {
+    trace_op(p, job, 0);
     const JobInfo J = job_at(p, &xmapR, &xmap1, job);
     if (J.kind == kOpSilu) {
       // SiLU*mul op of a chain (same arithmetic as w4a16_silu_mul), spread over every consumer thread of
       // every CTA once the gate-up op that writes GU (and the readers of `out`) are done.
       if (threadIdx.x == 0) wait_op(p, max(J.dep_x, J.dep_y));
       named_bar_sync(1, kWarps * 32);
+      trace_op(p, job, 1);
       const int F = J.N, vecs = F / 8;
       const long long total = (long long)p.M * vecs;
       const uint16_t* GU = reinterpret_cast<const uint16_t*>(J.packed);
@@ -396,6 +413,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       }
       named_bar_sync(1, kWarps * 32);
       if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+      trace_op(p, job, 2);
+      trace_op(p, job, 3);
       continue;
     }
     const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
@@ -641,7 +660,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     auto stage_begin = [&](int i) {
       if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
       else mbar_wait_a(ready_base + 8 * s, ph);
-      if (i == 0) trace_ma(p, 1);
+      if (i == 0) { trace_ma(p, 1); trace_op(p, job, 1); }
     };
     auto stage_end = [&]() {
       __syncwarp();
@@ -677,12 +696,14 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       }
     }
     trace_ma(p, 2);
+    trace_op(p, job, 2);
     if (cur_t >= 0) flush(cur_t, seg_u0, u_end);
     trace_ma(p, 3);
     if (chain) {   // this CTA's share of the op is written: count it
       named_bar_sync(1, kWarps * 32);
       if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
     }
+    trace_op(p, job, 3);
   }
   if (chain && threadIdx.x == 0) {
     // The last CTA out re-arms the op counters for the next run of the chain (every CTA has finished
@@ -746,6 +767,16 @@ inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 1) * 4 + 25
 
 }  // namespace ma
 }  // namespace w4
+
+extern "C" int w4a16_debug_op_trace(void* host, size_t bytes) {
+#if W4A16_MMA_DIAG
+  return cudaMemcpyFromSymbol(host, w4::ma::g_op_trace, bytes < sizeof(w4::ma::g_op_trace) ? bytes : sizeof(w4::ma::g_op_trace)) ==
+                 cudaSuccess ? 0 : -5;
+#else
+  (void)host; (void)bytes;
+  return -1;
+#endif
+}
 
 extern "C" int w4a16_debug_trace_mma(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, w4::ma::g_trace_ma, bytes < sizeof(w4::ma::g_trace_ma) ? bytes : sizeof(w4::ma::g_trace_ma)) ==
@@ -888,6 +919,9 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   p.jobs = reinterpret_cast<const w4::ma::ChainJob*>(dev_plan);
   p.n_jobs = n_ops;
   p.slots = w4::ma::kChainSlots;
+  static int dbg = -1;
+  if (dbg < 0) { const char* e = getenv("W4A16_MMA_DEBUG"); dbg = e ? atoi(e) : 0; }
+  p.dbg = dbg;
   const bool sym = mode == W4A16_SYM, s = fam == W4A16_FAMILY_MMA_SYNC_S;
   switch (w4::ma::ntb_of(M)) {
     case 1:

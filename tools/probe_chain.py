@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Diagnostics: per-op timeline of the persistent chain kernel (needs the diag build: make diag;
+W4A16_LIB=diag W4A16_MMA_DEBUG=64). Prints, per op kind, medians over layers of: the op's span (first CTA
+start -> last CTA done), the CTAs' wait before their first stage, compute time, flush time, and skew."""
+import argparse, ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2505_22179_b200 as w4
+from paper_2505_22179_b200 import tp
+from paper_2505_22179_b200._lib import lib
+import synth
+ap = argparse.ArgumentParser()
+ap.add_argument("--M", type=int, default=8)
+ap.add_argument("--layers", type=int, default=8)
+a = ap.parse_args()
+mat_id = {n: i for i, n in enumerate(tp.MATRICES)}
+st = tp.VerifyStack(tp.LLAMA3_70B, a.layers, 64, lambda l, n, K, N, out: synth.gpu(0, synth.tensor_id(l, mat_id[n], 0), synth.WEIGHT, K, N, out=out))
+for buf, tid in ((st.x_qkv, 1), (st.x_o, 2), (st.x_mlp, 3)):
+    synth.gpu(0, synth.tensor_id(0xFFF, tid, 0), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+ch = st.chains(a.M)[0]
+for _ in range(3):
+    ch()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); ch(); e1.record(); torch.cuda.synchronize()
+print(f"chain {a.layers} layers M={a.M}: {e0.elapsed_time(e1) * 1e3:.1f} us")
+G, NOPS = 296, 512
+buf = np.zeros((G, NOPS, 4), dtype=np.uint64)
+lib.w4a16_debug_op_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert lib.w4a16_debug_op_trace(buf.ctypes.data, buf.nbytes) == 0
+n = ch.n
+G = int((buf[:, 0, 0] > 0).sum())   # CTAs of this chain
+b = buf[:G, :n, :].astype(np.int64)
+t0 = b[:, 0, 0].min()
+b -= t0
+kinds = ["qkv", "o", "gate_up", "silu", "down"]
+print(f"{'op':8s} {'span':>7s} {'wait1st':>8s} {'compute':>8s} {'flush':>7s} {'skewStart':>9s} {'skewDone':>8s}  (us, medians over layers)")
+for k, name in enumerate(kinds):
+    rows = []
+    for j in range(k, n, 5):
+        s, f1, l, d = b[:, j, 0], b[:, j, 1], b[:, j, 2], b[:, j, 3]
+        rows.append([d.max() - s.min(), np.median(f1 - s), np.median(l - f1), np.median(d - l), s.max() - s.min(), d.max() - d.min()])
+    r = np.median(np.array(rows), axis=0) / 1e3
+    print(f"{name:8s} " + " ".join(f"{x:8.2f}" for x in r))
+ends = [b[:, j, 3].max() for j in range(n)]
+print("total span us:", (max(ends)) / 1e3)
+# per-CTA spread of the compute phase (first stage -> last stage) for each op kind, summed over layers
+for k, name in enumerate(kinds):
+    comp = np.zeros(G)
+    for j in range(k, n, 5):
+        comp += (b[:, j, 2] - b[:, j, 1]) / 1e3
+    q = np.percentile(comp, [0, 10, 50, 90, 100])
+    order = np.argsort(comp)
+    print(f"{name:8s} compute per CTA (sum over layers) p0/10/50/90/100: " + " ".join(f"{x:7.1f}" for x in q),
+          "| slowest CTAs", order[-6:].tolist(), "| fastest", order[:6].tolist())
