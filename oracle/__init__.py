@@ -43,6 +43,8 @@ def _load():
     L.orc_layout_pack.argtypes = [vp, vp, vp, i32, i32, i32, vp]; L.orc_layout_pack.restype = i32
     L.orc_layout_unpack.argtypes = [vp, i32, i32, i32, vp, vp, vp]; L.orc_layout_unpack.restype = i32
     L.orc_accept.argtypes = [vp, vp, vp, i32, vp]; L.orc_accept.restype = i32
+    L.orc_tree_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]; L.orc_tree_attention.restype = i32
+    L.orc_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp]; L.orc_kv_compact.restype = i32
     L.orc_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, i32]; L.orc_lmhead_argmax.restype = i32
     return L
 
@@ -187,3 +189,30 @@ def lmhead_argmax(H, W, nthreads=1, want_logits=False):
     if L.orc_lmhead_argmax(_p(H), _p(W), M, K, V, _p(idx), _p(val), _p(lg), int(nthreads)) != 0:
         raise ValueError("orc_lmhead_argmax: bad arguments")
     return (idx, val, lg) if want_logits else (idx, val)
+
+
+def tree_attention(Q, Kc, Vc, parents):
+    """fp64 O[M, Hq, D] of the tree-masked verify attention. Q fp16 [M, Hq, D]; Kc, Vc fp16
+    [L + M, Hkv, D]; parents int32 [M]."""
+    Q, Kc, Vc = _u16(Q), _u16(Kc), _u16(Vc)
+    M, Hq, D = Q.shape
+    Lt, Hkv, D2 = Kc.shape
+    if D2 != D or Vc.shape != Kc.shape or Lt < M:
+        raise ValueError("tree_attention: shapes")
+    par = np.ascontiguousarray(parents, dtype=np.int32)
+    O = np.zeros((M, Hq, D), dtype=np.float64)
+    if L.orc_tree_attention(_p(Q), _p(Kc), _p(Vc), _p(par), M, Lt - M, Hq, Hkv, D, _p(O)) != 0:
+        raise ValueError("orc_tree_attention: bad arguments")
+    return O
+
+
+def kv_compact(Kc, Vc, L_prefix, accept_out):
+    """In-place on copies: returns (Kc', Vc') (input dtype) with the accepted path's rows moved behind the root."""
+    dt = np.asarray(Kc).dtype
+    Kc = _u16(Kc).copy()
+    Vc = _u16(Vc).copy()
+    Lt, Hkv, D = Kc.shape
+    out = np.ascontiguousarray(accept_out, dtype=np.int32)
+    if L.orc_kv_compact(_p(Kc), _p(Vc), int(L_prefix), Hkv, D, _p(out)) != 0:
+        raise ValueError("orc_kv_compact: bad arguments")
+    return (Kc.view(np.float16), Vc.view(np.float16)) if dt == np.float16 else (Kc, Vc)

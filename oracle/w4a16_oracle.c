@@ -347,3 +347,61 @@ int orc_lmhead_argmax(const uint16_t* H, const uint16_t* W, int M, int K, int V,
   if (!logits) free(L);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------------------
+ * Tree-masked verify attention (ancestry mask S:129-132) and KV compaction.
+ * Straight from the definitions: for every (row, head) the list of visible cache rows, scores in fp64,
+ * softmax with the maximum subtracted, the weighted sum of values in fp64.
+ * ---------------------------------------------------------------------------------------------------- */
+int orc_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc, const int32_t* parents, int M, int L,
+                       int Hq, int Hkv, int D, double* O) {
+  if (!Q || !Kc || !Vc || !parents || !O || M < 1 || L < 0 || Hq < 1 || Hkv < 1 || D < 1 || Hq % Hkv) return -1;
+  if (parents[0] != -1) return -1;
+  for (int i = 1; i < M; ++i) if (parents[i] < 0 || parents[i] >= i) return -1;
+  const int rows = L + M, grp = Hq / Hkv;
+  int* vis = (int*)malloc(sizeof(int) * (size_t)rows);
+  double* sc = (double*)malloc(sizeof(double) * (size_t)rows);
+  const double scale = 1.0 / sqrt((double)D);
+  for (int i = 0; i < M; ++i) {
+    int nv = 0;
+    for (int r = 0; r < L; ++r) vis[nv++] = r;                            /* the cached prefix */
+    for (int a = i; a >= 0; a = a == 0 ? -1 : parents[a]) vis[nv++] = L + a;   /* i and its ancestors */
+    for (int h = 0; h < Hq; ++h) {
+      const int g = h / grp;
+      const uint16_t* q = Q + ((size_t)i * Hq + h) * D;
+      double mx = -HUGE_VAL;
+      for (int t = 0; t < nv; ++t) {
+        const uint16_t* k = Kc + ((size_t)vis[t] * Hkv + g) * D;
+        double acc = 0.0;
+        for (int d = 0; d < D; ++d) acc += orc_half_to_double(q[d]) * orc_half_to_double(k[d]);
+        sc[t] = acc * scale;
+        if (sc[t] > mx) mx = sc[t];
+      }
+      double den = 0.0;
+      for (int t = 0; t < nv; ++t) { sc[t] = exp(sc[t] - mx); den += sc[t]; }
+      double* o = O + ((size_t)i * Hq + h) * D;
+      for (int d = 0; d < D; ++d) o[d] = 0.0;
+      for (int t = 0; t < nv; ++t) {
+        const uint16_t* v = Vc + ((size_t)vis[t] * Hkv + g) * D;
+        const double w = sc[t] / den;
+        for (int d = 0; d < D; ++d) o[d] += w * orc_half_to_double(v[d]);
+      }
+    }
+  }
+  free(vis); free(sc);
+  return 0;
+}
+
+int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out) {
+  if (!Kc || !Vc || !accept_out || L < 0 || Hkv < 1 || D < 1) return -1;
+  const int n = accept_out[0];
+  const size_t row = (size_t)Hkv * D;
+  for (int k = 1; k <= n; ++k) {   /* path[k-1] >= k, so ascending k never overwrites a row still to be read */
+    const int src = L + accept_out[3 + k - 1], dst = L + k;
+    if (src != dst) {
+      memmove(Kc + (size_t)dst * row, Kc + (size_t)src * row, row * sizeof(uint16_t));
+      memmove(Vc + (size_t)dst * row, Vc + (size_t)src * row, row * sizeof(uint16_t));
+    }
+  }
+  return 0;
+}

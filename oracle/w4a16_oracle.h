@@ -18,6 +18,11 @@
  *   - lmhead_argmax: the target's greedy token per verify row: logits[m][v] =
  *                 sum_k H[m][k] * W[v][k] in fp64 (FP16 LM head, reading R12), argmax over v with ties to the
  *                 lowest id — the target_argmax input of accept.
+ *   - tree_attention: attention of the verify rows over the KV cache with the draft tree's ancestry mask
+ *                 (row i sees the cached prefix and the tree rows that are i or
+ *                 an ancestor of i; P:80-82 tree drafts), softmax in fp64.
+ *   - kv_compact: after acceptance keep the root and the accepted path's rows, in order (S:159-164
+ *                 cache_select of the accepted root-to-leaf path).
  * The arithmetic works on plain arrays: codes uint8 [K][N], scales/zeros fp16 [K/group][N]. The byte layout
  * of the ABI's packed blob is a separate pair of functions (layout_pack / layout_unpack), re-derived here
  * from its definition in include/w4a16.h (not shared):
@@ -89,6 +94,19 @@ int orc_accept(const int32_t* tokens, const int32_t* parents, const int32_t* tar
  * receives all M x V values. nthreads splits the vocabulary; the result does not depend on it. */
 int orc_lmhead_argmax(const uint16_t* H, const uint16_t* W, int M, int K, int V, int32_t* out_idx, double* out_val,
                       double* logits, int nthreads);
+
+/* Tree-masked verify attention. Q fp16 [M][Hq][D]; Kc, Vc fp16 [L + M][Hkv][D] (the cached
+ * prefix at rows 0..L-1, the M verify rows' own keys/values at L..L+M-1); parents [M] (parents[0] = -1,
+ * parents[i] < i). Query row i, head h attends kv head g = h / (Hq / Hkv) at every prefix row and at rows
+ * L + j for j = i or an ancestor of i. O fp64 [M][Hq][D] = softmax(q.k / sqrt(D)) . v over those
+ * rows, everything in fp64 (scores, max-subtracted exp, normaliser, weighted sum). Returns 0 / -1. */
+int orc_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc, const int32_t* parents, int M, int L,
+                       int Hq, int Hkv, int D, double* O);
+
+/* KV-cache compaction after acceptance (cache_select of the accepted path): with accept_out of
+ * orc_accept (out[0] = accepted length n, out[3..3+n) = path node indices), row L + k of Kc and Vc becomes
+ * the former row L + path[k-1] for k = 1..n (row L, the root, stays). Rows are Hkv * D fp16 wide. */
+int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out);
 
 #ifdef __cplusplus
 }

@@ -465,3 +465,109 @@ def test_lmhead_argmax_planted_winner_and_thread_invariance():
     idx7, val7 = oracle.lmhead_argmax(H, W, nthreads=7)
     assert np.array_equal(idx1, plant)
     assert np.array_equal(idx1, idx7) and np.array_equal(val1, val7)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Tree-masked verify attention + KV compaction
+# ---------------------------------------------------------------------------------------------------
+def _attn_inputs(rng, M, L, Hq, Hkv, D, scale=1.0):
+    Q = (scale * rng.standard_normal((M, Hq, D))).astype(np.float16)
+    K = (scale * rng.standard_normal((L + M, Hkv, D))).astype(np.float16)
+    V = rng.standard_normal((L + M, Hkv, D)).astype(np.float16)
+    return Q, K, V
+
+
+def _dense_masked_attention(Q, K, V, mask):
+    # numpy float64: explicit boolean mask [M, L+M], softmax over the visible rows (library-routine formulation)
+    M, Hq, D = Q.shape
+    Hkv = K.shape[1]
+    g = Hq // Hkv
+    Qf, Kf, Vf = Q.astype(np.float64), K.astype(np.float64), V.astype(np.float64)
+    O = np.zeros((M, Hq, D))
+    for h in range(Hq):
+        S = Qf[:, h, :] @ Kf[:, h // g, :].T / np.sqrt(D)
+        S = np.where(mask, S, -np.inf)
+        P = np.exp(S - S.max(axis=1, keepdims=True))
+        P /= P.sum(axis=1, keepdims=True)
+        O[:, h, :] = P @ Vf[:, h // g, :]
+    return O
+
+
+def test_tree_attention_sequence_draft_is_causal_attention():
+    rng = np.random.default_rng(21)
+    M, L, Hq, Hkv, D = 7, 40, 8, 2, 64
+    Q, K, V = _attn_inputs(rng, M, L, Hq, Hkv, D)
+    mask = np.zeros((M, L + M), dtype=bool)
+    mask[:, :L] = True
+    mask[:, L:] = np.tril(np.ones((M, M), dtype=bool))      # causal over the new rows
+    O = oracle.tree_attention(Q, K, V, np.arange(-1, M - 1))
+    assert np.allclose(O, _dense_masked_attention(Q, K, V, mask), rtol=0, atol=1e-12)
+
+
+def test_tree_attention_equals_its_root_to_node_path_as_a_sequence():
+    # path invariance: node i of a tree sees exactly what the last row of the sequence (root .. i) sees
+    rng = np.random.default_rng(22)
+    M, L, Hq, Hkv, D = 12, 17, 4, 2, 32
+    Q, K, V = _attn_inputs(rng, M, L, Hq, Hkv, D)
+    par = [-1, 0, 0, 1, 1, 2, 3, 3, 5, 8, 0, 10]
+    O = oracle.tree_attention(Q, K, V, par)
+    for i in range(M):
+        path = []
+        a = i
+        while a != -1:
+            path.append(a)
+            a = par[a]
+        path = path[::-1]
+        n = len(path)
+        Qs = Q[path]
+        Ks = np.concatenate([K[:L], K[[L + p for p in path]]])
+        Vs = np.concatenate([V[:L], V[[L + p for p in path]]])
+        Os = oracle.tree_attention(Qs, Ks, Vs, np.arange(-1, n - 1))
+        assert np.allclose(O[i], Os[-1], rtol=0, atol=1e-12)
+
+
+def test_tree_attention_closed_forms_and_gqa_mapping():
+    rng = np.random.default_rng(23)
+    M, L, Hq, Hkv, D = 5, 0, 4, 2, 16
+    Q, K, V = _attn_inputs(rng, M, L, Hq, Hkv, D)
+    par = [-1, 0, 1, 1, 0]
+    O = oracle.tree_attention(Q, K, V, par)
+    assert np.array_equal(O[0], V[0][[h // 2 for h in range(Hq)]].astype(np.float64))   # root, empty prefix
+    # equal keys -> uniform weights -> mean of the visible values (node 3 sees rows 0, 1, 3)
+    K2 = np.repeat(K[:1], L + M, axis=0)
+    O2 = oracle.tree_attention(Q, K2, V, par)
+    vis = [0, 1, 3]
+    assert np.allclose(O2[3], V[vis].astype(np.float64).mean(axis=0)[[h // 2 for h in range(Hq)]], rtol=0, atol=1e-12)
+    # heads of one group share the kv head; identical queries in different groups differ
+    Q3 = Q.copy()
+    Q3[:, 1] = Q3[:, 0]
+    Q3[:, 2] = Q3[:, 0]
+    O3 = oracle.tree_attention(Q3, K, V, par)
+    assert np.array_equal(O3[:, 0], O3[:, 1])
+    assert not np.allclose(O3[:, 0], O3[:, 2])
+
+
+def test_kv_compact_worked_example_and_chain_equivalence():
+    rng = np.random.default_rng(24)
+    L, Hq, Hkv, D = 9, 4, 2, 16
+    tok = [100, 11, 12, 21, 22, 23, 31, 32]
+    par = [-1, 0, 0, 1, 1, 2, 3, 5]
+    am = [12, 99, 23, 31, 99, 32, 99, 40]
+    acc = oracle.accept(tok, par, am)[4]            # accepted path [2, 5, 7] (tests/golden/accept_8node.txt)
+    assert list(acc[3:6]) == [2, 5, 7] and acc[0] == 3
+    M = len(tok)
+    Q, K, V = _attn_inputs(rng, M + 1, L, Hq, Hkv, D)
+    K, V = K[:L + M], V[:L + M]
+    Kc, Vc = oracle.kv_compact(K, V, L, acc)
+    assert np.array_equal(Kc[:L + 1], K[:L + 1]) and np.array_equal(Vc[:L + 1], V[:L + 1])
+    for k, p in enumerate([2, 5, 7], start=1):
+        assert np.array_equal(Kc[L + k], K[L + p]) and np.array_equal(Vc[L + k], V[L + p])
+    # the next token (bonus position) attends prefix + root + path: on the compacted cache it is a sequence
+    # row; on the original tree it is a new child of the accepted leaf (node 7)
+    qn, kn, vn = Q[M:M + 1], rng.standard_normal((1, Hkv, D)).astype(np.float16), rng.standard_normal((1, Hkv, D)).astype(np.float16)
+    n = 1 + 3
+    Kseq = np.concatenate([Kc[:L + n], kn])
+    Vseq = np.concatenate([Vc[:L + n], vn])
+    Oseq = oracle.tree_attention(np.concatenate([Q[[0, 2, 5, 7]], qn]), Kseq, Vseq, np.arange(-1, n))
+    Otree = oracle.tree_attention(np.concatenate([Q[:M], qn]), np.concatenate([K, kn]), np.concatenate([V, vn]), par + [7])
+    assert np.allclose(Oseq[-1], Otree[-1], rtol=0, atol=1e-12)
