@@ -135,6 +135,24 @@ size_t w4a16_lmhead_workspace_bytes(int M, int K, int V);
 int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int M, int K, int V, int32_t* out_argmax,
                         float* out_max, void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
 
+/* w4a16_tree_attention — tree-masked verify attention: the M verify rows (root + draft
+ * tree) attend the cached prefix and, inside the tree, themselves and their ancestors only (the
+ * ancestry mask). Q: fp16 [M][Hq][D]; Kc, Vc: fp16 [L + M][Hkv][D] (prefix rows 0..L-1, the verify
+ * rows' own keys/values at L..L+M-1); parents: int32 [M] on the device, a valid tree (parents[0] = -1,
+ * parents[i] < i; verify_accept reports malformed trees). O[m][h] = softmax_j(q.k_j / sqrt(D)) . v_j over the
+ * visible rows j, kv head h / (Hq / Hkv) (GQA); fp32 scores / softmax / accumulation, fp16 probabilities and
+ * output. D == 128, 1 <= M <= 64, Hq % Hkv == 0, L >= 0. workspace: w4a16_tree_attention_workspace_bytes(). */
+size_t w4a16_tree_attention_workspace_bytes(int M, int L, int Hq, int Hkv, int D);
+int w4a16_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc, const int32_t* parents, int M,
+                         int L, int Hq, int Hkv, int D, uint16_t* O, void* workspace, size_t workspace_bytes,
+                         w4a16_stream_t stream);
+/* w4a16_kv_compact — after verify_accept, keep the accepted path in the cache (S:159-164 cache_select):
+ * rows L + k of Kc and Vc (each Hkv * D fp16) become the former rows L + path[k-1], k = 1..accepted, where
+ * accept_out is verify_accept's device output (read on the device: no host synchronisation). Row L (the root)
+ * stays. Call once per layer. D % 8 == 0. */
+int w4a16_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out,
+                     w4a16_stream_t stream);
+
 /* w4a16_silu_mul — Llama MLP glue between the fused gate-up GEMM and the down GEMM of the verify forward
  * (not a step of the paper's method): GU is fp16 [M][2F] holding [gate | up] per row (the
  * rank-local shard layout of tp.py), out is fp16 [M][F], out[m][j] = fp16_rne(silu(gate) * up) in fp32.

@@ -40,6 +40,9 @@ ABI_SYMBOLS = (
     "w4a16_chain_run",
     "w4a16_lmhead_workspace_bytes",
     "w4a16_lmhead_argmax",
+    "w4a16_tree_attention_workspace_bytes",
+    "w4a16_tree_attention",
+    "w4a16_kv_compact",
 )
 W4A16_OP_GEMM, W4A16_OP_SILU_MUL = 0, 1
 
@@ -79,6 +82,12 @@ def _load():
     lib.w4a16_lmhead_workspace_bytes.restype = sz
     lib.w4a16_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     lib.w4a16_lmhead_argmax.restype = i32
+    lib.w4a16_tree_attention_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
+    lib.w4a16_tree_attention_workspace_bytes.restype = sz
+    lib.w4a16_tree_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, sz, vp]
+    lib.w4a16_tree_attention.restype = i32
+    lib.w4a16_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp, vp]
+    lib.w4a16_kv_compact.restype = i32
     lib.w4a16_chain_plan_bytes.argtypes = [i32]
     lib.w4a16_chain_plan_bytes.restype = sz
     lib.w4a16_chain_workspace_bytes.argtypes = [vp, i32, i32, i32]

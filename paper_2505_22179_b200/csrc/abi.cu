@@ -13,6 +13,10 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 extern "C" size_t w4a16_lmhead_workspace_bytes_sms(int num_sms);
+extern "C" size_t w4a16_tree_attention_workspace_bytes_sms(int M, int L, int Hq, int Hkv, int sms);
+extern "C" int w4a16_launch_tree_attention(const uint16_t*, const uint16_t*, const uint16_t*, const int32_t*, int, int,
+                                           int, int, uint16_t*, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_kv_compact(uint16_t*, uint16_t*, int, int, int, const int32_t*, cudaStream_t);
 extern "C" int w4a16_launch_lmhead_argmax(const uint16_t*, const uint16_t*, int, int, int, int32_t*, float*, void*, int,
                                           cudaStream_t);
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op*, int, int, int, int);
@@ -168,6 +172,41 @@ extern "C" int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int 
   if (sms <= 0) return W4A16_ERR_CUDA;
   if (workspace_bytes < w4a16_lmhead_workspace_bytes_sms(sms)) return W4A16_ERR_WORKSPACE;
   return w4a16_launch_lmhead_argmax(H, W_lm, M, K, V, out_argmax, out_max, workspace, sms, (cudaStream_t)stream);
+}
+
+namespace {
+int check_attn(int M, int L, int Hq, int Hkv, int D) {
+  if (M < 1 || M > W4A16_MAX_M || L < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || D != 128) return W4A16_ERR_SHAPE;
+  return W4A16_OK;
+}
+}  // namespace
+
+extern "C" size_t w4a16_tree_attention_workspace_bytes(int M, int L, int Hq, int Hkv, int D) {
+  if (check_attn(M, L, Hq, Hkv, D) != W4A16_OK) return 0;
+  const int sms = num_sms_of_current_device();
+  return sms > 0 ? w4a16_tree_attention_workspace_bytes_sms(M, L, Hq, Hkv, sms) : 0;
+}
+
+extern "C" int w4a16_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc, const int32_t* parents,
+                                    int M, int L, int Hq, int Hkv, int D, uint16_t* O, void* workspace,
+                                    size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!Q || !Kc || !Vc || !parents || !O || !workspace) return W4A16_ERR_ARG;
+  if (int e = check_attn(M, L, Hq, Hkv, D)) return e;
+  if (!aligned16(Q) || !aligned16(Kc) || !aligned16(Vc) || !aligned16(O) || !aligned16(workspace) ||
+      (reinterpret_cast<uintptr_t>(parents) & 3))
+    return W4A16_ERR_ALIGN;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  if (workspace_bytes < w4a16_tree_attention_workspace_bytes_sms(M, L, Hq, Hkv, sms)) return W4A16_ERR_WORKSPACE;
+  return w4a16_launch_tree_attention(Q, Kc, Vc, parents, M, L, Hq, Hkv, O, workspace, sms, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out,
+                                w4a16_stream_t stream) {
+  if (!Kc || !Vc || !accept_out) return W4A16_ERR_ARG;
+  if (L < 0 || Hkv < 1 || D < 8 || D % 8) return W4A16_ERR_SHAPE;
+  if (!aligned16(Kc) || !aligned16(Vc) || (reinterpret_cast<uintptr_t>(accept_out) & 3)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_kv_compact(Kc, Vc, L, Hkv, D, accept_out, (cudaStream_t)stream);
 }
 
 extern "C" const char* w4a16_status_string(int status) {

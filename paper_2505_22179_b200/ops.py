@@ -122,6 +122,29 @@ def alloc_lmhead_workspace(M_max: int, K: int, V: int, device=None) -> torch.Ten
     return torch.zeros(n, dtype=torch.uint8, device=device or "cuda")
 
 
+def w4a16_tree_attention_workspace_bytes(M: int, L: int, Hq: int, Hkv: int, D: int = 128) -> int:
+    return int(lib.w4a16_tree_attention_workspace_bytes(M, L, Hq, Hkv, D))
+
+
+def w4a16_tree_attention(Q, Kc, Vc, parents, O, workspace, stream=None):
+    """O [M, Hq, D] = tree-masked attention of Q [M, Hq, D] over Kc/Vc [L + M, Hkv, D]."""
+    M, Hq, D = Q.shape
+    Lt, Hkv, D2 = Kc.shape
+    if D2 != D or tuple(Vc.shape) != tuple(Kc.shape) or tuple(O.shape) != tuple(Q.shape) or Lt < M:
+        raise W4A16Error("w4a16_tree_attention: shapes")
+    check(lib.w4a16_tree_attention(_ptr(Q, torch.float16, "Q"), _ptr(Kc, torch.float16, "Kc"), _ptr(Vc, torch.float16, "Vc"),
+                                   _ptr(parents, torch.int32, "parents"), M, Lt - M, Hq, Hkv, D,
+                                   _ptr(O, torch.float16, "O"), _ptr(workspace, None, "workspace"),
+                                   workspace.numel() * workspace.element_size(), _stream(stream)), "w4a16_tree_attention")
+
+
+def w4a16_kv_compact(Kc, Vc, L: int, accept_out, stream=None):
+    """In place: cache rows L + k <- rows L + path[k-1] of the verify_accept result."""
+    _, Hkv, D = Kc.shape
+    check(lib.w4a16_kv_compact(_ptr(Kc, torch.float16, "Kc"), _ptr(Vc, torch.float16, "Vc"), L, Hkv, D,
+                               _ptr(accept_out, torch.int32, "accept_out"), _stream(stream)), "w4a16_kv_compact")
+
+
 def w4a16_silu_mul(GU, out, stream=None):
     M, F2 = GU.shape
     check(lib.w4a16_silu_mul(_ptr(GU, torch.float16, "GU"), M, F2 // 2, _ptr(out, torch.float16, "out"),

@@ -1,0 +1,100 @@
+"""Tree-masked verify attention and KV compaction (include/w4a16.h w4a16_tree_attention,
+w4a16_kv_compact) against the CPU oracle.
+
+Tolerance (derived): the kernel rounds the softmax probabilities to fp16 for the P.V MMA
+(relative error <= 2^-11 per weight) and the output to fp16 (2^-11 |O|), everything else in fp32; with
+|v| = O(1) this stays below 4e-3 * (1 + |O|). Masking is checked structurally as well: perturbing the
+keys/values of tree rows that are not ancestors of a row leaves that row's output bit-identical. The KV
+compaction moves bytes and must be bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 4e-3
+
+
+def _w4():
+    import paper_2505_22179_b200 as w4
+    return w4
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _gpu_attn(Q, K, V, par):
+    w4 = _w4()
+    M, Hq, D = Q.shape
+    Lt, Hkv, _ = K.shape
+    Qd, Kd, Vd = _t(Q), _t(K), _t(V)
+    O = torch.full((M, Hq, D), float("nan"), dtype=torch.float16, device="cuda")
+    ws = torch.empty(w4.w4a16_tree_attention_workspace_bytes(M, Lt - M, Hq, Hkv, D), dtype=torch.uint8, device="cuda")
+    w4.w4a16_tree_attention(Qd, Kd, Vd, _t(np.asarray(par, dtype=np.int32)), O, ws)
+    torch.cuda.synchronize()
+    return O.float().cpu().numpy().astype(np.float64)
+
+
+def _inputs(seed, M, L, Hq, Hkv, D=128):
+    rng = np.random.default_rng(seed)
+    Q = (0.5 * rng.standard_normal((M, Hq, D))).astype(np.float16)
+    K = (0.5 * rng.standard_normal((L + M, Hkv, D))).astype(np.float16)
+    V = rng.standard_normal((L + M, Hkv, D)).astype(np.float16)
+    return Q, K, V
+
+
+@pytest.mark.parametrize("M,L,Hq,Hkv,kind", [(1, 0, 8, 1, "seq"), (1, 37, 8, 8, "seq"), (7, 100, 8, 2, "seq"),
+                                             (8, 64, 16, 2, "tree"), (16, 300, 16, 2, "tree"), (49, 513, 64, 8, "tree"),
+                                             (61, 1000, 64, 8, "tree"), (64, 130, 8, 1, "seq")])
+def test_tree_attention_vs_oracle(M, L, Hq, Hkv, kind):
+    Q, K, V = _inputs(M * 1000 + L, M, L, Hq, Hkv)
+    if kind == "seq":
+        par = np.arange(-1, M - 1, dtype=np.int32)
+    else:
+        _, par = synth.eagle_tree(np.random.default_rng(M + L), M - 1, 6)
+        par = np.asarray(par, dtype=np.int32)
+    ref = oracle.tree_attention(Q, K, V, par)
+    got = _gpu_attn(Q, K, V, par)
+    err = np.abs(got - ref)
+    assert np.all(err <= TOL * (1 + np.abs(ref))), f"max err {err.max():.3g}"
+
+
+def test_tree_attention_masks_non_ancestors_exactly():
+    M, L, Hq, Hkv = 12, 50, 8, 2
+    Q, K, V = _inputs(7, M, L, Hq, Hkv)
+    par = np.array([-1, 0, 0, 1, 1, 2, 3, 3, 5, 8, 0, 10], dtype=np.int32)
+    base = _gpu_attn(Q, K, V, par)
+    rng = np.random.default_rng(8)
+    for i in (4, 9, 11):
+        anc, a = set(), i
+        while a != -1:
+            anc.add(a)
+            a = int(par[a])
+        others = [j for j in range(M) if j not in anc]
+        K2, V2 = K.copy(), V.copy()
+        K2[[L + j for j in others]] = rng.standard_normal((len(others), Hkv, 128)).astype(np.float16)
+        V2[[L + j for j in others]] = rng.standard_normal((len(others), Hkv, 128)).astype(np.float16)
+        pert = _gpu_attn(Q, K2, V2, par)
+        assert np.array_equal(pert[i], base[i]), f"row {i} sees a non-ancestor"
+
+
+def test_kv_compact_bit_exact_after_gpu_accept():
+    w4 = _w4()
+    L, Hkv, D = 33, 8, 128
+    tok = [100, 11, 12, 21, 22, 23, 31, 32]
+    par = [-1, 0, 0, 1, 1, 2, 3, 5]
+    am = [12, 99, 23, 31, 99, 32, 99, 40]
+    M = len(tok)
+    _, K, V = _inputs(9, M, L, 8, Hkv)
+    out = torch.empty(3 + M, dtype=torch.int32, device="cuda")
+    w4.verify_accept(_t(np.array(tok, dtype=np.int32)), _t(np.array(par, dtype=np.int32)),
+                     _t(np.array(am, dtype=np.int32)), out)
+    Kd, Vd = _t(K), _t(V)
+    w4.w4a16_kv_compact(Kd, Vd, L, out)
+    torch.cuda.synchronize()
+    Kr, Vr = oracle.kv_compact(K, V, L, oracle.accept(tok, par, am)[4])
+    assert np.array_equal(Kd.cpu().numpy().view(np.uint16), Kr.view(np.uint16))
+    assert np.array_equal(Vd.cpu().numpy().view(np.uint16), Vr.view(np.uint16))
