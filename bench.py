@@ -424,6 +424,38 @@ def main():
               "weight_bytes": hb, "bound": "hbm"}
         log(f"lm head + argmax: {1e3 * msl:.1f} us ({lm['frac_hbm']:.2f} of HBM)")
         del heads, gl
+    # tree-masked verify attention over a 2048-token cached prefix (Llama-3-70B: 64 q heads,
+    # 8 kv heads, head 128) at the headline width (sequence draft) and at the BASELINE config-5 tree of 60
+    # drafts, plus the KV compaction that follows acceptance; per layer (x80 for the forward).
+    attn = None
+    if args.lm_head and rank == 0:
+        Lctx, Hq, Hkv, D = 2048, dims.n_q // world, dims.n_kv // world, dims.head
+        attn = {"row": "f2", "context": Lctx, "heads": [Hq, Hkv, D]}
+        for Mq, kind in ((M, "sequence"), (61, "eagle2_tree_60")):
+            Qa = synth.gpu(args.seed, synth.tensor_id(0xFFD, 1, Mq), synth.ACT, Mq, Hq * D).view(Mq, Hq, D)
+            Ka = synth.gpu(args.seed, synth.tensor_id(0xFFD, 2, Mq), synth.ACT, Lctx + Mq, Hkv * D).view(Lctx + Mq, Hkv, D)
+            Va = synth.gpu(args.seed, synth.tensor_id(0xFFD, 3, Mq), synth.ACT, Lctx + Mq, Hkv * D).view(Lctx + Mq, Hkv, D)
+            if kind == "sequence":
+                par_a = torch.arange(-1, Mq - 1, dtype=torch.int32, device=dev)
+            else:
+                _, pa = synth.eagle_tree(np.random.default_rng(args.seed), Mq - 1, 6)
+                par_a = torch.tensor(pa, dtype=torch.int32, device=dev)
+            Oa = torch.empty(Mq, Hq, D, dtype=torch.float16, device=dev)
+            wsa = torch.empty(w4.w4a16_tree_attention_workspace_bytes(Mq, Lctx, Hq, Hkv, D), dtype=torch.uint8, device=dev)
+            acc_a = torch.zeros(3 + Mq, dtype=torch.int32, device=dev)
+            with torch.cuda.stream(stream):
+                w4.w4a16_tree_attention(Qa, Ka, Va, par_a, Oa, wsa, stream=stream)
+            torch.cuda.synchronize()
+            ga = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga, stream=stream):
+                for _ in range(20):
+                    w4.w4a16_tree_attention(Qa, Ka, Va, par_a, Oa, wsa, stream=stream)
+            msa = time_graph(ga, 5, 2) / 20
+            kv_bytes = 2 * (Lctx + Mq) * Hkv * D * 2
+            attn[kind] = {"M": Mq, "us_per_layer": 1e3 * msa, "kv_GBps": kv_bytes / (msa * 1e-3) / 1e9,
+                          "us_per_forward_80_layers": 80 * 1e3 * msa}
+            log(f"tree attention M={Mq} ({kind}): {1e3 * msa:.1f} us per layer")
+            del ga
     clk = clocks.stop() if clocks else None
 
     cpu = None
@@ -450,7 +482,7 @@ def main():
             "us_per_layer": 1e3 * ms / n_layers,
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
-            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm,
+            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
             "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
                     "api": "VerifyStack.verify_host (pinned host buffers, graph replay, accept result read back)",
