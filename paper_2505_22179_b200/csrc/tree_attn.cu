@@ -26,7 +26,7 @@ constexpr int kRowsBlk = 64;        // query rows per CTA
 constexpr int kKv = 64;             // KV positions per chunk
 constexpr int kThreads = 128;       // 4 warps x 16 rows
 constexpr int kTileBytes = 64 * kD * 2;   // 16 KB: 64 rows x 256 B
-constexpr int kSmem = kTileBytes * 5 + 64 * 8 + 1024;   // Q, 2 x (K, V), ancestor masks
+constexpr int kSmem = kTileBytes * 5 + 64 * 8 + 64 * 4 + 1024;   // Q, 2 x (K, V), ancestor masks, parents
 
 struct Params {
   const uint16_t* Q;
@@ -70,8 +70,15 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
   const int ch0 = split * p.chunks_per_split;
   const int ch1 = min(ch0 + p.chunks_per_split, (P + kKv - 1) / kKv);
 
-  if (tid == 0) {   // ancestor masks: bit j of anc[m] <=> tree row j is m or an ancestor of m
-    for (int m = 0; m < p.M; ++m) anc[m] = (1ull << m) | (m > 0 ? anc[p.parents[m]] : 0ull);
+  // ancestor masks: bit j of anc[m] <=> tree row j is m or an ancestor of m. The parents go to shared
+  // memory in one parallel load; then each token walks up its own path (depth <= M) in shared memory.
+  int* spar = reinterpret_cast<int*>(anc + 64);
+  if (tid < p.M) spar[tid] = p.parents[tid];
+  __syncthreads();
+  if (tid < p.M) {
+    unsigned long long a = 0;
+    for (int x = tid; x >= 0; x = spar[x]) a |= 1ull << x;
+    anc[tid] = a;
   }
   // Q block: row r -> (token m = r / G, head g*G + r % G)
   for (int i = tid; i < kRowsBlk * 16; i += kThreads) {
