@@ -181,6 +181,9 @@ __device__ __forceinline__ uint16_t lds16(uint32_t addr) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
+}
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
@@ -527,15 +530,17 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
       uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
+      // One ldmatrix.x4 per chunk: matrix q = (mt, hf) is the 8 rows 32rq + 16mt + 8hf + 0..7 of the
+      // chunk, and lane (g8, c4) receives word c4 of row g8 — exactly its code word (conflict-free: the
+      // XOR chunk layout spreads the 8 rows over all 32 banks).
+      {
+        const int lr = 32 * rq + 8 * (lane >> 3) + (lane & 7);   // lanes 8q..8q+7: rows of matrix q
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            const int r = rows[mt][hf], pch = 2 * kh + cc;
-            wq[cc][mt][hf] = lds32(ub + r * 64 + ((pch ^ ((r >> 1) & 3)) << 4) + 4 * c4);
-          }
+        for (int cc = 0; cc < 2; ++cc) {
+          const int pch = 2 * kh + cc;
+          ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[cc][0][0], wq[cc][0][1], wq[cc][1][0], wq[cc][1][1]);
+        }
+      }
       float sc[2][2], zrow[2][2];
       __half2 zp[2][2];
 #pragma unroll
