@@ -137,7 +137,7 @@ __device__ unsigned long long g_trace_ma[kTraceCtas][8];
 // consumer warp 0 starts the op, has its first stage, finished its last stage, and has counted the op done.
 constexpr int kOpTraceCtas = 296, kOpTraceOps = 512;
 #if W4A16_MMA_DIAG
-__device__ unsigned long long g_op_trace[kOpTraceCtas][kOpTraceOps][4];
+__device__ unsigned long long g_op_trace[kOpTraceCtas][kOpTraceOps][8];
 #endif
 __device__ __forceinline__ void trace_op(const GemmParams& p, int job, int ev) {
 #if W4A16_MMA_DIAG
@@ -499,7 +499,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       }
       if (threadIdx.x == 0) {
         const int want = c_last - c_first;
+        trace_op(p, job, 4);
         while (ld_acquire_gpu(&J.counters[t]) != want) __nanosleep(32);
+        trace_op(p, job, 5);
         J.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch
       }
       named_bar_sync(2, 4 * 32);
@@ -703,9 +705,12 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     trace_ma(p, 2);
     trace_op(p, job, 2);
     if (cur_t >= 0) flush(cur_t, seg_u0, u_end);
+    trace_op(p, job, 6);
     trace_ma(p, 3);
-    if (chain) {   // this CTA's share of the op is written: count it
-      named_bar_sync(1, kWarps * 32);
+    // This CTA's share of the op is written: count it. Only the four warps that store Y / partials (group 0,
+    // k-half 0) take part; the other warps are already streaming the next op.
+    if (chain && grp == 0 && kh == 0) {
+      named_bar_sync(2, 4 * 32);
       if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
     }
     trace_op(p, job, 3);

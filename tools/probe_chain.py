@@ -26,7 +26,7 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); ch(); e1.record(); torch.cuda.synchronize()
 print(f"chain {a.layers} layers M={a.M}: {e0.elapsed_time(e1) * 1e3:.1f} us")
 G, NOPS = 296, 512
-buf = np.zeros((G, NOPS, 4), dtype=np.uint64)
+buf = np.zeros((G, NOPS, 8), dtype=np.uint64)
 lib.w4a16_debug_op_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert lib.w4a16_debug_op_trace(buf.ctypes.data, buf.nbytes) == 0
 n = ch.n
@@ -54,3 +54,17 @@ for k, name in enumerate(kinds):
     order = np.argsort(comp)
     print(f"{name:8s} compute per CTA (sum over layers) p0/10/50/90/100: " + " ".join(f"{x:7.1f}" for x in q),
           "| slowest CTAs", order[-6:].tolist(), "| fastest", order[:6].tolist())
+
+# last-segment flush decomposition: owner wait (slots 4 -> 5) and flush end (slot 6) vs loop end (slot 2)
+for k, name in enumerate(kinds):
+    if name == "silu":
+        continue
+    ow, fl, dn = [], [], []
+    for j in range(k, n, 5):
+        w = b[:, j, 5] - b[:, j, 4]
+        own = (buf[:G, j, 4] > 0) & (buf[:G, j, 5] >= buf[:G, j, 4])
+        if own.any():
+            ow.append(np.median(w[own]) / 1e3)
+        fl.append(np.median(b[:, j, 6] - b[:, j, 2]) / 1e3)
+        dn.append(np.median(b[:, j, 3] - b[:, j, 6]) / 1e3)
+    print(f"{name:8s} owner wait (median over owners) {np.median(ow) if ow else 0:6.2f} us | last flush {np.median(fl):6.2f} us | done-count {np.median(dn):6.2f} us")
