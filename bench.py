@@ -177,7 +177,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"oracle sample of the llama3-70b W4A16 verify forward at M={M}", "M": M},
+        "config": {"workload": f"llama3-70b W4A16 g128 {args.mode} verify forward: 80 decoder layers (QKV, O, gate-up, "
+                               f"SiLU*mul, down) + verify_accept; BASELINE configs 3-4", "M": M, "layers": 80, "tp": args.gpus,
+                   "parallelism": f"tp{args.gpus}",
+                   "timing": "the oracle on a bounded sample of this workload (see cpu_baseline.sample), host cores"},
         "cpu_baseline": {"value": value, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
