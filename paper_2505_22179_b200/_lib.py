@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libw4a16_diag.so" if os.environ.get("W4A16_LIB") == "diag" else "libw4a16.so")
+# W4A16_LIB=<name> loads libw4a16_<name>.so (diagnostic builds only: make diag); never set by tests or bench
+LIB_PATH = os.path.join(_HERE, f"libw4a16_{os.environ['W4A16_LIB']}.so" if os.environ.get("W4A16_LIB") else "libw4a16.so")
 
 W4A16_OK = 0
 W4A16_ASYM = 0
