@@ -164,6 +164,11 @@ __device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
 // MMA column j (fragment group g8 = j) carries token pi(j) of its 8-token block: with it, the 8 lanes of each
 // quarter-warp phase of an activation LDS.128 read rows {r, r + 4}, whose SWIZZLE_128B chunk positions differ
 // in the high bit, instead of rows {r, r + 1}, which collide on the same four bank groups (2-way conflict).
+#ifndef W4_MA_EXP
+#define W4_MA_EXP 0   // cost experiments only (tools/probe_exp.sh; WRONG results): bit0 no per-unit post-scale /
+                      // offset correction, bit1 no LOP3 (raw words as A), bit2 no activation loads, bit3 no
+                      // scale/zero loads
+#endif
 __device__ __forceinline__ int tok_pi(int j) { return (j >> 1) | ((j & 1) << 2); }
 
 __device__ __forceinline__ int unit_begin(int c, int U, int G) { return (int)(((long long)c * U) / G); }
@@ -529,7 +534,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         for (int tb = 0; tb < NTB; ++tb) {
           const int m = 8 * tb + tok_pi(g8);                    // MMA column g8 carries token tok_pi(g8)
           const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
-          xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
+          if (W4_MA_EXP & 4) xr[cc][tb] = make_uint4(0x3c003c00u + m, 0x3c003c00u, 0x3c003c00u ^ jx, 0x3c003c00u);
+          else xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
       uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
       // One ldmatrix.x4 per chunk: matrix q = (mt, hf) is the 8 rows 32rq + 16mt + 8hf + 0..7 of the
@@ -554,6 +560,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
             zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
             zrow[mt][hf] = 8.f;
+          } else if (W4_MA_EXP & 8) {
+            sc[mt][hf] = 0.01f * (r + 1);
+            zrow[mt][hf] = 8.f;
+            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);
           } else {
             const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
             sc[mt][hf] = __low2float(sz);
@@ -618,7 +628,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                gacc[mi][tb][e] = fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
+                gacc[mi][tb][e] = (W4_MA_EXP & 1) ? acc[mg * kMtPer + mi][tb][e]
+                                                  : fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -628,8 +639,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                 const int mt = mg * kMtPer + mi;
                 const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
                 const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-                const uint32_t a0 = lop3_and_or(qa, 0x000F000Fu, 0x64006400u), a1 = lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
-                const uint32_t a2 = lop3_and_or(qa, 0x00F000F0u, 0x54005400u), a3 = lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
+                const uint32_t a0 = (W4_MA_EXP & 2) ? qa : lop3_and_or(qa, 0x000F000Fu, 0x64006400u);
+                const uint32_t a1 = (W4_MA_EXP & 2) ? qb : lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
+                const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : lop3_and_or(qa, 0x00F000F0u, 0x54005400u);
+                const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
 #pragma unroll
                 for (int tb = 0; tb < NTB; ++tb) {
                   const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
@@ -641,6 +654,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 #pragma unroll
             for (int tb = 0; tb < NTB; ++tb) {
               const int mt = mg * kMtPer + mi;
+              if (W4_MA_EXP & 1) {
+                acc[mt][tb][0] = gacc[mi][tb][0]; acc[mt][tb][1] = gacc[mi][tb][1];
+                acc[mt][tb][2] = gacc[mi][tb][2]; acc[mt][tb][3] = gacc[mi][tb][3];
+                continue;
+              }
               acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mi][tb][0], acc[mt][tb][0]);
               acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mi][tb][1], acc[mt][tb][1]);
               acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mi][tb][2], acc[mt][tb][2]);
