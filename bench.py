@@ -396,8 +396,13 @@ def main():
             try:
                 with open(ncu_path) as f:
                     d = json.load(f)["derived"]
-                roofline["traffic"] = d["dram_traffic_bytes"]
-                roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT)
+                # the capture may cover a shorter stack (the chain capture is 8 layers): DRAM bytes per packed
+                # weight byte from ncu, times this launch's packed weight bytes
+                per_w = d["dram_traffic_bytes"] / d["algorithmic_bytes"]
+                w_launch = stack.weight_bytes / len(chains) if chains is not None else stack.layers[0]["gate_up"].weight_bytes
+                roofline["traffic"] = per_w * w_launch
+                roofline["traffic_over_weight_bytes"] = per_w
+                roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT) + " (dram__bytes_read.sum + dram__bytes_write.sum, scaled per weight byte)"
             except Exception:
                 pass
     # FP16 LM head [M, hidden] x [hidden, vocab] with the greedy argmax fused (the target_argmax
