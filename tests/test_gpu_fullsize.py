@@ -120,3 +120,57 @@ def test_verify_stack_against_oracle(dims, layers, chains):
     assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r)))
     out = st.accept_out[:3 + M].cpu().numpy()
     assert np.array_equal(out, oracle.accept(tok, par, am)[4])
+
+
+@pytest.mark.timeout(600)
+def test_verify_stack_tp2_shard_chains_match_op_by_op():
+    # tp = 2, rank 0 of a single-process NCCL group (the all-reduce is then the identity): the shard's
+    # per-segment chains ([QKV, O] | all-reduce | [gate-up, SiLU*mul, down] | all-reduce) must give exactly the
+    # op-by-op launches, and the shard GEMMs must match the oracle on the rank-0 shard weights.
+    import socket
+    import torch.distributed as dist
+    from paper_2505_22179_b200 import tp
+    own_pg = not dist.is_initialized()
+    if own_pg:
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        _tp2_body(dist, tp)
+    finally:
+        if own_pg:
+            dist.destroy_process_group()
+
+
+def _tp2_body(dist, tp):
+    d = tp.ModelDims("small", hidden=4096, ffn=8192, n_q=32, n_kv=8, head=128, layers=2)
+    Wh = {}
+
+    def make_weight(l, name, K, N, out):
+        synth.gpu(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
+        Wh[name] = synth.host(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
+
+    M = 8
+    st = tp.VerifyStack(d, 2, 16, make_weight, tp_size=2, tp_rank=0, group=dist.group.WORLD)
+    for j, buf in enumerate((st.x_qkv, st.x_o, st.x_mlp)):
+        synth.gpu(32, j, synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+    assert st.chains(M) is not None and len(st.chains(M)) == 4     # two segments per layer
+    outs = {}
+    for chains in (True, False):
+        st.use_chains = chains
+        st.forward(M)
+        torch.cuda.synchronize()
+        outs[chains] = [t[:M].clone() for t in (st.y_qkv, st.y_o, st.y_gu, st.act, st.y_down)]
+    for a, b in zip(outs[True], outs[False]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+    def ref(name, X_u16):
+        c, s_, z, _ = oracle.quantize(Wh[name])
+        return oracle.gemm(X_u16, c, s_, z, nthreads=NPROC)
+
+    for name, xin, yout in (("qkv", st.x_qkv, st.y_qkv), ("o", st.x_o, st.y_o), ("down", st.act, st.y_down)):
+        r = ref(name, _to_u16(xin[:M]))
+        y = yout[:M].float().cpu().numpy()
+        assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), name
