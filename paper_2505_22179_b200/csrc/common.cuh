@@ -2,6 +2,7 @@
 // Internal to libw4a16.so; not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -12,6 +13,20 @@ namespace w4 {
 // GEMM workspace: a fixed region of tile counters (same offset for every shape, so GEMMs of different N
 // can share one workspace), then the fp32 split-K partials (include/w4a16.h).
 constexpr size_t kCounterBytes = (size_t)(W4A16_MAX_N / 128) * 4;
+
+// One op of a chain: the device copy of a w4a16_chain_plan entry (include/w4a16.h), shared by both GEMM
+// families (the activation tensor maps are encoded for the family the plan was made for).
+enum { kOpGemm = W4A16_OP_GEMM, kOpSilu = W4A16_OP_SILU_MUL };
+struct alignas(64) ChainJob {
+  CUtensorMap xmapR;       // activation boxes of one stage's units (3-D SWIZZLE_128B)
+  CUtensorMap xmap1;       // activation box of one unit
+  const uint8_t* packed;   // GEMM: packed weights.  SILU: GU [M][2N]
+  uint16_t* Y;             // GEMM: Y [M][N].  SILU: out [M][N]
+  int kind, K, N, Gk, U;
+  int dep_x;               // earlier op whose completion this op's X reads wait for (-1: none)
+  int dep_y;               // earlier op whose completion this op's Y writes wait for (WAR / WAW; -1: none)
+  int cnt_off;             // this op's first tile counter
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

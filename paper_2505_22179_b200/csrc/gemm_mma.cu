@@ -68,19 +68,11 @@ struct Cfg {
   static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + 1024;
 };
 
-// One op of a chain: the device copy of a w4a16_chain_plan entry (include/w4a16.h). A single w4a16_gemm is
-// a one-op list whose fields come from GemmParams and the kernel's tensor-map parameters.
-enum { kOpGemm = W4A16_OP_GEMM, kOpSilu = W4A16_OP_SILU_MUL };
-struct alignas(64) ChainJob {
-  CUtensorMap xmapR;       // activation boxes of kR units (3-D SWIZZLE_128B)
-  CUtensorMap xmap1;       // activation box of one unit
-  const uint8_t* packed;   // GEMM: packed weights.  SILU: GU [M][2N]
-  uint16_t* Y;             // GEMM: Y [M][N].  SILU: out [M][N]
-  int kind, K, N, Gk, U;
-  int dep_x;               // earlier op whose completion this op's X reads wait for (-1: none)
-  int dep_y;               // earlier op whose completion this op's Y writes wait for (WAR / WAW; -1: none)
-  int cnt_off;             // this op's first tile counter
-};
+// A single w4a16_gemm is a one-op list whose fields come from GemmParams and the kernel's tensor-map
+// parameters; a chain's ops are w4::ChainJob entries (common.cuh).
+using w4::ChainJob;
+using w4::kOpGemm;
+using w4::kOpSilu;
 
 struct GemmParams {
   const uint8_t* packed;
@@ -829,8 +821,11 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
 // ---- chains (include/w4a16.h) ----
 namespace {
 int chain_family(int M, int family) {
-  if (family == W4A16_FAMILY_AUTO) family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_MMA_SYNC_S;
-  if (M < 1 || M > 16) return W4A16_ERR_SHAPE;   // chains serve the mma.sync families (M <= 16)
+  if (M < 1 || M > W4A16_MAX_M) return W4A16_ERR_SHAPE;
+  if (family == W4A16_FAMILY_AUTO)
+    family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : M <= 16 ? W4A16_FAMILY_MMA_SYNC_S : W4A16_FAMILY_TCGEN05;
+  if (family == W4A16_FAMILY_TCGEN05) return family;
+  if (M > 16) return W4A16_ERR_SHAPE;   // the mma.sync families serve M <= 16
   if (family != W4A16_FAMILY_MMA_SYNC && family != W4A16_FAMILY_MMA_SYNC_S) return W4A16_ERR_ARG;
   return family;
 }
@@ -873,18 +868,25 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
   *tiles = t;
   return W4A16_OK;
 }
-int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }
+int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }   // the tcgen05 family: one CTA per SM too
 }  // namespace
+
+extern "C" void w4a16_tc_chain_geometry(int M, int* mpad, int* kr);
+extern "C" size_t w4a16_tc_chain_partial_bytes(int M, int G);
+extern "C" int w4a16_launch_chain_tc(const void*, int, int, int, void*, size_t, size_t, int, cudaStream_t);
+static_assert(w4::ma::kCtasPerSm == 1, "chains of both families use one CTA per SM");
 
 extern "C" size_t w4a16_chain_plan_bytes(int n_ops) { return n_ops > 0 ? (size_t)n_ops * sizeof(w4::ma::ChainJob) : 0; }
 
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op* ops, int n_ops, int M, int family, int sms) {
-  if (chain_family(M, family) < 0 || sms <= 0) return 0;
+  const int fam = chain_family(M, family);
+  if (fam < 0 || sms <= 0) return 0;
   long long tiles = 0;
   int mode = 0;
   const int G = chain_ctas(sms);
   if (check_ops(ops, n_ops, M, G, &tiles, &mode) != W4A16_OK) return 0;
-  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
+  const size_t pb = fam == W4A16_FAMILY_TCGEN05 ? w4a16_tc_chain_partial_bytes(M, G) : w4::ma::chain_partial_bytes(M, G);
+  return pb + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
 }
 
 extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes,
@@ -897,7 +899,12 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
   long long tiles = 0;
   int mode = 0;
   if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
-  const int mpad = 8 * w4::ma::ntb_of(M);
+  int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the family's stages
+  if (fam == W4A16_FAMILY_TCGEN05) {
+    int kr = 0;
+    w4a16_tc_chain_geometry(M, &mpad, &kr);
+    depth = 2 * kr;
+  }
   w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
   int cnt = 0;
   for (int j = 0; j < n_ops; ++j) {
@@ -915,7 +922,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
       J.cnt_off = cnt;
       cnt += o.N / 128;
       const uint16_t* X = reinterpret_cast<const uint16_t*>(o.X);
-      if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, 2 * w4::ma::kR)) return e;
+      if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, depth)) return e;
       if (int e = w4::encode_x_sw128(&J.xmap1, X, M, o.K, mpad, 2)) return e;
     }
     // dependencies from buffer overlaps: RAW for X; WAR / WAW for Y. Completion of op i implies the
@@ -935,6 +942,8 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   const int fam = chain_family(M, family);
   if (fam < 0) return fam;
   if (!dev_plan || !ws || n_ops < 1 || (mode != W4A16_ASYM && mode != W4A16_SYM)) return W4A16_ERR_ARG;
+  if (fam == W4A16_FAMILY_TCGEN05)
+    return w4a16_launch_chain_tc(dev_plan, n_ops, M, mode, ws, ws_bytes, w4::ma::chain_done_bytes(n_ops), sms, stream);
   w4::ma::GemmParams p;
   memset(&p, 0, sizeof(p));
   p.G = chain_ctas(sms);

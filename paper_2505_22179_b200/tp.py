@@ -152,8 +152,9 @@ class VerifyStack:
 
     def chains(self, M: int):
         """Persistent chains for width M (include/w4a16.h w4a16_chain_*): the whole stack in ONE launch at
-        tp = 1; at tp > 1 one launch per segment between all-reduces. None where chains do not apply
-        (M > 16, or a shard too small to give every CTA a unit): then every op is launched on its own."""
+        tp = 1; at tp > 1 one launch per segment between all-reduces (mma.sync families for M <= 16, the tcgen05
+        family above). None where chains do not apply (a shard too small to give every CTA a unit): then every
+        op is launched on its own."""
         if M not in self._chains:
             try:
                 segs = [self._layer_ops(L, M) for L in self.layers]
