@@ -152,10 +152,14 @@ class VerifyStack:
 
     def chains(self, M: int):
         """Persistent chains for width M (include/w4a16.h w4a16_chain_*): the whole stack in ONE launch at
-        tp = 1; at tp > 1 one launch per segment between all-reduces (mma.sync families for M <= 16, the tcgen05
-        family above). None where chains do not apply (a shard too small to give every CTA a unit): then every
-        op is launched on its own."""
+        tp = 1; at tp > 1 one launch per segment between all-reduces (mma.sync families, M <= 16). None for
+        M > 16 or where a shard is too small to give every CTA a unit: then every op is launched on its own."""
         if M not in self._chains:
+            if M > 16:
+                # tcgen05-family chains exist (w4a16_chain_* with W4A16_FAMILY_TCGEN05, bit-identical) but were
+                # measured no faster than PDL-chained launches for M > 16 (DESIGN.md §5.3): launch op by op
+                self._chains[M] = None
+                return None
             try:
                 segs = [self._layer_ops(L, M) for L in self.layers]
                 if self.t == 1:
