@@ -745,11 +745,8 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
   if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * kR)) return e;
   if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
   auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
-  static bool attr_set = false;   // benign race: idempotent attribute
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
-    attr_set = true;
-  }
+  static unsigned long long attr_set = 0;
+  if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
   return launch_pdl(kern, dim3(p.G), dim3(threads_for<kScaleInA>()), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
                                                                                              : W4A16_ERR_CUDA;
 }
@@ -758,11 +755,8 @@ template <int NTB, bool SYM, bool kScaleInA>
 static int launch_chain_t(const GemmParams& p, cudaStream_t stream) {
   using C = Cfg<NTB, SYM>;
   auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
-  static bool attr_set = false;   // benign race: idempotent attribute
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess) return W4A16_ERR_CUDA;
-    attr_set = true;
-  }
+  static unsigned long long attr_set = 0;
+  if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
   CUtensorMap unused;
   memset(&unused, 0, sizeof(unused));
   // Cooperative: the owner-reduced tile fixup and the op dependencies need all G CTAs co-resident.

@@ -543,12 +543,8 @@ int launch(const uint16_t* X, const Params& p, cudaStream_t stream) {
   if (int e = w4::encode_x_sw128(&mapR, X, p.M, p.K, MPAD, 2 * C::kR)) return e;
   if (int e = w4::encode_x_sw128(&map1, X, p.M, p.K, MPAD, 2)) return e;
   auto kern = gemm_w4a16_tc_kernel<MPAD, SYM>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess)
-      return W4A16_ERR_CUDA;
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (!w4::ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
   return launch_pdl(kern, dim3(p.G), dim3(kThreads), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
                                                                                              : W4A16_ERR_CUDA;
 }
@@ -557,12 +553,8 @@ template <int MPAD, bool SYM>
 int launch_chain(const Params& p, cudaStream_t stream) {
   using C = Cfg<MPAD, SYM>;
   auto kern = gemm_w4a16_tc_kernel<MPAD, SYM>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess)
-      return W4A16_ERR_CUDA;
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (!w4::ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
   CUtensorMap unused;
   memset(&unused, 0, sizeof(unused));
   cudaLaunchConfig_t cfg = {};

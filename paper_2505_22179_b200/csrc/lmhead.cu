@@ -217,12 +217,8 @@ int launch(const uint16_t* H, const uint16_t* W, const Params& p, cudaStream_t s
   if (int e = encode_x_sw128(&wmap, W, p.V, p.K, kRows, 2)) return e;
   if (int e = encode_x_sw128(&hmap, H, p.M, p.K, C::kMpad, 2)) return e;
   auto kern = lmhead_argmax_kernel<NTB>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess)
-      return W4A16_ERR_CUDA;
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (!ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
   return launch_pdl(kern, dim3(p.G), dim3(kThreads), C::kSmem, stream, wmap, hmap, p) == cudaSuccess ? W4A16_OK
                                                                                          : W4A16_ERR_CUDA;
 }

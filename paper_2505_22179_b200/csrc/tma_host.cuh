@@ -37,6 +37,19 @@ inline int encode_x_sw128(CUtensorMap* map, const uint16_t* X, int M, int K, int
   return W4A16_OK;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is per device,
+// so a process driving several GPUs must set it on each (the flag word is per template instance).
+template <typename Kern>
+inline bool ensure_smem_attr(Kern kern, int bytes, unsigned long long& done_mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  const unsigned long long bit = 1ull << dev;
+  if (__atomic_load_n(&done_mask, __ATOMIC_ACQUIRE) & bit) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  __atomic_fetch_or(&done_mask, bit, __ATOMIC_RELEASE);
+  return true;
+}
+
 // Launch with programmatic stream serialization: the kernel may begin while the previous kernel in the
 // stream drains; it must call griddepcontrol.wait before touching anything that kernel writes.
 template <typename Kern, typename... Args>

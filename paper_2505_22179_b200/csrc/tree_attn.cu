@@ -16,6 +16,7 @@
 // w4a16_kv_compact: for k = 1..accepted, cache row L + k <- row L + path[k-1] (path[k-1] >= k, so ascending
 // k never overwrites a row still to be read); reads the acceptance result from device memory.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "w4a16.h"
 
 namespace w4 {
@@ -274,13 +275,8 @@ extern "C" int w4a16_launch_tree_attention(const uint16_t* Q, const uint16_t* K,
   p.m_part = p.o_part + rows * w4::ta::kD;
   p.l_part = p.m_part + rows;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)w4::ta::kD);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(w4::ta::tree_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, w4::ta::kSmem) !=
-        cudaSuccess)
-      return W4A16_ERR_CUDA;
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (!w4::ensure_smem_attr(w4::ta::tree_attn_kernel, w4::ta::kSmem, attr)) return W4A16_ERR_CUDA;
   w4::ta::tree_attn_kernel<<<dim3(p.splits, p.qblocks, Hkv), w4::ta::kThreads, w4::ta::kSmem, stream>>>(p);
   w4::ta::tree_attn_combine<<<dim3(p.R, Hkv), w4::ta::kD, 0, stream>>>(p, O);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
