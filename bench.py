@@ -405,6 +405,65 @@ def main():
                 roofline["traffic_source"] = os.path.relpath(ncu_path, ROOT) + " (dram__bytes_read.sum + dram__bytes_write.sum, scaled per weight byte)"
             except Exception:
                 pass
+    # BASELINE configs 1 and 2 beside the headline (config 3-4): a single 4096x4096 W4A16 GEMM at M=8 with
+    # acceptance on the 8-node tree (config 1), and the Llama-3-8B linear stack's M sweep (config 2).
+    other_configs = None
+    if args.lm_head and rank == 0 and world == 1:
+        other_configs = {}
+        R1 = 64   # distinct 4096x4096 weights back to back (64 x 8.9 MB >> L2)
+        lins = []
+        for r in range(R1):
+            Wt = synth.gpu(args.seed, synth.tensor_id(0xFFC, r, 0), synth.WEIGHT, 4096, 4096)
+            lins.append(w4.pack_linear(Wt))
+            del Wt
+        X1 = synth.gpu(args.seed, synth.tensor_id(0xFFC, 255, 0), synth.ACT, 8, 4096)
+        Y1 = torch.empty(8, 4096, dtype=torch.float16, device=dev)
+        ws1 = w4.alloc_workspace(8, [(4096, 4096)], device=dev)
+        tok8 = torch.tensor([100, 11, 12, 21, 22, 23, 31, 32], dtype=torch.int32, device=dev)
+        par8 = torch.tensor([-1, 0, 0, 1, 1, 2, 3, 5], dtype=torch.int32, device=dev)
+        am8 = torch.tensor([12, 99, 23, 31, 99, 32, 99, 40], dtype=torch.int32, device=dev)
+        out8 = torch.empty(11, dtype=torch.int32, device=dev)
+        with torch.cuda.stream(stream):
+            for l in lins:
+                l(X1, Y1, ws1, stream)
+            w4.verify_accept(tok8, par8, am8, out8, stream=stream)
+        torch.cuda.synchronize()
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=stream):
+            for l in lins:
+                l(X1, Y1, ws1, stream)
+        ms1 = time_graph(g1, 5, 2) / R1
+        ga = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga, stream=stream):
+            for _ in range(50):
+                w4.verify_accept(tok8, par8, am8, out8, stream=stream)
+        msa = time_graph(ga, 5, 2) / 50
+        wb1 = lins[0].weight_bytes
+        other_configs["config1_gemm4096_M8"] = {"us": 1e3 * ms1, "TBps": wb1 / (ms1 * 1e-3) / 1e12,
+                                                "frac_hbm": wb1 / (ms1 * 1e-3) / 1e9 / peak_gbs,
+                                                "accept_8node_us": 1e3 * msa,
+                                                "note": "64 distinct weights back to back in a CUDA graph"}
+        del lins, g1, ga
+        log(f"config 1: {1e3 * ms1:.2f} us per 4096x4096 GEMM at M=8, accept {1e3 * msa:.2f} us")
+        d8 = tp.LLAMA3_8B
+
+        def make8(l, name, K, N, out):
+            synth.gpu(args.seed, synth.tensor_id(l, mat_id[name], 0xEE), synth.WEIGHT, K, N, out=out)
+
+        st8 = tp.VerifyStack(d8, d8.layers, 64, make8, device=dev)
+        for buf, tid in ((st8.x_qkv, 1), (st8.x_o, 2), (st8.x_mlp, 3)):
+            synth.gpu(args.seed, synth.tensor_id(0xFFB, tid, 0), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+        sw8 = {}
+        for M8 in (1, 4, 8, 16, 32, 64):
+            g8 = st8.capture(M8)
+            ms8 = time_graph(g8, 10, 3)
+            sw8[str(M8)] = {"ms_per_forward": ms8, "TBps": st8.weight_bytes / (ms8 * 1e-3) / 1e12,
+                            "frac_hbm": st8.weight_bytes / (ms8 * 1e-3) / 1e9 / peak_gbs}
+        other_configs["config2_llama3_8b_sweep"] = {"layers": d8.layers, "weight_bytes": st8.weight_bytes,
+                                                    "m_sweep": sw8}
+        log("config 2 (8B) sweep: " + ", ".join(f"M={k}: {v['ms_per_forward']:.3f} ms" for k, v in sw8.items()))
+        del st8
+        torch.cuda.empty_cache()
     # FP16 LM head [M, hidden] x [hidden, vocab] with the greedy argmax fused (the target_argmax
     # that verify_accept consumes), measured on its own: its weights (2.1 GB fp16) are not W4A16 bytes.
     lm = None
@@ -491,6 +550,7 @@ def main():
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
+            "other_configs": other_configs,
             "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
                     "api": "VerifyStack.verify_host (pinned host buffers, graph replay, accept result read back)",
