@@ -396,6 +396,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   for (int job = 0; job < p.n_jobs; ++job) {
     trace_op(p, job, 0);
     const JobInfo J = job_at(p, &xmapR, &xmap1, job);
+    if (W4A16_MMA_DIAG && (p.dbg & 64)) {   // diagnostics: when the descriptor has arrived
+      volatile int sink = J.U + J.Gk;
+      (void)sink;
+      trace_op(p, job, 7);
+    }
     if (J.kind == kOpSilu) {
       // SiLU*mul op of a chain (same arithmetic as w4a16_silu_mul), spread over every consumer thread of
       // every CTA once the gate-up op that writes GU (and the readers of `out`) are done.

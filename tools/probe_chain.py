@@ -68,3 +68,8 @@ for k, name in enumerate(kinds):
         fl.append(np.median(b[:, j, 6] - b[:, j, 2]) / 1e3)
         dn.append(np.median(b[:, j, 3] - b[:, j, 6]) / 1e3)
     print(f"{name:8s} owner wait (median over owners) {np.median(ow) if ow else 0:6.2f} us | last flush {np.median(fl):6.2f} us | done-count {np.median(dn):6.2f} us")
+
+# op start -> descriptor loaded (slot 7) vs -> first stage ready (slot 1)
+for k, name in enumerate(kinds):
+    d = [np.median(b[:, j, 7] - b[:, j, 0]) / 1e3 for j in range(k, n, 5) if (buf[:G, j, 7] > 0).all()]
+    print(f"{name:8s} descriptor load {np.median(d) if d else float('nan'):6.2f} us")
