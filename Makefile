@@ -45,6 +45,6 @@ oracle/libw4a16_oracle.so: oracle/w4a16_oracle.c oracle/w4a16_oracle.h
 	gcc -O2 -fPIC -shared -ffp-contract=off -fno-fast-math -o $@ oracle/w4a16_oracle.c -lm -lpthread
 
 clean:
-	rm -rf build $(LIB) synth/*.so oracle/*.so
+	rm -rf build $(LIB) $(DIAG_LIB) synth/*.so oracle/*.so
 
 .PHONY: all clean diag

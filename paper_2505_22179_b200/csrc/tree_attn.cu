@@ -27,7 +27,12 @@ constexpr int kRowsBlk = 64;        // query rows per CTA
 constexpr int kKv = 64;             // KV positions per chunk
 constexpr int kThreads = 128;       // 4 warps x 16 rows
 constexpr int kTileBytes = 64 * kD * 2;   // 16 KB: 64 rows x 256 B
-constexpr int kSmem = kTileBytes * 5 + 64 * 8 + 64 * 4 + 1024;   // Q, 2 x (K, V), ancestor masks, parents
+#ifndef W4_TA_BUFS
+#define W4_TA_BUFS 1
+#endif
+constexpr int kKvBufs = W4_TA_BUFS;       // K/V chunk buffers: 2 = double-buffered, 1 = more CTAs per SM
+constexpr int kSmem = kTileBytes * (1 + 2 * kKvBufs) + 64 * 8 + 64 * 4 + 1024;   // Q, (K, V) x bufs, masks, parents
+constexpr int kCtasPerSmEst = kKvBufs == 2 ? 2 : 3;
 
 struct Params {
   const uint16_t* Q;
@@ -63,8 +68,8 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) { return h22u(__fl
 __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_u32(smem), sK0 = sQ + kTileBytes, sV0 = sQ + 3 * kTileBytes;
-  unsigned long long* anc = reinterpret_cast<unsigned long long*>(smem + 5 * kTileBytes);
+  const uint32_t sQ = smem_u32(smem), sK0 = sQ + kTileBytes, sV0 = sQ + (1 + kKvBufs) * kTileBytes;
+  unsigned long long* anc = reinterpret_cast<unsigned long long*>(smem + (1 + 2 * kKvBufs) * kTileBytes);
   const int split = blockIdx.x, qb = blockIdx.y, g = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, c4 = lane & 3;
   const int P = p.L + p.M;
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
       cp_async16(sV0 + buf * kTileBytes + tile_off(r, c), p.V + off, ok);
     }
   };
-  if (ch0 < ch1) load_kv(ch0, 0);
+  if (kKvBufs == 2 && ch0 < ch1) load_kv(ch0, 0);
   cp_async_commit();
 
   // this lane's two query rows (g8, g8 + 8 of the warp's 16) and their tokens
@@ -109,10 +114,16 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
   float mx[2] = {-INFINITY, -INFINITY}, sum[2] = {0.f, 0.f};
 
   for (int ch = ch0; ch < ch1; ++ch) {
-    const int buf = (ch - ch0) & 1;
-    if (ch + 1 < ch1) load_kv(ch + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait1();
+    const int buf = kKvBufs == 2 ? (ch - ch0) & 1 : 0;
+    if (kKvBufs == 2) {
+      if (ch + 1 < ch1) load_kv(ch + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait1();
+    } else {
+      load_kv(ch, 0);
+      cp_async_commit();
+      cp_async_wait0();
+    }
     __syncthreads();
     const uint32_t sK = sK0 + buf * kTileBytes, sV = sV0 + buf * kTileBytes;
     // S = Q K^T: 16 rows x 64 positions per warp
@@ -208,23 +219,44 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
 }
 
 // Merge the splits: O = sum_s 2^(m_s - m*) O_s / sum_s 2^(m_s - m*) l_s, fp16 out.
-__global__ void __launch_bounds__(kD) tree_attn_combine(const Params p, uint16_t* __restrict__ O) {
-  const int r = blockIdx.x, g = blockIdx.y, d = threadIdx.x;
+// Merge the splits: O = sum_s 2^(m_s - m*) O_s / sum_s 2^(m_s - m*) l_s, fp16 out. One warp per query row
+// (lanes over the 128 head dims as float4), 8 rows per block.
+__global__ void __launch_bounds__(256) tree_attn_combine(const Params p, uint16_t* __restrict__ O) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + warp, g = blockIdx.y;
   if (r >= p.R) return;
   const int Rpad = p.qblocks * kRowsBlk;
   float mstar = -INFINITY;
-  for (int sp = 0; sp < p.splits; ++sp) mstar = fmaxf(mstar, p.m_part[((size_t)sp * p.Hkv + g) * Rpad + r]);
-  float num = 0.f, den = 0.f;
-  for (int sp = 0; sp < p.splits; ++sp) {
-    const size_t i = ((size_t)sp * p.Hkv + g) * Rpad + r;
-    const float ms = p.m_part[i];
-    if (ms == -INFINITY) continue;
-    const float w = exp2f(ms - mstar);
-    num += w * p.o_part[i * kD + d];
-    den += w * p.l_part[i];
+  for (int sp = lane; sp < p.splits; sp += 32) mstar = fmaxf(mstar, __ldcg(&p.m_part[((size_t)sp * p.Hkv + g) * Rpad + r]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mstar = fmaxf(mstar, __shfl_xor_sync(0xffffffffu, mstar, off));
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+  float den = 0.f;
+  for (int sp0 = 0; sp0 < p.splits; sp0 += 4) {   // four splits' loads in flight at a time
+    float ms[4], l[4];
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int sp = min(sp0 + u, p.splits - 1);
+      const size_t i = ((size_t)sp * p.Hkv + g) * Rpad + r;
+      ms[u] = sp0 + u < p.splits ? __ldcg(&p.m_part[i]) : -INFINITY;
+      l[u] = __ldcg(&p.l_part[i]);
+      v[u] = __ldcg(reinterpret_cast<const float4*>(p.o_part + i * kD) + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (ms[u] == -INFINITY) continue;
+      const float w = exp2f(ms[u] - mstar);
+      num.x += w * v[u].x; num.y += w * v[u].y; num.z += w * v[u].z; num.w += w * v[u].w;
+      den += w * l[u];
+    }
   }
+  const float inv = 1.f / den;
   const int m = r / p.G, h = g * p.G + r % p.G;
-  O[((size_t)m * p.Hq + h) * kD + d] = __half_as_ushort(__float2half_rn(num / den));
+  uint2 out;
+  out.x = pack_h2(num.x * inv, num.y * inv);
+  out.y = pack_h2(num.z * inv, num.w * inv);
+  *reinterpret_cast<uint2*>(O + ((size_t)m * p.Hq + h) * kD + 4 * lane) = out;
 }
 
 __global__ void kv_compact_kernel(uint16_t* K, uint16_t* V, int L, int row_vec, const int32_t* __restrict__ acc) {
@@ -249,8 +281,9 @@ void plan_splits(int M, int L, int Hq, int Hkv, int sms, int* qblocks, int* spli
   const int G = Hq / Hkv, R = M * G;
   *qblocks = (R + w4::ta::kRowsBlk - 1) / w4::ta::kRowsBlk;
   const int chunks = (L + M + w4::ta::kKv - 1) / w4::ta::kKv;
-  int s = (2 * sms + Hkv * *qblocks - 1) / (Hkv * *qblocks);
-  s = s < 1 ? 1 : s > chunks ? chunks : s;
+  int s = (w4::ta::kCtasPerSmEst * sms + Hkv * *qblocks - 1) / (Hkv * *qblocks);
+  const int max_s = (chunks + 1) / 2;   // at least two chunks per split where there are two (fewer partials to merge)
+  s = s < 1 ? 1 : s > max_s ? max_s : s;
   *cps = (chunks + s - 1) / s;
   *splits = (chunks + *cps - 1) / *cps;
 }
@@ -278,7 +311,7 @@ extern "C" int w4a16_launch_tree_attention(const uint16_t* Q, const uint16_t* K,
   static unsigned long long attr = 0;
   if (!w4::ensure_smem_attr(w4::ta::tree_attn_kernel, w4::ta::kSmem, attr)) return W4A16_ERR_CUDA;
   w4::ta::tree_attn_kernel<<<dim3(p.splits, p.qblocks, Hkv), w4::ta::kThreads, w4::ta::kSmem, stream>>>(p);
-  w4::ta::tree_attn_combine<<<dim3(p.R, Hkv), w4::ta::kD, 0, stream>>>(p, O);
+  w4::ta::tree_attn_combine<<<dim3((p.R + 7) / 8, Hkv), 256, 0, stream>>>(p, O);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
