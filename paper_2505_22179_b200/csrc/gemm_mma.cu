@@ -51,7 +51,7 @@ constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 
 #define W4_MA_CTAS 2
 #endif
 constexpr int kCtasPerSm = kGroups >= 2 ? 1 : W4_MA_CTAS;   // resident CTAs per SM
-constexpr int kSmemBudget = (kCtasPerSm == 1 ? 224 : kCtasPerSm == 2 ? 112 : 74) * 1024;
+constexpr int kSmemBudget = kCtasPerSm == 1 ? 227 * 1024 - 512 : (kCtasPerSm == 2 ? 112 : 74) * 1024;   // 512 B static
 
 template <int NTB, bool SYM>
 struct Cfg {
