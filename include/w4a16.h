@@ -188,9 +188,8 @@ size_t w4a16_chain_workspace_bytes(const w4a16_op* ops, int n_ops, int M, int fa
 /* Encode the chain (job table with TMA descriptors of every X, dependency indices) for width M into the
  * HOST buffer `plan` (w4a16_chain_plan_bytes(n_ops) bytes). The caller copies it to device memory once
  * (e.g. cudaMemcpy) and passes that copy to w4a16_chain_run for as long as the buffers stay where they
- * are. family: W4A16_FAMILY_AUTO (as w4a16_gemm_family) or an explicit family valid for M (the mma.sync
- * families for M <= 16, W4A16_FAMILY_TCGEN05 for any M <= 64). Validates every op like w4a16_gemm /
- * w4a16_silu_mul; in-place ops are rejected. */
+ * are. family: W4A16_FAMILY_AUTO or an explicit family valid for M (chains serve the mma.sync families,
+ * M <= 16). Validates every op like w4a16_gemm / w4a16_silu_mul; in-place ops are rejected. */
 int w4a16_chain_plan(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes);
 /* Run a chain: dev_plan = device copy of the plan for (n_ops, M, family); mode = the GEMMs' mode.
  * workspace: at least w4a16_chain_workspace_bytes(ops, n_ops, M, family) zero-initialised bytes, used by

@@ -820,11 +820,8 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
 // ---- chains (include/w4a16.h) ----
 namespace {
 int chain_family(int M, int family) {
-  if (M < 1 || M > W4A16_MAX_M) return W4A16_ERR_SHAPE;
-  if (family == W4A16_FAMILY_AUTO)
-    family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : M <= 16 ? W4A16_FAMILY_MMA_SYNC_S : W4A16_FAMILY_TCGEN05;
-  if (family == W4A16_FAMILY_TCGEN05) return family;
-  if (M > 16) return W4A16_ERR_SHAPE;   // the mma.sync families serve M <= 16
+  if (family == W4A16_FAMILY_AUTO) family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_MMA_SYNC_S;
+  if (M < 1 || M > 16) return W4A16_ERR_SHAPE;   // chains serve the mma.sync families (M <= 16)
   if (family != W4A16_FAMILY_MMA_SYNC && family != W4A16_FAMILY_MMA_SYNC_S) return W4A16_ERR_ARG;
   return family;
 }
@@ -870,22 +867,16 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
 int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }   // the tcgen05 family: one CTA per SM too
 }  // namespace
 
-extern "C" void w4a16_tc_chain_geometry(int M, int* mpad, int* kr);
-extern "C" size_t w4a16_tc_chain_partial_bytes(int M, int G);
-extern "C" int w4a16_launch_chain_tc(const void*, int, int, int, void*, size_t, size_t, int, cudaStream_t);
-static_assert(w4::ma::kCtasPerSm == 1, "chains of both families use one CTA per SM");
 
 extern "C" size_t w4a16_chain_plan_bytes(int n_ops) { return n_ops > 0 ? (size_t)n_ops * sizeof(w4::ma::ChainJob) : 0; }
 
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op* ops, int n_ops, int M, int family, int sms) {
-  const int fam = chain_family(M, family);
-  if (fam < 0 || sms <= 0) return 0;
+  if (chain_family(M, family) < 0 || sms <= 0) return 0;
   long long tiles = 0;
   int mode = 0;
   const int G = chain_ctas(sms);
   if (check_ops(ops, n_ops, M, G, &tiles, &mode) != W4A16_OK) return 0;
-  const size_t pb = fam == W4A16_FAMILY_TCGEN05 ? w4a16_tc_chain_partial_bytes(M, G) : w4::ma::chain_partial_bytes(M, G);
-  return pb + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
+  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
 }
 
 extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes,
@@ -898,12 +889,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
   long long tiles = 0;
   int mode = 0;
   if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
-  int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the family's stages
-  if (fam == W4A16_FAMILY_TCGEN05) {
-    int kr = 0;
-    w4a16_tc_chain_geometry(M, &mpad, &kr);
-    depth = 2 * kr;
-  }
+  const int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the stages
   w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
   int cnt = 0;
   for (int j = 0; j < n_ops; ++j) {
@@ -941,8 +927,6 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   const int fam = chain_family(M, family);
   if (fam < 0) return fam;
   if (!dev_plan || !ws || n_ops < 1 || (mode != W4A16_ASYM && mode != W4A16_SYM)) return W4A16_ERR_ARG;
-  if (fam == W4A16_FAMILY_TCGEN05)
-    return w4a16_launch_chain_tc(dev_plan, n_ops, M, mode, ws, ws_bytes, w4::ma::chain_done_bytes(n_ops), sms, stream);
   w4::ma::GemmParams p;
   memset(&p, 0, sizeof(p));
   p.G = chain_ctas(sms);

@@ -23,7 +23,6 @@
 //  * epilogue (after the stage's A hand-off): tcgen05.ld of the accumulator (thread = row), fp16 store of
 //    Y, or — for a tile split across CTAs — fp32 partial + ordered last-arriver reduction (as family A).
 #include <cstdlib>
-#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -69,36 +68,7 @@ struct Params {
   int* counters;     // [W4A16_MAX_N/128], shared by every shape (fixed offset)
   int M, K, N, Gk, U, G;
   int dbg;           // diagnostics only (W4A16_TC_DEBUG): bit0 skip MMA, bit1 skip dequant, bit2 skip X TMA
-  const ChainJob* jobs;   // chain: the op table (device); nullptr: single GEMM
-  int n_jobs;             // 1 for a single GEMM
-  int* done;              // chain: [n_jobs] CTAs that finished each op, then the exit counter
-  int slots;              // chain: partial-slot ring length in ops (1 for a single GEMM)
 };
-
-struct JobT {
-  const uint8_t* packed;
-  uint16_t* Y;
-  const CUtensorMap* mR;
-  const CUtensorMap* m1;
-  int* counters;
-  int kind, N, Gk, U, dep_x, dep_y;
-};
-__device__ __forceinline__ JobT job_at(const Params& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
-  JobT J;
-  if (p.jobs == nullptr) {
-    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters;
-    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1;
-  } else {
-    const ChainJob* c = p.jobs + j;
-    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + c->cnt_off;
-    J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y;
-  }
-  return J;
-}
-__device__ __forceinline__ void wait_op(const Params& p, int j) {
-  if (j < 0) return;
-  while (ld_acquire_gpu(&p.done[j]) < p.G) __nanosleep(64);
-}
 
 // Diagnostics only (W4A16_TC_DEBUG bit 8): per-stage %globaltimer stamps of CTA 0 (tools/probe_tc.py).
 constexpr int kTraceStages = 64;
@@ -208,7 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool chain = p.jobs != nullptr;
+  const int u_begin = unit_begin(blockIdx.x, p.U, p.G), u_end = unit_begin(blockIdx.x + 1, p.U, p.G);
+  const int n_stages = (u_end - u_begin + kR - 1) / kR;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_base = smem_u32(smem);
 
@@ -220,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
   }
   if (warp == kMmaWarp) tmem_alloc(&s_tmem, kTmemCols);
-  if (warp == kProducerWarp && lane == 0 && !chain) {
+  if (warp == kProducerWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapR)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
   }
@@ -231,68 +202,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
 
   if (warp == kProducerWarp) {
     // ---------------- producer ----------------
-    // Weights are issued as soon as a ring slot frees; a stage's activations wait in a FIFO until they may
-    // be read (griddepcontrol.wait for a single GEMM; the producing op's completion in a chain), so the
-    // weight stream runs ahead across op boundaries (the chain design of gemm_mma.cu).
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int q_s[8], q_j[8], q_u0[8], q_nu[8];
-      int q_head = 0, q_n = 0, ok_upto = -1;
-      bool pdl_done = chain;
-      auto issue_x = [&](int s, const JobT& J, int u0, int nu) {
+      auto load_w = [&](int i, int s) {   // packed weights (never written by a preceding kernel)
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+        mbar_expect_tx(&full_bar[s], ((p.dbg & 4) ? 0 : nu * C::kXUnit) + nu * C::kTB);
+        bulk_g2s(smem + s * C::kStage + C::kXStage, p.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+      };
+      auto load_x = [&](int i, int s) {   // activations (after griddepcontrol.wait)
         if (p.dbg & 4) return;
-        const int g0 = u0 % J.Gk;
+        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0), g0 = u0 % p.Gk;
         const uint32_t st = smem_base + s * C::kStage;
-        if (nu == kR && g0 + kR <= J.Gk) {   // the stage's units share an n-tile: one 3-D TMA
-          tma_3d(st, J.mR, 0, 0, 2 * g0, &full_bar[s]);
+        if (nu == kR && g0 + kR <= p.Gk) {   // the stage's units share an n-tile: one 3-D TMA
+          tma_3d(st, &xmapR, 0, 0, 2 * g0, &full_bar[s]);
         } else {
-          for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, J.m1, 0, 0, 2 * ((u0 + j) % J.Gk), &full_bar[s]);
+          for (int j = 0; j < nu; ++j) tma_3d(st + j * C::kXUnit, &xmap1, 0, 0, 2 * ((u0 + j) % p.Gk), &full_bar[s]);
         }
       };
-      auto drain = [&](bool block) {
-        while (q_n > 0) {
-          if (!pdl_done) {
-            if (!block) return;
-            pdl_wait();
-            pdl_done = true;
-          }
-          const JobT J = job_at(p, &xmapR, &xmap1, q_j[q_head]);
-          if (J.dep_x > ok_upto) {
-            if (ld_acquire_gpu(&p.done[J.dep_x]) < p.G) {
-              if (!block) return;
-              wait_op(p, J.dep_x);
-            }
-            ok_upto = J.dep_x;
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-          }
-          issue_x(q_s[q_head], J, q_u0[q_head], q_nu[q_head]);
-          q_head = (q_head + 1) & 7;
-          --q_n;
-        }
-      };
-      int s = 0, issued = 0;
-      uint32_t ph = 0;
-      for (int job = 0; job < p.n_jobs; ++job) {
-        const JobT J = job_at(p, &xmapR, &xmap1, job);
-        if (J.kind != kOpGemm) continue;
-        const int u_begin = unit_begin(blockIdx.x, J.U, p.G), u_end = unit_begin(blockIdx.x + 1, J.U, p.G);
-        for (int u0 = u_begin; u0 < u_end; u0 += kR) {
-          const int nu = min(kR, u_end - u0);
-          if (issued >= S) {
-            if (!pdl_done) drain(true);
-            while (!mbar_try_wait(&empty_bar[s], ph ^ 1)) drain(false);
-          }
-          mbar_expect_tx(&full_bar[s], ((p.dbg & 4) ? 0 : nu * C::kXUnit) + nu * C::kTB);
-          bulk_g2s(smem + s * C::kStage + C::kXStage, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
-          const int e = (q_head + q_n) & 7;
-          q_s[e] = s; q_j[e] = job; q_u0[e] = u0; q_nu[e] = nu;
-          ++q_n;
-          drain(false);
-          ++issued;
-          if (++s == S) { s = 0; ph ^= 1; }
-        }
+      const int pre = min(S, n_stages);
+      for (int i = 0; i < pre; ++i) { trace(p, 0, i); load_w(i, i); }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) { load_x(i, i); trace(p, 1, i); }
+      int s = pre % S;
+      uint32_t ph = pre == S ? 1 : 0;
+      for (int i = pre; i < n_stages; ++i) {
+        wait_bar(p, &empty_bar[s], ph ^ 1);
+        trace(p, 0, i);
+        load_w(i, s);
+        load_x(i, s);
+        trace(p, 1, i);
+        if (++s == S) { s = 0; ph ^= 1; }
       }
-      drain(true);
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (whole warp converged; elect.sync issues) ----------------
@@ -302,15 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     int s = 0, b = 0;
     uint32_t ph = 0, aph = 0;
     uint32_t accph[2] = {0, 0};
-    int nseg = 0, a = 1;
-    const uint32_t desc_hi = (uint32_t)(kDescSW128 >> 32);
-    for (int job = 0; job < p.n_jobs; ++job) {
-    const JobT J = job_at(p, &xmapR, &xmap1, job);
-    if (J.kind != kOpGemm) continue;
-    const int u_begin = unit_begin(blockIdx.x, J.U, p.G), u_end = unit_begin(blockIdx.x + 1, J.U, p.G);
-    const int n_stages = (u_end - u_begin + kR - 1) / kR;
-    int t = u_begin / J.Gk, boundary = (t + 1) * J.Gk;
+    int t = u_begin / p.Gk, boundary = (t + 1) * p.Gk, nseg = 0, a = 1;
     bool fresh = true;   // the next unit starts a segment
+    const uint32_t desc_hi = (uint32_t)(kDescSW128 >> 32);
     for (int i = 0; i < n_stages; ++i) {
       const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
       wait_bar(p, &full_bar[s], ph);
@@ -323,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
         const int jend = min(nu, ja + kAU);
         for (int j = ja; j < jend; ++j) {
           const int u = u0 + j;
-          if (u == boundary) { ++t; boundary += J.Gk; fresh = true; }
+          if (u == boundary) { ++t; boundary += p.Gk; fresh = true; }
           const bool seg_start = fresh;
           if (seg_start) {
             a ^= 1;
@@ -360,7 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       __syncwarp();
       if (++s == S) { s = 0; ph ^= 1; }
     }
-    }
   } else {
     // ---------------- dequant + epilogue (warps 0..15) ----------------
     pdl_wait();   // Y / workspace writes must follow the preceding kernel
@@ -371,34 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     int s = 0, b = 0;
     uint32_t ph = 0, aph = 0;
     uint32_t accph[2] = {0, 0};
-    int nseg = 0;   // segments so far (all ops): selects the TMEM accumulator buffer, like the MMA warp
-    for (int job = 0; job < p.n_jobs; ++job) {
-    const JobT J = job_at(p, &xmapR, &xmap1, job);
-    if (J.kind == kOpSilu) {
-      // SiLU*mul op of a chain (w4a16_silu_mul's arithmetic) over all 512 dequant threads of every CTA
-      if (threadIdx.x == 0) wait_op(p, max(J.dep_x, J.dep_y));
-      named_bar_sync(1, kDqWarps * 32);
-      const int F = J.N, vecs = F / 8;
-      const long long total = (long long)p.M * vecs;
-      const uint16_t* GU = reinterpret_cast<const uint16_t*>(J.packed);
-      for (long long i = (long long)blockIdx.x * (kDqWarps * 32) + threadIdx.x; i < total; i += (long long)p.G * (kDqWarps * 32)) {
-        const int m = (int)(i / vecs), v = (int)(i % vecs);
-        const uint4 g = __ldcg(reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + (size_t)v * 8));
-        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + F + (size_t)v * 8));
-        *reinterpret_cast<uint4*>(J.Y + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
-      }
-      named_bar_sync(1, kDqWarps * 32);
-      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
-      continue;
-    }
-    const int u_begin = unit_begin(blockIdx.x, J.U, p.G), u_end = unit_begin(blockIdx.x + 1, J.U, p.G);
-    const int n_stages = (u_end - u_begin + kR - 1) / kR;
-    int cur_t = -1, seg_u0 = u_begin, boundary = 0;
-    const int nseg0 = nseg;   // this op's first segment
-    // Y writes (and this op's partial slots) wait for the earlier ops that read / write the same buffers
-    const int wdep = chain ? max(J.dep_y, job - p.slots) : -1;
-    bool y_ready = wdep < 0;
-    float* part = p.partials + (size_t)(job % p.slots) * (2 * p.G) * MPAD * kTileN;
+    int cur_t = -1, seg_u0 = u_begin, nseg = 0, boundary = 0;
 
     auto epilogue = [&](int t, int sg0, int sg1, int seg_index) {
       const int a = seg_index & 1;
@@ -417,42 +323,36 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty_bar[a]);
-      if (!y_ready) {   // the earlier ops that read / write this op's Y are complete
-        if (threadIdx.x == 0) wait_op(p, wdep);
-        named_bar_sync(1, kDqWarps * 32);
-        y_ready = true;
-      }
-      const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
+      const int tile_u0 = t * p.Gk, tile_u1 = tile_u0 + p.Gk;
       const int n = t * kTileN + row;
       const int m0 = h * kCols;
       if (sg0 == tile_u0 && sg1 == tile_u1) {
 #pragma unroll
         for (int i = 0; i < kCols; ++i)
-          if (m0 + i < p.M) J.Y[(size_t)(m0 + i) * J.N + n] = __half_as_ushort(__float2half_rn(acc[i]));
+          if (m0 + i < p.M) p.Y[(size_t)(m0 + i) * p.N + n] = __half_as_ushort(__float2half_rn(acc[i]));
         return;
       }
-      // split tile: slot 0 = this CTA's first segment of the op, slot 1 = its last
-      const int slot = 2 * blockIdx.x + (seg_index == nseg0 ? 0 : 1);
+      const int slot = 2 * blockIdx.x + (seg_index == 0 ? 0 : 1);
 #pragma unroll
-      for (int i = 0; i < kCols; ++i) __stcg(&part[((size_t)slot * MPAD + m0 + i) * kTileN + row], acc[i]);
+      for (int i = 0; i < kCols; ++i) __stcg(&p.partials[((size_t)slot * MPAD + m0 + i) * kTileN + row], acc[i]);
       __threadfence();
       named_bar_sync(1, kDqWarps * 32);
-      const int c_first = cta_of_unit(tile_u0, J.U, p.G), c_last = cta_of_unit(tile_u1 - 1, J.U, p.G);
-      if (threadIdx.x == 0) s_last = (atomicAdd(&J.counters[t], 1) == c_last - c_first);
+      const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
+      if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[t], 1) == c_last - c_first);
       named_bar_sync(1, kDqWarps * 32);
       if (!s_last) return;
       __threadfence();
 #pragma unroll
       for (int i = 0; i < kCols; ++i) acc[i] = 0.f;
       for (int c = c_first; c <= c_last; ++c) {
-        const int sl = 2 * c + (unit_begin(c, J.U, p.G) >= tile_u0 ? 0 : 1);
+        const int sl = 2 * c + (unit_begin(c, p.U, p.G) >= tile_u0 ? 0 : 1);
 #pragma unroll
-        for (int i = 0; i < kCols; ++i) acc[i] += __ldcg(&part[((size_t)sl * MPAD + m0 + i) * kTileN + row]);
+        for (int i = 0; i < kCols; ++i) acc[i] += __ldcg(&p.partials[((size_t)sl * MPAD + m0 + i) * kTileN + row]);
       }
 #pragma unroll
       for (int i = 0; i < kCols; ++i)
-        if (m0 + i < p.M) J.Y[(size_t)(m0 + i) * J.N + n] = __half_as_ushort(__float2half_rn(acc[i]));
-      if (threadIdx.x == 0) J.counters[t] = 0;
+        if (m0 + i < p.M) p.Y[(size_t)(m0 + i) * p.N + n] = __half_as_ushort(__float2half_rn(acc[i]));
+      if (threadIdx.x == 0) p.counters[t] = 0;
     };
 
     int pend_t[kAU], pend_u0[kAU], pend_u1[kAU], pend_idx[kAU];
@@ -470,8 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
           const int u = u0 + j;
           if (u == boundary || cur_t < 0) {
             if (cur_t >= 0) { pend_t[npend] = cur_t; pend_u0[npend] = seg_u0; pend_u1[npend] = u; pend_idx[npend] = nseg - 1; ++npend; }
-            cur_t = cur_t < 0 ? u / J.Gk : cur_t + 1;
-            boundary = (cur_t + 1) * J.Gk;
+            cur_t = cur_t < 0 ? u / p.Gk : cur_t + 1;
+            boundary = (cur_t + 1) * p.Gk;
             seg_u0 = u;
             ++nseg;
           }
@@ -512,20 +412,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       if (++s == S) { s = 0; ph ^= 1; }
     }
     if (cur_t >= 0) epilogue(cur_t, seg_u0, u_end, nseg - 1);
-    if (chain) {   // this CTA's share of the op is written: count it
-      named_bar_sync(1, kDqWarps * 32);
-      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
-    }
-    }
-    if (chain && threadIdx.x == 0) {   // the last CTA out re-arms the op counters for the next run
-      __threadfence();
-      if (atomicAdd(&p.done[p.n_jobs], 1) == p.G - 1) {
-        __threadfence();
-        for (int j = 0; j < p.n_jobs; ++j) p.done[j] = 0;
-        p.done[p.n_jobs] = 0;
-        __threadfence();
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -549,67 +435,8 @@ int launch(const uint16_t* X, const Params& p, cudaStream_t stream) {
                                                                                              : W4A16_ERR_CUDA;
 }
 
-template <int MPAD, bool SYM>
-int launch_chain(const Params& p, cudaStream_t stream) {
-  using C = Cfg<MPAD, SYM>;
-  auto kern = gemm_w4a16_tc_kernel<MPAD, SYM>;
-  static unsigned long long attr = 0;
-  if (!w4::ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
-  CUtensorMap unused;
-  memset(&unused, 0, sizeof(unused));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.G);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr_[1];
-  attr_[0].id = cudaLaunchAttributeCooperative;   // the split fixup and the op dependencies need co-residency
-  attr_[0].val.cooperative = 1;
-  cfg.attrs = attr_;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, unused, unused, p) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
-}
-
-constexpr int kChainSlots = 8;
-
 }  // namespace tc
 }  // namespace w4
-
-// ---- chains on the tcgen05 family (include/w4a16.h w4a16_chain_*; planned in gemm_mma.cu) ----
-extern "C" void w4a16_tc_chain_geometry(int M, int* mpad, int* kr) {
-  *mpad = (M + 15) / 16 * 16;
-  *kr = *mpad <= 32 ? 4 : 2;   // Cfg<MPAD>::kR
-}
-extern "C" size_t w4a16_tc_chain_partial_bytes(int M, int G) {
-  const int mpad = (M + 15) / 16 * 16;
-  return (size_t)w4::tc::kChainSlots * 2 * G * mpad * w4::tc::kTileN * 4;
-}
-extern "C" int w4a16_launch_chain_tc(const void* dev_plan, int n_ops, int M, int mode, void* ws, size_t ws_bytes,
-                                     size_t done_bytes, int sms, cudaStream_t stream) {
-  w4::tc::Params p;
-  memset(&p, 0, sizeof(p));
-  p.G = sms;
-  p.M = M;
-  const size_t pb = w4a16_tc_chain_partial_bytes(M, p.G);
-  if (ws_bytes < pb + done_bytes) return W4A16_ERR_WORKSPACE;
-  p.partials = reinterpret_cast<float*>(ws);
-  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb);
-  p.counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb + done_bytes);
-  p.jobs = reinterpret_cast<const w4::ChainJob*>(dev_plan);
-  p.n_jobs = n_ops;
-  p.slots = w4::tc::kChainSlots;
-  static int dbg = -1;
-  if (dbg < 0) { const char* e = getenv("W4A16_TC_DEBUG"); dbg = e ? atoi(e) : 0; }
-  p.dbg = dbg;
-  const bool sym = mode == W4A16_SYM;
-  switch ((M + 15) / 16 * 16) {
-    case 16: return sym ? w4::tc::launch_chain<16, true>(p, stream) : w4::tc::launch_chain<16, false>(p, stream);
-    case 32: return sym ? w4::tc::launch_chain<32, true>(p, stream) : w4::tc::launch_chain<32, false>(p, stream);
-    case 48: return sym ? w4::tc::launch_chain<48, true>(p, stream) : w4::tc::launch_chain<48, false>(p, stream);
-    case 64: return sym ? w4::tc::launch_chain<64, true>(p, stream) : w4::tc::launch_chain<64, false>(p, stream);
-    default: return W4A16_ERR_SHAPE;
-  }
-}
 
 extern "C" int w4a16_tc_plan_ctas(int K, int N, int num_sms) {
   const long long U = (long long)(N / w4::tc::kTileN) * (K / w4::tc::kTileK);
@@ -642,10 +469,6 @@ extern "C" int w4a16_launch_gemm_tc(const uint16_t* X, const void* packed, uint1
   const size_t counters = w4::kCounterBytes;
   p.counters = reinterpret_cast<int*>(ws);
   p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counters);
-  p.jobs = nullptr;
-  p.n_jobs = 1;
-  p.done = nullptr;
-  p.slots = 1;
   const int mpad = (M + 15) / 16 * 16;
   const bool sym = mode == W4A16_SYM;
 #define W4_TC_CASE(MP) \

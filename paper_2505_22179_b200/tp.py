@@ -155,9 +155,7 @@ class VerifyStack:
         tp = 1; at tp > 1 one launch per segment between all-reduces (mma.sync families, M <= 16). None for
         M > 16 or where a shard is too small to give every CTA a unit: then every op is launched on its own."""
         if M not in self._chains:
-            if M > 16:
-                # tcgen05-family chains exist (w4a16_chain_* with W4A16_FAMILY_TCGEN05, bit-identical) but were
-                # measured no faster than PDL-chained launches for M > 16 (DESIGN.md §5.3): launch op by op
+            if M > 16:   # chains serve the mma.sync families; the tcgen05 family is launched op by op
                 self._chains[M] = None
                 return None
             try:

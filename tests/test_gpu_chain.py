@@ -56,8 +56,7 @@ def _run_eager(ops, family, ws):
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("M,family", [(M, f) for f in (0, 2) for M in (1, 5, 8, 9, 16)] +
-                         [(M, 1) for M in (1, 16, 17, 40, 64)])
+@pytest.mark.parametrize("M,family", [(M, f) for f in (0, 2) for M in (1, 5, 8, 9, 16)])
 def test_chain_mlp_stack_bit_exact_vs_single_ops(M, family):
     w4 = _w4()
     H, F = 2048, 2560
@@ -142,10 +141,7 @@ def test_chain_rejects_bad_ops():
     X = torch.zeros((M, 2048), dtype=torch.float16, device="cuda")
     Y = torch.zeros((M, 2560), dtype=torch.float16, device="cuda")
     with pytest.raises(w4.W4A16Error):
-        w4.Chain([("gemm", X, pl, Y)], 65)           # M <= 64
-    with pytest.raises(w4.W4A16Error):
-        w4.Chain([("gemm", X, pl, Y)], 8, family=0)  # shapes must match M (X has 8 rows: fine) ...
-        w4.Chain([("gemm", X[:4], pl, Y[:4])], 17, family=0)   # ... and the mma.sync families serve M <= 16
+        w4.Chain([("gemm", X, pl, Y)], 17)           # chains serve M <= 16 (the mma.sync families)
     small = w4.pack_linear(synth.gpu(0, 2, synth.WEIGHT, 256, 256))
     with pytest.raises(w4.W4A16Error):               # fewer units than CTAs
         w4.Chain([("gemm", X[:, :256].contiguous(), small, Y[:, :256].contiguous())], M)
