@@ -162,8 +162,8 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
 /* ---- Chains: a verify forward's whole sequence of ops in ONE persistent launch ----------------------
  * A verify forward is a long sequence of small W4A16 GEMMs (4 per decoder layer, 320 for Llama-3-70B)
  * whose weights never depend on earlier ops. Launched one by one, every GEMM pays its own pipeline fill
- * and drain (measured ~6 us each on B200). A chain runs the sequence in one persistent
- * kernel (one CTA group per SM): the weight stream (TMA) runs ahead across op boundaries, and an op waits
+ * and drain (a fixed ~8 us per GEMM on B200). A chain runs the sequence in one persistent
+ * kernel (one CTA per SM): the weight stream (TMA) runs ahead across op boundaries, and an op waits
  * only where it reads a buffer an earlier op writes (RAW), or writes a buffer an earlier op reads or
  * writes (WAR / WAW). The dependencies are derived on the host from the ops' buffer ranges.
  * Each GEMM op computes exactly what w4a16_gemm_ex of the same family computes (same split plan, same
@@ -193,7 +193,8 @@ size_t w4a16_chain_workspace_bytes(const w4a16_op* ops, int n_ops, int M, int fa
 int w4a16_chain_plan(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes);
 /* Run a chain: dev_plan = device copy of the plan for (n_ops, M, family); mode = the GEMMs' mode.
  * workspace: at least w4a16_chain_workspace_bytes(ops, n_ops, M, family) zero-initialised bytes, used by
- * this chain's plan only. Every GEMM of a chain needs (K/128)*(N/128) >= 2 * SM count. Async on `stream`. */
+ * this chain's plan only. Every GEMM of a chain needs (K/128)*(N/128) >= the SM count (every CTA owns a
+ * unit). Async on `stream`. */
 int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family, void* workspace,
                     size_t workspace_bytes, w4a16_stream_t stream);
 
