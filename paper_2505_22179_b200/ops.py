@@ -191,7 +191,9 @@ class Chain:
     The plan (TMA descriptors, dependencies) is encoded once by the library into host memory and copied to
     the device here; the tensors must stay where they are while the chain is in use (references are kept)."""
 
-    def __init__(self, ops, M: int, family=W4A16_FAMILY_AUTO, device=None):
+    def __init__(self, ops, M: int, family=W4A16_FAMILY_AUTO, device=None, workspace=None):
+        """workspace: optional zero-initialised uint8 tensor to use instead of a private one. Chains that run
+        one after another on one stream may share it (each run re-arms its counters; partials are scratch)."""
         self.M, self.family = M, family
         self._keep = []
         arr = (W4A16Op * len(ops))()
@@ -225,7 +227,12 @@ class Chain:
         wsb = int(lib.w4a16_chain_workspace_bytes(ctypes.addressof(arr), self.n, M, family))
         if wsb == 0:
             raise W4A16Error("w4a16_chain_workspace_bytes: bad chain")
-        self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+        if workspace is not None:
+            if workspace.numel() * workspace.element_size() < wsb:
+                raise W4A16Error(f"chain workspace too small ({workspace.numel()} < {wsb} bytes)")
+            self.ws = workspace
+        else:
+            self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
     def __call__(self, stream=None):
         check(lib.w4a16_chain_run(self.plan.data_ptr(), self.n, self.M, self.mode, self.family, self.ws.data_ptr(),

@@ -163,7 +163,11 @@ class VerifyStack:
                 if self.t == 1:
                     self._chains[M] = [Chain([op for a, b in segs for op in a + b], M, device=self.device)]
                 else:
-                    self._chains[M] = [Chain(seg, M, device=self.device) for a, b in segs for seg in (a, b)]
+                    # the per-segment chains run one after another on one stream: they share one workspace
+                    first = [Chain(seg, M, device=self.device) for seg in segs[0]]
+                    ws = max((c.ws for c in first), key=lambda t: t.numel())
+                    self._chains[M] = [Chain(seg, M, device=self.device, workspace=ws) for a, b in segs
+                                       for seg in (a, b)]
             except W4A16Error:
                 self._chains[M] = None
         return self._chains[M]
