@@ -273,6 +273,17 @@ def main():
     log(f"captured M={args.M}")
     ms = time_graph(gH, args.steps, args.warmup)
     log(f"headline M={args.M}: {ms:.3f} ms/step")
+    # per-step distribution (median and p10/p90 over replays), events around every replay
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+        for i in range(args.steps):
+            gH.replay()
+            ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per_step = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+    pct = lambda q: per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]
+    step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9), "n": len(per_step)}
     value = bytes_all_ranks / (ms * 1e-3) / 1e12
 
     # M sweep (same protocol)
@@ -546,7 +557,7 @@ def main():
                        "weight_bytes_per_step": bytes_all_ranks,
                        "l2": f"{bytes_all_ranks / 1e9:.1f} GB of weights per step >> 126 MB L2 (no flush needed)",
                        "timing": "CUDA graph replay, CUDA events on the launching stream, max over ranks"},
-            "us_per_layer": 1e3 * ms / n_layers,
+            "us_per_layer": 1e3 * ms / n_layers, "ms_per_step_distribution": step_dist,
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
