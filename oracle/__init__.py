@@ -45,6 +45,7 @@ def _load():
     L.orc_accept.argtypes = [vp, vp, vp, i32, vp]; L.orc_accept.restype = i32
     L.orc_tree_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]; L.orc_tree_attention.restype = i32
     L.orc_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp]; L.orc_kv_compact.restype = i32
+    L.orc_hadamard.argtypes = [vp, i32, i32, i32, vp]; L.orc_hadamard.restype = i32
     L.orc_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, i32]; L.orc_lmhead_argmax.restype = i32
     return L
 
@@ -216,3 +217,13 @@ def kv_compact(Kc, Vc, L_prefix, accept_out):
     if L.orc_kv_compact(_p(Kc), _p(Vc), int(L_prefix), Hkv, D, _p(out)) != 0:
         raise ValueError("orc_kv_compact: bad arguments")
     return (Kc.view(np.float16), Vc.view(np.float16)) if dt == np.float16 else (Kc, Vc)
+
+
+def hadamard(X, B=128):
+    """fp64 block Hadamard rotation along the last axis: X fp16 [M, K] -> fp64 [M, K]."""
+    X = _u16(X)
+    M, K = X.shape
+    Y = np.zeros((M, K), dtype=np.float64)
+    if L.orc_hadamard(_p(X), M, K, int(B), _p(Y)) != 0:
+        raise ValueError("orc_hadamard: bad arguments")
+    return Y

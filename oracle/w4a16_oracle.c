@@ -405,3 +405,22 @@ int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int3
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------------------
+ * Block Hadamard rotation: the definition, one output at a time.
+ * ---------------------------------------------------------------------------------------------------- */
+int orc_hadamard(const uint16_t* X, int M, int K, int B, double* Y) {
+  if (!X || !Y || M < 1 || B < 1 || (B & (B - 1)) || K < B || K % B) return -1;
+  const double norm = 1.0 / sqrt((double)B);
+  for (int m = 0; m < M; ++m)
+    for (int b = 0; b < K; b += B)
+      for (int i = 0; i < B; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < B; ++j) {
+          const double x = orc_half_to_double(X[(size_t)m * K + b + j]);
+          acc += (__builtin_popcount((unsigned)(i & j)) & 1) ? -x : x;
+        }
+        Y[(size_t)m * K + b + i] = acc * norm;
+      }
+  return 0;
+}

@@ -23,6 +23,8 @@
  *                 an ancestor of i; P:80-82 tree drafts), softmax in fp64.
  *   - kv_compact: after acceptance keep the root and the accepted path's rows, in order (S:159-164
  *                 cache_select of the accepted root-to-leaf path).
+ *   - hadamard:   the rotation of W4A16+Rot (QuaRot-style Hadamard rotation):
+ *                 block-diagonal normalised Sylvester Hadamard along k, y = x (I (x) H_B) / sqrt(B).
  * The arithmetic works on plain arrays: codes uint8 [K][N], scales/zeros fp16 [K/group][N]. The byte layout
  * of the ABI's packed blob is a separate pair of functions (layout_pack / layout_unpack), re-derived here
  * from its definition in include/w4a16.h (not shared):
@@ -107,6 +109,11 @@ int orc_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc
  * orc_accept (out[0] = accepted length n, out[3..3+n) = path node indices), row L + k of Kc and Vc becomes
  * the former row L + path[k-1] for k = 1..n (row L, the root, stays). Rows are Hkv * D fp16 wide. */
 int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out);
+
+/* Block Hadamard rotation (W4A16+Rot): for every row m and block b of B
+ * consecutive k (B a power of two dividing K), Y[m][bB + i] = sum_j (-1)^popcount(i & j) X[m][bB + j] / sqrt(B),
+ * in fp64 straight from the definition (Sylvester order). Y fp64 [M][K]. Returns 0 / -1. */
+int orc_hadamard(const uint16_t* X, int M, int K, int B, double* Y);
 
 #ifdef __cplusplus
 }

@@ -571,3 +571,36 @@ def test_kv_compact_worked_example_and_chain_equivalence():
     Oseq = oracle.tree_attention(np.concatenate([Q[[0, 2, 5, 7]], qn]), Kseq, Vseq, np.arange(-1, n))
     Otree = oracle.tree_attention(np.concatenate([Q[:M], qn]), np.concatenate([K, kn]), np.concatenate([V, vn]), par + [7])
     assert np.allclose(Oseq[-1], Otree[-1], rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Block Hadamard rotation of W4A16+Rot
+# ---------------------------------------------------------------------------------------------------
+def test_hadamard_matches_scipy_and_is_orthogonal():
+    import scipy.linalg
+    rng = np.random.default_rng(31)
+    for B, K in ((8, 32), (64, 128), (128, 512)):
+        X = rng.standard_normal((3, K)).astype(np.float16)
+        Y = oracle.hadamard(X, B)
+        H = scipy.linalg.hadamard(B).astype(np.float64) / np.sqrt(B)      # library routine (Sylvester order)
+        ref = np.concatenate([X[:, b:b + B].astype(np.float64) @ H.T for b in range(0, K, B)], axis=1)
+        assert np.allclose(Y, ref, rtol=0, atol=1e-12)
+        # orthogonal and symmetric: applying it twice gives the input back (to fp64 rounding)
+        Y2 = np.concatenate([Y[:, b:b + B] @ H.T for b in range(0, K, B)], axis=1)
+        assert np.allclose(Y2, X.astype(np.float64), rtol=0, atol=1e-12)
+    # a basis vector maps to a scaled Hadamard column
+    e = np.zeros((1, 128), dtype=np.float16)
+    e[0, 5] = 1
+    assert np.allclose(oracle.hadamard(e, 128)[0], scipy.linalg.hadamard(128)[:, 5] / np.sqrt(128), rtol=0, atol=0)
+
+
+def test_hadamard_rotation_leaves_the_product_invariant():
+    # x W = (x H)(H^T W): the rotation is folded into the weights offline, applied to activations online
+    import scipy.linalg
+    rng = np.random.default_rng(32)
+    K, N, B = 256, 40, 128
+    X = rng.standard_normal((4, K)).astype(np.float16)
+    W = rng.standard_normal((K, N))
+    H = scipy.linalg.hadamard(B) / np.sqrt(B)
+    HW = np.concatenate([H @ W[b:b + B] for b in range(0, K, B)], axis=0)   # H symmetric: H^T = H
+    assert np.allclose(oracle.hadamard(X, B) @ HW, X.astype(np.float64) @ W, rtol=0, atol=1e-10)
