@@ -153,6 +153,13 @@ int w4a16_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* 
 int w4a16_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int32_t* accept_out,
                      w4a16_stream_t stream);
 
+/* w4a16_hadamard — the online activation rotation of W4A16+Rot (QuaRot-style):
+ * Y[m][bB + i] = fp16_rne(sum_j (-1)^popcount(i & j) X[m][bB + j] / sqrt(B)) for every row m and block b of
+ * B consecutive k (block-diagonal normalised Sylvester Hadamard; H is symmetric and orthogonal, so with the
+ * weights rotated offline the same way, W' = H W before w4a16_pack, X W = (X H)(H W)). fp32 arithmetic.
+ * X, Y: fp16 [M][K]; Y may equal X (in place). block in {64, 128, 256, 512, 1024}, K % block == 0, M >= 1. */
+int w4a16_hadamard(const uint16_t* X, uint16_t* Y, int M, int K, int block, w4a16_stream_t stream);
+
 /* w4a16_silu_mul — Llama MLP glue between the fused gate-up GEMM and the down GEMM of the verify forward
  * (not a step of the paper's method): GU is fp16 [M][2F] holding [gate | up] per row (the
  * rank-local shard layout of tp.py), out is fp16 [M][F], out[m][j] = fp16_rne(silu(gate) * up) in fp32.

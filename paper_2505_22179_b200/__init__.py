@@ -12,5 +12,5 @@ from .ops import (  # noqa: F401
     verify_accept, w4a16_status_string, w4a16_gemm_family, w4a16_silu_mul,
     PackedLinear, pack_linear, alloc_workspace, w4a16_packed_bytes, Chain,
     w4a16_lmhead_argmax, w4a16_lmhead_workspace_bytes, alloc_lmhead_workspace,
-    w4a16_tree_attention, w4a16_tree_attention_workspace_bytes, w4a16_kv_compact,
+    w4a16_tree_attention, w4a16_tree_attention_workspace_bytes, w4a16_kv_compact, w4a16_hadamard,
 )

@@ -44,6 +44,7 @@ ABI_SYMBOLS = (
     "w4a16_tree_attention_workspace_bytes",
     "w4a16_tree_attention",
     "w4a16_kv_compact",
+    "w4a16_hadamard",
 )
 W4A16_OP_GEMM, W4A16_OP_SILU_MUL = 0, 1
 
@@ -89,6 +90,8 @@ def _load():
     lib.w4a16_tree_attention.restype = i32
     lib.w4a16_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp, vp]
     lib.w4a16_kv_compact.restype = i32
+    lib.w4a16_hadamard.argtypes = [vp, vp, i32, i32, i32, vp]
+    lib.w4a16_hadamard.restype = i32
     lib.w4a16_chain_plan_bytes.argtypes = [i32]
     lib.w4a16_chain_plan_bytes.restype = sz
     lib.w4a16_chain_workspace_bytes.argtypes = [vp, i32, i32, i32]

@@ -13,6 +13,7 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 extern "C" size_t w4a16_lmhead_workspace_bytes_sms(int num_sms);
+extern "C" int w4a16_launch_hadamard(const uint16_t*, uint16_t*, int, int, int, cudaStream_t);
 extern "C" size_t w4a16_tree_attention_workspace_bytes_sms(int M, int L, int Hq, int Hkv, int sms);
 extern "C" int w4a16_launch_tree_attention(const uint16_t*, const uint16_t*, const uint16_t*, const int32_t*, int, int,
                                            int, int, uint16_t*, void*, int, cudaStream_t);
@@ -207,6 +208,13 @@ extern "C" int w4a16_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int 
   if (L < 0 || Hkv < 1 || D < 8 || D % 8) return W4A16_ERR_SHAPE;
   if (!aligned16(Kc) || !aligned16(Vc) || (reinterpret_cast<uintptr_t>(accept_out) & 3)) return W4A16_ERR_ALIGN;
   return w4a16_launch_kv_compact(Kc, Vc, L, Hkv, D, accept_out, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_hadamard(const uint16_t* X, uint16_t* Y, int M, int K, int block, w4a16_stream_t stream) {
+  if (!X || !Y) return W4A16_ERR_ARG;
+  if (M < 1 || block < 64 || block > 1024 || (block & (block - 1)) || K < block || K % block) return W4A16_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(X) & 3) || (reinterpret_cast<uintptr_t>(Y) & 3)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_hadamard(X, Y, M, K, block, (cudaStream_t)stream);
 }
 
 extern "C" const char* w4a16_status_string(int status) {

@@ -145,6 +145,13 @@ def w4a16_kv_compact(Kc, Vc, L: int, accept_out, stream=None):
                                _ptr(accept_out, torch.int32, "accept_out"), _stream(stream)), "w4a16_kv_compact")
 
 
+def w4a16_hadamard(X, Y, block: int = 128, stream=None):
+    """Y [M, K] = X rotated by the block Hadamard of size `block` along K. Y may be X."""
+    M, K = X.shape
+    check(lib.w4a16_hadamard(_ptr(X, torch.float16, "X"), _ptr(Y, torch.float16, "Y"), M, K, block, _stream(stream)),
+          "w4a16_hadamard")
+
+
 def w4a16_silu_mul(GU, out, stream=None):
     M, F2 = GU.shape
     check(lib.w4a16_silu_mul(_ptr(GU, torch.float16, "GU"), M, F2 // 2, _ptr(out, torch.float16, "out"),
