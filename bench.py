@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--sweep", default="1,2,4,7,8,16,24,32,49,61,64", help="comma list of M for the M sweep ('' = none)")
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "fused"],
+                    help="tp > 1: NCCL all-reduces between per-segment chains, or ALLREDUCE ops inside one chain "
+                         "per forward over CUDA-IPC peer memory (include/w4a16.h; not yet validated on multi-GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-kernels", dest="kernels", action="store_false", help="skip the per-kernel breakdown")
@@ -227,7 +230,7 @@ def main():
 
     t0 = time.perf_counter()
     stack = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
-                           device=dev)
+                           device=dev, allreduce=args.allreduce)
     build_s = time.perf_counter() - t0
     log(f"built {n_layers} layers ({stack.weight_bytes / 1e9:.2f} GB packed) in {build_s:.1f}s")
     # activations (seeded, in HBM) and a draft tree of the headline width
@@ -554,6 +557,7 @@ def main():
             "config": {"workload": f"{dims.name} W4A16 g128 {args.mode} verify forward: {n_layers} decoder layers "
                                    f"(QKV, O, gate-up, SiLU*mul, down) + verify_accept; BASELINE configs 3-4",
                        "M": args.M, "layers": n_layers, "tp": world, "parallelism": f"tp{world}",
+                       "allreduce": "none" if world == 1 else args.allreduce,
                        "weight_bytes_per_step": bytes_all_ranks,
                        "l2": f"{bytes_all_ranks / 1e9:.1f} GB of weights per step >> 126 MB L2 (no flush needed)",
                        "timing": "CUDA graph replay, CUDA events on the launching stream, max over ranks"},

@@ -177,15 +177,54 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
  * reduction order: bit-identical results); each SILU_MUL op exactly what w4a16_silu_mul computes.
  * All G CTAs of a chain must be co-resident: do not run other kernels concurrently with a chain on the
  * same device (it is launched as a cooperative kernel). */
-enum { W4A16_OP_GEMM = 0, W4A16_OP_SILU_MUL = 1 };
+enum { W4A16_OP_GEMM = 0, W4A16_OP_SILU_MUL = 1, W4A16_OP_ALLREDUCE = 2 };
 typedef struct {
-  int kind;            /* W4A16_OP_GEMM or W4A16_OP_SILU_MUL */
-  const void* X;       /* GEMM: X [M][K] fp16.  SILU_MUL: GU [M][2N] fp16 ([gate | up] per row) */
-  const void* packed;  /* GEMM: packed weight blob of w4a16_pack (K x N, `mode`).  SILU_MUL: NULL */
-  void* Y;             /* GEMM: Y [M][N] fp16.  SILU_MUL: out [M][N] fp16 */
-  int K, N;            /* GEMM: as w4a16_gemm.  SILU_MUL: K = 2N, N = F (N % 8 == 0) */
+  int kind;            /* W4A16_OP_GEMM, W4A16_OP_SILU_MUL or W4A16_OP_ALLREDUCE */
+  const void* X;       /* GEMM: X [M][K] fp16.  SILU_MUL: GU [M][2N] fp16 ([gate | up] per row).
+                        * ALLREDUCE: this rank's partial P [M][N] fp16, inside its symmetric region */
+  const void* packed;  /* GEMM: packed weight blob of w4a16_pack (K x N, `mode`).  SILU_MUL: NULL.
+                        * ALLREDUCE: HOST pointer to the w4a16_peer_group (read by w4a16_chain_plan only) */
+  void* Y;             /* GEMM: Y [M][N] fp16.  SILU_MUL: out [M][N] fp16.  ALLREDUCE: out [M][N] fp16 */
+  int K, N;            /* GEMM: as w4a16_gemm.  SILU_MUL: K = 2N, N = F (N % 8 == 0).  ALLREDUCE: K = N, N % 8 == 0 */
   int mode;            /* GEMM: W4A16_ASYM or W4A16_SYM; every GEMM of a chain uses the same mode */
 } w4a16_op;
+
+/* ---- Tensor-parallel all-reduce inside a chain ------------------------------
+ * The row-parallel GEMMs of a t-way tensor-parallel verify forward (O and down: each rank multiplies its
+ * K-shard, Megatron layout) produce partial sums P_r that are summed over the ranks. An
+ * ALLREDUCE op does that sum INSIDE the chain, one-shot over peer memory (NVLink / NVSwitch loads), so a
+ * whole tensor-parallel forward stays one persistent launch per rank instead of 2 launches + 2 NCCL
+ * all-reduces per layer:
+ *   out[m][n] = fp16_rne( sum_{r = 0 .. world-1, in rank order} (float) P_r[m][n] )     (fp32 sum)
+ * identical on every rank (same operands, same order). Protocol: once every earlier op of this rank is
+ * complete, the rank stores a ready flag (the chain's run epoch) into each rank's flag area; every CTA
+ * waits for all `world` flags, then reads its slice of every P_r through the peer mappings.
+ * Symmetric region: each rank allocates one device region of the same size (w4a16_ipc_alloc, zero-filled)
+ * and maps every peer's (w4a16_ipc_open); the P buffers and a flag area (w4a16_peer_flag_bytes, at the
+ * same offset on every rank) live in it. Rules (checked by w4a16_chain_plan): every ALLREDUCE of a chain
+ * names the same group; X lies inside base[rank]; and cyclically between an ALLREDUCE that reads a
+ * buffer and the next op that writes it there is another ALLREDUCE (that op's flags prove every peer has
+ * finished reading — two alternating partial buffers, as in a decoder layer's O and down, satisfy it).
+ * Every rank runs the same sequence of chains over the group. A wait that does not complete within ~10 s
+ * (a peer that never arrives) traps the kernel instead of hanging the device. */
+#define W4A16_MAX_PEERS 8
+typedef struct {
+  void* base[W4A16_MAX_PEERS];   /* every rank's symmetric region as mapped in this process; base[rank] is local */
+  size_t bytes;                  /* region size (identical on every rank) */
+  size_t flag_offset;            /* flag area offset inside each region (identical on every rank, 256-B aligned) */
+  int flag_slots;                /* ALLREDUCE ops the flag area serves (per chain: one slot per ALLREDUCE op) */
+  int world, rank;               /* 1 <= world <= W4A16_MAX_PEERS, 0 <= rank < world */
+} w4a16_peer_group;
+/* Bytes of a flag area for `flag_slots` ALLREDUCE ops (a run counter plus world ready flags per slot). */
+size_t w4a16_peer_flag_bytes(int flag_slots);
+/* Symmetric-region plumbing (CUDA IPC; one process per GPU). w4a16_ipc_alloc: cudaMalloc `bytes` on the
+ * current device, zero it, and write its 64-byte IPC handle to handle_out. w4a16_ipc_open: map a peer's
+ * region (handle from w4a16_ipc_alloc in another process) into this process, peer access enabled.
+ * w4a16_ipc_close / w4a16_ipc_free undo them. W4A16_ERR_CUDA on failure. */
+int w4a16_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+int w4a16_ipc_open(const void* handle, void** dev_ptr);
+int w4a16_ipc_close(void* dev_ptr);
+int w4a16_ipc_free(void* dev_ptr);
 
 /* Bytes of the plan (host buffer) for n_ops ops. */
 size_t w4a16_chain_plan_bytes(int n_ops);

@@ -46,6 +46,7 @@ def _load():
     L.orc_tree_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]; L.orc_tree_attention.restype = i32
     L.orc_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp]; L.orc_kv_compact.restype = i32
     L.orc_hadamard.argtypes = [vp, i32, i32, i32, vp]; L.orc_hadamard.restype = i32
+    L.orc_allreduce.argtypes = [vp, i32, ctypes.c_size_t, vp]; L.orc_allreduce.restype = i32
     L.orc_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, i32]; L.orc_lmhead_argmax.restype = i32
     return L
 
@@ -227,3 +228,13 @@ def hadamard(X, B=128):
     if L.orc_hadamard(_p(X), M, K, int(B), _p(Y)) != 0:
         raise ValueError("orc_hadamard: bad arguments")
     return Y
+
+
+def allreduce(P):
+    """Sum over tensor-parallel ranks: P fp16 [T, ...] -> fp16 [...], fp64 sum rounded once."""
+    P = _u16(P)
+    T = P.shape[0]
+    out = np.zeros(P.shape[1:], dtype=np.uint16)
+    if L.orc_allreduce(_p(P), T, out.size, _p(out)) != 0:
+        raise ValueError("orc_allreduce: bad arguments")
+    return out

@@ -424,3 +424,13 @@ int orc_hadamard(const uint16_t* X, int M, int K, int B, double* Y) {
       }
   return 0;
 }
+
+int orc_allreduce(const uint16_t* P, int T, size_t n, uint16_t* out) {
+  if (!P || !out || T < 1) return -1;
+  for (size_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int r = 0; r < T; ++r) acc += orc_half_to_double(P[(size_t)r * n + i]);
+    out[i] = orc_double_to_half(acc);
+  }
+  return 0;
+}

@@ -23,6 +23,7 @@
  *                 an ancestor of i; P:80-82 tree drafts), softmax in fp64.
  *   - kv_compact: after acceptance keep the root and the accepted path's rows, in order (S:159-164
  *                 cache_select of the accepted root-to-leaf path).
+ *   - allreduce:  the sum over tensor-parallel ranks of row-parallel partial products.
  *   - hadamard:   the rotation of W4A16+Rot (QuaRot-style Hadamard rotation):
  *                 block-diagonal normalised Sylvester Hadamard along k, y = x (I (x) H_B) / sqrt(B).
  * The arithmetic works on plain arrays: codes uint8 [K][N], scales/zeros fp16 [K/group][N]. The byte layout
@@ -114,6 +115,11 @@ int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int3
  * consecutive k (B a power of two dividing K), Y[m][bB + i] = sum_j (-1)^popcount(i & j) X[m][bB + j] / sqrt(B),
  * in fp64 straight from the definition (Sylvester order). Y fp64 [M][K]. Returns 0 / -1. */
 int orc_hadamard(const uint16_t* X, int M, int K, int B, double* Y);
+
+/* Tensor-parallel all-reduce of row-parallel partial sums (Megatron row-parallel O / down,
+ * y = sum over ranks of the rank's K-shard product): out[i] = fp16_rne(sum_{r < T} P[r][i]), the sum in
+ * fp64 (exact for T <= 8 fp16 terms of moderate range), rounded once. P fp16 [T][n]. Returns 0 / -1. */
+int orc_allreduce(const uint16_t* P, int T, size_t n, uint16_t* out);
 
 #ifdef __cplusplus
 }

@@ -45,14 +45,26 @@ ABI_SYMBOLS = (
     "w4a16_tree_attention",
     "w4a16_kv_compact",
     "w4a16_hadamard",
+    "w4a16_peer_flag_bytes",
+    "w4a16_ipc_alloc",
+    "w4a16_ipc_open",
+    "w4a16_ipc_close",
+    "w4a16_ipc_free",
 )
-W4A16_OP_GEMM, W4A16_OP_SILU_MUL = 0, 1
+W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE = 0, 1, 2
+W4A16_MAX_PEERS = 8
 
 
 class W4A16Op(ctypes.Structure):
     """struct w4a16_op of include/w4a16.h."""
     _fields_ = [("kind", ctypes.c_int), ("X", ctypes.c_void_p), ("packed", ctypes.c_void_p), ("Y", ctypes.c_void_p),
                 ("K", ctypes.c_int), ("N", ctypes.c_int), ("mode", ctypes.c_int)]
+
+
+class W4A16PeerGroup(ctypes.Structure):
+    """struct w4a16_peer_group of include/w4a16.h (host side; read by w4a16_chain_plan only)."""
+    _fields_ = [("base", ctypes.c_void_p * W4A16_MAX_PEERS), ("bytes", ctypes.c_size_t), ("flag_offset", ctypes.c_size_t),
+                ("flag_slots", ctypes.c_int), ("world", ctypes.c_int), ("rank", ctypes.c_int)]
 
 
 class W4A16Error(RuntimeError):
@@ -98,7 +110,21 @@ def _load():
     lib.w4a16_chain_workspace_bytes.restype = sz
     lib.w4a16_chain_plan.argtypes = [vp, i32, i32, i32, vp, sz]
     lib.w4a16_chain_run.argtypes = [vp, i32, i32, i32, i32, vp, sz, vp]
-    for name in ("w4a16_chain_plan", "w4a16_chain_run", "w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
+    if not hasattr(lib, "w4a16_chain_run_sms") and os.environ.get("W4A16_LIB"):
+        return lib   # an older diagnostics build (A/B timing only): chains without ALLREDUCE ops
+    lib.w4a16_peer_flag_bytes.argtypes = [i32]
+    lib.w4a16_peer_flag_bytes.restype = sz
+    lib.w4a16_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
+    lib.w4a16_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.w4a16_ipc_close.argtypes = [vp]
+    lib.w4a16_ipc_free.argtypes = [vp]
+    # test hooks (exported, not in the header): chains planned / run for a given SM count, non-cooperatively
+    lib.w4a16_chain_workspace_bytes_sms.argtypes = [vp, i32, i32, i32, i32]
+    lib.w4a16_chain_workspace_bytes_sms.restype = sz
+    lib.w4a16_chain_plan_sms.argtypes = [vp, i32, i32, i32, vp, sz, i32]
+    lib.w4a16_chain_run_sms.argtypes = [vp, i32, i32, i32, i32, vp, sz, i32, vp]
+    for name in ("w4a16_ipc_alloc", "w4a16_ipc_open", "w4a16_ipc_close", "w4a16_ipc_free", "w4a16_chain_plan_sms",
+                 "w4a16_chain_run_sms", "w4a16_chain_plan", "w4a16_chain_run", "w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
                  "w4a16_gemm_family", "w4a16_silu_mul"):
         getattr(lib, name).restype = i32
     return lib

@@ -2,6 +2,7 @@
 // dispatch to the kernels in pack.cu, gemm_mma.cu, gemm_tc.cu and accept.cu. No device allocation, no
 // host synchronisation, no global state beyond a per-device SM-count cache.
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 #include "w4a16.h"
 
@@ -22,7 +23,7 @@ extern "C" int w4a16_launch_lmhead_argmax(const uint16_t*, const uint16_t*, int,
                                           cudaStream_t);
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op*, int, int, int, int);
 extern "C" int w4a16_chain_plan_sms(const w4a16_op*, int, int, int, void*, size_t, int);
-extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, cudaStream_t);
+extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, int, cudaStream_t);
 extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
                                      cudaStream_t);
 
@@ -153,7 +154,53 @@ extern "C" int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode,
   if (!aligned16(dev_plan) || !aligned16(workspace)) return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
-  return w4a16_launch_chain_mma(dev_plan, n_ops, M, mode, family, workspace, workspace_bytes, sms, (cudaStream_t)stream);
+  return w4a16_launch_chain_mma(dev_plan, n_ops, M, mode, family, workspace, workspace_bytes, sms, 1, (cudaStream_t)stream);
+}
+
+// Test hook (not part of include/w4a16.h): a chain planned with w4a16_chain_plan_sms for `sms` SMs, launched
+// without the cooperative attribute so that several such chains can share one device side by side
+// (tests/test_gpu_allreduce.py simulates tensor-parallel ranks that way on a single GPU).
+extern "C" int w4a16_chain_run_sms(const void* dev_plan, int n_ops, int M, int mode, int family, void* workspace,
+                                   size_t workspace_bytes, int sms, w4a16_stream_t stream) {
+  if (!dev_plan || !workspace) return W4A16_ERR_ARG;
+  if (!aligned16(dev_plan) || !aligned16(workspace)) return W4A16_ERR_ALIGN;
+  const int dev_sms = num_sms_of_current_device();
+  if (dev_sms <= 0) return W4A16_ERR_CUDA;
+  if (sms < 1 || sms > dev_sms) return W4A16_ERR_ARG;
+  return w4a16_launch_chain_mma(dev_plan, n_ops, M, mode, family, workspace, workspace_bytes, sms, 0, (cudaStream_t)stream);
+}
+
+// ---- symmetric regions (CUDA IPC) ----
+extern "C" int w4a16_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out || bytes == 0) return W4A16_ERR_ARG;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return W4A16_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+    cudaFree(p);
+    return W4A16_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  *dev_ptr = p;
+  return W4A16_OK;
+}
+
+extern "C" int w4a16_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return W4A16_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+extern "C" int w4a16_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return W4A16_ERR_ARG;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+extern "C" int w4a16_ipc_free(void* dev_ptr) {
+  if (!dev_ptr) return W4A16_ERR_ARG;
+  return cudaFree(dev_ptr) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
 extern "C" size_t w4a16_lmhead_workspace_bytes(int M, int K, int V) {

@@ -16,7 +16,7 @@ constexpr size_t kCounterBytes = (size_t)(W4A16_MAX_N / 128) * 4;
 
 // One op of a chain: the device copy of a w4a16_chain_plan entry (include/w4a16.h), shared by both GEMM
 // families (the activation tensor maps are encoded for the family the plan was made for).
-enum { kOpGemm = W4A16_OP_GEMM, kOpSilu = W4A16_OP_SILU_MUL };
+enum { kOpGemm = W4A16_OP_GEMM, kOpSilu = W4A16_OP_SILU_MUL, kOpAllReduce = W4A16_OP_ALLREDUCE };
 struct alignas(64) ChainJob {
   CUtensorMap xmapR;       // activation boxes of one stage's units (3-D SWIZZLE_128B)
   CUtensorMap xmap1;       // activation box of one unit
@@ -26,6 +26,14 @@ struct alignas(64) ChainJob {
   int dep_x;               // earlier op whose completion this op's X reads wait for (-1: none)
   int dep_y;               // earlier op whose completion this op's Y writes wait for (WAR / WAW; -1: none)
   int cnt_off;             // this op's first tile counter
+  // ALLREDUCE (include/w4a16.h): every rank's partial as mapped here (rank order), this rank's ready flag in
+  // every rank's flag area, this rank's own `world` ready flags of the op's slot, the group's run counter
+  // (local). Job 0 also carries the run counter when the chain has ALLREDUCE ops (advanced at chain end).
+  const uint16_t* peer_x[W4A16_MAX_PEERS];
+  uint32_t* peer_flag[W4A16_MAX_PEERS];
+  uint32_t* my_flags;
+  uint32_t* epoch;
+  int world;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -189,6 +197,21 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// System-scope (cross-GPU, NVLink peer memory) release store / acquire load of a flag word.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 // (w & mask) | magic in one LOP3.
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t w, uint32_t mask, uint32_t magic) {

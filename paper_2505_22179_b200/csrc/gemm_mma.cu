@@ -73,6 +73,7 @@ struct Cfg {
 using w4::ChainJob;
 using w4::kOpGemm;
 using w4::kOpSilu;
+using w4::kOpAllReduce;
 
 struct GemmParams {
   const uint8_t* packed;
@@ -186,6 +187,69 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Tensor-parallel all-reduce op of a chain (include/w4a16.h W4A16_OP_ALLREDUCE): one-shot
+// over peer memory, run by every consumer thread of every CTA. Out of line: it keeps the GEMM loop's registers.
+#ifndef W4_AR_INLINE
+#define W4_AR_INLINE 0
+#endif
+template <int kThreadsAR>
+#if W4_AR_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void allreduce_op(const GemmParams& p, int job, int cta) {
+  const ChainJob* cj = p.jobs + job;
+  const int world = cj->world;
+  if (threadIdx.x == 0) {
+    wait_op(p, job - 1);   // every earlier op of this rank is complete (its partial P included)
+    const uint32_t e = __ldcg(cj->epoch) + 1u;
+    if (cta == 0) {
+      // P (written by every CTA, released to this thread through done[]) -> visible to the peers first
+      fence_acq_rel_sys();
+      for (int q = 0; q < world; ++q) st_release_sys(cj->peer_flag[q], e);
+    }
+    const unsigned long long t0 = globaltimer_ns();
+    for (int q = 0; q < world; ++q) {
+      while ((int)(ld_acquire_sys(cj->my_flags + q) - e) < 0) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > 10000000000ull) __trap();   // a peer never arrived: fail, do not hang
+      }
+    }
+  }
+  named_bar_sync(1, kThreadsAR);
+  trace_op(p, job, 1);
+  const int vecs = cj->N / 8;
+  const long long total = (long long)p.M * vecs;
+  uint4* Y = reinterpret_cast<uint4*>(cj->Y);
+  for (long long i = (long long)cta * kThreadsAR + threadIdx.x; i < total; i += (long long)p.G * kThreadsAR) {
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = 0.f;
+    for (int q = 0; q < world; ++q) {   // rank order: the same sum on every rank
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(cj->peer_x[q]) + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+        a[2 * k] += f.x;
+        a[2 * k + 1] += f.y;
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 h = __floats2half2_rn(a[2 * k], a[2 * k + 1]);
+      o[k] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    Y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  named_bar_sync(1, kThreadsAR);
+  if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+  trace_op(p, job, 2);
+  trace_op(p, job, 3);
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
@@ -420,6 +484,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
       trace_op(p, job, 2);
       trace_op(p, job, 3);
+      continue;
+    }
+    if (J.kind == kOpAllReduce) {
+      allreduce_op<kWarps * 32>(p, job, cta);
       continue;
     }
     const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
@@ -738,6 +806,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       __threadfence();
       for (int j = 0; j < p.n_jobs; ++j) p.done[j] = 0;
       p.done[p.n_jobs] = 0;
+      if (p.jobs[0].epoch != nullptr) *p.jobs[0].epoch += 1u;   // the group's next run (ALLREDUCE flags)
       __threadfence();
     }
   }
@@ -757,7 +826,7 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
-static int launch_chain_t(const GemmParams& p, cudaStream_t stream) {
+static int launch_chain_t(const GemmParams& p, bool cooperative, cudaStream_t stream) {
   using C = Cfg<NTB, SYM>;
   auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
   static unsigned long long attr_set = 0;
@@ -774,7 +843,7 @@ static int launch_chain_t(const GemmParams& p, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cooperative ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, unused, unused, p) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
@@ -840,6 +909,8 @@ Span y_span(const w4a16_op& o, int M) {
 int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, int* mode) {
   if (!ops || n_ops < 1) return W4A16_ERR_ARG;
   long long t = 0;
+  int n_ar = 0;
+  const w4a16_peer_group* group = nullptr;
   *mode = -1;
   for (int j = 0; j < n_ops; ++j) {
     const w4a16_op& o = ops[j];
@@ -855,10 +926,38 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
       t += o.N / 128;
     } else if (o.kind == W4A16_OP_SILU_MUL) {
       if (o.N < 8 || o.N % 8 || o.K != 2 * o.N) return W4A16_ERR_SHAPE;
+    } else if (o.kind == W4A16_OP_ALLREDUCE) {
+      if (o.N < 8 || o.N % 8 || o.K != o.N) return W4A16_ERR_SHAPE;
+      const w4a16_peer_group* g = reinterpret_cast<const w4a16_peer_group*>(o.packed);
+      if (!g) return W4A16_ERR_ARG;
+      if (n_ar == 0) group = g;
+      else if (g != group) return W4A16_ERR_ARG;   // one group per chain
+      ++n_ar;
+      if (g->world < 1 || g->world > W4A16_MAX_PEERS || g->rank < 0 || g->rank >= g->world) return W4A16_ERR_ARG;
+      if (g->flag_offset % 256 || g->flag_slots < 1) return W4A16_ERR_ARG;
+      if (n_ar > g->flag_slots || g->flag_offset + w4a16_peer_flag_bytes(g->flag_slots) > g->bytes) return W4A16_ERR_ARG;
+      for (int q = 0; q < g->world; ++q)
+        if (!g->base[q] || !al16(g->base[q])) return W4A16_ERR_ARG;
+      const uintptr_t b0 = reinterpret_cast<uintptr_t>(g->base[g->rank]);
+      const Span xs = x_span(o, M), flags = {b0 + g->flag_offset, b0 + g->flag_offset + w4a16_peer_flag_bytes(g->flag_slots)};
+      if (xs.a < b0 || xs.b > b0 + g->bytes || overlaps(xs, flags)) return W4A16_ERR_ARG;   // P inside the region
     } else {
       return W4A16_ERR_ARG;
     }
     if (overlaps(x_span(o, M), y_span(o, M))) return W4A16_ERR_ARG;   // in-place ops are not supported
+  }
+  // Peers read an ALLREDUCE's X after the op's flags: the next op that writes that buffer (cyclically:
+  // every rank runs the chain again) must come after another ALLREDUCE, whose flags prove every peer has
+  // finished reading it (include/w4a16.h).
+  for (int b = 0; b < n_ops; ++b) {
+    if (ops[b].kind != W4A16_OP_ALLREDUCE) continue;
+    bool fenced = false;
+    for (int d = 1; d <= n_ops; ++d) {
+      const w4a16_op& c = ops[(b + d) % n_ops];
+      if (overlaps(y_span(c, M), x_span(ops[b], M)) && !fenced) return W4A16_ERR_ARG;
+      if (c.kind == W4A16_OP_ALLREDUCE && d < n_ops) fenced = true;
+      if (fenced) break;
+    }
   }
   if (*mode < 0) *mode = W4A16_ASYM;
   *tiles = t;
@@ -867,6 +966,10 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
 int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }   // the tcgen05 family: one CTA per SM too
 }  // namespace
 
+
+extern "C" size_t w4a16_peer_flag_bytes(int flag_slots) {
+  return flag_slots > 0 ? ((size_t)(16 + flag_slots * W4A16_MAX_PEERS) * 4 + 255) / 256 * 256 : 0;
+}
 
 extern "C" size_t w4a16_chain_plan_bytes(int n_ops) { return n_ops > 0 ? (size_t)n_ops * sizeof(w4::ma::ChainJob) : 0; }
 
@@ -891,7 +994,8 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
   if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
   const int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the stages
   w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
-  int cnt = 0;
+  int cnt = 0, ar_slot = 0;
+  uint32_t* epoch = nullptr;   // the group's run counter, advanced by the last CTA of every run
   for (int j = 0; j < n_ops; ++j) {
     const w4a16_op& o = ops[j];
     w4::ma::ChainJob& J = jobs[j];
@@ -909,6 +1013,21 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
       const uint16_t* X = reinterpret_cast<const uint16_t*>(o.X);
       if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, depth)) return e;
       if (int e = w4::encode_x_sw128(&J.xmap1, X, M, o.K, mpad, 2)) return e;
+    } else if (o.kind == W4A16_OP_ALLREDUCE) {
+      const w4a16_peer_group* g = reinterpret_cast<const w4a16_peer_group*>(o.packed);
+      const size_t off = reinterpret_cast<uintptr_t>(o.X) - reinterpret_cast<uintptr_t>(g->base[g->rank]);
+      auto flag_word = [&](int q, size_t word) {
+        return reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(g->base[q]) + g->flag_offset) + word;
+      };
+      J.world = g->world;
+      for (int q = 0; q < g->world; ++q) {
+        J.peer_x[q] = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(g->base[q]) + off);
+        J.peer_flag[q] = flag_word(q, 16 + (size_t)ar_slot * W4A16_MAX_PEERS + g->rank);   // slot ar_slot, from this rank
+      }
+      J.my_flags = flag_word(g->rank, 16 + (size_t)ar_slot * W4A16_MAX_PEERS);
+      J.epoch = flag_word(g->rank, 0);
+      if (!epoch) epoch = J.epoch;
+      ++ar_slot;
     }
     // dependencies from buffer overlaps: RAW for X; WAR / WAW for Y. Completion of op i implies the
     // completion of every op before it, so the latest conflicting op is enough.
@@ -919,11 +1038,14 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
       if (J.dep_y < 0 && (overlaps(y_span(ops[i], M), y_span(o, M)) || overlaps(x_span(ops[i], M), y_span(o, M)))) J.dep_y = i;
     }
   }
+  jobs[0].epoch = epoch;
   return W4A16_OK;
 }
 
+// cooperative = 0 only for tests that run several small chains side by side on one device (simulated
+// tensor-parallel ranks, tests/test_gpu_allreduce.py); their grids together fit the device.
 extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, int mode, int family, void* ws,
-                                      size_t ws_bytes, int sms, cudaStream_t stream) {
+                                      size_t ws_bytes, int sms, int cooperative, cudaStream_t stream) {
   const int fam = chain_family(M, family);
   if (fam < 0) return fam;
   if (!dev_plan || !ws || n_ops < 1 || (mode != W4A16_ASYM && mode != W4A16_SYM)) return W4A16_ERR_ARG;
@@ -945,11 +1067,11 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   const bool sym = mode == W4A16_SYM, s = fam == W4A16_FAMILY_MMA_SYNC_S;
   switch (w4::ma::ntb_of(M)) {
     case 1:
-      if (s) return sym ? w4::ma::launch_chain_t<1, true, true>(p, stream) : w4::ma::launch_chain_t<1, false, true>(p, stream);
-      return sym ? w4::ma::launch_chain_t<1, true, false>(p, stream) : w4::ma::launch_chain_t<1, false, false>(p, stream);
+      if (s) return sym ? w4::ma::launch_chain_t<1, true, true>(p, cooperative != 0, stream) : w4::ma::launch_chain_t<1, false, true>(p, cooperative != 0, stream);
+      return sym ? w4::ma::launch_chain_t<1, true, false>(p, cooperative != 0, stream) : w4::ma::launch_chain_t<1, false, false>(p, cooperative != 0, stream);
     case 2:
-      if (s) return sym ? w4::ma::launch_chain_t<2, true, true>(p, stream) : w4::ma::launch_chain_t<2, false, true>(p, stream);
-      return sym ? w4::ma::launch_chain_t<2, true, false>(p, stream) : w4::ma::launch_chain_t<2, false, false>(p, stream);
+      if (s) return sym ? w4::ma::launch_chain_t<2, true, true>(p, cooperative != 0, stream) : w4::ma::launch_chain_t<2, false, true>(p, cooperative != 0, stream);
+      return sym ? w4::ma::launch_chain_t<2, true, false>(p, cooperative != 0, stream) : w4::ma::launch_chain_t<2, false, false>(p, cooperative != 0, stream);
     default:
       return W4A16_ERR_SHAPE;
   }

@@ -33,8 +33,18 @@ namespace w4 {
 namespace tc {
 
 constexpr int kTileN = 128, kTileK = 128;
-constexpr int kAU = 2;                            // units per TMEM A buffer (A step)
-constexpr int kNumA = 3;                          // TMEM A buffers, kAU * 64 columns each
+#ifndef W4_TC_AU
+#define W4_TC_AU 2
+#endif
+#ifndef W4_TC_NUMA
+#define W4_TC_NUMA 3
+#endif
+#ifndef W4_TC_ACCB
+#define W4_TC_ACCB 2
+#endif
+constexpr int kAU = W4_TC_AU;                     // units per TMEM A buffer (A step)
+constexpr int kNumA = W4_TC_NUMA;                 // TMEM A buffers, kAU * 64 columns each
+constexpr int kAccB = W4_TC_ACCB;                 // accumulator buffers, 64 columns each
 constexpr int kDqWarps = 16;                      // warps 0..15: dequant + epilogue (4 per SMSP)
 constexpr int kKParts = kDqWarps / 4;             // each unit row's 128 k split into 4 x 32 (one 16 B chunk)
 constexpr int kProducerWarp = kDqWarps;           // warp 16 (SMSP 0)
@@ -44,6 +54,7 @@ constexpr int kMmaWarp = kDqWarps + 1;            // warp 17 (SMSP 1)
 constexpr int kThreads = (kDqWarps + 2) * 32;     // 576
 constexpr int kAccCol = kNumA * kAU * 64;         // 384: two accumulator buffers of 64 columns
 constexpr int kTmemCols = 512;
+static_assert(kAccCol + kAccB * 64 <= kTmemCols && kAccB >= 1 && kAccB <= 2, "TMEM budget");
 
 // A pipeline stage = R consecutive units: one bulk copy of R * TB contiguous weight bytes (the TMA
 // engine costs ~100-350 cycles per issued copy, so fewer, larger copies are what reaches HBM speed) plus
@@ -260,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
           if (u == boundary) { ++t; boundary += p.Gk; fresh = true; }
           const bool seg_start = fresh;
           if (seg_start) {
-            a ^= 1;
-            if (nseg >= 2) { wait_bar(p, &accempty_bar[a], accph[a]); accph[a] ^= 1; tc_fence_after(); }
+            a = kAccB == 1 ? 0 : (a ^ 1);
+            if (nseg >= kAccB) { wait_bar(p, &accempty_bar[a], accph[a]); accph[a] ^= 1; tc_fence_after(); }
             ++nseg;
             fresh = false;
           }
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
     int cur_t = -1, seg_u0 = u_begin, nseg = 0, boundary = 0;
 
     auto epilogue = [&](int t, int sg0, int sg1, int seg_index) {
-      const int a = seg_index & 1;
+      const int a = seg_index % kAccB;
       wait_bar(p, &accfull_bar[a], accph[a]);
       accph[a] ^= 1;
       tc_fence_after();

@@ -14,7 +14,7 @@ from ._lib import (  # noqa: F401
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
     W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S,
-    W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16Op,
+    W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE, W4A16_MAX_PEERS, W4A16Op, W4A16PeerGroup,
 )
 
 
@@ -198,10 +198,12 @@ class Chain:
     The plan (TMA descriptors, dependencies) is encoded once by the library into host memory and copied to
     the device here; the tensors must stay where they are while the chain is in use (references are kept)."""
 
-    def __init__(self, ops, M: int, family=W4A16_FAMILY_AUTO, device=None, workspace=None):
+    def __init__(self, ops, M: int, family=W4A16_FAMILY_AUTO, device=None, workspace=None, sms: Optional[int] = None):
         """workspace: optional zero-initialised uint8 tensor to use instead of a private one. Chains that run
-        one after another on one stream may share it (each run re-arms its counters; partials are scratch)."""
-        self.M, self.family = M, family
+        one after another on one stream may share it (each run re-arms its counters; partials are scratch).
+        sms: tests only — plan for that many SMs and launch non-cooperatively, so that several chains can run
+        side by side on one device (simulated tensor-parallel ranks)."""
+        self.M, self.family, self.sms = M, family, sms
         self._keep = []
         arr = (W4A16Op * len(ops))()
         mode = W4A16_ASYM
@@ -214,6 +216,14 @@ class Chain:
                                  _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode)
                 mode = pl.mode
                 self._keep += [X, pl.packed, Y]
+            elif op[0] == "allreduce":
+                _, P, out, group = op
+                if P.shape != out.shape or P.shape[0] != M:
+                    raise W4A16Error(f"chain op {i}: allreduce shapes")
+                N = P.shape[1]
+                arr[i] = W4A16Op(W4A16_OP_ALLREDUCE, _ptr(P, torch.float16, "P"), ctypes.addressof(group.desc),
+                                 _ptr(out, torch.float16, "out"), N, N, 0)
+                self._keep += [P, out, group]
             elif op[0] == "silu_mul":
                 _, GU, out = op
                 F = out.shape[1]
@@ -227,11 +237,16 @@ class Chain:
         self.n, self.mode = len(ops), mode
         nbytes = int(lib.w4a16_chain_plan_bytes(self.n))
         host = (ctypes.c_uint8 * nbytes)()
-        check(lib.w4a16_chain_plan(ctypes.addressof(arr), self.n, M, family, ctypes.addressof(host), nbytes),
-              "w4a16_chain_plan")
+        if sms is None:
+            check(lib.w4a16_chain_plan(ctypes.addressof(arr), self.n, M, family, ctypes.addressof(host), nbytes),
+                  "w4a16_chain_plan")
+        else:
+            check(lib.w4a16_chain_plan_sms(ctypes.addressof(arr), self.n, M, family, ctypes.addressof(host), nbytes, sms),
+                  "w4a16_chain_plan_sms")
         dev = torch.device(device) if device is not None else self._keep[0].device
         self.plan = torch.frombuffer(bytearray(host), dtype=torch.uint8).to(dev)
-        wsb = int(lib.w4a16_chain_workspace_bytes(ctypes.addressof(arr), self.n, M, family))
+        wsb = int(lib.w4a16_chain_workspace_bytes(ctypes.addressof(arr), self.n, M, family) if sms is None else
+                  lib.w4a16_chain_workspace_bytes_sms(ctypes.addressof(arr), self.n, M, family, sms))
         if wsb == 0:
             raise W4A16Error("w4a16_chain_workspace_bytes: bad chain")
         if workspace is not None:
@@ -242,5 +257,100 @@ class Chain:
             self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
     def __call__(self, stream=None):
+        if self.sms is not None:
+            check(lib.w4a16_chain_run_sms(self.plan.data_ptr(), self.n, self.M, self.mode, self.family,
+                                          self.ws.data_ptr(), self.ws.numel(), self.sms, _stream(stream)),
+                  "w4a16_chain_run_sms")
+            return
         check(lib.w4a16_chain_run(self.plan.data_ptr(), self.n, self.M, self.mode, self.family, self.ws.data_ptr(),
                                   self.ws.numel(), _stream(stream)), "w4a16_chain_run")
+
+
+def w4a16_peer_flag_bytes(flag_slots: int) -> int:
+    return int(lib.w4a16_peer_flag_bytes(int(flag_slots)))
+
+
+class _DevBuf:
+    """A raw device allocation exposed to torch through __cuda_array_interface__ (uint8, 1-D)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class PeerGroup:
+    """A tensor-parallel group's symmetric regions (include/w4a16.h w4a16_peer_group), as seen by one rank.
+
+    Each rank owns one device region of `nbytes`; the flag area of `flag_slots` ALLREDUCE ops sits at
+    offset 0 and buffers are carved after it with alloc() — every rank must call alloc() with the same
+    shapes in the same order, so each buffer has the same offset on every rank. Build with PeerGroup.ipc
+    (one process per GPU, CUDA IPC) or PeerGroup.simulated (tests: `world` regions on one device)."""
+
+    def __init__(self, bases, local: torch.Tensor, nbytes: int, flag_slots: int, world: int, rank: int, closer=None):
+        if not 1 <= world <= W4A16_MAX_PEERS or not 0 <= rank < world or len(bases) != world:
+            raise W4A16Error(f"peer group: world={world}, rank={rank}")
+        self.world, self.rank, self.nbytes, self.flag_slots = world, rank, nbytes, flag_slots
+        self.local = local
+        self.desc = W4A16PeerGroup()
+        for q, b in enumerate(bases):
+            self.desc.base[q] = b
+        self.desc.bytes, self.desc.flag_offset, self.desc.flag_slots = nbytes, 0, flag_slots
+        self.desc.world, self.desc.rank = world, rank
+        self._next = (w4a16_peer_flag_bytes(flag_slots) + 255) // 256 * 256
+        self._closer = closer
+
+    def alloc(self, *shape, dtype=torch.float16) -> torch.Tensor:
+        """The next symmetric buffer (same offset on every rank), 256-byte aligned."""
+        n = 1
+        for d in shape:
+            n *= d
+        nb = n * torch.empty((), dtype=dtype).element_size()
+        if self._next + nb > self.nbytes:
+            raise W4A16Error(f"peer region full ({self._next} + {nb} > {self.nbytes} bytes)")
+        t = self.local[self._next: self._next + nb].view(dtype).view(*shape)
+        self._next += (nb + 255) // 256 * 256
+        return t
+
+    @staticmethod
+    def simulated(world: int, nbytes: int, flag_slots: int, device=None):
+        """Tests: `world` zero-filled regions on ONE device, one PeerGroup per simulated rank."""
+        regs = [torch.zeros(nbytes, dtype=torch.uint8, device=device) for _ in range(world)]
+        bases = [r.data_ptr() for r in regs]
+        groups = [PeerGroup(bases, regs[r], nbytes, flag_slots, world, r) for r in range(world)]
+        for g in groups:
+            g._regions = regs   # keep every region alive
+        return groups
+
+    @staticmethod
+    def ipc(nbytes: int, flag_slots: int, group=None):
+        """One process per GPU: allocate this rank's region, exchange CUDA IPC handles over `group` (any
+        torch.distributed backend) and map every peer's region."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        check(lib.w4a16_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "w4a16_ipc_alloc")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        bases, opened = [], []
+        for q, h in enumerate(handles):
+            if q == rank:
+                bases.append(ptr.value)
+                continue
+            hb = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+            p = ctypes.c_void_p()
+            check(lib.w4a16_ipc_open(hb, ctypes.byref(p)), "w4a16_ipc_open")
+            bases.append(p.value)
+            opened.append(p.value)
+        local = torch.as_tensor(_DevBuf(ptr.value, nbytes), device=torch.device("cuda", torch.cuda.current_device()))
+
+        def closer():
+            for p in opened:
+                lib.w4a16_ipc_close(p)
+            lib.w4a16_ipc_free(ptr.value)
+        return PeerGroup(bases, local, nbytes, flag_slots, world, rank, closer)
+
+    def close(self):
+        if self._closer is not None:
+            self._closer()
+            self._closer = None

@@ -17,8 +17,8 @@ from typing import Callable, List, Optional
 import torch
 import torch.distributed as dist
 
-from .ops import (W4A16_ASYM, Chain, PackedLinear, W4A16Error, alloc_workspace, pack_linear, verify_accept,
-                  w4a16_silu_mul)
+from .ops import (W4A16_ASYM, Chain, PackedLinear, PeerGroup, W4A16Error, alloc_workspace, pack_linear,
+                  verify_accept, w4a16_peer_flag_bytes, w4a16_silu_mul)
 
 
 @dataclass(frozen=True)
@@ -95,9 +95,16 @@ class VerifyStack:
     it is packed with w4a16_pack and dropped, so only the int4 shards stay resident."""
 
     def __init__(self, dims: ModelDims, n_layers: int, M_max: int, make_weight: Callable, tp_size: int = 1,
-                 tp_rank: int = 0, group=None, mode: int = W4A16_ASYM, device=None):
+                 tp_rank: int = 0, group=None, mode: int = W4A16_ASYM, device=None, allreduce: str = "nccl",
+                 peer_group: Optional[PeerGroup] = None, chain_sms: Optional[int] = None):
+        """allreduce: "nccl" or "fused" (tp > 1). peer_group / chain_sms: tests only — a PeerGroup.simulated
+        rank and the SM share of its chains, to run several ranks side by side on one GPU."""
+        if allreduce not in ("nccl", "fused"):
+            raise ValueError(f"allreduce={allreduce!r}")
         self.d, self.n_layers, self.M_max = dims, n_layers, M_max
         self.t, self.r, self.group, self.mode = tp_size, tp_rank, group, mode
+        self.fused = allreduce == "fused" and tp_size > 1
+        self.chain_sms = chain_sms
         self.device = torch.device(device or "cuda")
         self.plan = shard_plan(dims, tp_size, tp_rank)
         biggest = max(s["K"] * s["N"] for s in self.plan.values())
@@ -121,10 +128,23 @@ class VerifyStack:
         self.x_o = torch.zeros(M_max, P["o"]["K"], **f16)
         self.x_mlp = torch.zeros(M_max, P["gate_up"]["K"], **f16)
         self.y_qkv = torch.empty(M_max, P["qkv"]["N"], **f16)
-        self.y_o = torch.empty(M_max, P["o"]["N"], **f16)
         self.y_gu = torch.empty(M_max, P["gate_up"]["N"], **f16)
         self.act = torch.empty(M_max, P["down"]["K"], **f16)
-        self.y_down = torch.empty(M_max, P["down"]["N"], **f16)
+        if self.fused:
+            # row-parallel partials live in the symmetric region (same offsets on every rank); the reduced
+            # outputs are ordinary local buffers
+            slots = 2 * n_layers
+            nbytes = w4a16_peer_flag_bytes(slots) + 2 * M_max * (P["o"]["N"] + P["down"]["N"]) + 4096
+            self.peers = peer_group if peer_group is not None else PeerGroup.ipc(nbytes, slots, group)
+            self.y_o = self.peers.alloc(M_max, P["o"]["N"])
+            self.y_down = self.peers.alloc(M_max, P["down"]["N"])
+            self.y_o_red = torch.empty(M_max, P["o"]["N"], **f16)
+            self.y_down_red = torch.empty(M_max, P["down"]["N"], **f16)
+        else:
+            self.peers = None
+            self.y_o = torch.empty(M_max, P["o"]["N"], **f16)
+            self.y_down = torch.empty(M_max, P["down"]["N"], **f16)
+            self.y_o_red, self.y_down_red = self.y_o, self.y_down   # NCCL reduces in place
         i32 = dict(dtype=torch.int32, device=self.device)
         self.tokens = torch.zeros(M_max, **i32)
         self.parents = torch.full((M_max,), -1, **i32)
@@ -145,10 +165,15 @@ class VerifyStack:
             dist.all_reduce(y, group=self.group)
 
     def _layer_ops(self, L, M):
-        """The layer's ops between its all-reduces: [QKV, O] and [gate-up, SiLU*mul, down]."""
-        return ([("gemm", self.x_qkv[:M], L["qkv"], self.y_qkv[:M]), ("gemm", self.x_o[:M], L["o"], self.y_o[:M])],
-                [("gemm", self.x_mlp[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
-                 ("gemm", self.act[:M], L["down"], self.y_down[:M])])
+        """The layer's ops between its all-reduces: [QKV, O] and [gate-up, SiLU*mul, down]; with the fused
+        all-reduce each segment ends with its ALLREDUCE op (partial in the peer region -> reduced output)."""
+        a = [("gemm", self.x_qkv[:M], L["qkv"], self.y_qkv[:M]), ("gemm", self.x_o[:M], L["o"], self.y_o[:M])]
+        b = [("gemm", self.x_mlp[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
+             ("gemm", self.act[:M], L["down"], self.y_down[:M])]
+        if self.fused:
+            a.append(("allreduce", self.y_o[:M], self.y_o_red[:M], self.peers))
+            b.append(("allreduce", self.y_down[:M], self.y_down_red[:M], self.peers))
+        return a, b
 
     def chains(self, M: int):
         """Persistent chains for width M (include/w4a16.h w4a16_chain_*): the whole stack in ONE launch at
@@ -160,8 +185,9 @@ class VerifyStack:
                 return None
             try:
                 segs = [self._layer_ops(L, M) for L in self.layers]
-                if self.t == 1:
-                    self._chains[M] = [Chain([op for a, b in segs for op in a + b], M, device=self.device)]
+                if self.t == 1 or self.fused:   # the whole forward in one launch
+                    self._chains[M] = [Chain([op for a, b in segs for op in a + b], M, device=self.device,
+                                             sms=self.chain_sms)]
                 else:
                     # the per-segment chains run one after another on one stream: they share one workspace
                     first = [Chain(seg, M, device=self.device) for seg in segs[0]]
@@ -178,7 +204,7 @@ class VerifyStack:
             raise ValueError(f"M={M} outside [1, {self.M_max}]")
         ch = self.chains(M) if self.use_chains else None
         if ch is not None:
-            if self.t == 1:
+            if self.t == 1 or self.fused:
                 ch[0](stream)
             else:
                 for i, c in enumerate(ch):
@@ -187,19 +213,26 @@ class VerifyStack:
             verify_accept(self.tokens[:M], self.parents[:M], self.argmax[:M], self.accept_out[:3 + M], stream)
             return
         ws = self.ws
+        # op by op (M > 16, or chains off): NCCL all-reduces; with the fused layout the partial is first
+        # copied to the reduced buffer (the ALLREDUCE op exists only inside chains)
+        o_out, d_out = (self.y_o_red[:M], self.y_down_red[:M]) if self.fused else (self.y_o[:M], self.y_down[:M])
         for L in self.layers:
             L["qkv"](self.x_qkv[:M], self.y_qkv[:M], ws, stream)
             L["o"](self.x_o[:M], self.y_o[:M], ws, stream)
-            self._allreduce(self.y_o[:M])
+            if self.fused:
+                o_out.copy_(self.y_o[:M])
+            self._allreduce(o_out)
             L["gate_up"](self.x_mlp[:M], self.y_gu[:M], ws, stream)
             w4a16_silu_mul(self.y_gu[:M], self.act[:M], stream)
             L["down"](self.act[:M], self.y_down[:M], ws, stream)
-            self._allreduce(self.y_down[:M])
+            if self.fused:
+                d_out.copy_(self.y_down[:M])
+            self._allreduce(d_out)
         verify_accept(self.tokens[:M], self.parents[:M], self.argmax[:M], self.accept_out[:3 + M], stream)
 
     def launches_per_forward(self, M: int = None) -> int:
-        """libw4a16 kernel launches per forward: one chain (tp = 1) or two per layer (tp > 1) plus the
-        acceptance; without chains 4 GEMMs + SiLU*mul per layer plus the acceptance."""
+        """libw4a16 kernel launches per forward: one chain (tp = 1, or the fused all-reduce) or two per layer
+        (tp > 1 with NCCL) plus the acceptance; without chains 4 GEMMs + SiLU*mul per layer plus the acceptance."""
         if M is not None and self.use_chains and self.chains(M) is not None:
             return len(self.chains(M)) + 1
         return 5 * self.n_layers + 1
@@ -241,10 +274,10 @@ class VerifyStack:
         else:
             self.forward(M)
         host_out["accept"][:3 + M].copy_(self.accept_out[:3 + M], non_blocking=True)
-        host_out["y"][:M].copy_(self.y_down[:M], non_blocking=True)
+        host_out["y"][:M].copy_(self.y_down_red[:M], non_blocking=True)
 
     def h2d_bytes(self, M: int) -> int:
         return 2 * M * (self.x_qkv.shape[1] + self.x_o.shape[1] + self.x_mlp.shape[1]) + 3 * 4 * M
 
     def d2h_bytes(self, M: int) -> int:
-        return 4 * (3 + M) + 2 * M * self.y_down.shape[1]
+        return 4 * (3 + M) + 2 * M * self.y_down_red.shape[1]
