@@ -311,6 +311,12 @@ class PeerGroup:
         self._next += (nb + 255) // 256 * 256
         return t
 
+    def peer_region(self, q: int) -> torch.Tensor:
+        """Rank q's whole region as mapped in this process (uint8 view; tests and diagnostics)."""
+        if q == self.rank:
+            return self.local
+        return torch.as_tensor(_DevBuf(self.desc.base[q], self.nbytes), device=self.local.device)
+
     @staticmethod
     def simulated(world: int, nbytes: int, flag_slots: int, device=None):
         """Tests: `world` zero-filled regions on ONE device, one PeerGroup per simulated rank."""
