@@ -44,8 +44,17 @@ constexpr int kGroups = W4_MA_GROUPS;              // consumer groups sharing on
 constexpr int kWarps = 8 * kGroups;                // per group: 4 row-quarters x 2 k-halves
 constexpr int kProducerWarp = kWarps;
 constexpr int kXsumWarp = kWarps + 1;              // activation sums (offset-code family only)
+#ifndef W4_MA_PUB
+#define W4_MA_PUB 1   // 1: a publisher warp issues the counter increments (fence + red) for the storing warps
+#endif
+// Publisher warp (W4_MA_PUB): the release of a tile / op counter costs the issuing thread a GPU-scope fence
+// (~1 us under load); the storing warps hand the increment to this warp through a shared-memory ring and
+// go straight on to the next units.
 template <bool kScaleInA>
-constexpr int threads_for() { return (kWarps + (kScaleInA ? 1 : 2)) * 32; }
+__host__ __device__ constexpr int pub_warp() { return kWarps + (kScaleInA ? 1 : 2); }
+template <bool kScaleInA>
+constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0)) * 32; }
+constexpr int kPubSlots = 8;
 constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
 #ifndef W4_MA_CTAS
 #define W4_MA_CTAS 2
@@ -267,6 +276,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   __shared__ __align__(8) uint64_t empty_bar[S];
   __shared__ __align__(8) uint64_t sums_bar[S];   // offset-code family: the stage's activation sums are ready
   __shared__ int s_last;
+  __shared__ __align__(8) uint64_t pub_full[kPubSlots], pub_empty[kPubSlots];
+  __shared__ int* pub_ptr[kPubSlots];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -278,6 +289,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); mbar_init(&sums_bar[s], 1); }
+    for (int s = 0; s < kPubSlots; ++s) { mbar_init(&pub_full[s], 1); mbar_init(&pub_empty[s], 1); }
     fence_mbar_init();
     pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
   }
@@ -438,8 +450,42 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     return;
   }
 
+  if (W4_MA_PUB && warp == pub_warp<kScaleInA>()) {
+    // ---------------- publisher ----------------
+    // Requests arrive in order from thread 0 (after a barrier of the threads whose stores they publish):
+    // mbarrier release/acquire (CTA scope) hands those stores to this warp; its GPU-scope fence + relaxed
+    // red then releases them to the CTAs that acquire the counter. nullptr ends the kernel's requests.
+    int slot = 0;
+    uint32_t ph = 0;
+    for (;;) {
+      mbar_wait(&pub_full[slot], ph);
+      int* ptr = pub_ptr[slot];
+      if (lane == 0) {
+        if (ptr) red_release_gpu_add(ptr, 1);
+        mbar_arrive(&pub_empty[slot]);
+      }
+      __syncwarp();
+      if (!ptr) break;
+      if (++slot == kPubSlots) { slot = 0; ph ^= 1; }
+    }
+    return;
+  }
+
   // ---------------- consumers ----------------
   trace_ma(p, 0);
+  int pub_s = 0;
+  uint32_t pub_ph = 0;
+  // thread 0 only, after a barrier of the threads whose global stores the increment releases
+  auto publish = [&](int* ptr) {
+    if (!W4_MA_PUB) {
+      if (ptr) red_release_gpu_add(ptr, 1);
+      return;
+    }
+    mbar_wait(&pub_empty[pub_s], pub_ph ^ 1);   // the slot's previous request is consumed
+    pub_ptr[pub_s] = ptr;
+    mbar_arrive(&pub_full[pub_s]);
+    if (++pub_s == kPubSlots) { pub_s = 0; pub_ph ^= 1; }
+  };
   pdl_wait();   // Y / workspace writes must follow the preceding kernel (returns at once when satisfied)
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
   const int rq = warp & 3, kh = (warp >> 2) & 1, grp = warp >> 3;   // row quarter, k half, unit group
@@ -481,7 +527,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         *reinterpret_cast<uint4*>(J.Y + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
       }
       named_bar_sync(1, kWarps * 32);
-      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+      if (threadIdx.x == 0) publish(&p.done[job]);
       trace_op(p, job, 2);
       trace_op(p, job, 3);
       continue;
@@ -564,7 +610,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int tb = 0; tb < NTB; ++tb)
             __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
         named_bar_sync(2, 4 * 32);
-        if (threadIdx.x == 0) red_release_gpu_add(&J.counters[t], 1);
+        if (threadIdx.x == 0) publish(&J.counters[t]);
         return;
       }
       if (threadIdx.x == 0) {
@@ -794,9 +840,16 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // k-half 0) take part; the other warps are already streaming the next op.
     if (chain && grp == 0 && kh == 0) {
       named_bar_sync(2, 4 * 32);
-      if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+      if (threadIdx.x == 0) publish(&p.done[job]);
     }
     trace_op(p, job, 3);
+  }
+  if (W4_MA_PUB && threadIdx.x == 0) {
+    // end the publisher's requests and wait until it has issued every increment
+    const int last = pub_s;
+    const uint32_t last_ph = pub_ph;
+    publish(nullptr);
+    mbar_wait(&pub_empty[last], last_ph);
   }
   if (chain && threadIdx.x == 0) {
     // The last CTA out re-arms the op counters for the next run of the chain (every CTA has finished
