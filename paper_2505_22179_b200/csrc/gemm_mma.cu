@@ -36,7 +36,6 @@ namespace w4 {
 namespace ma {
 
 constexpr int kTileN = 128, kTileK = 128;
-constexpr int kUnitWBytes = kTileN * kTileK / 2;   // 8192
 #ifndef W4_MA_GROUPS
 #define W4_MA_GROUPS 2
 #endif
@@ -275,7 +274,6 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   __shared__ __align__(8) uint64_t full_bar[S];
   __shared__ __align__(8) uint64_t empty_bar[S];
   __shared__ __align__(8) uint64_t sums_bar[S];   // offset-code family: the stage's activation sums are ready
-  __shared__ int s_last;
   __shared__ __align__(8) uint64_t pub_full[kPubSlots], pub_empty[kPubSlots];
   __shared__ int* pub_ptr[kPubSlots];
 

@@ -12,3 +12,9 @@ timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytes
     -k "independent or rejects" > $OUT/sanitize_chain.log 2>&1; echo "chain memcheck rc=$?"; grep -E "ERROR SUMMARY|passed" $OUT/sanitize_chain.log | tail -2
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_lmhead.py tests/test_gpu_tree_attn.py -x -q \
     -k "not full_size and not 61 and not 49" > $OUT/sanitize_f23.log 2>&1; echo "f2/f3 memcheck rc=$?"; grep -E "ERROR SUMMARY|passed" $OUT/sanitize_f23.log | tail -2
+# the publisher-warp handshake and the ALLREDUCE op (world 1 only: the sanitizer serialises kernels, so
+# simulated ranks side by side would wait for each other until the 10 s trap)
+for tool in racecheck synccheck memcheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_chain.py tests/test_gpu_allreduce.py -x -q \
+      -k "independent or (simulated_ranks and 1-8-0)" > $OUT/sanitize_chain_$tool.log 2>&1; echo "chain $tool rc=$?"; grep -E "ERROR SUMMARY|passed" $OUT/sanitize_chain_$tool.log | tail -2
+done
