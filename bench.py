@@ -52,9 +52,10 @@ def parse():
     ap.add_argument("--sweep", default="1,2,4,7,8,16,24,32,49,61,64", help="comma list of M for the M sweep ('' = none)")
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "fused"],
-                    help="tp > 1: NCCL all-reduces between per-segment chains, or ALLREDUCE ops inside one chain "
-                         "per forward over CUDA-IPC peer memory (include/w4a16.h; not yet validated on multi-GPU)")
+    ap.add_argument("--allreduce", default="auto", choices=["auto", "nccl", "fused"],
+                    help="tp > 1: ALLREDUCE ops inside one chain per forward over CUDA-IPC peer memory (fused, "
+                         "include/w4a16.h) or NCCL all-reduces between per-segment chains; auto = fused if its "
+                         "setup and a start-up check against the NCCL path pass on every rank, else nccl")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-kernels", dest="kernels", action="store_false", help="skip the per-kernel breakdown")
@@ -228,19 +229,59 @@ def main():
     def make_weight(l, name, K, N, out):
         synth.gpu(args.seed, synth.tensor_id(l, mat_id[name], rank), synth.WEIGHT, K, N, out=out)
 
+    def build(allreduce):
+        st = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
+                            device=dev, allreduce=allreduce)
+        # activations (seeded, in HBM) and a draft tree of the headline width
+        for name, buf, tid in (("x_qkv", st.x_qkv, 1), ("x_o", st.x_o, 2), ("x_mlp", st.x_mlp, 3)):
+            synth.gpu(args.seed, synth.tensor_id(0xFFF, tid, rank), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+        rng = np.random.default_rng(args.seed)
+        tok, par = synth.eagle_tree(rng, M_max - 1, 6)
+        am = synth.target_argmax_for(rng, tok, par, 0.7)
+        st.set_tree(tok, par, am)
+        torch.cuda.synchronize()
+        return st
+
+    def fused_matches_nccl(st) -> bool:
+        """One forward at M = min(8, M_max) through the fused chain vs the same forward op by op with NCCL."""
+        m = min(8, M_max)
+        dist.barrier(device_ids=[local])
+        st.forward(m)
+        torch.cuda.synchronize()
+        got = [st.y_o_red[:m].float().clone(), st.y_down_red[:m].float().clone()]
+        st.use_chains = False
+        st.forward(m)
+        torch.cuda.synchronize()
+        st.use_chains = True
+        want = [st.y_o_red[:m].float(), st.y_down_red[:m].float()]
+        return all(bool(torch.all((g - w).abs() <= 1e-2 * (1 + w.abs())).item()) for g, w in zip(got, want))
+
     t0 = time.perf_counter()
-    stack = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
-                           device=dev, allreduce=args.allreduce)
+    allreduce_used = "none" if world == 1 else args.allreduce
+    stack = None
+    if world > 1 and args.allreduce in ("auto", "fused"):
+        ok = True
+        try:
+            stack = build("fused")
+            ok = fused_matches_nccl(stack)
+        except Exception as e:   # setup failure (IPC / peer access): every rank learns it below
+            log(f"fused all-reduce unavailable on rank {rank}: {e!r}")
+            ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            allreduce_used = "fused"
+        elif args.allreduce == "fused":
+            raise SystemExit("--allreduce fused: setup or start-up check failed")
+        else:
+            log("falling back to NCCL all-reduces")
+            stack = None   # its peer region stays mapped (a few MB): freeing it needs every peer to unmap first
+            torch.cuda.empty_cache()
+            allreduce_used = "nccl"
+    if stack is None:
+        stack = build("nccl")
     build_s = time.perf_counter() - t0
-    log(f"built {n_layers} layers ({stack.weight_bytes / 1e9:.2f} GB packed) in {build_s:.1f}s")
-    # activations (seeded, in HBM) and a draft tree of the headline width
-    for name, buf, tid in (("x_qkv", stack.x_qkv, 1), ("x_o", stack.x_o, 2), ("x_mlp", stack.x_mlp, 3)):
-        synth.gpu(args.seed, synth.tensor_id(0xFFF, tid, rank), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
-    rng = np.random.default_rng(args.seed)
-    tok, par = synth.eagle_tree(rng, M_max - 1, 6)
-    am = synth.target_argmax_for(rng, tok, par, 0.7)
-    stack.set_tree(tok, par, am)
-    torch.cuda.synchronize()
+    log(f"built {n_layers} layers ({stack.weight_bytes / 1e9:.2f} GB packed) in {build_s:.1f}s, all-reduce: {allreduce_used}")
 
     def barrier():
         if world > 1:
@@ -557,7 +598,7 @@ def main():
             "config": {"workload": f"{dims.name} W4A16 g128 {args.mode} verify forward: {n_layers} decoder layers "
                                    f"(QKV, O, gate-up, SiLU*mul, down) + verify_accept; BASELINE configs 3-4",
                        "M": args.M, "layers": n_layers, "tp": world, "parallelism": f"tp{world}",
-                       "allreduce": "none" if world == 1 else args.allreduce,
+                       "allreduce": allreduce_used,
                        "weight_bytes_per_step": bytes_all_ranks,
                        "l2": f"{bytes_all_ranks / 1e9:.1f} GB of weights per step >> 126 MB L2 (no flush needed)",
                        "timing": "CUDA graph replay, CUDA events on the launching stream, max over ranks"},

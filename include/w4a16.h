@@ -205,7 +205,7 @@ typedef struct {
  * names the same group; X lies inside base[rank]; and cyclically between an ALLREDUCE that reads a
  * buffer and the next op that writes it there is another ALLREDUCE (that op's flags prove every peer has
  * finished reading — two alternating partial buffers, as in a decoder layer's O and down, satisfy it).
- * Every rank runs the same sequence of chains over the group. A wait that does not complete within ~10 s
+ * Every rank runs the same sequence of chains over the group. A wait that does not complete within ~60 s
  * (a peer that never arrives) traps the kernel instead of hanging the device. */
 #define W4A16_MAX_PEERS 8
 typedef struct {

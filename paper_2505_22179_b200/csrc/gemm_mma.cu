@@ -223,7 +223,7 @@ void allreduce_op(const GemmParams& p, int job, int cta) {
     for (int q = 0; q < world; ++q) {
       while ((int)(ld_acquire_sys(cj->my_flags + q) - e) < 0) {
         __nanosleep(128);
-        if (globaltimer_ns() - t0 > 10000000000ull) __trap();   // a peer never arrived: fail, do not hang
+        if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // a peer never arrived: fail, do not hang
       }
     }
   }

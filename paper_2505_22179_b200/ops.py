@@ -10,7 +10,7 @@ from typing import Optional
 import torch
 
 from ._lib import (  # noqa: F401
-    lib, check, status_string, W4A16Error,
+    lib, check, status_string, W4A16Error, W4A16_OK,
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
     W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S,
@@ -335,25 +335,41 @@ class PeerGroup:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         ptr = ctypes.c_void_p()
         handle = (ctypes.c_uint8 * 64)()
-        check(lib.w4a16_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "w4a16_ipc_alloc")
+        st = lib.w4a16_ipc_alloc(nbytes, ctypes.byref(ptr), handle)
+        # every step is agreed on by all ranks (a rank that fails still takes part in the collectives, so
+        # no rank is left waiting in one)
         handles = [None] * world
-        dist.all_gather_object(handles, bytes(handle), group=group)
+        dist.all_gather_object(handles, (st, bytes(handle)), group=group)
         bases, opened = [], []
-        for q, h in enumerate(handles):
+
+        def closer():
+            for p in opened:
+                lib.w4a16_ipc_close(p)
+            if st == W4A16_OK:
+                lib.w4a16_ipc_free(ptr.value)
+        if any(s != W4A16_OK for s, _ in handles):
+            closer()
+            raise W4A16Error(f"w4a16_ipc_alloc failed on rank(s) {[q for q, (s, _) in enumerate(handles) if s != W4A16_OK]}")
+        err = W4A16_OK
+        for q, (_, h) in enumerate(handles):
             if q == rank:
                 bases.append(ptr.value)
                 continue
             hb = (ctypes.c_uint8 * 64).from_buffer_copy(h)
             p = ctypes.c_void_p()
-            check(lib.w4a16_ipc_open(hb, ctypes.byref(p)), "w4a16_ipc_open")
+            e = lib.w4a16_ipc_open(hb, ctypes.byref(p))
+            if e != W4A16_OK:
+                err = e
+                bases.append(None)
+                continue
             bases.append(p.value)
             opened.append(p.value)
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        if any(e != W4A16_OK for e in errs):
+            closer()
+            raise W4A16Error(f"w4a16_ipc_open failed on rank(s) {[q for q, e in enumerate(errs) if e != W4A16_OK]}")
         local = torch.as_tensor(_DevBuf(ptr.value, nbytes), device=torch.device("cuda", torch.cuda.current_device()))
-
-        def closer():
-            for p in opened:
-                lib.w4a16_ipc_close(p)
-            lib.w4a16_ipc_free(ptr.value)
         return PeerGroup(bases, local, nbytes, flag_slots, world, rank, closer)
 
     def close(self):
