@@ -65,7 +65,11 @@ struct Cfg {
   static constexpr int kTB = SYM ? 8448 : 8704;                              // packed bytes per unit
   static constexpr int kXBox = MPAD * 128;                                   // one 64-k SW128 box
   static constexpr int kXUnit = 2 * kXBox;
+#ifdef W4_TC_NOX   // diagnostics only: stages without activation slices (valid with W4A16_TC_DEBUG = 5 or 7)
+  static constexpr int kXStage = 0;
+#else
   static constexpr int kXStage = kR * kXUnit;
+#endif
   static constexpr int kStage = (kXStage + kR * kTB + 1023) / 1024 * 1024;
   static constexpr int kStages = (208 * 1024) / kStage > 8 ? 8 : (208 * 1024) / kStage;
   static constexpr int kSmem = kStages * kStage + 1024;                      // + alignment slack
