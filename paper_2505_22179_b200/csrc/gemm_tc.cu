@@ -122,6 +122,10 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int ncols) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
+#ifdef W4_TC_ARRIVE   // diagnostics only (valid with W4A16_TC_DEBUG bit 0: no MMAs): plain arrive instead of commit
+  mbar_arrive(bar);
+  return;
+#endif
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // D[tmem] (+)= A[tmem] * B[smem desc]
