@@ -578,6 +578,41 @@ def main():
                           "us_per_forward_80_layers": 80 * 1e3 * msa}
             log(f"tree attention M={Mq} ({kind}): {1e3 * msa:.1f} us per layer")
             del ga
+    # the in-chain ALLREDUCE op's own cost on one GPU — a world-1 group (ready flags, system
+    # fences, the grid-wide wait, the reduce pass; no NVLink reads): 16 layers as one chain with and without
+    # an ALLREDUCE after every O and down GEMM.
+    ar = None
+    if args.lm_head and world == 1 and M <= 16 and n_layers >= 16:
+        try:
+            nl = 16
+            g1 = w4.PeerGroup.simulated(1, 1 << 22, 2 * nl, device=dev)[0]
+            Hd = dims.hidden
+            P_o, P_d = g1.alloc(M, Hd), g1.alloc(M, Hd)
+            r_o, r_d = (torch.empty(M, Hd, dtype=torch.float16, device=dev) for _ in range(2))
+            plain, fused = [], []
+            for L in stack.layers[:nl]:
+                qa, qb = stack._layer_ops(L, M)
+                plain += qa + qb
+                fused += [qa[0], ("gemm", stack.x_o[:M], L["o"], P_o), ("allreduce", P_o, r_o, g1),
+                          qb[0], qb[1], ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
+            t_ch = {}
+            for name, ops in (("plain", plain), ("allreduce", fused)):
+                ch = w4.Chain(ops, M)
+                with torch.cuda.stream(stream):
+                    ch(stream)
+                torch.cuda.synchronize()
+                gch = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gch, stream=stream):
+                    ch(stream)
+                t_ch[name] = time_graph(gch, 10, 3)
+                del gch
+            ar = {"row": "f1", "M": M, "layers": nl, "ops": 2 * nl, "world": 1,
+                  "chain_ms": t_ch["plain"], "chain_with_allreduce_ms": t_ch["allreduce"],
+                  "us_per_allreduce_op": 1e3 * (t_ch["allreduce"] - t_ch["plain"]) / (2 * nl),
+                  "note": "world-1 group on one GPU: protocol + grid-wide wait + reduce pass; NVLink reads not included"}
+            log(f"in-chain ALLREDUCE (world 1): {ar['us_per_allreduce_op']:.2f} us per op")
+        except Exception as e:   # never let the side measurement break the bench line
+            ar = {"row": "f1", "error": repr(e)}
     clk = clocks.stop() if clocks else None
 
     cpu = None
@@ -606,6 +641,7 @@ def main():
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
+            "allreduce_in_chain": ar,
             "other_configs": other_configs,
             "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
