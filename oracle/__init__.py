@@ -47,6 +47,8 @@ def _load():
     L.orc_kv_compact.argtypes = [vp, vp, i32, i32, i32, vp]; L.orc_kv_compact.restype = i32
     L.orc_hadamard.argtypes = [vp, i32, i32, i32, vp]; L.orc_hadamard.restype = i32
     L.orc_allreduce.argtypes = [vp, i32, ctypes.c_size_t, vp]; L.orc_allreduce.restype = i32
+    L.orc_quantize_act_int8.argtypes = [vp, i32, i32, vp, vp, vp]; L.orc_quantize_act_int8.restype = i32
+    L.orc_gemm_w4a8.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp]; L.orc_gemm_w4a8.restype = i32
     L.orc_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, i32]; L.orc_lmhead_argmax.restype = i32
     return L
 
@@ -238,3 +240,29 @@ def allreduce(P):
     if L.orc_allreduce(_p(P), T, out.size, _p(out)) != 0:
         raise ValueError("orc_allreduce: bad arguments")
     return out
+
+
+def quantize_act_int8(X):
+    """W4A8 activations (reading R21): fp16 [M, K] -> (Xq int8 [M, K], sx fp32 [M], xsum int32 [M, K/128])."""
+    X = _u16(X)
+    M, K = X.shape
+    Xq = np.zeros((M, K), dtype=np.int8)
+    sx = np.zeros(M, dtype=np.float32)
+    xs = np.zeros((M, K // 128), dtype=np.int32)
+    if L.orc_quantize_act_int8(_p(X), M, K, _p(Xq), _p(sx), _p(xs)) != 0:
+        raise ValueError("orc_quantize_act_int8: bad arguments")
+    return Xq, sx, xs
+
+
+def gemm_w4a8(Xq, sx, codes, sc):
+    """W4A8 GEMM on SYM g128 weights (codes uint8 [K, N], scales fp16 bits [K/128, N]) -> fp64 [M, N]."""
+    Xq = np.ascontiguousarray(Xq, dtype=np.int8)
+    sx = np.ascontiguousarray(sx, dtype=np.float32)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    sc = _u16(sc)
+    M, K = Xq.shape
+    N = codes.shape[1]
+    Y = np.zeros((M, N), dtype=np.float64)
+    if L.orc_gemm_w4a8(_p(Xq), _p(sx), _p(codes), _p(sc), M, K, N, _p(Y)) != 0:
+        raise ValueError("orc_gemm_w4a8: bad arguments")
+    return Y

@@ -434,3 +434,46 @@ int orc_allreduce(const uint16_t* P, int T, size_t n, uint16_t* out) {
   }
   return 0;
 }
+
+int orc_quantize_act_int8(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum) {
+  if (!X || !Xq || !sx || !xsum || M < 1 || K < 128 || K % 128) return -1;
+  for (int m = 0; m < M; ++m) {
+    const uint16_t* xr = X + (size_t)m * K;
+    float amax = 0.0f;
+    for (int k = 0; k < K; ++k) {
+      const float a = fabsf(orc_half_to_float(xr[k]));
+      if (a > amax) amax = a;
+    }
+    const float inv = amax > 0.0f ? 127.0f / amax : 0.0f;
+    sx[m] = amax / 127.0f;
+    for (int g = 0; g < K / 128; ++g) {
+      int32_t sum = 0;
+      for (int k = g * 128; k < (g + 1) * 128; ++k) {
+        float q = nearbyintf(orc_half_to_float(xr[k]) * inv);   /* default rounding mode: nearest even */
+        if (q > 127.0f) q = 127.0f;
+        if (q < -127.0f) q = -127.0f;
+        Xq[(size_t)m * K + k] = (int8_t)q;
+        sum += (int32_t)q;
+      }
+      xsum[(size_t)m * (K / 128) + g] = sum;
+    }
+  }
+  return 0;
+}
+
+int orc_gemm_w4a8(const int8_t* Xq, const float* sx, const uint8_t* codes, const uint16_t* scales, int M, int K, int N,
+                  double* Y) {
+  if (!Xq || !sx || !codes || !scales || !Y || M < 1 || K < 128 || K % 128 || N < 1) return -1;
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < N; ++n) {
+      double acc = 0.0;
+      for (int g = 0; g < K / 128; ++g) {
+        long long dot = 0;
+        for (int k = g * 128; k < (g + 1) * 128; ++k)
+          dot += (long long)Xq[(size_t)m * K + k] * ((int)codes[(size_t)k * N + n] - 8);
+        acc += orc_half_to_double(scales[(size_t)g * N + n]) * (double)dot;
+      }
+      Y[(size_t)m * N + n] = (double)sx[m] * acc;
+    }
+  return 0;
+}

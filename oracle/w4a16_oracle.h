@@ -23,6 +23,7 @@
  *                 an ancestor of i; P:80-82 tree drafts), softmax in fp64.
  *   - kv_compact: after acceptance keep the root and the accepted path's rows, in order (S:159-164
  *                 cache_select of the accepted root-to-leaf path).
+ *   - w4a8:       per-token int8 activation quantisation and the W4A8 GEMM.
  *   - allreduce:  the sum over tensor-parallel ranks of row-parallel partial products.
  *   - hadamard:   the rotation of W4A16+Rot (QuaRot-style Hadamard rotation):
  *                 block-diagonal normalised Sylvester Hadamard along k, y = x (I (x) H_B) / sqrt(B).
@@ -115,6 +116,17 @@ int orc_kv_compact(uint16_t* Kc, uint16_t* Vc, int L, int Hkv, int D, const int3
  * consecutive k (B a power of two dividing K), Y[m][bB + i] = sum_j (-1)^popcount(i & j) X[m][bB + j] / sqrt(B),
  * in fp64 straight from the definition (Sylvester order). Y fp64 [M][K]. Returns 0 / -1. */
 int orc_hadamard(const uint16_t* X, int M, int K, int B, double* Y);
+
+/* W4A8 (4-bit weights, 8-bit activations on INT8 tensor cores, QQQ-style
+ * symmetric). Reading R21: per-token symmetric int8 activations, decided in IEEE fp32 exactly
+ * as written: amax = max_k |x[m][k]|; inv = 127.0f / amax (0 if amax == 0); q = clamp(rne(x * inv), -127, 127);
+ * sx[m] = amax / 127.0f; xsum[m][g] = sum of q over k-group g (128). Returns 0 / -1. */
+int orc_quantize_act_int8(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum);
+/* W4A8 GEMM on SYM group-128 weights (codes q in [0,15], z = 8, fp16 scale s[g][n]):
+ * Y[m][n] = sx[m] * sum_g s[g][n] * sum_{k in g} Xq[m][k] * (q[k][n] - 8), inner sums exact integers, the rest
+ * in fp64. Y fp64 [M][N]. Returns 0 / -1. */
+int orc_gemm_w4a8(const int8_t* Xq, const float* sx, const uint8_t* codes, const uint16_t* scales, int M, int K, int N,
+                  double* Y);
 
 /* Tensor-parallel all-reduce of row-parallel partial sums (Megatron row-parallel O / down,
  * y = sum over ranks of the rank's K-shard product): out[i] = fp16_rne(sum_{r < T} P[r][i]), the sum in
