@@ -10,7 +10,7 @@ BUILD := build/obj
 
 LIB := paper_2505_22179_b200/libw4a16.so
 OBJS := $(BUILD)/abi.o $(BUILD)/pack.o $(BUILD)/gemm_mma.o $(BUILD)/accept.o $(BUILD)/mlp_glue.o $(BUILD)/gemm_tc.o \
-        $(BUILD)/lmhead.o $(BUILD)/tree_attn.o $(BUILD)/hadamard.o
+        $(BUILD)/lmhead.o $(BUILD)/tree_attn.o $(BUILD)/hadamard.o $(BUILD)/w4a8.o
 
 all: $(LIB) synth/libsynth_host.so synth/libsynth_gpu.so oracle/libw4a16_oracle.so
 

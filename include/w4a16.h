@@ -244,6 +244,22 @@ int w4a16_chain_plan(const w4a16_op* ops, int n_ops, int M, int family, void* pl
 int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family, void* workspace,
                     size_t workspace_bytes, w4a16_stream_t stream);
 
+/* ---- W4A8 variant (4-bit weights with 8-bit activations on INT8 tensor cores,
+ * QQQ-style symmetric; reading R21 in DESIGN.md) --------------------------------------------------------
+ * w4a8_quantize_act: per-token symmetric int8 activations, decided in IEEE fp32 exactly as
+ *   amax = max_k |X[m][k]|; inv = 127 / amax (0 if amax == 0); Xq = clamp(rne(X * inv), -127, 127);
+ *   sx[m] = amax / 127; xsum[m][g] = sum of Xq[m][k] over k-group g (128 k).
+ *   X fp16 [M][K], Xq int8 [M][K], sx fp32 [M], xsum int32 [M][K/128]; K % 128 == 0, 1 <= M <= W4A16_MAX_M;
+ *   all device pointers, Xq 4-byte aligned.
+ * w4a8_gemm: Y[m][n] = fp16_rne(sx[m] * sum_g s[g][n] * (sum_{k in g} Xq[m][k] * q[k][n] - 8 * xsum[m][g]))
+ *   on the SYM (z = 8) blob of w4a16_pack (K x N, group 128): int32-exact group sums (INT8 MMA), fp32 group
+ *   scaling in k order, per-split partials summed in split order (deterministic). workspace: at least
+ *   w4a8_workspace_bytes(M, K, N) bytes (scratch; no initialisation needed). */
+int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, w4a16_stream_t stream);
+size_t w4a8_workspace_bytes(int M, int K, int N);
+int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K, int N,
+              void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
+
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 

@@ -13,5 +13,5 @@ from .ops import (  # noqa: F401
     PackedLinear, pack_linear, alloc_workspace, w4a16_packed_bytes, Chain,
     w4a16_lmhead_argmax, w4a16_lmhead_workspace_bytes, alloc_lmhead_workspace,
     w4a16_tree_attention, w4a16_tree_attention_workspace_bytes, w4a16_kv_compact, w4a16_hadamard,
-    PeerGroup, w4a16_peer_flag_bytes,
+    PeerGroup, w4a16_peer_flag_bytes, w4a8_quantize_act, w4a8_workspace_bytes, w4a8_gemm,
 )

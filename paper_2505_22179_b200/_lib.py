@@ -50,6 +50,9 @@ ABI_SYMBOLS = (
     "w4a16_ipc_open",
     "w4a16_ipc_close",
     "w4a16_ipc_free",
+    "w4a8_quantize_act",
+    "w4a8_workspace_bytes",
+    "w4a8_gemm",
 )
 W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE = 0, 1, 2
 W4A16_MAX_PEERS = 8
@@ -104,6 +107,12 @@ def _load():
     lib.w4a16_kv_compact.restype = i32
     lib.w4a16_hadamard.argtypes = [vp, vp, i32, i32, i32, vp]
     lib.w4a16_hadamard.restype = i32
+    lib.w4a8_quantize_act.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    lib.w4a8_quantize_act.restype = i32
+    lib.w4a8_workspace_bytes.argtypes = [i32, i32, i32]
+    lib.w4a8_workspace_bytes.restype = sz
+    lib.w4a8_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, sz, vp]
+    lib.w4a8_gemm.restype = i32
     lib.w4a16_chain_plan_bytes.argtypes = [i32]
     lib.w4a16_chain_plan_bytes.restype = sz
     lib.w4a16_chain_workspace_bytes.argtypes = [vp, i32, i32, i32]

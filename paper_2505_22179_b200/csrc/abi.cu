@@ -24,6 +24,10 @@ extern "C" int w4a16_launch_lmhead_argmax(const uint16_t*, const uint16_t*, int,
 extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op*, int, int, int, int);
 extern "C" int w4a16_chain_plan_sms(const w4a16_op*, int, int, int, void*, size_t, int);
 extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, int, cudaStream_t);
+extern "C" size_t w4a8_workspace_bytes_sms(int, int, int, int);
+extern "C" int w4a8_launch_quantize(const uint16_t*, int, int, int8_t*, float*, int32_t*, cudaStream_t);
+extern "C" int w4a8_launch_gemm(const int8_t*, const float*, const int32_t*, const void*, uint16_t*, int, int, int, void*, int,
+                                cudaStream_t);
 extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
                                      cudaStream_t);
 
@@ -274,4 +278,31 @@ extern "C" const char* w4a16_status_string(int status) {
     case W4A16_ERR_CUDA: return "W4A16_ERR_CUDA: CUDA launch or query failed";
     default: return "unknown w4a16 status";
   }
+}
+
+// ---- W4A8 (f4) ----
+extern "C" int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, w4a16_stream_t stream) {
+  if (!X || !Xq || !sx || !xsum) return W4A16_ERR_ARG;
+  if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128) return W4A16_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(Xq) & 3u) || (reinterpret_cast<uintptr_t>(X) & 1u)) return W4A16_ERR_ALIGN;
+  return w4a8_launch_quantize(X, M, K, Xq, sx, xsum, (cudaStream_t)stream);
+}
+
+extern "C" size_t w4a8_workspace_bytes(int M, int K, int N) {
+  if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128) return 0;
+  const int sms = num_sms_of_current_device();
+  return sms > 0 ? w4a8_workspace_bytes_sms(M, K, N, sms) : 0;
+}
+
+extern "C" int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K, int N,
+                         void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+  if (!Xq || !sx || !xsum || !packed || !Y || !workspace) return W4A16_ERR_ARG;
+  if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128 || N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(Xq) & 3u) || (reinterpret_cast<uintptr_t>(packed) & 3u) || (reinterpret_cast<uintptr_t>(Y) & 1u) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 3u))
+    return W4A16_ERR_ALIGN;
+  const int sms = num_sms_of_current_device();
+  if (sms <= 0) return W4A16_ERR_CUDA;
+  if (workspace_bytes < w4a8_workspace_bytes_sms(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+  return w4a8_launch_gemm(Xq, sx, xsum, packed, Y, M, K, N, workspace, sms, (cudaStream_t)stream);
 }

@@ -1,0 +1,188 @@
+// w4a8.cu — W4A8 variant (4-bit weights, 8-bit activations on INT8 tensor
+// cores, QQQ-style symmetric; reading R21 in DESIGN.md): per-token int8 activation quantisation and the
+// W4A8 GEMM on the SYM group-128 blob of w4a16_pack.
+//
+// GEMM: integer MMA `mma.sync.m16n8k32.row.col.s32.u8.s8.s32` with the weights' raw 4-bit codes q in [0,15]
+// as the unsigned A operand (swap-AB: 16 output columns x 32 k) and the int8 activations as B; per k-group
+// the exact int32 sum is corrected by -8 * sum(x_q) (precomputed per token and group), scaled by the
+// group's fp16 scale into an fp32 accumulator; the token scale and the fp16 rounding come last. First
+// correct version: one n-tile x k-range per CTA, code words read straight from global memory.
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "w4a16.h"
+
+namespace w4 {
+namespace a8 {
+
+constexpr int kTile = 128;      // n-tile rows = k-group
+constexpr int kTB = 8448;       // SYM unit bytes (8192 codes + 128 fp16 scales)
+constexpr int kWarps = 8;       // 16 output columns (tile rows) each
+
+// ---- activation quantisation: one CTA per token row ----
+__global__ void __launch_bounds__(256) quant_kernel(const __half* __restrict__ X, int K, int8_t* __restrict__ Xq,
+                                                    float* __restrict__ sx, int32_t* __restrict__ xsum) {
+  const int m = blockIdx.x;
+  const __half* xr = X + (size_t)m * K;
+  __shared__ float s_red[8];
+  float amax = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) amax = fmaxf(amax, fabsf(__half2float(xr[k])));
+  for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = s_red[0];
+  for (int w = 1; w < 8; ++w) amax = fmaxf(amax, s_red[w]);
+  const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
+  if (threadIdx.x == 0) sx[m] = __fdiv_rn(amax, 127.f);
+  // groups of 128: each warp takes whole groups, 4 values per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = warp; g < K / kTile; g += 8) {
+    int sum = 0;
+    char4 q4;
+    int8_t q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float v = rintf(__fmul_rn(__half2float(xr[g * kTile + lane * 4 + j]), inv));
+      v = fminf(fmaxf(v, -127.f), 127.f);
+      q[j] = (int8_t)(int)v;
+      sum += q[j];
+    }
+    q4.x = q[0]; q4.y = q[1]; q4.z = q[2]; q4.w = q[3];
+    *reinterpret_cast<char4*>(Xq + (size_t)m * K + g * kTile + lane * 4) = q4;
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) xsum[(size_t)m * (K / kTile) + g] = sum;
+  }
+}
+
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(sel));
+  return r;
+}
+// 8 codes of one 32-bit word (physical nibble slot (i%2)*4 + i/2 holds logical k offset i) -> bytes in
+// logical order: lo = k 0..3, hi = k 4..7 (values 0..15).
+__device__ __forceinline__ uint32_t codes_lo(uint32_t w) { return prmt((w & 0x000F000Fu) | ((w << 4) & 0x0F000F00u), 0x3120); }
+__device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
+  return prmt(((w >> 8) & 0x000F000Fu) | ((w >> 4) & 0x0F000F00u), 0x3120);
+}
+
+// ---- GEMM: CTA = (n-tile, k-split); warp w owns tile rows 16w..16w+15; NTB token blocks of 8 ----
+template <int NTB>
+__global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restrict__ Xq, const int32_t* __restrict__ xsum,
+                                                          const uint8_t* __restrict__ packed, float* __restrict__ part,
+                                                          int M, int K, int N, int g_per_split) {
+  const int t = blockIdx.x, split = blockIdx.y, Gk = K / kTile;
+  const int g0 = split * g_per_split, g1 = min(Gk, g0 + g_per_split);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, c4 = lane & 3;
+  const int r0 = warp * 16 + g8, r1 = r0 + 8;   // tile rows of this lane (A rows g / g+8)
+  float out[NTB][4];
+#pragma unroll
+  for (int tb = 0; tb < NTB; ++tb) out[tb][0] = out[tb][1] = out[tb][2] = out[tb][3] = 0.f;
+  for (int g = g0; g < g1; ++g) {
+    const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
+    int acc[NTB][4];
+#pragma unroll
+    for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0;
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {   // 32 k per MMA; chunk kb of each row = words 4kb..4kb+3
+      auto word = [&](int r, int wi) {
+        return __ldg(reinterpret_cast<const uint32_t*>(unit + r * 64 + ((kb ^ ((r >> 1) & 3)) << 4) + wi * 4));
+      };
+      // A fragment: a0 = row g k 4c..4c+3 (word c/2, half c%2), a1 = row g+8, a2/a3: k 16+4c.. (word 2+c/2)
+      const uint32_t w00 = word(r0, c4 >> 1), w01 = word(r0, 2 + (c4 >> 1));
+      const uint32_t w10 = word(r1, c4 >> 1), w11 = word(r1, 2 + (c4 >> 1));
+      const bool hi = c4 & 1;
+      const uint32_t a0 = hi ? codes_hi(w00) : codes_lo(w00), a2 = hi ? codes_hi(w01) : codes_lo(w01);
+      const uint32_t a1 = hi ? codes_hi(w10) : codes_lo(w10), a3 = hi ? codes_hi(w11) : codes_lo(w11);
+      const int kk = g * kTile + kb * 32;
+#pragma unroll
+      for (int tb = 0; tb < NTB; ++tb) {
+        const int m = tb * 8 + g8;   // B column g8 = token
+        uint32_t b0 = 0, b1 = 0;
+        if (m < M) {
+          const int8_t* xr = Xq + (size_t)m * K + kk;
+          b0 = __ldg(reinterpret_cast<const uint32_t*>(xr + 4 * c4));
+          b1 = __ldg(reinterpret_cast<const uint32_t*>(xr + 16 + 4 * c4));
+        }
+        mma_u8s8(acc[tb], a0, a1, a2, a3, b0, b1);
+      }
+    }
+    // group epilogue: D[row][col]: d0,d1 = (r0, tokens 2c, 2c+1), d2,d3 = (r1, same tokens)
+    const float s0 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r0));
+    const float s1 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r1));
+#pragma unroll
+    for (int tb = 0; tb < NTB; ++tb) {
+      const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
+      const int xs0 = m0 < M ? __ldg(xsum + (size_t)m0 * Gk + g) : 0;
+      const int xs1 = m1 < M ? __ldg(xsum + (size_t)m1 * Gk + g) : 0;
+      out[tb][0] = fmaf(s0, (float)(acc[tb][0] - 8 * xs0), out[tb][0]);
+      out[tb][1] = fmaf(s0, (float)(acc[tb][1] - 8 * xs1), out[tb][1]);
+      out[tb][2] = fmaf(s1, (float)(acc[tb][2] - 8 * xs0), out[tb][2]);
+      out[tb][3] = fmaf(s1, (float)(acc[tb][3] - 8 * xs1), out[tb][3]);
+    }
+  }
+  float* P = part + (size_t)split * M * N;
+  const int n0 = t * kTile + r0, n1 = t * kTile + r1;
+#pragma unroll
+  for (int tb = 0; tb < NTB; ++tb) {
+    const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
+    if (m0 < M) { P[(size_t)m0 * N + n0] = out[tb][0]; P[(size_t)m0 * N + n1] = out[tb][2]; }
+    if (m1 < M) { P[(size_t)m1 * N + n0] = out[tb][1]; P[(size_t)m1 * N + n1] = out[tb][3]; }
+  }
+}
+
+// Y[m][n] = fp16_rne(sx[m] * sum over splits in order of part[split][m][n])
+__global__ void finish_kernel(const float* __restrict__ part, const float* __restrict__ sx, __half* __restrict__ Y, int M, int N,
+                              int splits) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)M * N) return;
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) acc += part[(size_t)s * M * N + i];
+  Y[i] = __float2half_rn(sx[i / N] * acc);
+}
+
+inline int splits_for(int K, int N, int num_sms) {
+  const int Gk = K / kTile, tiles = N / kTile;
+  int s = (2 * num_sms + tiles - 1) / tiles;
+  return s < 1 ? 1 : (s > Gk ? Gk : s);
+}
+
+}  // namespace a8
+}  // namespace w4
+
+extern "C" size_t w4a8_workspace_bytes_sms(int M, int K, int N, int num_sms) {
+  return (size_t)w4::a8::splits_for(K, N, num_sms) * M * N * 4;
+}
+
+extern "C" int w4a8_launch_quantize(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, cudaStream_t stream) {
+  w4::a8::quant_kernel<<<M, 256, 0, stream>>>(reinterpret_cast<const __half*>(X), K, Xq, sx, xsum);
+  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+extern "C" int w4a8_launch_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M,
+                                int K, int N, void* ws, int num_sms, cudaStream_t stream) {
+  const int splits = w4::a8::splits_for(K, N, num_sms), Gk = K / w4::a8::kTile;
+  const int gps = (Gk + splits - 1) / splits;
+  const int used = (Gk + gps - 1) / gps;
+  float* part = reinterpret_cast<float*>(ws);
+  const dim3 grid(N / w4::a8::kTile, used);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(packed);
+  switch ((M + 7) / 8) {
+#define W4A8_CASE(T) \
+  case T: w4::a8::gemm_kernel<T><<<grid, w4::a8::kWarps * 32, 0, stream>>>(Xq, xsum, pk, part, M, K, N, gps); break;
+    W4A8_CASE(1) W4A8_CASE(2) W4A8_CASE(3) W4A8_CASE(4) W4A8_CASE(5) W4A8_CASE(6) W4A8_CASE(7) W4A8_CASE(8)
+#undef W4A8_CASE
+    default: return W4A16_ERR_SHAPE;
+  }
+  const size_t total = (size_t)M * N;
+  w4::a8::finish_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(part, sx, reinterpret_cast<__half*>(Y), M, N, used);
+  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}

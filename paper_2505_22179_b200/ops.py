@@ -376,3 +376,30 @@ class PeerGroup:
         if self._closer is not None:
             self._closer()
             self._closer = None
+
+
+# ---- W4A8 (include/w4a16.h) ----
+def w4a8_quantize_act(X, Xq, sx, xsum, stream=None):
+    """Per-token int8 activations: X fp16 [M, K] -> Xq int8 [M, K], sx fp32 [M], xsum int32 [M, K/128]."""
+    M, K = X.shape
+    if Xq.dtype != torch.int8 or sx.dtype != torch.float32 or xsum.dtype != torch.int32:
+        raise W4A16Error("w4a8_quantize_act: dtypes")
+    if tuple(Xq.shape) != (M, K) or sx.numel() < M or tuple(xsum.shape) != (M, K // 128):
+        raise W4A16Error("w4a8_quantize_act: shapes")
+    check(lib.w4a8_quantize_act(_ptr(X, torch.float16, "X"), M, K, Xq.data_ptr(), sx.data_ptr(), xsum.data_ptr(),
+                                _stream(stream)), "w4a8_quantize_act")
+
+
+def w4a8_workspace_bytes(M: int, K: int, N: int) -> int:
+    return int(lib.w4a8_workspace_bytes(M, K, N))
+
+
+def w4a8_gemm(Xq, sx, xsum, packed, Y, workspace, stream=None):
+    """Y [M, N] fp16 = W4A8 GEMM of the quantised activations with a SYM w4a16_pack blob (K x N)."""
+    M, K = Xq.shape
+    N = Y.shape[1]
+    if Xq.dtype != torch.int8 or Y.shape[0] != M:
+        raise W4A16Error("w4a8_gemm: shapes / dtypes")
+    check(lib.w4a8_gemm(Xq.data_ptr(), sx.data_ptr(), xsum.data_ptr(), _ptr(packed, None, "packed"),
+                        _ptr(Y, torch.float16, "Y"), M, K, N, workspace.data_ptr(),
+                        workspace.numel() * workspace.element_size(), _stream(stream)), "w4a8_gemm")
