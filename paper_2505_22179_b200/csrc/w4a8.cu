@@ -75,49 +75,70 @@ __device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
 }
 
 // ---- GEMM: CTA = (n-tile, k-split); warp w owns tile rows 16w..16w+15; NTB token blocks of 8 ----
+// Per unit (k-group) the CTA stages the M x 128 int8 activation slice in shared memory once (double
+// buffered, rows padded to 144 B so the 8 token rows of a B fragment hit distinct banks), and every thread
+// prefetches the next unit's 16 code words into registers while the current unit's MMAs run.
+constexpr int kXRow = 144;
 template <int NTB>
 __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restrict__ Xq, const int32_t* __restrict__ xsum,
                                                           const uint8_t* __restrict__ packed, float* __restrict__ part,
                                                           int M, int K, int N, int g_per_split) {
+  __shared__ __align__(16) uint8_t xs[2][NTB * 8][kXRow];
   const int t = blockIdx.x, split = blockIdx.y, Gk = K / kTile;
   const int g0 = split * g_per_split, g1 = min(Gk, g0 + g_per_split);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, c4 = lane & 3;
   const int r0 = warp * 16 + g8, r1 = r0 + 8;   // tile rows of this lane (A rows g / g+8)
+  const int sw0 = (r0 >> 1) & 3, sw1 = (r1 >> 1) & 3, wo = (c4 >> 1) * 4;
+  auto load_words = [&](int g, uint32_t (&w)[16]) {
+    const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      w[4 * kb + 0] = __ldg(reinterpret_cast<const uint32_t*>(unit + r0 * 64 + ((kb ^ sw0) << 4) + wo));
+      w[4 * kb + 1] = __ldg(reinterpret_cast<const uint32_t*>(unit + r0 * 64 + ((kb ^ sw0) << 4) + 8 + wo));
+      w[4 * kb + 2] = __ldg(reinterpret_cast<const uint32_t*>(unit + r1 * 64 + ((kb ^ sw1) << 4) + wo));
+      w[4 * kb + 3] = __ldg(reinterpret_cast<const uint32_t*>(unit + r1 * 64 + ((kb ^ sw1) << 4) + 8 + wo));
+    }
+  };
+  auto stage_x = [&](int g, int buf) {   // M x 128 bytes, 16 B per thread per pass
+    for (int i = threadIdx.x; i < M * 8; i += kWarps * 32) {
+      const int m = i >> 3, c = i & 7;
+      *reinterpret_cast<uint4*>(&xs[buf][m][c * 16]) = __ldg(reinterpret_cast<const uint4*>(Xq + (size_t)m * K + g * kTile) + c);
+    }
+  };
   float out[NTB][4];
 #pragma unroll
   for (int tb = 0; tb < NTB; ++tb) out[tb][0] = out[tb][1] = out[tb][2] = out[tb][3] = 0.f;
-  for (int g = g0; g < g1; ++g) {
+  // rows >= M of the staged slices stay zero
+  for (int i = threadIdx.x; i < 2 * NTB * 8 * kXRow / 16; i += kWarps * 32) reinterpret_cast<uint4*>(&xs[0][0][0])[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  uint32_t wn[16];
+  if (g0 < g1) { load_words(g0, wn); stage_x(g0, 0); }
+  __syncthreads();
+  const bool hi = c4 & 1;
+  for (int g = g0, buf = 0; g < g1; ++g, buf ^= 1) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = wn[i];
+    if (g + 1 < g1) { load_words(g + 1, wn); stage_x(g + 1, buf ^ 1); }
     const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
+    const float s0 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r0));
+    const float s1 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r1));
     int acc[NTB][4];
 #pragma unroll
     for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0;
 #pragma unroll
-    for (int kb = 0; kb < 4; ++kb) {   // 32 k per MMA; chunk kb of each row = words 4kb..4kb+3
-      auto word = [&](int r, int wi) {
-        return __ldg(reinterpret_cast<const uint32_t*>(unit + r * 64 + ((kb ^ ((r >> 1) & 3)) << 4) + wi * 4));
-      };
-      // A fragment: a0 = row g k 4c..4c+3 (word c/2, half c%2), a1 = row g+8, a2/a3: k 16+4c.. (word 2+c/2)
-      const uint32_t w00 = word(r0, c4 >> 1), w01 = word(r0, 2 + (c4 >> 1));
-      const uint32_t w10 = word(r1, c4 >> 1), w11 = word(r1, 2 + (c4 >> 1));
-      const bool hi = c4 & 1;
-      const uint32_t a0 = hi ? codes_hi(w00) : codes_lo(w00), a2 = hi ? codes_hi(w01) : codes_lo(w01);
-      const uint32_t a1 = hi ? codes_hi(w10) : codes_lo(w10), a3 = hi ? codes_hi(w11) : codes_lo(w11);
-      const int kk = g * kTile + kb * 32;
+    for (int kb = 0; kb < 4; ++kb) {   // 32 k per MMA
+      const uint32_t a0 = hi ? codes_hi(w[4 * kb + 0]) : codes_lo(w[4 * kb + 0]);
+      const uint32_t a2 = hi ? codes_hi(w[4 * kb + 1]) : codes_lo(w[4 * kb + 1]);
+      const uint32_t a1 = hi ? codes_hi(w[4 * kb + 2]) : codes_lo(w[4 * kb + 2]);
+      const uint32_t a3 = hi ? codes_hi(w[4 * kb + 3]) : codes_lo(w[4 * kb + 3]);
 #pragma unroll
       for (int tb = 0; tb < NTB; ++tb) {
-        const int m = tb * 8 + g8;   // B column g8 = token
-        uint32_t b0 = 0, b1 = 0;
-        if (m < M) {
-          const int8_t* xr = Xq + (size_t)m * K + kk;
-          b0 = __ldg(reinterpret_cast<const uint32_t*>(xr + 4 * c4));
-          b1 = __ldg(reinterpret_cast<const uint32_t*>(xr + 16 + 4 * c4));
-        }
-        mma_u8s8(acc[tb], a0, a1, a2, a3, b0, b1);
+        const uint8_t* xr = &xs[buf][tb * 8 + g8][kb * 32 + 4 * c4];
+        mma_u8s8(acc[tb], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(xr), *reinterpret_cast<const uint32_t*>(xr + 16));
       }
     }
     // group epilogue: D[row][col]: d0,d1 = (r0, tokens 2c, 2c+1), d2,d3 = (r1, same tokens)
-    const float s0 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r0));
-    const float s1 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r1));
 #pragma unroll
     for (int tb = 0; tb < NTB; ++tb) {
       const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
@@ -128,6 +149,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
       out[tb][2] = fmaf(s1, (float)(acc[tb][2] - 8 * xs0), out[tb][2]);
       out[tb][3] = fmaf(s1, (float)(acc[tb][3] - 8 * xs1), out[tb][3]);
     }
+    __syncthreads();   // buffer buf is refilled two units later; the next unit's slice is complete
   }
   float* P = part + (size_t)split * M * N;
   const int n0 = t * kTile + r0, n1 = t * kTile + r1;
