@@ -11,6 +11,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include "tma_host.cuh"
 #include "w4a16.h"
 
 namespace w4 {
@@ -75,51 +76,62 @@ __device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
 }
 
 // ---- GEMM: CTA = (n-tile, k-split); warp w owns tile rows 16w..16w+15; NTB token blocks of 8 ----
-// Per unit (k-group) the CTA stages the M x 128 int8 activation slice in shared memory once (double
-// buffered, rows padded to 144 B so the 8 token rows of a B fragment hit distinct banks), and every thread
-// prefetches the next unit's 16 code words into registers while the current unit's MMAs run.
+// A kStages-deep cp.async ring per CTA: each unit's 8 KB of code words (coalesced 16-byte copies by all
+// threads) and its M x 128 int8 activation slice (rows padded to 144 B so the 8 token rows of a B
+// fragment hit distinct banks); fragments are then read from shared memory.
 constexpr int kXRow = 144;
+constexpr int kStages = 4;
+template <int NTB>
+constexpr int smem_bytes() { return kStages * (8192 + NTB * 8 * kXRow); }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int NTB>
 __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restrict__ Xq, const int32_t* __restrict__ xsum,
                                                           const uint8_t* __restrict__ packed, float* __restrict__ part,
                                                           int M, int K, int N, int g_per_split) {
-  __shared__ __align__(16) uint8_t xs[2][NTB * 8][kXRow];
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* wsm = smem;                                   // [kStages][8192]
+  uint8_t* xsm = smem + kStages * 8192;                  // [kStages][NTB*8][kXRow]
   const int t = blockIdx.x, split = blockIdx.y, Gk = K / kTile;
   const int g0 = split * g_per_split, g1 = min(Gk, g0 + g_per_split);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, c4 = lane & 3;
   const int r0 = warp * 16 + g8, r1 = r0 + 8;   // tile rows of this lane (A rows g / g+8)
   const int sw0 = (r0 >> 1) & 3, sw1 = (r1 >> 1) & 3, wo = (c4 >> 1) * 4;
-  auto load_words = [&](int g, uint32_t (&w)[16]) {
+  // activation rows >= M stay zero
+  for (int i = threadIdx.x; i < kStages * NTB * 8 * kXRow / 16; i += kWarps * 32) reinterpret_cast<uint4*>(xsm)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  auto issue = [&](int g) {
+    const int st = (g - g0) % kStages;
     const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
-#pragma unroll
-    for (int kb = 0; kb < 4; ++kb) {
-      w[4 * kb + 0] = __ldg(reinterpret_cast<const uint32_t*>(unit + r0 * 64 + ((kb ^ sw0) << 4) + wo));
-      w[4 * kb + 1] = __ldg(reinterpret_cast<const uint32_t*>(unit + r0 * 64 + ((kb ^ sw0) << 4) + 8 + wo));
-      w[4 * kb + 2] = __ldg(reinterpret_cast<const uint32_t*>(unit + r1 * 64 + ((kb ^ sw1) << 4) + wo));
-      w[4 * kb + 3] = __ldg(reinterpret_cast<const uint32_t*>(unit + r1 * 64 + ((kb ^ sw1) << 4) + 8 + wo));
-    }
-  };
-  auto stage_x = [&](int g, int buf) {   // M x 128 bytes, 16 B per thread per pass
+    for (int i = threadIdx.x; i < 8192 / 16; i += kWarps * 32) cp_async16(wsm + st * 8192 + i * 16, unit + i * 16);
     for (int i = threadIdx.x; i < M * 8; i += kWarps * 32) {
       const int m = i >> 3, c = i & 7;
-      *reinterpret_cast<uint4*>(&xs[buf][m][c * 16]) = __ldg(reinterpret_cast<const uint4*>(Xq + (size_t)m * K + g * kTile) + c);
+      cp_async16(xsm + (st * NTB * 8 + m) * kXRow + c * 16, Xq + (size_t)m * K + g * kTile + c * 16);
     }
   };
   float out[NTB][4];
 #pragma unroll
   for (int tb = 0; tb < NTB; ++tb) out[tb][0] = out[tb][1] = out[tb][2] = out[tb][3] = 0.f;
-  // rows >= M of the staged slices stay zero
-  for (int i = threadIdx.x; i < 2 * NTB * 8 * kXRow / 16; i += kWarps * 32) reinterpret_cast<uint4*>(&xs[0][0][0])[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  uint32_t wn[16];
-  if (g0 < g1) { load_words(g0, wn); stage_x(g0, 0); }
-  __syncthreads();
-  const bool hi = c4 & 1;
-  for (int g = g0, buf = 0; g < g1; ++g, buf ^= 1) {
-    uint32_t w[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) w[i] = wn[i];
-    if (g + 1 < g1) { load_words(g + 1, wn); stage_x(g + 1, buf ^ 1); }
+  for (int i = 0; i < kStages - 1; ++i) {
+    if (g0 + i < g1) issue(g0 + i);
+    cp_commit();
+  }
+  const bool hi = c4 & 1;
+  for (int g = g0; g < g1; ++g) {
+    if (g + kStages - 1 < g1) issue(g + kStages - 1);
+    cp_commit();
+    cp_wait<kStages - 1>();
+    __syncthreads();
+    const int st = (g - g0) % kStages;
+    const uint8_t* wst = wsm + st * 8192;
+    const uint8_t* xst = xsm + st * NTB * 8 * kXRow;
     const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
     const float s0 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r0));
     const float s1 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r1));
@@ -128,13 +140,15 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
     for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0;
 #pragma unroll
     for (int kb = 0; kb < 4; ++kb) {   // 32 k per MMA
-      const uint32_t a0 = hi ? codes_hi(w[4 * kb + 0]) : codes_lo(w[4 * kb + 0]);
-      const uint32_t a2 = hi ? codes_hi(w[4 * kb + 1]) : codes_lo(w[4 * kb + 1]);
-      const uint32_t a1 = hi ? codes_hi(w[4 * kb + 2]) : codes_lo(w[4 * kb + 2]);
-      const uint32_t a3 = hi ? codes_hi(w[4 * kb + 3]) : codes_lo(w[4 * kb + 3]);
+      const uint32_t w0 = *reinterpret_cast<const uint32_t*>(wst + r0 * 64 + ((kb ^ sw0) << 4) + wo);
+      const uint32_t w1 = *reinterpret_cast<const uint32_t*>(wst + r0 * 64 + ((kb ^ sw0) << 4) + 8 + wo);
+      const uint32_t w2 = *reinterpret_cast<const uint32_t*>(wst + r1 * 64 + ((kb ^ sw1) << 4) + wo);
+      const uint32_t w3 = *reinterpret_cast<const uint32_t*>(wst + r1 * 64 + ((kb ^ sw1) << 4) + 8 + wo);
+      const uint32_t a0 = hi ? codes_hi(w0) : codes_lo(w0), a2 = hi ? codes_hi(w1) : codes_lo(w1);
+      const uint32_t a1 = hi ? codes_hi(w2) : codes_lo(w2), a3 = hi ? codes_hi(w3) : codes_lo(w3);
 #pragma unroll
       for (int tb = 0; tb < NTB; ++tb) {
-        const uint8_t* xr = &xs[buf][tb * 8 + g8][kb * 32 + 4 * c4];
+        const uint8_t* xr = xst + (tb * 8 + g8) * kXRow + kb * 32 + 4 * c4;
         mma_u8s8(acc[tb], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(xr), *reinterpret_cast<const uint32_t*>(xr + 16));
       }
     }
@@ -149,8 +163,9 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
       out[tb][2] = fmaf(s1, (float)(acc[tb][2] - 8 * xs0), out[tb][2]);
       out[tb][3] = fmaf(s1, (float)(acc[tb][3] - 8 * xs1), out[tb][3]);
     }
-    __syncthreads();   // buffer buf is refilled two units later; the next unit's slice is complete
+    __syncthreads();   // this stage is refilled by the next iteration's issue
   }
+  cp_wait<0>();
   float* P = part + (size_t)split * M * N;
   const int n0 = t * kTile + r0, n1 = t * kTile + r1;
 #pragma unroll
@@ -172,9 +187,16 @@ __global__ void finish_kernel(const float* __restrict__ part, const float* __res
 }
 
 inline int splits_for(int K, int N, int num_sms) {
-  const int Gk = K / kTile, tiles = N / kTile;
-  int s = (2 * num_sms + tiles - 1) / tiles;
-  return s < 1 ? 1 : (s > Gk ? Gk : s);
+  // k-splits that fill the resident CTA slots (2 per SM) in whole waves best, each split >= 4 units
+  const int Gk = K / kTile, tiles = N / kTile, slots = 2 * num_sms;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 16 && sp * 4 <= Gk; ++sp) {
+    const double waves = (double)tiles * sp / slots;
+    const double eff = waves / (double)((tiles * sp + slots - 1) / slots);
+    if (eff > best_eff + 1e-3) { best_eff = eff; best = sp; }
+  }
+  return best;
 }
 
 }  // namespace a8
@@ -198,8 +220,13 @@ extern "C" int w4a8_launch_gemm(const int8_t* Xq, const float* sx, const int32_t
   const dim3 grid(N / w4::a8::kTile, used);
   const uint8_t* pk = reinterpret_cast<const uint8_t*>(packed);
   switch ((M + 7) / 8) {
-#define W4A8_CASE(T) \
-  case T: w4::a8::gemm_kernel<T><<<grid, w4::a8::kWarps * 32, 0, stream>>>(Xq, xsum, pk, part, M, K, N, gps); break;
+#define W4A8_CASE(T)                                                                                         \
+  case T: {                                                                                                  \
+    static unsigned long long attr_set = 0;                                                                  \
+    if (!w4::ensure_smem_attr(w4::a8::gemm_kernel<T>, w4::a8::smem_bytes<T>(), attr_set)) return W4A16_ERR_CUDA; \
+    w4::a8::gemm_kernel<T><<<grid, w4::a8::kWarps * 32, w4::a8::smem_bytes<T>(), stream>>>(Xq, xsum, pk, part, M, K, N, gps); \
+    break;                                                                                                   \
+  }
     W4A8_CASE(1) W4A8_CASE(2) W4A8_CASE(3) W4A8_CASE(4) W4A8_CASE(5) W4A8_CASE(6) W4A8_CASE(7) W4A8_CASE(8)
 #undef W4A8_CASE
     default: return W4A16_ERR_SHAPE;
