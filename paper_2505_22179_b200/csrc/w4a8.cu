@@ -82,10 +82,13 @@ __device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
 constexpr int kXRow = 144;
 constexpr int kStages = 4;
 template <int NTB>
-constexpr int smem_bytes() { return kStages * (8192 + NTB * 8 * kXRow); }
+constexpr int smem_bytes() { return kStages * (kTB + NTB * 8 * kXRow + NTB * 8 * 4); }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -96,8 +99,9 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
                                                           const uint8_t* __restrict__ packed, float* __restrict__ part,
                                                           int M, int K, int N, int g_per_split) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* wsm = smem;                                   // [kStages][8192]
-  uint8_t* xsm = smem + kStages * 8192;                  // [kStages][NTB*8][kXRow]
+  uint8_t* wsm = smem;                                   // [kStages][kTB]: code words + fp16 scales
+  uint8_t* xsm = smem + kStages * kTB;                   // [kStages][NTB*8][kXRow]
+  int* ssm = reinterpret_cast<int*>(xsm + kStages * NTB * 8 * kXRow);   // [kStages][NTB*8] group sums
   const int t = blockIdx.x, split = blockIdx.y, Gk = K / kTile;
   const int g0 = split * g_per_split, g1 = min(Gk, g0 + g_per_split);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, c4 = lane & 3;
@@ -109,7 +113,8 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
   auto issue = [&](int g) {
     const int st = (g - g0) % kStages;
     const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
-    for (int i = threadIdx.x; i < 8192 / 16; i += kWarps * 32) cp_async16(wsm + st * 8192 + i * 16, unit + i * 16);
+    for (int i = threadIdx.x; i < kTB / 16; i += kWarps * 32) cp_async16(wsm + st * kTB + i * 16, unit + i * 16);
+    for (int m = threadIdx.x; m < M; m += kWarps * 32) cp_async4(ssm + st * NTB * 8 + m, xsum + (size_t)m * Gk + g);
     for (int i = threadIdx.x; i < M * 8; i += kWarps * 32) {
       const int m = i >> 3, c = i & 7;
       cp_async16(xsm + (st * NTB * 8 + m) * kXRow + c * 16, Xq + (size_t)m * K + g * kTile + c * 16);
@@ -130,11 +135,11 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
     cp_wait<kStages - 1>();
     __syncthreads();
     const int st = (g - g0) % kStages;
-    const uint8_t* wst = wsm + st * 8192;
+    const uint8_t* wst = wsm + st * kTB;
     const uint8_t* xst = xsm + st * NTB * 8 * kXRow;
-    const uint8_t* unit = packed + ((size_t)t * Gk + g) * kTB;
-    const float s0 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r0));
-    const float s1 = __half2float(__ldg(reinterpret_cast<const __half*>(unit + 8192) + r1));
+    const int* sst = ssm + st * NTB * 8;
+    const float s0 = __half2float(reinterpret_cast<const __half*>(wst + 8192)[r0]);
+    const float s1 = __half2float(reinterpret_cast<const __half*>(wst + 8192)[r1]);
     int acc[NTB][4];
 #pragma unroll
     for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0;
@@ -156,8 +161,8 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
 #pragma unroll
     for (int tb = 0; tb < NTB; ++tb) {
       const int m0 = tb * 8 + 2 * c4, m1 = m0 + 1;
-      const int xs0 = m0 < M ? __ldg(xsum + (size_t)m0 * Gk + g) : 0;
-      const int xs1 = m1 < M ? __ldg(xsum + (size_t)m1 * Gk + g) : 0;
+      const int xs0 = m0 < M ? sst[m0] : 0;
+      const int xs1 = m1 < M ? sst[m1] : 0;
       out[tb][0] = fmaf(s0, (float)(acc[tb][0] - 8 * xs0), out[tb][0]);
       out[tb][1] = fmaf(s0, (float)(acc[tb][1] - 8 * xs1), out[tb][1]);
       out[tb][2] = fmaf(s1, (float)(acc[tb][2] - 8 * xs0), out[tb][2]);
