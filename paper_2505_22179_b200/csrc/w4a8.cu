@@ -191,9 +191,10 @@ __global__ void finish_kernel(const float* __restrict__ part, const float* __res
   Y[i] = __float2half_rn(sx[i / N] * acc);
 }
 
-inline int splits_for(int K, int N, int num_sms) {
-  // k-splits that fill the resident CTA slots (2 per SM) in whole waves best, each split >= 4 units
-  const int Gk = K / kTile, tiles = N / kTile, slots = 2 * num_sms;
+inline int splits_for(int M, int K, int N, int num_sms) {
+  // k-splits that fill the resident CTA slots in whole waves best, each split >= 4 units. Resident CTAs per
+  // SM from the kernels' register use (ptxas: ~60 registers up to 32 tokens -> 4 CTAs, ~120 above -> 2)
+  const int Gk = K / kTile, tiles = N / kTile, slots = (M <= 32 ? 4 : 2) * num_sms;
   int best = 1;
   double best_eff = 0.0;
   for (int sp = 1; sp <= 16 && sp * 4 <= Gk; ++sp) {
@@ -208,7 +209,7 @@ inline int splits_for(int K, int N, int num_sms) {
 }  // namespace w4
 
 extern "C" size_t w4a8_workspace_bytes_sms(int M, int K, int N, int num_sms) {
-  return (size_t)w4::a8::splits_for(K, N, num_sms) * M * N * 4;
+  return (size_t)w4::a8::splits_for(M, K, N, num_sms) * M * N * 4;
 }
 
 extern "C" int w4a8_launch_quantize(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, cudaStream_t stream) {
@@ -218,7 +219,7 @@ extern "C" int w4a8_launch_quantize(const uint16_t* X, int M, int K, int8_t* Xq,
 
 extern "C" int w4a8_launch_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M,
                                 int K, int N, void* ws, int num_sms, cudaStream_t stream) {
-  const int splits = w4::a8::splits_for(K, N, num_sms), Gk = K / w4::a8::kTile;
+  const int splits = w4::a8::splits_for(M, K, N, num_sms), Gk = K / w4::a8::kTile;
   const int gps = (Gk + splits - 1) / splits;
   const int used = (Gk + gps - 1) / gps;
   float* part = reinterpret_cast<float*>(ws);
