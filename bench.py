@@ -613,6 +613,40 @@ def main():
             log(f"in-chain ALLREDUCE (world 1): {ar['us_per_allreduce_op']:.2f} us per op")
         except Exception as e:   # never let the side measurement break the bench line
             ar = {"row": "f1", "error": repr(e)}
+    # per-token int8 quantisation + INT8-MMA GEMM on a SYM blob of the 70B gate-up shape at
+    # the headline width (the stack itself is W4A16; this is the variant's own kernel pair).
+    a8 = None
+    if args.lm_head and rank == 0 and world == 1:
+        try:
+            Ka, Na = dims.hidden, 2 * dims.ffn
+            Wa = torch.empty(Ka, Na, dtype=torch.float16, device=dev)
+            synth.gpu(args.seed, synth.tensor_id(0xFFC, 1, 0), synth.WEIGHT, Ka, Na, out=Wa)
+            pla = w4.pack_linear(Wa, mode=w4.W4A16_SYM)
+            del Wa
+            Xa = synth.gpu(args.seed, synth.tensor_id(0xFFC, 2, 0), synth.ACT, M, Ka)
+            Xqa = torch.empty(M, Ka, dtype=torch.int8, device=dev)
+            sxa = torch.empty(M, dtype=torch.float32, device=dev)
+            xsa = torch.empty(M, Ka // 128, dtype=torch.int32, device=dev)
+            wsa8 = torch.empty(w4.w4a8_workspace_bytes(M, Ka, Na), dtype=torch.uint8, device=dev)
+            Ya = torch.empty(M, Na, dtype=torch.float16, device=dev)
+            with torch.cuda.stream(stream):
+                w4.w4a8_quantize_act(Xa, Xqa, sxa, xsa, stream=stream)
+                w4.w4a8_gemm(Xqa, sxa, xsa, pla.packed, Ya, wsa8, stream=stream)
+            torch.cuda.synchronize()
+            g8a = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g8a, stream=stream):
+                for _ in range(10):
+                    w4.w4a8_quantize_act(Xa, Xqa, sxa, xsa, stream=stream)
+                    w4.w4a8_gemm(Xqa, sxa, xsa, pla.packed, Ya, wsa8, stream=stream)
+            ms8 = time_graph(g8a, 5, 2) / 10
+            wb8 = Ka * Na // 2 + (Ka // 128) * Na * 2
+            a8 = {"row": "f4", "shape": [M, Ka, Na], "mode": "SYM g128 weights, per-token int8 activations",
+                  "us": 1e3 * ms8, "TBps": wb8 / (ms8 * 1e-3) / 1e12, "frac_hbm": wb8 / (ms8 * 1e-3) / 1e9 / peak_gbs,
+                  "note": "quantise + GEMM per call; first version (DESIGN 5.10)"}
+            log(f"W4A8 gate-up M={M}: {1e3 * ms8:.1f} us ({a8['TBps']:.2f} TB/s)")
+            del g8a
+        except Exception as e:   # never let the side measurement break the bench line
+            a8 = {"row": "f4", "error": repr(e)}
     clk = clocks.stop() if clocks else None
 
     cpu = None
@@ -641,7 +675,7 @@ def main():
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
-            "allreduce_in_chain": ar,
+            "allreduce_in_chain": ar, "w4a8_gemm": a8,
             "other_configs": other_configs,
             "e2e": {"value": bytes_all_ranks / (ms_e2e * 1e-3) / 1e12, "unit": "TB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": stack.h2d_bytes(M), "d2h_bytes_per_step": stack.d2h_bytes(M),
