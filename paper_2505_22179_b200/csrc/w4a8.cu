@@ -81,6 +81,9 @@ __device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
 // fragment hit distinct banks); fragments are then read from shared memory.
 constexpr int kXRow = 144;
 constexpr int kStages = 4;
+#ifndef W4A8_MIN_UNITS
+#define W4A8_MIN_UNITS 8   // fewest k-groups per split (4: -7 % at M = 64, 16: +25 % at M <= 16)
+#endif
 template <int NTB>
 constexpr int smem_bytes() { return kStages * (kTB + NTB * 8 * kXRow + NTB * 8 * 4); }
 
@@ -197,7 +200,7 @@ inline int splits_for(int M, int K, int N, int num_sms) {
   const int Gk = K / kTile, tiles = N / kTile, slots = (M <= 32 ? 4 : 2) * num_sms;
   int best = 1;
   double best_eff = 0.0;
-  for (int sp = 1; sp <= 16 && sp * 4 <= Gk; ++sp) {
+  for (int sp = 1; sp <= 16 && sp * W4A8_MIN_UNITS <= Gk; ++sp) {
     const double waves = (double)tiles * sp / slots;
     const double eff = waves / (double)((tiles * sp + slots - 1) / slots);
     if (eff > best_eff + 1e-3) { best_eff = eff; best = sp; }
