@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
     if (g0 + i < g1) issue(g0 + i);
     cp_commit();
   }
-  const bool hi = c4 & 1;
+  const uint32_t sh = (c4 & 1) ? 8u : 0u;   // lanes with odd c4 take k 4..7 of each word
   for (int g = g0; g < g1; ++g) {
     if (g + kStages - 1 < g1) issue(g + kStages - 1);
     cp_commit();
@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
       const uint32_t w1 = *reinterpret_cast<const uint32_t*>(wst + r0 * 64 + ((kb ^ sw0) << 4) + 8 + wo);
       const uint32_t w2 = *reinterpret_cast<const uint32_t*>(wst + r1 * 64 + ((kb ^ sw1) << 4) + wo);
       const uint32_t w3 = *reinterpret_cast<const uint32_t*>(wst + r1 * 64 + ((kb ^ sw1) << 4) + 8 + wo);
-      const uint32_t a0 = hi ? codes_hi(w0) : codes_lo(w0), a2 = hi ? codes_hi(w1) : codes_lo(w1);
-      const uint32_t a1 = hi ? codes_hi(w2) : codes_lo(w2), a3 = hi ? codes_hi(w3) : codes_lo(w3);
+      // k 4..7 of a word are k 0..3 of the word shifted right by 8 (codes_hi(w) == codes_lo(w >> 8))
+      const uint32_t a0 = codes_lo(w0 >> sh), a2 = codes_lo(w1 >> sh);
+      const uint32_t a1 = codes_lo(w2 >> sh), a3 = codes_lo(w3 >> sh);
 #pragma unroll
       for (int tb = 0; tb < NTB; ++tb) {
         const uint8_t* xr = xst + (tb * 8 + g8) * kXRow + kb * 32 + 4 * c4;
