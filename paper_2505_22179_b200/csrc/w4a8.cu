@@ -80,7 +80,15 @@ __device__ __forceinline__ uint32_t codes_hi(uint32_t w) {
 // threads) and its M x 128 int8 activation slice (rows padded to 144 B so the 8 token rows of a B
 // fragment hit distinct banks); fragments are then read from shared memory.
 constexpr int kXRow = 144;
-constexpr int kStages = 4;
+#ifndef W4A8_STAGES
+#define W4A8_STAGES 4
+#endif
+constexpr int kStages = W4A8_STAGES;
+#ifndef W4A8_UPS
+#define W4A8_UPS 1   // units per CTA barrier (the ring holds kStages units, kStages / W4A8_UPS groups)
+#endif
+constexpr int kUps = W4A8_UPS;
+static_assert(kStages % kUps == 0 && kStages / kUps >= 2, "ring of at least two unit groups");
 #ifndef W4A8_MIN_UNITS
 #define W4A8_MIN_UNITS 8   // fewest k-groups per split (4: -7 % at M = 64, 16: +25 % at M <= 16)
 #endif
@@ -127,16 +135,22 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
 #pragma unroll
   for (int tb = 0; tb < NTB; ++tb) out[tb][0] = out[tb][1] = out[tb][2] = out[tb][3] = 0.f;
 #pragma unroll
-  for (int i = 0; i < kStages - 1; ++i) {
+  for (int i = 0; i < kStages - kUps; ++i) {
     if (g0 + i < g1) issue(g0 + i);
-    cp_commit();
+    if (i % kUps == kUps - 1) cp_commit();
   }
   const uint32_t sh = (c4 & 1) ? 8u : 0u;   // lanes with odd c4 take k 4..7 of each word
-  for (int g = g0; g < g1; ++g) {
-    if (g + kStages - 1 < g1) issue(g + kStages - 1);
+  for (int gb = g0; gb < g1; gb += kUps) {
+#pragma unroll
+    for (int i = 0; i < kUps; ++i)
+      if (gb + kStages - kUps + i < g1) issue(gb + kStages - kUps + i);
     cp_commit();
-    cp_wait<kStages - 1>();
+    cp_wait<kStages / kUps - 1>();
     __syncthreads();
+#pragma unroll
+    for (int ui = 0; ui < kUps; ++ui) {
+    const int g = gb + ui;
+    if (g >= g1) break;
     const int st = (g - g0) % kStages;
     const uint8_t* wst = wsm + st * kTB;
     const uint8_t* xst = xsm + st * NTB * 8 * kXRow;
@@ -172,7 +186,8 @@ __global__ void __launch_bounds__(kWarps * 32) gemm_kernel(const int8_t* __restr
       out[tb][2] = fmaf(s1, (float)(acc[tb][2] - 8 * xs0), out[tb][2]);
       out[tb][3] = fmaf(s1, (float)(acc[tb][3] - 8 * xs1), out[tb][3]);
     }
-    __syncthreads();   // this stage is refilled by the next iteration's issue
+    }
+    __syncthreads();   // these stages are refilled by the next iteration's issue
   }
   cp_wait<0>();
   float* P = part + (size_t)split * M * N;
