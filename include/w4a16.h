@@ -75,6 +75,9 @@ size_t w4a16_packed_bytes(int K, int N, int group, int mode);
  *   ASYM: wmin = min(min w, 0), wmax = max(max w, 0); equal -> (-1, 1); s = fp16_rne((wmax-wmin)/15);
  *         z = clamp(rne(-wmin/s), 0, 15); q = clamp(rne(w/s) + z, 0, 15)     (fp32 arithmetic, RNE)
  *   SYM:  amax = max|w| (0 -> 1); s = fp16_rne(2*amax/15); z = 8; q = clamp(rne(w/s) + 8, 0, 15)
+ *         This is the GPTQ / Marlin symmetric storage convention (codes 0..15 around z = 8, so w = -amax may
+ *         take code 0 = -8s; reading R1). It is NOT SPEC's symmetric scheme (s = amax/7, half-away rounding,
+ *         codes -7..7), which binds only SPEC's CPU program.
  *   A scale that underflows to 0 is recomputed from the range (-1, 1).
  * Output: `packed`, w4a16_packed_bytes(K, N, group, mode) bytes in the layout above.
  * Non-finite weights count as 0 and set *dev_status = W4A16_DEV_NONFINITE; otherwise *dev_status is
@@ -141,7 +144,9 @@ int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int M, int K, i
  * rows' own keys/values at L..L+M-1); parents: int32 [M] on the device, a valid tree (parents[0] = -1,
  * parents[i] < i; verify_accept reports malformed trees). O[m][h] = softmax_j(q.k_j / sqrt(D)) . v_j over the
  * visible rows j, kv head h / (Hq / Hkv) (GQA); fp32 scores / softmax / accumulation, fp16 probabilities and
- * output. D == 128, 1 <= M <= 64, Hq % Hkv == 0, L >= 0. workspace: w4a16_tree_attention_workspace_bytes(). */
+ * output. D == 128, 1 <= M <= 64, Hq % Hkv == 0, L >= 0. workspace: w4a16_tree_attention_workspace_bytes().
+ * A row m whose ancestry walk meets a parent outside [-1, m) (a malformed tree) sees the prefix and itself
+ * only; the walk never loops (each valid step strictly decreases the row index). */
 size_t w4a16_tree_attention_workspace_bytes(int M, int L, int Hq, int Hkv, int D);
 int w4a16_tree_attention(const uint16_t* Q, const uint16_t* Kc, const uint16_t* Vc, const int32_t* parents, int M,
                          int L, int Hq, int Hkv, int D, uint16_t* O, void* workspace, size_t workspace_bytes,
@@ -250,11 +255,12 @@ int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family
  *   amax = max_k |X[m][k]|; inv = 127 / amax (0 if amax == 0); Xq = clamp(rne(X * inv), -127, 127);
  *   sx[m] = amax / 127; xsum[m][g] = sum of Xq[m][k] over k-group g (128 k).
  *   X fp16 [M][K], Xq int8 [M][K], sx fp32 [M], xsum int32 [M][K/128]; K % 128 == 0, 1 <= M <= W4A16_MAX_M;
- *   all device pointers, Xq 4-byte aligned.
+ *   all device pointers; Xq 16-byte aligned, sx and xsum 4-byte aligned (else W4A16_ERR_ALIGN).
  * w4a8_gemm: Y[m][n] = fp16_rne(sx[m] * sum_g s[g][n] * (sum_{k in g} Xq[m][k] * q[k][n] - 8 * xsum[m][g]))
  *   on the SYM (z = 8) blob of w4a16_pack (K x N, group 128): int32-exact group sums (INT8 MMA), fp32 group
  *   scaling in k order, per-split partials summed in split order (deterministic). workspace: at least
- *   w4a8_workspace_bytes(M, K, N) bytes (scratch; no initialisation needed). */
+ *   w4a8_workspace_bytes(M, K, N) bytes (scratch; no initialisation needed). Xq, packed and workspace
+ *   16-byte aligned (16-byte copies), sx and xsum 4-byte aligned, else W4A16_ERR_ALIGN. */
 int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, w4a16_stream_t stream);
 size_t w4a8_workspace_bytes(int M, int K, int N);
 int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K, int N,

@@ -284,7 +284,9 @@ extern "C" const char* w4a16_status_string(int status) {
 extern "C" int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, w4a16_stream_t stream) {
   if (!X || !Xq || !sx || !xsum) return W4A16_ERR_ARG;
   if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128) return W4A16_ERR_SHAPE;
-  if ((reinterpret_cast<uintptr_t>(Xq) & 3u) || (reinterpret_cast<uintptr_t>(X) & 1u)) return W4A16_ERR_ALIGN;
+  if ((reinterpret_cast<uintptr_t>(Xq) & 15u) || (reinterpret_cast<uintptr_t>(X) & 1u) || (reinterpret_cast<uintptr_t>(sx) & 3u) ||
+      (reinterpret_cast<uintptr_t>(xsum) & 3u))
+    return W4A16_ERR_ALIGN;
   return w4a8_launch_quantize(X, M, K, Xq, sx, xsum, (cudaStream_t)stream);
 }
 
@@ -298,8 +300,10 @@ extern "C" int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum,
                          void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
   if (!Xq || !sx || !xsum || !packed || !Y || !workspace) return W4A16_ERR_ARG;
   if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128 || N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
-  if ((reinterpret_cast<uintptr_t>(Xq) & 3u) || (reinterpret_cast<uintptr_t>(packed) & 3u) || (reinterpret_cast<uintptr_t>(Y) & 1u) ||
-      (reinterpret_cast<uintptr_t>(workspace) & 3u))
+  // the GEMM streams Xq and the blob with 16-byte cp.async copies: a smaller alignment would fault on the device
+  if ((reinterpret_cast<uintptr_t>(Xq) & 15u) || (reinterpret_cast<uintptr_t>(packed) & 15u) || (reinterpret_cast<uintptr_t>(Y) & 1u) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 15u) || (reinterpret_cast<uintptr_t>(sx) & 3u) ||
+      (reinterpret_cast<uintptr_t>(xsum) & 3u))
     return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;

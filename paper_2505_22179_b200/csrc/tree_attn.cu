@@ -82,8 +82,15 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
   if (tid < p.M) spar[tid] = p.parents[tid];
   __syncthreads();
   if (tid < p.M) {
-    unsigned long long a = 0;
-    for (int x = tid; x >= 0; x = spar[x]) a |= 1ull << x;
+    // A parent outside [-1, x) is invalid: such a row sees the prefix and itself only. Every step of a valid
+    // walk strictly decreases x, so the walk ends within M steps (no hang on a cyclic "tree").
+    unsigned long long a = 1ull << tid;
+    for (int x = tid; x >= 0;) {
+      const int px = spar[x];
+      if (px < -1 || px >= x) { a = 1ull << tid; break; }
+      if (px >= 0) a |= 1ull << px;
+      x = px;
+    }
     anc[tid] = a;
   }
   // Q block: row r -> (token m = r / G, head g*G + r % G)

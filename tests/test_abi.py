@@ -65,6 +65,14 @@ def test_host_validation_before_any_cuda_call():
     assert lib.verify_accept(A, A, A, 1025, A, None) == -2
     assert lib.verify_accept(None, A, A, 8, A, None) == -1
     assert lib.w4a16_gemm_workspace_bytes(8, 4000, 4096, 128) == 0
+    # W4A8: the GEMM reads Xq and the blob with 16-byte copies, so 4- or 8-byte alignment is rejected on the host
+    # w4a8_quantize_act(X, M, K, Xq, sx, xsum, stream); w4a8_gemm(Xq, sx, xsum, packed, Y, M, K, N, ws, ws_bytes, stream)
+    assert lib.w4a8_quantize_act(A, 8, 4096, A + 4, A, A, None) == -3
+    assert lib.w4a8_quantize_act(A, 8, 4096, A, A + 2, A, None) == -3
+    assert lib.w4a8_quantize_act(A, 8, 4096, A, A, A + 1, None) == -3
+    for xq, pk, sx, xs in ((A + 4, A, A, A), (A + 8, A, A, A), (A, A + 4, A, A), (A, A + 8, A, A), (A, A, A + 2, A),
+                           (A, A, A, A + 2)):
+        assert lib.w4a8_gemm(xq, sx, xs, pk, A, 8, 4096, 4096, A, 1 << 30, None) == -3
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")

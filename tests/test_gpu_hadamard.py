@@ -75,8 +75,15 @@ def test_rotated_w4a16_gemm_end_to_end():
     ws = w4.alloc_workspace(M, [(K, N)])
     pl(Xr, Y, ws)
     torch.cuda.synchronize()
+    # the oracle's own rotation of the HOST activations (fp64, one rounding) feeds the oracle GEMM; the GPU's
+    # rotated activations must agree with it to <= 1 fp16 ulp (test_hadamard_vs_oracle), and a 1-ulp input
+    # difference moves Y by <= 2^-11 * sum_k |x_k w_k|, far inside the GEMM tolerance
+    xr_ref = oracle.hadamard(X, B)
+    xr16 = np.array([oracle.double_to_half(v) for v in xr_ref.ravel()], dtype=np.uint16).reshape(xr_ref.shape)
+    d = _half_ulp_diff(Xr.view(torch.int16).cpu().numpy().view(np.uint16), xr16)
+    assert d.max() <= 1
     qw, sc, ze, _ = oracle.quantize(HW16.view(np.uint16))
-    ref = oracle.gemm(Xr.view(torch.int16).cpu().numpy().view(np.uint16), qw, sc, ze)
+    ref = oracle.gemm(xr16, qw, sc, ze)
     y = Y.float().cpu().numpy().astype(np.float64)
     assert np.all(np.abs(y - ref) <= 1e-2 * (1 + np.abs(ref)))
     # against the unrotated exact product: only 4-bit quantisation noise remains (round-to-nearest over 16

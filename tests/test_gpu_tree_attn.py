@@ -98,3 +98,36 @@ def test_kv_compact_bit_exact_after_gpu_accept():
     Kr, Vr = oracle.kv_compact(K, V, L, oracle.accept(tok, par, am)[4])
     assert np.array_equal(Kd.cpu().numpy().view(np.uint16), Kr.view(np.uint16))
     assert np.array_equal(Vd.cpu().numpy().view(np.uint16), Vr.view(np.uint16))
+
+
+@pytest.mark.timeout(60)
+def test_tree_attention_malformed_parents_do_not_hang():
+    # a cycle (3 -> 5 -> 3), a self-loop (6 -> 6) and an out-of-range parent (9 -> 40 >= M): the kernel must
+    # finish, and a row whose ancestry walk meets an invalid link sees the prefix and itself only
+    # (include/w4a16.h) — which the oracle computes for parents[row] = -1
+    M, L, Hq, Hkv = 12, 50, 8, 2
+    Q, K, V = _inputs(77, M, L, Hq, Hkv)
+    par = np.arange(-1, M - 1, dtype=np.int32)
+    par[3], par[5], par[6], par[9] = 5, 3, 6, 40
+    par[10] = 9                                   # valid link into an invalid row: invalid too
+    got = _gpu_attn(Q, K, V, par)
+
+    def walk_ok(x):
+        while x >= 0:
+            px = int(par[x])
+            if px < -1 or px >= x:
+                return False
+            x = px
+        return True
+
+    bad = [x for x in range(M) if not walk_ok(x)]
+    assert bad == [3, 4, 5, 6, 7, 8, 9, 10, 11]
+    # valid rows 0..2 (a chain): the oracle on that sub-tree (their keys sit at L..L+2)
+    ref = oracle.tree_attention(Q[:3], K[:L + 3], V[:L + 3], par[:3])
+    assert np.all(np.abs(got[:3] - ref) <= TOL * (1 + np.abs(ref)))
+    # each invalid row: the oracle on a one-row problem over the prefix plus that row's own key / value
+    for x in bad:
+        Kx = np.concatenate([K[:L], K[L + x:L + x + 1]])
+        Vx = np.concatenate([V[:L], V[L + x:L + x + 1]])
+        ref = oracle.tree_attention(Q[x:x + 1], Kx, Vx, np.array([-1], dtype=np.int32))
+        assert np.all(np.abs(got[x:x + 1] - ref) <= TOL * (1 + np.abs(ref))), x

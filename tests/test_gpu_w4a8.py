@@ -58,8 +58,14 @@ def test_w4a8_gemm_vs_oracle(M, K, N):
     Y = torch.full((M, N), float("nan"), dtype=torch.float16, device="cuda")
     w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y, ws)
     torch.cuda.synchronize()
+    # the oracle quantises the HOST activations itself; the GPU's codes / scales / group sums must equal them
+    # bit for bit, and only the oracle's own values feed the oracle GEMM
+    q_ref, s_ref, xs_ref = oracle.quantize_act_int8(X.view(torch.int16).cpu().numpy().view(np.uint16))
+    assert np.array_equal(Xq.cpu().numpy(), q_ref)
+    assert np.array_equal(sx.cpu().numpy().view(np.uint32), s_ref.view(np.uint32))
+    assert np.array_equal(xs.cpu().numpy(), xs_ref)
     codes, sc, _, _ = oracle.quantize(W, 128, SYM)
-    ref = oracle.gemm_w4a8(Xq.cpu().numpy(), sx.cpu().numpy(), codes, sc)
+    ref = oracle.gemm_w4a8(q_ref, s_ref, codes, sc)
     y = Y.float().cpu().numpy().astype(np.float64)
     assert np.all(np.isfinite(y))
     assert np.all(np.abs(y - ref) <= 1e-3 * (1 + np.abs(ref))), np.abs(y - ref).max()

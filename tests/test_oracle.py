@@ -177,6 +177,49 @@ def test_pack_spec_example_sym():
     assert [float(x) for x in Wh[:4, 0]] == [float(x) for x in g["w_hat"][0]]
 
 
+def _f(vals):
+    return [float(x) for x in vals]
+
+
+def test_pack_rne_ties_golden_asym():
+    # reading R4 (round half to even, GPTQ torch.round): exact ties of the zero point -wmin/s = 2.5 and of
+    # the codes w/s = k + 0.5 (tests/golden/rne_ties.txt derives every value; half-away-from-zero fails it)
+    g = _read_golden("rne_ties.txt")
+    w = _f(g["asym_w"][0])
+    W = np.zeros((128, 2), dtype=np.float16)
+    W[: len(w), 1] = w
+    codes, sc, ze, st = oracle.quantize(W, mode=oracle.ASYM)
+    assert st == 0
+    assert int(sc[0, 1]) == int(g["asym_scale"][0][0], 16)
+    assert float(ze.view(np.float16)[0, 1]) == float(g["asym_zero"][0][0])
+    assert [int(c) for c in codes[: len(w), 1]] == [int(c) for c in g["asym_codes"][0]]
+    assert int(codes[len(w), 1]) == int(g["asym_codes"][0][-1])   # the padding zeros code to z
+    Wh = oracle.dequantize(codes, sc, ze, mode=oracle.ASYM).view(np.float16)
+    assert [float(x) for x in Wh[: len(w), 1]] == _f(g["asym_w_hat"][0])
+
+
+def test_pack_rne_ties_golden_sym():
+    g = _read_golden("rne_ties.txt")
+    w = _f(g["sym_w"][0])
+    W = np.zeros((128, 1), dtype=np.float16)
+    W[: len(w), 0] = w
+    codes, sc, ze, st = oracle.quantize(W, mode=oracle.SYM)
+    assert int(sc[0, 0]) == int(g["sym_scale"][0][0], 16)
+    assert [int(c) for c in codes[: len(w), 0]] == [int(c) for c in g["sym_codes"][0]]
+
+
+def test_w4a8_act_rne_ties_golden():
+    # reading R21: per-token int8 codes decided by RNE in fp32 (tests/golden/rne_ties.txt)
+    g = _read_golden("rne_ties.txt")
+    x = _f(g["act_x"][0])
+    X = np.zeros((1, 128), dtype=np.float16)
+    X[0, : len(x)] = x
+    Xq, sx, xs = oracle.quantize_act_int8(X)
+    assert float(sx[0]) == float(g["act_sx"][0][0])
+    assert [int(v) for v in Xq[0, : len(x)]] == [int(v) for v in g["act_q"][0]]
+    assert int(xs[0, 0]) == sum(int(v) for v in g["act_q"][0])
+
+
 @pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
 def test_pack_all_zero_group(mode):
     # reading R15 (GPTQ): an all-zero group gets the range (-1, 1): s = fp16(2/15), q = z = 8, w_hat = 0
