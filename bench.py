@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--mode", default="asym", choices=["asym", "sym"])
     ap.add_argument("--sweep", default="1,2,4,7,8,16,24,32,49,61,64", help="comma list of M for the M sweep ('' = none)")
     ap.add_argument("--sweep-steps", type=int, default=10)
+    ap.add_argument("--windows", type=int, default=3, help="timed windows of --steps replays; the headline is their median")
+    ap.add_argument("--sym-sweep", default="1,8,16,64", help="M sweep of the same stack in the paper's own GPTQ "
+                    "symmetric format (P:103; '' = none)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--allreduce", default="auto", choices=["auto", "nccl", "fused"],
                     help="tp > 1: ALLREDUCE ops inside one chain per forward over CUDA-IPC peer memory (fused, "
@@ -130,52 +133,113 @@ class ClockSampler:
 # CPU baseline: the oracle as it stands, on a bounded sample of the workload
 # --------------------------------------------------------------------------------------------------
 _SAMPLE = {}
+SHAPES_70B = {"qkv": (8192, 10240), "o": (8192, 8192), "gate_up": (8192, 57344), "down": (28672, 8192)}
 
 
-def oracle_sample(M, seed, repeats=1):
-    """Time oracle.gemm (+ oracle.accept) on a slice of one 70B layer: the O projection restricted to
-    1024 output columns (K=8192, N=1024) at width M. Returns (TB/s of weight bytes, seconds, sample text)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _slice_inputs(K, N, M, seed):
+    """Oracle inputs for a K x N W4A16 GEMM at width M, built once (untimed, like the GPU arm's resident
+    inputs): codes uniform in [0, 15], per-group fp16 scales / zeros, seeded activations. The oracle's cost
+    does not depend on the values, so the codes come from numpy instead of quantising generated weights."""
     import numpy as np
 
-    import oracle
     import synth
-    K, N = 8192, 1024
-    key = (M, seed)
-    if key not in _SAMPLE:  # inputs are built once (untimed), like the GPU arm's resident inputs
-        W = synth.host(seed, 9001, synth.WEIGHT, K, N)
-        X = synth.host(seed, 9002, synth.ACT, M, K)
-        qw, sc, ze, _ = oracle.quantize(W)
-        rng = np.random.default_rng(seed)
-        tok, par = synth.eagle_tree(rng, max(M - 1, 0), 6)
-        am = synth.target_argmax_for(rng, tok, par, 0.7)
-        _SAMPLE[key] = (X, qw, sc, ze, tok, par, am)
-    X, qw, sc, ze, tok, par, am = _SAMPLE[key]
-    threads = os.cpu_count() or 1
+    key = (K, N, M, seed)
+    if key not in _SAMPLE:
+        rng = np.random.default_rng(seed + K + 7 * N)
+        codes = rng.integers(0, 16, size=(K, N), dtype=np.uint8)
+        sc = np.full((K // 128, N), np.float16(0.0023).view(np.uint16), dtype=np.uint16)
+        ze = rng.integers(0, 16, size=(K // 128, N)).astype(np.float16).view(np.uint16)
+        X = synth.host(seed, 9002 + K, synth.ACT, M, K)
+        _SAMPLE[key] = (X, codes, sc, ze)
+    return _SAMPLE[key]
+
+
+def _tree(M, seed):
+    import numpy as np
+
+    import synth
+    rng = np.random.default_rng(seed)
+    tok, par = synth.eagle_tree(rng, max(M - 1, 0), 6)
+    return tok, par, synth.target_argmax_for(rng, tok, par, 0.7)
+
+
+def oracle_layer_slice(M, seed, den=64, threads=None):
+    """Time the oracle on one Llama-3-70B decoder layer restricted to 1/den of every matrix's output columns
+    (QKV, O, gate-up, down) at width M, plus oracle.accept on an M-node tree. Returns (TB/s of the slice's
+    W4 weight bytes, seconds, sample text, threads). The per-column cost is uniform, so this is the layer's
+    throughput on this host."""
+    import oracle
+    threads = threads or (os.cpu_count() or 1)
+    ins = [(_slice_inputs(K, N // den, M, seed), K, N // den) for K, N in SHAPES_70B.values()]
+    tok, par, am = _tree(M, seed)
     t0 = time.perf_counter()
-    for _ in range(repeats):
-        oracle.gemm(X, qw, sc, ze, nthreads=threads)
-        oracle.accept(tok, par, am)
-    dt = (time.perf_counter() - t0) / repeats
-    wbytes = K * N // 2 + (K // 128) * N * 4
-    sample = (f"oracle.gemm fp64 on a 70B O-projection slice K=8192 N=1024 ({wbytes / 1e6:.2f} MB of W4 weights) "
-              f"at M={M} + oracle.accept on a {M}-node tree, {threads} threads")
+    for (X, c, sc, ze), K, N in ins:
+        oracle.gemm(X, c, sc, ze, nthreads=threads)
+    oracle.accept(tok, par, am)
+    dt = time.perf_counter() - t0
+    wbytes = sum(K * N // 2 + (K // 128) * N * 4 for _, K, N in ins)
+    sample = (f"oracle.gemm (fp64) on one Llama-3-70B layer restricted to 1/{den} of each matrix's output columns "
+              f"({wbytes / 1e6:.2f} MB of W4 weights) at M={M} + oracle.accept on a {M}-node tree, {threads} threads")
     return wbytes / dt / 1e12, dt, sample, threads
 
 
+def cpu_baseline_plan(M_head, seed):
+    """BASELINE.md's CPU-baseline plan: config 1 on 1 thread and on all host threads; one 70B
+    layer at M in {1, M_head, 64} on all threads (timed on a column slice, per-column cost uniform),
+    extrapolated x80 to the stack and labelled so; the CPU model string."""
+    import oracle
+    threads = os.cpu_count() or 1
+    out = {"cpu_model": cpu_model(), "nproc": threads}
+    X, c, sc, ze = _slice_inputs(4096, 4096, 8, seed)
+    tok8 = [100, 11, 12, 21, 22, 23, 31, 32]
+    par8 = [-1, 0, 0, 1, 1, 2, 3, 5]
+    am8 = [12, 99, 23, 31, 99, 32, 99, 40]
+    c1 = {}
+    for th in sorted({1, threads}):
+        t0 = time.perf_counter()
+        oracle.gemm(X, c, sc, ze, nthreads=th)
+        oracle.accept(tok8, par8, am8)
+        c1[f"threads_{th}"] = {"s": time.perf_counter() - t0}
+    wb1 = 4096 * 4096 // 2 + 32 * 4096 * 4
+    for v in c1.values():
+        v["TBps"] = wb1 / v["s"] / 1e12
+    out["config1_gemm4096_M8_plus_accept8"] = c1
+    layer = {}
+    for M in sorted({1, M_head, 64}):
+        v, dt, sample, th = oracle_layer_slice(M, seed, den=32, threads=threads)
+        per_layer = dt * 32
+        layer[str(M)] = {"TBps": v, "s_per_layer": per_layer, "s_per_80_layer_forward_extrapolated": 80 * per_layer,
+                         "timed_on": "1/32 of every matrix's output columns (x32 for the layer, x80 for the stack)"}
+    out["llama3_70b_layer"] = layer
+    return out
+
+
 def run_reference(args):
+    """--impl reference: the task's reference arm for this tier = the oracle as it stands on the host cores,
+    each step a bounded sample of the same workload (one 70B layer on 1/64 of its columns at width M)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     M = args.M
     for _ in range(args.warmup):
-        oracle_sample(M, args.seed)
-    times, v = [], None
+        oracle_layer_slice(M, args.seed)
+    times, wbytes, sample, threads = [], None, "", 1
     for _ in range(args.steps):
-        v, dt, sample, threads = oracle_sample(M, args.seed)
+        v, dt, sample, threads = oracle_layer_slice(M, args.seed)
         times.append(dt)
+        wbytes = v * dt * 1e12
     tot = sum(times)
-    K, N = 8192, 1024
-    wbytes = K * N // 2 + (K // 128) * N * 4
     value = wbytes * len(times) / tot / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": args.gpus,
@@ -185,7 +249,8 @@ def run_reference(args):
                                f"SiLU*mul, down) + verify_accept; BASELINE configs 3-4", "M": M, "layers": 80, "tp": args.gpus,
                    "parallelism": f"tp{args.gpus}",
                    "timing": "the oracle on a bounded sample of this workload (see cpu_baseline.sample), host cores"},
-        "cpu_baseline": {"value": value, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -229,12 +294,14 @@ def main():
     def make_weight(l, name, K, N, out):
         synth.gpu(args.seed, synth.tensor_id(l, mat_id[name], rank), synth.WEIGHT, K, N, out=out)
 
-    def build(allreduce):
+    def build(allreduce, mode=mode):
+        # weights scaled at build time (powers of two) so every GEMM output keeps O(1) RMS along the forward's
+        # data flow (tp.py: the norms are outside the hot path); the same calibration input on every rank
+        x0 = synth.gpu(args.seed, synth.tensor_id(0xFFF, 9, 0), synth.ACT, 8, dims.hidden)
         st = tp.VerifyStack(dims, n_layers, M_max, make_weight, tp_size=world, tp_rank=rank, group=group, mode=mode,
-                            device=dev, allreduce=allreduce)
-        # activations (seeded, in HBM) and a draft tree of the headline width
-        for name, buf, tid in (("x_qkv", st.x_qkv, 1), ("x_o", st.x_o, 2), ("x_mlp", st.x_mlp, 3)):
-            synth.gpu(args.seed, synth.tensor_id(0xFFF, tid, rank), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+                            device=dev, allreduce=allreduce, calibrate=x0)
+        # the forward's input hidden state (seeded, in HBM, identical on every rank) and a draft tree
+        synth.gpu(args.seed, synth.tensor_id(0xFFF, 1, 0), synth.ACT, st.x_in.shape[0], st.x_in.shape[1], out=st.x_in)
         rng = np.random.default_rng(args.seed)
         tok, par = synth.eagle_tree(rng, M_max - 1, 6)
         am = synth.target_argmax_for(rng, tok, par, 0.7)
@@ -297,26 +364,34 @@ def main():
 
     stream = torch.cuda.Stream(dev)
 
-    def time_graph(g, steps, warmup):
+    def time_graph(g, steps, warmup, windows=1):
+        """ms per step: `windows` timed windows of exactly `steps` replays each (barrier + synchronize on both
+        sides, CUDA events on the launching stream, max over ranks); the median window is returned."""
         with torch.cuda.stream(stream):
             for _ in range(warmup):
                 g.replay()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(steps):
-                g.replay()
-            e1.record(stream)
-        barrier()
-        return max_over_ranks(e0.elapsed_time(e1)) / steps  # ms per step
+        res = []
+        for _ in range(windows):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(steps):
+                    g.replay()
+                e1.record(stream)
+            barrier()
+            res.append(max_over_ranks(e0.elapsed_time(e1)) / steps)
+        time_graph.windows = res
+        return statistics.median(res)
 
     clocks = ClockSampler(local) if rank == 0 else None
     bytes_all_ranks = stack.weight_bytes * world  # shards partition the model: == full model bytes
     gH = stack.capture(args.M)
     log(f"captured M={args.M}")
-    ms = time_graph(gH, args.steps, args.warmup)
-    log(f"headline M={args.M}: {ms:.3f} ms/step")
+    ms = time_graph(gH, args.steps, args.warmup, windows=args.windows)
+    windows_ms = list(time_graph.windows)
+    log(f"headline M={args.M}: {ms:.3f} ms/step (median of {args.windows} windows: "
+        + ", ".join(f"{w:.3f}" for w in windows_ms) + ")")
     # per-step distribution (SURVEY 8(d): median and p10/p90 over replays), events around every replay
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with torch.cuda.stream(stream):
@@ -345,6 +420,23 @@ def main():
         ratio_64 = m_sweep["64"]["ms_per_forward"] / m_sweep["1"]["ms_per_forward"]
     else:
         ratio_64 = None
+    # the same stack in the paper's own weight format, GPTQ symmetric g128 (z = 8, no zero bytes)
+    sym_sweep = None
+    sym_ms = [int(x) for x in args.sym_sweep.split(",") if x.strip()] if args.mode == "asym" else []
+    if sym_ms:
+        try:
+            st_sym = build("nccl", mode=w4.W4A16_SYM)
+            bs = st_sym.weight_bytes * world
+            sym_sweep = {"weight_bytes_per_step": bs, "format": "GPTQ symmetric g128 (z = 8): 0.515625 B/weight"}
+            for M in sym_ms:
+                msM = time_graph(st_sym.capture(M), args.sweep_steps, 3)
+                sym_sweep[str(M)] = {"ms_per_forward": msM, "TBps": bs / (msM * 1e-3) / 1e12,
+                                     "frac_hbm": bs / (msM * 1e-3) / 1e9 / (hbm_peak()[0] * world)}
+                log(f"SYM sweep M={M}: {msM:.3f} ms/forward")
+            del st_sym
+            torch.cuda.empty_cache()
+        except Exception as e:   # never let the side measurement break the bench line
+            sym_sweep = {"error": repr(e)}
     hier = {}
     for k, (M, tau, cite) in TAU.items():
         if str(M) in m_sweep:
@@ -353,8 +445,7 @@ def main():
     # e2e through the public API: pinned host inputs -> device -> forward -> accept result + hidden -> host
     M = args.M
     pin = dict(pin_memory=True)
-    host_in = {"x_qkv": stack.x_qkv.cpu().pin_memory(), "x_o": stack.x_o.cpu().pin_memory(),
-               "x_mlp": stack.x_mlp.cpu().pin_memory(), "tokens": stack.tokens.cpu().pin_memory(),
+    host_in = {"x_in": stack.x_in.cpu().pin_memory(), "tokens": stack.tokens.cpu().pin_memory(),
                "parents": stack.parents.cpu().pin_memory(), "argmax": stack.argmax.cpu().pin_memory()}
     host_out = {"accept": torch.empty(3 + M_max, dtype=torch.int32, **pin),
                 "y": torch.empty(M_max, stack.y_down.shape[1], dtype=torch.float16, **pin)}
@@ -380,7 +471,7 @@ def main():
         P = stack.plan
         for name in tp.MATRICES:
             s = P[name]
-            xin = {"qkv": stack.x_qkv, "o": stack.x_o, "gate_up": stack.x_mlp, "down": stack.act}[name][:M]
+            xin = {"qkv": stack.x_in, "o": stack.x_o, "gate_up": stack.y_o_red, "down": stack.act}[name][:M]
             yout = {"qkv": stack.y_qkv, "o": stack.y_o, "gate_up": stack.y_gu, "down": stack.y_down}[name][:M]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):
@@ -505,9 +596,9 @@ def main():
         def make8(l, name, K, N, out):
             synth.gpu(args.seed, synth.tensor_id(l, mat_id[name], 0xEE), synth.WEIGHT, K, N, out=out)
 
-        st8 = tp.VerifyStack(d8, d8.layers, 64, make8, device=dev)
-        for buf, tid in ((st8.x_qkv, 1), (st8.x_o, 2), (st8.x_mlp, 3)):
-            synth.gpu(args.seed, synth.tensor_id(0xFFB, tid, 0), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+        st8 = tp.VerifyStack(d8, d8.layers, 64, make8, device=dev,
+                             calibrate=synth.gpu(args.seed, synth.tensor_id(0xFFB, 9, 0), synth.ACT, 8, d8.hidden))
+        synth.gpu(args.seed, synth.tensor_id(0xFFB, 1, 0), synth.ACT, 64, d8.hidden, out=st8.x_in)
         sw8 = {}
         for M8 in (1, 4, 8, 16, 32, 64):
             g8 = st8.capture(M8)
@@ -590,11 +681,13 @@ def main():
             P_o, P_d = g1.alloc(M, Hd), g1.alloc(M, Hd)
             r_o, r_d = (torch.empty(M, Hd, dtype=torch.float16, device=dev) for _ in range(2))
             plain, fused = [], []
-            for L in stack.layers[:nl]:
-                qa, qb = stack._layer_ops(L, M)
+            for l, L in enumerate(stack.layers[:nl]):
+                qa, qb = stack._layer_ops(L, M, l)
                 plain += qa + qb
-                fused += [qa[0], ("gemm", stack.x_o[:M], L["o"], P_o), ("allreduce", P_o, r_o, g1),
-                          qb[0], qb[1], ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
+                h = stack.x_in[:M] if l == 0 else r_d
+                fused += [("gemm", h, L["qkv"], stack.y_qkv[:M]), ("gemm", stack.q_part(M), L["o"], P_o),
+                          ("allreduce", P_o, r_o, g1), ("gemm", r_o, L["gate_up"], stack.y_gu[:M]), qb[1],
+                          ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
             t_ch = {}
             for name, ops in (("plain", plain), ("allreduce", fused)):
                 ch = w4.Chain(ops, M)
@@ -651,29 +744,43 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, sample, threads = oracle_sample(M, args.seed)
-        reps = max(1, min(500, int(10.0 / max(dt, 1e-3))))
-        v, dt, sample, threads = oracle_sample(M, args.seed, repeats=reps)
-        cpu = {"value": v, "unit": "TB/s", "cores": threads, "kind": "oracle",
-               "sample": sample + f", mean of {reps} runs ({dt:.2f} s each)"}
+        v, dt, sample, threads = oracle_layer_slice(M, args.seed)
+        reps = max(1, min(50, int(6.0 / max(dt, 1e-3))))
+        ts = [oracle_layer_slice(M, args.seed)[1] for _ in range(reps)]
+        dt = statistics.median(ts)
+        wb = sum(K * (N // 64) // 2 + (K // 128) * (N // 64) * 4 for K, N in SHAPES_70B.values())
+        cpu = {"value": wb / dt / 1e12, "unit": "TB/s", "cores": threads, "kind": "oracle",
+               "sample": sample + f", median of {reps} runs ({dt:.2f} s each)", "cpu_model": cpu_model()}
+        log(f"cpu baseline (oracle, headline M): {cpu['value'] * 1e3:.3f} GB/s")
+        try:
+            cpu["plan"] = cpu_baseline_plan(M, args.seed)
+            log("cpu baseline plan: " + json.dumps(cpu["plan"]))
+        except Exception as e:   # never let the side measurement break the bench line
+            cpu["plan"] = {"error": repr(e)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16",
-            "data": "synthetic (seeded counter-based generator: N(0,0.018^2) weights with 2% x8 outlier groups, "
-                    "N(0,1.15^2) activations with 4 x16 outlier channels; EAGLE-2-shaped draft tree)",
+            "data": "synthetic (seeded counter-based generator: N(0,0.018^2) weights with 2% x8 outlier groups, each "
+                    "matrix scaled once by a power of two so its output RMS stays in [0.7, 1.4] along the data flow "
+                    "(stand-in for the excluded norms); N(0,1.15^2) input activations with 4 x16 outlier channels; "
+                    "EAGLE-2-shaped draft tree)",
             "config": {"workload": f"{dims.name} W4A16 g128 {args.mode} verify forward: {n_layers} decoder layers "
-                                   f"(QKV, O, gate-up, SiLU*mul, down) + verify_accept; BASELINE configs 3-4",
+                                   f"(QKV -> O -> gate-up -> SiLU*mul -> down -> next layer, each GEMM reading the "
+                                   f"previous one's output; attention/norms out of scope) + verify_accept; "
+                                   f"BASELINE configs 3-4",
                        "M": args.M, "layers": n_layers, "tp": world, "parallelism": f"tp{world}",
                        "allreduce": allreduce_used,
                        "weight_bytes_per_step": bytes_all_ranks,
                        "l2": f"{bytes_all_ranks / 1e9:.1f} GB of weights per step >> 126 MB L2 (no flush needed)",
-                       "timing": "CUDA graph replay, CUDA events on the launching stream, max over ranks"},
+                       "timing": f"CUDA graph replay, CUDA events on the launching stream, max over ranks; headline = median of "
+                                 f"{args.windows} windows of {args.steps} steps"},
             "us_per_layer": 1e3 * ms / n_layers, "ms_per_step_distribution": step_dist,
             "frac_hbm": value * 1e3 / (peak_gbs * world),
             "m_sweep": m_sweep, "ratio_M64_over_M1": ratio_64, "hierarchical_us_per_token": hier,
+            "m_sweep_sym": sym_sweep, "headline_windows_ms": windows_ms,
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu, "lm_head_argmax": lm, "tree_attention": attn,
             "allreduce_in_chain": ar, "w4a8_gemm": a8,
             "other_configs": other_configs,

@@ -192,6 +192,8 @@ typedef struct {
   void* Y;             /* GEMM: Y [M][N] fp16.  SILU_MUL: out [M][N] fp16.  ALLREDUCE: out [M][N] fp16 */
   int K, N;            /* GEMM: as w4a16_gemm.  SILU_MUL: K = 2N, N = F (N % 8 == 0).  ALLREDUCE: K = N, N % 8 == 0 */
   int mode;            /* GEMM: W4A16_ASYM or W4A16_SYM; every GEMM of a chain uses the same mode */
+  int ldx;             /* GEMM: row stride of X in elements; 0 = K (contiguous), else ldx >= K and ldx % 8 == 0
+                        * (e.g. the first K columns of a wider [M][ldx] buffer). Other kinds: 0 */
 } w4a16_op;
 
 /* ---- Tensor-parallel all-reduce inside a chain ------------------------------

@@ -61,7 +61,7 @@ W4A16_MAX_PEERS = 8
 class W4A16Op(ctypes.Structure):
     """struct w4a16_op of include/w4a16.h."""
     _fields_ = [("kind", ctypes.c_int), ("X", ctypes.c_void_p), ("packed", ctypes.c_void_p), ("Y", ctypes.c_void_p),
-                ("K", ctypes.c_int), ("N", ctypes.c_int), ("mode", ctypes.c_int)]
+                ("K", ctypes.c_int), ("N", ctypes.c_int), ("mode", ctypes.c_int), ("ldx", ctypes.c_int)]
 
 
 class W4A16PeerGroup(ctypes.Structure):

@@ -948,9 +948,10 @@ int chain_family(int M, int family) {
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 struct Span { uintptr_t a, b; };
 bool overlaps(Span x, Span y) { return x.a < y.b && y.a < x.b; }
-Span x_span(const w4a16_op& o, int M) {
+int ldx_of(const w4a16_op& o) { return o.kind == W4A16_OP_GEMM && o.ldx > 0 ? o.ldx : o.K; }
+Span x_span(const w4a16_op& o, int M) {   // rows of X with their row stride (gaps between rows included)
   const uintptr_t a = reinterpret_cast<uintptr_t>(o.X);
-  return {a, a + (size_t)M * (size_t)o.K * 2};
+  return {a, a + ((size_t)(M - 1) * (size_t)ldx_of(o) + (size_t)o.K) * 2};
 }
 Span y_span(const w4a16_op& o, int M) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(o.Y);
@@ -973,6 +974,7 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
       *mode = o.mode;
       if (!al16(o.packed)) return W4A16_ERR_ALIGN;
       if (o.K <= 0 || o.N <= 0 || o.K % 128 || o.N % 128 || o.N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
+      if (o.ldx != 0 && (o.ldx < o.K || o.ldx % 8)) return W4A16_ERR_SHAPE;
       if ((long long)(o.K / 128) * (o.N / 128) < G) return W4A16_ERR_SHAPE;   // every CTA owns >= 1 unit
       t += o.N / 128;
     } else if (o.kind == W4A16_OP_SILU_MUL) {
@@ -1062,8 +1064,8 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
       J.cnt_off = cnt;
       cnt += o.N / 128;
       const uint16_t* X = reinterpret_cast<const uint16_t*>(o.X);
-      if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, depth)) return e;
-      if (int e = w4::encode_x_sw128(&J.xmap1, X, M, o.K, mpad, 2)) return e;
+      if (int e = w4::encode_x_sw128(&J.xmapR, X, M, o.K, mpad, depth, ldx_of(o))) return e;
+      if (int e = w4::encode_x_sw128(&J.xmap1, X, M, o.K, mpad, 2, ldx_of(o))) return e;
     } else if (o.kind == W4A16_OP_ALLREDUCE) {
       const w4a16_peer_group* g = reinterpret_cast<const w4a16_peer_group*>(o.packed);
       const size_t off = reinterpret_cast<uintptr_t>(o.X) - reinterpret_cast<uintptr_t>(g->base[g->rank]);

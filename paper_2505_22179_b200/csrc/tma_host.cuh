@@ -23,11 +23,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // X [M][K] fp16 viewed as 3-D (64 k-in-box, M rows, K/64 boxes) with box (64, mpad, depth) and 128B swizzle:
 // one TMA lands `depth` consecutive 64-k boxes as [box][row][128 B] = back-to-back K-major SW128 atoms
 // (16-byte chunk j of row m stored at chunk position j ^ (m % 8)); rows >= M are zero-filled.
-inline int encode_x_sw128(CUtensorMap* map, const uint16_t* X, int M, int K, int mpad, int depth) {
+// ldx: row stride of X in elements (0 = K; else >= K and a multiple of 8 so rows stay 16-byte aligned).
+inline int encode_x_sw128(CUtensorMap* map, const uint16_t* X, int M, int K, int mpad, int depth, int ldx = 0) {
   auto enc = get_encode();
   if (!enc) return W4A16_ERR_CUDA;
   const cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
-  const cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+  const cuuint64_t strides[2] = {(cuuint64_t)(ldx > 0 ? ldx : K) * 2, 128};
   const cuuint32_t box[3] = {64, (cuuint32_t)mpad, (cuuint32_t)depth};
   const cuuint32_t estr[3] = {1, 1, 1};
   if (enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(X), dims, strides, box, estr,

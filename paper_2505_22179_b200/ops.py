@@ -38,6 +38,20 @@ def _ptr(t: Optional[torch.Tensor], dtype=None, name="tensor") -> Optional[int]:
     return t.data_ptr()
 
 
+def _ptr_rows(t: torch.Tensor, name="tensor") -> int:
+    """Pointer of a 2-D fp16 CUDA tensor whose rows are contiguous (a column slice of a wider buffer allowed)."""
+    if not t.is_cuda:
+        raise W4A16Error(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float16 or t.dim() != 2 or t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+        raise W4A16Error(f"{name} must be a row-major fp16 [M, K] view")
+    return t.data_ptr()
+
+
+def _ldx(t: torch.Tensor) -> int:
+    """Row stride of X for w4a16_op.ldx: 0 when contiguous."""
+    return 0 if t.is_contiguous() or t.shape[0] == 1 else int(t.stride(0))
+
+
 def w4a16_packed_bytes(K: int, N: int, mode=W4A16_ASYM, group=W4A16_GROUP) -> int:
     n = int(lib.w4a16_packed_bytes(K, N, group, mode))
     if n == 0:
@@ -212,8 +226,8 @@ class Chain:
                 _, X, pl, Y = op
                 if X.shape[0] != M or Y.shape[0] != M or X.shape[1] != pl.K or Y.shape[1] != pl.N:
                     raise W4A16Error(f"chain op {i}: shapes do not match M={M}, K={pl.K}, N={pl.N}")
-                arr[i] = W4A16Op(W4A16_OP_GEMM, _ptr(X, torch.float16, "X"), _ptr(pl.packed, None, "packed"),
-                                 _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode)
+                arr[i] = W4A16Op(W4A16_OP_GEMM, _ptr_rows(X, "X"), _ptr(pl.packed, None, "packed"),
+                                 _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode, _ldx(X))
                 mode = pl.mode
                 self._keep += [X, pl.packed, Y]
             elif op[0] == "allreduce":

@@ -6,11 +6,19 @@ One process per GPU. Megatron-style partition of each Llama decoder layer's line
     columns, stored locally as [gate_r | up_r] so w4a16_silu_mul pairs them);
   * row-parallel (split K): O (rank's heads) and down (rank's FFN slice); each rank produces a partial
     Y[M, hidden] that an all-reduce (NCCL over NVLink/NVSwitch, via torch.distributed) sums.
-Attention, norms and residual adds are outside the hot path: each layer's QKV, O and
-gate-up inputs are caller-provided activation buffers of their real shapes; gate-up -> SiLU*mul -> down is
-chained as in the model. Every compute step is a libw4a16.so kernel; torch supplies memory, streams,
-CUDA graphs and the process group.
+Data flow of one verify forward (the dependencies of a real decoder stack: the target
+verifies the draft "in one forward pass"):
+  h_0 = x_in;  per layer l:  qkv = h_l . W_qkv;  o = qkv[:, :K_o] . W_o  (the attention stub: the rank's query
+  columns stand in for the attention output, whose kernel is SURVEY §8(f) f2 and outside the timed stack);
+  [all-reduce];  gu = o . W_gu;  act = silu(gate) * up;  h_{l+1} = act . W_down  [all-reduce].
+Attention, norms and residual adds are outside the hot path. So every GEMM reads what the previous one
+wrote: QKV -> O -> gate-up -> SiLU*mul -> down -> QKV of the next layer (read-after-write edges, which a
+persistent chain must honour). Because the norms are absent, `calibrate=True` rescales each synthetic weight
+once at build time by a power of two so that its output has RMS in [1/sqrt(2), sqrt(2)] on the actual data flow (a stand-in for RMSNorm that keeps
+activations O(1) through 80 layers). Every compute step is a libw4a16.so kernel; torch supplies memory,
+streams, CUDA graphs and the process group.
 """
+import math
 from dataclasses import dataclass
 from typing import Callable, List, Optional
 
@@ -96,9 +104,12 @@ class VerifyStack:
 
     def __init__(self, dims: ModelDims, n_layers: int, M_max: int, make_weight: Callable, tp_size: int = 1,
                  tp_rank: int = 0, group=None, mode: int = W4A16_ASYM, device=None, allreduce: str = "nccl",
-                 peer_group: Optional[PeerGroup] = None, chain_sms: Optional[int] = None):
+                 peer_group: Optional[PeerGroup] = None, chain_sms: Optional[int] = None,
+                 calibrate: Optional[torch.Tensor] = None):
         """allreduce: "nccl" or "fused" (tp > 1). peer_group / chain_sms: tests only — a PeerGroup.simulated
-        rank and the SM share of its chains, to run several ranks side by side on one GPU."""
+        rank and the SM share of its chains, to run several ranks side by side on one GPU.
+        calibrate: optional [Mc, hidden] fp16 input; each weight is scaled once (before packing) so that its
+        GEMM output on the forward's data flow from that input has unit RMS (module docstring)."""
         if allreduce not in ("nccl", "fused"):
             raise ValueError(f"allreduce={allreduce!r}")
         self.d, self.n_layers, self.M_max = dims, n_layers, M_max
@@ -111,6 +122,8 @@ class VerifyStack:
         tmp = torch.empty(biggest, dtype=torch.float16, device=self.device)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.layers: List[dict] = []
+        self.calib_scale: List[dict] = []
+        cal = None if calibrate is None else _Calibration(self, calibrate)
         for l in range(n_layers):
             mats = {}
             for name in MATRICES:
@@ -118,16 +131,17 @@ class VerifyStack:
                 W = tmp[: s["K"] * s["N"]].view(s["K"], s["N"])
                 make_weight(l, name, s["K"], s["N"], W)
                 mats[name] = pack_linear(W, mode=mode, dev_status=self.status)
+                if cal is not None:
+                    mats[name] = cal.step(l, name, W, mats[name])
             self.layers.append(mats)
-        del tmp
+        del tmp, cal
         torch.cuda.synchronize(self.device)
         f16 = dict(dtype=torch.float16, device=self.device)
         P = self.plan
-        # activation inputs (caller fills) and per-layer scratch outputs
-        self.x_qkv = torch.zeros(M_max, P["qkv"]["K"], **f16)
-        self.x_o = torch.zeros(M_max, P["o"]["K"], **f16)
-        self.x_mlp = torch.zeros(M_max, P["gate_up"]["K"], **f16)
-        self.y_qkv = torch.empty(M_max, P["qkv"]["N"], **f16)
+        # the forward's input hidden state (caller fills) and per-layer scratch outputs (module docstring)
+        self.x_in = torch.zeros(M_max, P["qkv"]["K"], **f16)
+        self.y_qkv = torch.zeros(M_max, P["qkv"]["N"], **f16)
+        self.x_o = torch.zeros(M_max, P["o"]["K"], **f16)   # op-by-op path only: contiguous copy of qkv[:, :K_o]
         self.y_gu = torch.empty(M_max, P["gate_up"]["N"], **f16)
         self.act = torch.empty(M_max, P["down"]["K"], **f16)
         if self.fused:
@@ -142,8 +156,8 @@ class VerifyStack:
             self.y_down_red = torch.empty(M_max, P["down"]["N"], **f16)
         else:
             self.peers = None
-            self.y_o = torch.empty(M_max, P["o"]["N"], **f16)
-            self.y_down = torch.empty(M_max, P["down"]["N"], **f16)
+            self.y_o = torch.zeros(M_max, P["o"]["N"], **f16)
+            self.y_down = torch.zeros(M_max, P["down"]["N"], **f16)
             self.y_o_red, self.y_down_red = self.y_o, self.y_down   # NCCL reduces in place
         i32 = dict(dtype=torch.int32, device=self.device)
         self.tokens = torch.zeros(M_max, **i32)
@@ -164,11 +178,19 @@ class VerifyStack:
         if self.t > 1:
             dist.all_reduce(y, group=self.group)
 
-    def _layer_ops(self, L, M):
+    def layer_input(self, l: int, M: int) -> torch.Tensor:
+        """h_l: the QKV input of layer l (x_in for layer 0, else the previous layer's reduced down output)."""
+        return self.x_in[:M] if l == 0 else self.y_down_red[:M]
+
+    def q_part(self, M: int) -> torch.Tensor:
+        """The attention stub: the rank's query columns of the QKV output (a strided [M, K_o] view)."""
+        return self.y_qkv[:M, : self.plan["o"]["K"]]
+
+    def _layer_ops(self, L, M, l=0):
         """The layer's ops between its all-reduces: [QKV, O] and [gate-up, SiLU*mul, down]; with the fused
         all-reduce each segment ends with its ALLREDUCE op (partial in the peer region -> reduced output)."""
-        a = [("gemm", self.x_qkv[:M], L["qkv"], self.y_qkv[:M]), ("gemm", self.x_o[:M], L["o"], self.y_o[:M])]
-        b = [("gemm", self.x_mlp[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
+        a = [("gemm", self.layer_input(l, M), L["qkv"], self.y_qkv[:M]), ("gemm", self.q_part(M), L["o"], self.y_o[:M])]
+        b = [("gemm", self.y_o_red[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
              ("gemm", self.act[:M], L["down"], self.y_down[:M])]
         if self.fused:
             a.append(("allreduce", self.y_o[:M], self.y_o_red[:M], self.peers))
@@ -184,7 +206,7 @@ class VerifyStack:
                 self._chains[M] = None
                 return None
             try:
-                segs = [self._layer_ops(L, M) for L in self.layers]
+                segs = [self._layer_ops(L, M, l) for l, L in enumerate(self.layers)]
                 if self.t == 1 or self.fused:   # the whole forward in one launch
                     self._chains[M] = [Chain([op for a, b in segs for op in a + b], M, device=self.device,
                                              sms=self.chain_sms)]
@@ -216,13 +238,14 @@ class VerifyStack:
         # op by op (M > 16, or chains off): NCCL all-reduces; with the fused layout the partial is first
         # copied to the reduced buffer (the ALLREDUCE op exists only inside chains)
         o_out, d_out = (self.y_o_red[:M], self.y_down_red[:M]) if self.fused else (self.y_o[:M], self.y_down[:M])
-        for L in self.layers:
-            L["qkv"](self.x_qkv[:M], self.y_qkv[:M], ws, stream)
+        for l, L in enumerate(self.layers):
+            L["qkv"](self.layer_input(l, M), self.y_qkv[:M], ws, stream)
+            self.x_o[:M].copy_(self.q_part(M))   # single GEMMs take contiguous X (chains read the strided view)
             L["o"](self.x_o[:M], self.y_o[:M], ws, stream)
             if self.fused:
                 o_out.copy_(self.y_o[:M])
             self._allreduce(o_out)
-            L["gate_up"](self.x_mlp[:M], self.y_gu[:M], ws, stream)
+            L["gate_up"](o_out, self.y_gu[:M], ws, stream)
             w4a16_silu_mul(self.y_gu[:M], self.act[:M], stream)
             L["down"](self.act[:M], self.y_down[:M], ws, stream)
             if self.fused:
@@ -263,9 +286,7 @@ class VerifyStack:
     def verify_host(self, M: int, host_in: dict, host_out: dict, graph: Optional[torch.cuda.CUDAGraph] = None):
         """End-to-end step through the public API: pinned host inputs -> device, forward (graph replay if
         given), accepted length / path / last hidden state -> pinned host. Async on the current stream."""
-        self.x_qkv[:M].copy_(host_in["x_qkv"][:M], non_blocking=True)
-        self.x_o[:M].copy_(host_in["x_o"][:M], non_blocking=True)
-        self.x_mlp[:M].copy_(host_in["x_mlp"][:M], non_blocking=True)
+        self.x_in[:M].copy_(host_in["x_in"][:M], non_blocking=True)
         self.tokens[:M].copy_(host_in["tokens"][:M], non_blocking=True)
         self.parents[:M].copy_(host_in["parents"][:M], non_blocking=True)
         self.argmax[:M].copy_(host_in["argmax"][:M], non_blocking=True)
@@ -277,7 +298,60 @@ class VerifyStack:
         host_out["y"][:M].copy_(self.y_down_red[:M], non_blocking=True)
 
     def h2d_bytes(self, M: int) -> int:
-        return 2 * M * (self.x_qkv.shape[1] + self.x_o.shape[1] + self.x_mlp.shape[1]) + 3 * 4 * M
+        return 2 * M * self.x_in.shape[1] + 3 * 4 * M
 
     def d2h_bytes(self, M: int) -> int:
         return 4 * (3 + M) + 2 * M * self.y_down_red.shape[1]
+
+
+class _Calibration:
+    """Build-time weight scaling of VerifyStack(calibrate=x0): runs the forward's data flow op by op from x0
+    through the layers as they are built (libw4a16 kernels; torch only for the RMS reduction and the scalar
+    multiply) and scales each weight by 1 / RMS of its output before packing it for good."""
+
+    def __init__(self, st: "VerifyStack", x0: torch.Tensor):
+        self.st = st
+        self.M = x0.shape[0]
+        P = st.plan
+        self.ws = alloc_workspace(self.M, [(s["K"], s["N"]) for s in P.values()], device=st.device)
+        self.h = x0.to(st.device).contiguous().clone()
+        self.q = self.o = self.act = None
+
+    def _rms(self, y: torch.Tensor, column_parallel: bool) -> float:
+        st = self.st
+        if st.t > 1 and not column_parallel:      # row-parallel: the model's output is the reduced sum
+            dist.all_reduce(y, group=st.group)
+        ss = torch.stack([(y.float() ** 2).sum(), torch.tensor(float(y.numel()), device=y.device)])
+        if st.t > 1 and column_parallel:          # column shards: RMS over the full output
+            dist.all_reduce(ss, group=st.group)
+        return float((ss[0] / ss[1]).sqrt().item())
+
+    def step(self, l: int, name: str, W: torch.Tensor, pl):
+        st, M = self.st, self.M
+        X = {"qkv": self.h, "o": self.q, "gate_up": self.o, "down": self.act}[name]
+        y = torch.empty(M, pl.N, dtype=torch.float16, device=st.device)
+        col = name in ("qkv", "gate_up")
+        pl(X, y, self.ws)
+        r = self._rms(y, col)
+        # a power of two: the scaled fp16 weight is exact (reproducible bit for bit on the host) and the
+        # output RMS lands in [1/sqrt(2), sqrt(2)] — each op is calibrated on its actual input, so it does
+        # not compound over the layers
+        alpha = 2.0 ** round(-math.log2(r)) if r > 0 and math.isfinite(r) else 1.0
+        W.mul_(alpha)
+        pl = pack_linear(W, mode=st.mode, dev_status=st.status)
+        pl(X, y, self.ws)
+        if not col and st.t > 1:
+            dist.all_reduce(y, group=st.group)
+        while len(st.calib_scale) <= l:
+            st.calib_scale.append({})
+        st.calib_scale[l][name] = alpha
+        if name == "qkv":
+            self.q = y[:, : st.plan["o"]["K"]].contiguous()
+        elif name == "o":
+            self.o = y
+        elif name == "gate_up":
+            self.act = torch.empty(M, st.plan["down"]["K"], dtype=torch.float16, device=st.device)
+            w4a16_silu_mul(y, self.act)
+        else:
+            self.h = y
+        return pl

@@ -72,25 +72,50 @@ def test_llama70b_tp8_shard_shapes_sym():
         _check_shape(s["K"], s["N"], [8, 49], tid=900 + i, mode=1)
 
 
+def _h16(y64):
+    """fp64 -> fp16 RNE (numpy's conversion; the oracle's own conversion is pinned against it)."""
+    return y64.astype(np.float16).view(np.uint16)
+
+
+def _oracle_stack(Wq, x_in_u16, layers, K_o, M):
+    """The verify forward's data flow (tp.py module docstring) on the ORACLE only, from the host input: each
+    GEMM output rounded to fp16 as the GPU stores it; SiLU*mul glue in fp64. Returns the last layer's buffers."""
+    h = x_in_u16
+    out = {}
+    for l in range(layers):
+        g = lambda name, X: oracle.gemm(X, *Wq[(l, name)], nthreads=NPROC)
+        out["qkv"] = g("qkv", h)
+        q = np.ascontiguousarray(_h16(out["qkv"])[:, :K_o])
+        out["o"] = g("o", q)
+        out["gate_up"] = g("gate_up", _h16(out["o"]))
+        gu = _h16(out["gate_up"]).view(np.float16).astype(np.float64)
+        F = gu.shape[1] // 2
+        out["act"] = gu[:, :F] / (1.0 + np.exp(-gu[:, :F])) * gu[:, F:]
+        out["down"] = g("down", _h16(out["act"]))
+        h = _h16(out["down"])
+    return out
+
+
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("dims,layers,chains", [((1024, 2048, 8, 2), 1, True), ((2560, 4096, 20, 4), 2, True),
                                                 ((2560, 4096, 20, 4), 2, False)])
 def test_verify_stack_against_oracle(dims, layers, chains):
     # tiny model: per-op launches (too few units for a chain); small model: the whole stack as one
-    # persistent chain, and the same stack op by op. Buffers hold the last layer's values.
+    # persistent chain, and the same stack op by op. The oracle runs the same data flow from the host input
+    # (QKV -> O on the query columns -> gate-up -> SiLU*mul -> down -> next layer); buffers hold the last layer.
     from paper_2505_22179_b200 import tp
     d = tp.ModelDims("tiny", hidden=dims[0], ffn=dims[1], n_q=dims[2], n_kv=dims[3], head=128, layers=layers)
-    Wh = {}
+    Wq = {}
 
     def make_weight(l, name, K, N, out):
         synth.gpu(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
-        Wh[name] = synth.host(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
+        c, s_, z, _ = oracle.quantize(synth.host(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N))
+        Wq[(l, name)] = (c, s_, z)
 
     M = 13
     st = tp.VerifyStack(d, layers, 16, make_weight)
     st.use_chains = chains
-    for j, buf in enumerate((st.x_qkv, st.x_o, st.x_mlp)):
-        synth.gpu(22, j, synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+    synth.gpu(22, 0, synth.ACT, 16, d.hidden, out=st.x_in)
     rng = np.random.default_rng(3)
     tok, par = synth.eagle_tree(rng, M - 1, 5)
     am = synth.target_argmax_for(rng, tok, par, 0.8)
@@ -100,24 +125,12 @@ def test_verify_stack_against_oracle(dims, layers, chains):
     torch.cuda.synchronize()
     if chains and dims[0] == 2560:
         assert st.chains(M) is not None
-
-    def ref(name, X_u16):
-        c, s_, z, _ = oracle.quantize(Wh[name])
-        return oracle.gemm(X_u16, c, s_, z, nthreads=NPROC)
-
-    for name, xin, yout in (("qkv", st.x_qkv, st.y_qkv), ("o", st.x_o, st.y_o), ("gate_up", st.x_mlp, st.y_gu)):
-        r = ref(name, _to_u16(xin[:M]))
-        y = yout[:M].float().cpu().numpy()
-        assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), name
-    # SiLU*mul glue (not the paper's method): fp32 reference of the GPU's own gate-up output
-    gu = st.y_gu[:M].float().cpu().numpy()
-    F = d.ffn
-    act_ref = gu[:, :F] / (1 + np.exp(-gu[:, :F])) * gu[:, F:]
-    act = st.act[:M].float().cpu().numpy()
-    assert np.all(np.abs(act - act_ref) <= 2e-3 * (1 + np.abs(act_ref)))
-    r = ref("down", _to_u16(st.act[:M]))
-    y = st.y_down[:M].float().cpu().numpy()
-    assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r)))
+    ref = _oracle_stack(Wq, synth.host(22, 0, synth.ACT, 16, d.hidden)[:M], layers, st.plan["o"]["K"], M)
+    for name, buf in (("qkv", st.y_qkv), ("o", st.y_o), ("gate_up", st.y_gu), ("act", st.act), ("down", st.y_down)):
+        r = ref[name]
+        y = buf[:M].float().cpu().numpy()
+        assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), (name, np.abs(y - r).max())
+    assert np.abs(ref["down"]).max() > 0.05             # the data flow did not collapse to zero
     out = st.accept_out[:3 + M].cpu().numpy()
     assert np.array_equal(out, oracle.accept(tok, par, am)[4])
 
@@ -150,12 +163,11 @@ def _tp2_body(dist, tp):
 
     def make_weight(l, name, K, N, out):
         synth.gpu(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
-        Wh[name] = synth.host(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
+        Wh[(l, name)] = synth.host(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
 
     M = 8
     st = tp.VerifyStack(d, 2, 16, make_weight, tp_size=2, tp_rank=0, group=dist.group.WORLD)
-    for j, buf in enumerate((st.x_qkv, st.x_o, st.x_mlp)):
-        synth.gpu(32, j, synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+    synth.gpu(32, 0, synth.ACT, 16, d.hidden, out=st.x_in)
     assert st.chains(M) is not None and len(st.chains(M)) == 4     # two segments per layer
     outs = {}
     for chains in (True, False):
@@ -166,11 +178,47 @@ def _tp2_body(dist, tp):
     for a, b in zip(outs[True], outs[False]):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
-    def ref(name, X_u16):
-        c, s_, z, _ = oracle.quantize(Wh[name])
-        return oracle.gemm(X_u16, c, s_, z, nthreads=NPROC)
-
-    for name, xin, yout in (("qkv", st.x_qkv, st.y_qkv), ("o", st.x_o, st.y_o), ("down", st.act, st.y_down)):
-        r = ref(name, _to_u16(xin[:M]))
+    # rank 0 of a 1-process group: the all-reduce is the identity, so the rank's shard stack is the oracle's
+    # data flow on the rank-0 shard weights (from the host input)
+    Wq = {(l, n): oracle.quantize(W)[:3] for (l, n), W in Wh.items()}
+    ref = _oracle_stack(Wq, synth.host(32, 0, synth.ACT, 16, d.hidden)[:M], 2, st.plan["o"]["K"], M)
+    for name, yout in (("qkv", st.y_qkv), ("o", st.y_o), ("down", st.y_down)):
+        r = ref[name]
         y = yout[:M].float().cpu().numpy()
         assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), name
+
+
+@pytest.mark.timeout(1200)
+def test_llama70b_chain_M8_bench_configuration_vs_oracle():
+    # The bench's exact launch configuration: Llama-3-70B layer shapes, the whole stack as ONE
+    # persistent chain at M = 8 (family MMA_SYNC, one CTA per SM), calibrated weights, real data flow. Two
+    # layers, so the down(0) -> QKV(1) edge is crossed. The oracle runs the same data flow from the host input
+    # on host-regenerated weights scaled by the same powers of two (tp.VerifyStack.calib_scale).
+    from paper_2505_22179_b200 import tp
+    d, layers, M = tp.LLAMA3_70B, 2, 8
+    tids = {}
+
+    def make_weight(l, name, K, N, out):
+        tids[(l, name)] = (synth.tensor_id(l, tp.MATRICES.index(name)), K, N)
+        synth.gpu(51, tids[(l, name)][0], synth.WEIGHT, K, N, out=out)
+
+    x0 = synth.gpu(52, 1, synth.ACT, M, d.hidden)
+    st = tp.VerifyStack(d, layers, M, make_weight, calibrate=x0)
+    synth.gpu(52, 0, synth.ACT, M, d.hidden, out=st.x_in)
+    ch = st.chains(M)
+    assert ch is not None and len(ch) == 1 and ch[0].n == 5 * layers
+    st.forward(M)
+    torch.cuda.synchronize()
+    Wq = {}
+    for (l, name), (tid, K, N) in tids.items():
+        a = st.calib_scale[l][name]
+        assert a == 2.0 ** round(np.log2(a))
+        W = synth.host(51, tid, synth.WEIGHT, K, N).view(np.float16).astype(np.float32) * np.float32(a)
+        Wq[(l, name)] = oracle.quantize(W.astype(np.float16).view(np.uint16))[:3]
+        del W
+    ref = _oracle_stack(Wq, synth.host(52, 0, synth.ACT, M, d.hidden), layers, st.plan["o"]["K"], M)
+    for name, buf in (("qkv", st.y_qkv), ("o", st.y_o), ("gate_up", st.y_gu), ("act", st.act), ("down", st.y_down)):
+        r = ref[name]
+        y = buf[:M].float().cpu().numpy()
+        assert np.all(np.abs(y - r) <= 1e-2 * (1 + np.abs(r))), (name, np.abs(y - r).max())
+        assert 0.3 < np.sqrt(np.mean(r ** 2)) < 3.0, name   # calibrated: O(1) activations
