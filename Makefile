@@ -10,7 +10,7 @@ BUILD := build/obj
 
 LIB := paper_2505_22179_b200/libw4a16.so
 OBJS := $(BUILD)/abi.o $(BUILD)/pack.o $(BUILD)/gemm_mma.o $(BUILD)/accept.o $(BUILD)/mlp_glue.o $(BUILD)/gemm_tc.o \
-        $(BUILD)/lmhead.o $(BUILD)/tree_attn.o $(BUILD)/hadamard.o $(BUILD)/w4a8.o
+        $(BUILD)/lmhead.o $(BUILD)/tree_attn.o $(BUILD)/hadamard.o $(BUILD)/w4a8.o $(BUILD)/gemm_tp.o
 
 all: $(LIB) synth/libsynth_host.so synth/libsynth_gpu.so oracle/libw4a16_oracle.so
 
@@ -20,7 +20,7 @@ $(BUILD):
 # pack.cu must not contract fp32 mul/add into FMA: its codes are bit-exact with the oracle.
 $(BUILD)/pack.o: $(CSRC)/pack.cu $(CSRC)/common.cuh include/w4a16.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) --fmad=false -c $< -o $@ 2> $(BUILD)/pack.ptxas.txt || (cat $(BUILD)/pack.ptxas.txt; false)
-$(BUILD)/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/tma_host.cuh include/w4a16.h | $(BUILD)
+$(BUILD)/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/tma_host.cuh $(CSRC)/tc_ptx.cuh include/w4a16.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
 # Diagnostics build (make diag): the same library with W4A16_MMA_DIAG=1 (skip-compute / skip-load / trace

@@ -58,7 +58,8 @@ typedef enum {
 
 enum { W4A16_ASYM = 0, W4A16_SYM = 1 };
 enum { W4A16_DEV_OK = 0, W4A16_DEV_NONFINITE = 1, W4A16_DEV_BAD_TREE = 2 };
-enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 = 1, W4A16_FAMILY_MMA_SYNC_S = 2 };
+enum { W4A16_FAMILY_AUTO = -1, W4A16_FAMILY_MMA_SYNC = 0, W4A16_FAMILY_TCGEN05 = 1, W4A16_FAMILY_MMA_SYNC_S = 2,
+       W4A16_FAMILY_TCGEN05_OC = 3 };
 #define W4A16_GROUP 128
 #define W4A16_MAX_M 64
 #define W4A16_MAX_TREE 1024
@@ -109,7 +110,9 @@ int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K,
 /* w4a16_gemm_ex — w4a16_gemm with an explicit kernel family: W4A16_FAMILY_AUTO (= w4a16_gemm),
  * W4A16_FAMILY_MMA_SYNC (mma.sync, group scale applied to fp32 group sums; M <= 16, else W4A16_ERR_SHAPE),
  * W4A16_FAMILY_MMA_SYNC_S (mma.sync, scale folded into the dequantised fp16 weights; M <= 16) or
- * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, weights in TMEM; any M <= 64). All compute the same definition
+ * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, exact w_hat in TMEM; any M <= 64) or W4A16_FAMILY_TCGEN05_OC
+ * (5th-gen tensor cores, offset codes 1024+q / 64+q in TMEM, per-unit TMEM accumulator, scale and offset
+ * correction per group in fp32; any M <= 64). All compute the same definition
  * (within the tolerance above); results are batch-invariant within one family. */
 int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
                   void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);

@@ -20,7 +20,7 @@ W4A16_GROUP = 128
 W4A16_MAX_M = 64
 W4A16_MAX_TREE = 1024
 W4A16_MAX_N = 1048576
-W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S = -1, 0, 1, 2
+W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05_OC = -1, 0, 1, 2, 3
 
 # Every symbol include/w4a16.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (

@@ -13,6 +13,8 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaS
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" size_t w4a16_tp_workspace_bytes(int M, int K, int N, int num_sms);
+extern "C" int w4a16_launch_gemm_tp(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 extern "C" size_t w4a16_lmhead_workspace_bytes_sms(int num_sms);
 extern "C" int w4a16_launch_hadamard(const uint16_t*, uint16_t*, int, int, int, cudaStream_t);
 extern "C" size_t w4a16_tree_attention_workspace_bytes_sms(int M, int L, int Hq, int Hkv, int sms);
@@ -82,7 +84,8 @@ extern "C" size_t w4a16_gemm_workspace_bytes(int M, int K, int N, int group) {
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return 0;
   const size_t a = w4a16_mma_workspace_bytes(M, K, N, sms), b = w4a16_tc_workspace_bytes(M, K, N, sms);
-  return a > b ? a : b;
+  const size_t c = w4a16_tp_workspace_bytes(M, K, N, sms);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
 extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
@@ -118,6 +121,10 @@ extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y,
   if (family == W4A16_FAMILY_TCGEN05) {
     if (!workspace || workspace_bytes < w4a16_tc_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
     return w4a16_launch_gemm_tc(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+  }
+  if (family == W4A16_FAMILY_TCGEN05_OC) {
+    if (!workspace || workspace_bytes < w4a16_tp_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+    return w4a16_launch_gemm_tp(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
   }
   return W4A16_ERR_ARG;
 }

@@ -141,7 +141,9 @@ def test_tp2_fused_stack_matches_tp1(M):
             if (l, name) not in full:
                 Kf, Nf = tp.shard_plan(dims, 1, 0)[name]["full"]
                 W = synth.gpu(31, 1000 + 10 * l + tp.MATRICES.index(name), synth.WEIGHT, Kf, Nf)
-                full[(l, name)] = W.mul_(1.0 / (0.018 * Kf ** 0.5))   # ~unit gain: O(1) activations through the stack
+                # ~unit gain (std of the generated weights incl. their outlier groups): O(1) activations through
+                # the dependent stack, so the absolute part of the tolerance stays meaningful in layer 2
+                full[(l, name)] = W.mul_(1.0 / (float(W.float().std()) * Kf ** 0.5))
             out.copy_(tp.shard_of(full[(l, name)], tp.shard_plan(dims, t, rank)[name]))
         return mk
 

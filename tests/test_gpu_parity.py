@@ -149,7 +149,7 @@ def problem(K, N, mode=0, seed=0):
     return _P[key]
 
 
-FAMILIES = [0, 2, 1]  # W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05
+FAMILIES = [0, 2, 1, 3]  # W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_TCGEN05_OC
 
 
 @pytest.mark.parametrize("family", FAMILIES)
