@@ -89,6 +89,11 @@ __device__ __forceinline__ float2 lds64f(uint32_t addr) {
 __device__ __forceinline__ void sts64f(uint32_t addr, float a, float b) {
   asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }
+__device__ __forceinline__ float lds32f(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds32u(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -98,6 +103,35 @@ __device__ __forceinline__ uint16_t lds16u(uint32_t addr) {
   uint16_t v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
+}
+
+// mbarrier wait with a suspend-time hint (as CUTLASS's ClusterBarrier::wait): a waiting thread is suspended
+// until the phase completes (or the hint expires) instead of re-issuing polls, so idle warps do not take
+// issue slots from the working ones. W4_TP_SPIN=1 selects the plain try_wait loop (diagnostics).
+#ifndef W4_TP_SPIN
+#define W4_TP_SPIN 0
+#endif
+__device__ __forceinline__ bool try_wait_hint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+// A wait that has not completed after ~30 s traps (a protocol bug fails the launch instead of hanging the GPU).
+__device__ __forceinline__ void wait(uint32_t bar, uint32_t parity) {
+#if W4_TP_SPIN
+  mbar_wait_a(bar, parity);
+#else
+  if (try_wait_hint(bar, parity)) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (!try_wait_hint(bar, parity))
+    if (globaltimer_ns() - t0 > 30000000000ull) __trap();
+#endif
 }
 
 // A ring position: slot index and the parity of the current round.

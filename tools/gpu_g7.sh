@@ -1,0 +1,6 @@
+OUT=gpurun_out; mkdir -p $OUT
+timeout 240 python -m pytest tests/test_gpu_parity.py -q --timeout 100 -k "3 and not stress" > $OUT/g7_parity.log 2>&1; echo "parity rc=$?"; grep -E "passed|failed|FAILED" $OUT/g7_parity.log | head -10
+for d in 0 15; do W4A16_TP_DEBUG=$d timeout 100 python tools/probe_fam.py --shapes gate_up --M 1,8,16,32,64 --families 3 --bytes 1e9 | sed "s/^/dbg=$d /"; done > $OUT/g7_probe.log 2>&1
+W4A16_TP_DEBUG=256 timeout 100 python tools/probe_fam.py --shapes gate_up --M 8 --families 3 --bytes 1e9 > $OUT/g7_trace.log 2>&1
+timeout 100 python tools/probe_fam.py --shapes qkv,o,down --M 8 --families 0,3 --bytes 1e9 >> $OUT/g7_probe.log 2>&1
+cat $OUT/g7_probe.log; head -30 $OUT/g7_trace.log

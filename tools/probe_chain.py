@@ -15,9 +15,9 @@ ap.add_argument("--M", type=int, default=8)
 ap.add_argument("--layers", type=int, default=8)
 a = ap.parse_args()
 mat_id = {n: i for i, n in enumerate(tp.MATRICES)}
-st = tp.VerifyStack(tp.LLAMA3_70B, a.layers, 64, lambda l, n, K, N, out: synth.gpu(0, synth.tensor_id(l, mat_id[n], 0), synth.WEIGHT, K, N, out=out))
-for buf, tid in ((st.x_qkv, 1), (st.x_o, 2), (st.x_mlp, 3)):
-    synth.gpu(0, synth.tensor_id(0xFFF, tid, 0), synth.ACT, buf.shape[0], buf.shape[1], out=buf)
+st = tp.VerifyStack(tp.LLAMA3_70B, a.layers, 64, lambda l, n, K, N, out: synth.gpu(0, synth.tensor_id(l, mat_id[n], 0), synth.WEIGHT, K, N, out=out),
+                    calibrate=synth.gpu(0, 9, synth.ACT, 8, 8192))
+synth.gpu(0, synth.tensor_id(0xFFF, 1, 0), synth.ACT, st.x_in.shape[0], st.x_in.shape[1], out=st.x_in)
 ch = st.chains(a.M)[0]
 for _ in range(3):
     ch()

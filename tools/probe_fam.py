@@ -57,3 +57,16 @@ for name in a.shapes.split(","):
                 print(json.dumps({"shape": name, "M": M, "family": fam, "error": repr(e)}), flush=True)
     del lins
     torch.cuda.empty_cache()
+
+if int(os.environ.get("W4A16_TP_DEBUG", "0")) & 256:
+    # per-unit timeline of CTA 0 of the last launch (gemm_tp.cu g_tp_trace), ns relative to the first event
+    import ctypes
+    import numpy as np
+    from paper_2505_22179_b200._lib import lib
+    buf = np.zeros((12, 128), dtype=np.uint64)
+    lib.w4a16_debug_trace_tp(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
+    names = ["X_issue", "W_issue", "D0_wfull", "D1_wfull", "D_aempty", "M_ready", "M_commit", "D_afull", "E_accfull", "E_done"]
+    t0 = int(buf[buf > 0].min()) if (buf > 0).any() else 0
+    print("unit " + " ".join(f"{n:>10}" for n in names))
+    for i in range(0, 64):
+        print(f"{i:4d} " + " ".join(f"{(int(buf[e, i]) - t0) if buf[e, i] else -1:10d}" for e in range(len(names))))
