@@ -25,7 +25,13 @@ struct alignas(64) ChainJob {
   int kind, K, N, Gk, U;
   int dep_x;               // earlier op whose completion this op's X reads wait for (-1: none)
   int dep_y;               // earlier op whose completion this op's Y writes wait for (WAR / WAW; -1: none)
-  int cnt_off;             // this op's first tile counter
+  int cnt_off;             // this op's first tile counter (and first tile-ready flag)
+  // Tile-level RAW dependency (family A chains): X is a column range of the Y of GEMM op dep_x, so the
+  // activation k-group g of this op is complete once that op's tile xf_off + g is written (its ready flag,
+  // at flags[xf_off + g], reached the run number). -1: wait for the whole op dep_x instead.
+  int xf_off;
+  int pub_tiles;           // 1: publish this op's tile-ready flags (a later op reads its Y tile by tile)
+  int n_tiles;             // job 0: tiles of all GEMM ops (counters, then as many tile-ready flags, in the workspace)
   // ALLREDUCE (include/w4a16.h): every rank's partial as mapped here (rank order), this rank's ready flag in
   // every rank's flag area, this rank's own `world` ready flags of the op's slot, the group's run counter
   // (local). Job 0 also carries the run counter when the chain has ALLREDUCE ops (advanced at chain end).
@@ -82,6 +88,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Non-blocking probe of a phase (mbarrier.test_wait never suspends the thread, unlike try_wait, which may wait
+// for a system-dependent time before returning false): for polling loops that interleave other work.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.b32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)

@@ -95,7 +95,10 @@ struct GemmParams {
   int dbg;           // diagnostics only (W4A16_MMA_DEBUG, W4A16_MMA_DIAG builds): bit0 skip compute, bit1 skip loads, bit2 backoff waits, bit4 trace
   const ChainJob* jobs;   // chain: the op table (device); nullptr: single GEMM
   int n_jobs;             // 1 for a single GEMM
-  int* done;              // chain: [n_jobs] CTAs that finished each op, then the exit counter
+  int* done;              // chain: [n_jobs] CTAs that finished each op; done[-2] = run number, done[-1] = exit counter
+                          // (fixed offsets: chains that share a workspace share them)
+  int* flags;             // chain: tile-ready flags (one per tile of every GEMM op, at the op's cnt_off): the run
+                          // number + 1 of the last run that wrote the tile's Y (run number at done[n_jobs + 1])
   int slots;              // chain: partial-slot ring length in ops (1 for a single GEMM)
 };
 
@@ -105,17 +108,24 @@ struct JobInfo {
   const CUtensorMap* mR;
   const CUtensorMap* m1;
   int* counters;
-  int kind, N, Gk, U, dep_x, dep_y;
+  int* flags;             // this op's tile-ready flags (chain) or nullptr
+  int kind, N, Gk, U, dep_x, dep_y, xf_off, pub_tiles;
+  int cs;                 // counter / flag stride (1: single GEMM; 2: chain, counters and flags interleaved)
 };
 __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
   JobInfo J;
   if (p.jobs == nullptr) {
-    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters;
-    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1;
+    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters; J.flags = nullptr; J.cs = 1;
+    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0;
   } else {
     const ChainJob* c = p.jobs + j;
-    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + c->cnt_off;
-    J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y;
+    // chain: tile counter and tile-ready flag interleaved per tile (same layout in every chain that shares the
+    // workspace, so one chain's flags never land on another's counters)
+    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + 2 * c->cnt_off;
+    J.flags = J.counters + 1;
+    J.cs = 2;
+    J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y; J.xf_off = c->xf_off;
+    J.pub_tiles = c->pub_tiles;
   }
   return J;
 }
@@ -123,7 +133,11 @@ __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap
 // every earlier op complete).
 __device__ __forceinline__ void wait_op(const GemmParams& p, int j) {
   if (j < 0) return;
-  while (ld_acquire_gpu(&p.done[j]) < p.G) __nanosleep(64);
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_gpu(&p.done[j]) < p.G) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // never hang the device on a protocol bug
+  }
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   __shared__ __align__(8) uint64_t sums_bar[S];   // offset-code family: the stage's activation sums are ready
   __shared__ __align__(8) uint64_t pub_full[kPubSlots], pub_empty[kPubSlots];
   __shared__ int* pub_ptr[kPubSlots];
+  __shared__ int pub_val[kPubSlots];   // 0: add 1 (counters); else store this value (tile-ready flags)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -318,6 +333,18 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, 2 * ((u0 + jj) % J.Gk), &full_bar[s]);
         }
       };
+      const int run = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile flags)
+      // Tile-level dependency: the stage's activation k-groups are complete once the producing op's tiles
+      // xf_off + g are written in this run (their flags reached run + 1).
+      auto tiles_ready = [&](const JobInfo& J, int u0, int nu) {
+        int g = u0 % J.Gk;
+        bool ok = true;
+        for (int jj = 0; jj < nu; ++jj) {
+          ok &= ld_acquire_gpu(&p.counters[2 * (J.xf_off + g) + 1]) > run;
+          if (++g == J.Gk) g = 0;
+        }
+        return ok;
+      };
       auto drain = [&](bool block) {   // issue queued activation loads whose producers are done
         while (q_n > 0) {
           if (!pdl_done) {
@@ -327,11 +354,22 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
           const JobInfo J = job_at(p, &xmapR, &xmap1, q_j[q_head]);
           if (J.dep_x > ok_upto) {
-            if (ld_acquire_gpu(&p.done[J.dep_x]) < p.G) {
+            if (ld_acquire_gpu(&p.done[J.dep_x]) >= p.G) {
+              ok_upto = J.dep_x;   // the whole producing op is complete: no more per-tile checks
+            } else if (J.xf_off >= 0) {
+              if (!tiles_ready(J, q_u0[q_head], q_nu[q_head])) {
+                if (!block) return;
+                const unsigned long long t0 = globaltimer_ns();
+                while (!tiles_ready(J, q_u0[q_head], q_nu[q_head])) {
+                  __nanosleep(64);
+                  if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // never hang the device
+                }
+              }
+            } else {
               if (!block) return;
               wait_op(p, J.dep_x);
+              ok_upto = J.dep_x;
             }
-            ok_upto = J.dep_x;
             fence_proxy_async_global();   // generic-proxy stores of other CTAs -> this TMA (async proxy) read
           }
           issue_x(q_s[q_head], J, q_u0[q_head], q_nu[q_head]);
@@ -349,7 +387,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           const int nu = min(kR, u_end - u0);
           if (issued >= S) {   // slot s must be released by the consumers first
             if (!pdl_done) drain(true);
-            while (!mbar_try_wait(&empty_bar[s], ph ^ 1)) drain(false);
+            while (!mbar_test_wait(&empty_bar[s], ph ^ 1)) drain(false);
           }
           if (W4A16_MMA_DIAG && (p.dbg & 2)) {   // diagnostics: no memory traffic, stale shared memory
             mbar_arrive(&full_bar[s]);
@@ -453,34 +491,55 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // Requests arrive in order from thread 0 (after a barrier of the threads whose stores they publish):
     // mbarrier release/acquire (CTA scope) hands those stores to this warp; its GPU-scope fence + relaxed
     // red then releases them to the CTAs that acquire the counter. nullptr ends the kernel's requests.
+    // Requests that queue up while a fence is in flight are issued together behind ONE fence (a GPU-scope
+    // fence costs ~1 us under load; op counts, tile counters and tile-ready flags all come through here).
     int slot = 0;
     uint32_t ph = 0;
     for (;;) {
       mbar_wait(&pub_full[slot], ph);
-      int* ptr = pub_ptr[slot];
-      if (lane == 0) {
-        if (ptr) red_release_gpu_add(ptr, 1);
-        mbar_arrive(&pub_empty[slot]);
+      int n = 1;   // consecutive full slots (at most kPubSlots)
+      {
+        int s2 = slot + 1 == kPubSlots ? 0 : slot + 1;
+        uint32_t p2 = s2 == 0 ? ph ^ 1 : ph;
+        while (n < kPubSlots && mbar_test_wait(&pub_full[s2], p2)) {
+          ++n;
+          if (++s2 == kPubSlots) { s2 = 0; p2 ^= 1; }
+        }
+      }
+      bool stop = false;
+      if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (int i = 0; i < n; ++i) {
+        int* ptr = pub_ptr[slot];
+        const int val = pub_val[slot];
+        if (lane == 0) {
+          if (ptr && val == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(ptr) : "memory");
+          if (ptr && val != 0) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
+          mbar_arrive(&pub_empty[slot]);
+        }
+        stop |= ptr == nullptr;
+        if (++slot == kPubSlots) { slot = 0; ph ^= 1; }
       }
       __syncwarp();
-      if (!ptr) break;
-      if (++slot == kPubSlots) { slot = 0; ph ^= 1; }
+      if (stop) break;
     }
     return;
   }
 
   // ---------------- consumers ----------------
   trace_ma(p, 0);
+  const int run_c = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile-ready flags)
   int pub_s = 0;
   uint32_t pub_ph = 0;
   // thread 0 only, after a barrier of the threads whose global stores the increment releases
-  auto publish = [&](int* ptr) {
+  auto publish = [&](int* ptr, int val = 0) {
     if (!W4_MA_PUB) {
-      if (ptr) red_release_gpu_add(ptr, 1);
+      if (ptr && val == 0) red_release_gpu_add(ptr, 1);
+      if (ptr && val != 0) asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
       return;
     }
     mbar_wait(&pub_empty[pub_s], pub_ph ^ 1);   // the slot's previous request is consumed
     pub_ptr[pub_s] = ptr;
+    pub_val[pub_s] = val;
     mbar_arrive(&pub_full[pub_s]);
     if (++pub_s == kPubSlots) { pub_s = 0; pub_ph ^= 1; }
   };
@@ -593,7 +652,12 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
         }
       };
-      if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); return; }
+      auto tile_written = [&]() {   // chain: the tile's Y is complete -> its ready flag (tile-level deps)
+        if (!chain || !J.pub_tiles) return;
+        named_bar_sync(2, 4 * 32);
+        if (threadIdx.x == 0) publish(&J.flags[J.cs * t], run_c + 1);
+      };
+      if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); tile_written(); return; }
       // Split tile: the tile's first CTA c_first owns it. It handles the tile's head as its
       // LAST segment of the op, so it finishes after every other contributor has long published its
       // (first-segment) fp32 partial: contributors store, then release-increment the tile counter and move
@@ -608,15 +672,15 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int tb = 0; tb < NTB; ++tb)
             __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
         named_bar_sync(2, 4 * 32);
-        if (threadIdx.x == 0) publish(&J.counters[t]);
+        if (threadIdx.x == 0) publish(&J.counters[J.cs * t]);
         return;
       }
       if (threadIdx.x == 0) {
         const int want = c_last - c_first;
         trace_op(p, job, 4);
-        while (ld_acquire_gpu(&J.counters[t]) != want) __nanosleep(32);
+        while (ld_acquire_gpu(&J.counters[J.cs * t]) != want) __nanosleep(32);
         trace_op(p, job, 5);
-        J.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch
+        J.counters[J.cs * t] = 0;   // every contributor has arrived: re-arm for the next launch
       }
       named_bar_sync(2, 4 * 32);
       for (int c = c_first + 1; c <= c_last; ++c) {
@@ -629,6 +693,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
       }
       store(acc);
+      tile_written();
     };
 
     // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
@@ -853,10 +918,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // The last CTA out re-arms the op counters for the next run of the chain (every CTA has finished
     // every access to them once it has counted itself out; the fences order its op counts first).
     __threadfence();
-    if (atomicAdd(&p.done[p.n_jobs], 1) == p.G - 1) {
+    if (atomicAdd(&p.done[-1], 1) == p.G - 1) {
       __threadfence();
       for (int j = 0; j < p.n_jobs; ++j) p.done[j] = 0;
-      p.done[p.n_jobs] = 0;
+      p.done[-1] = 0;
+      p.done[-2] += 1;   // the next run's number (tile-ready flags hold run + 1)
       if (p.jobs[0].epoch != nullptr) *p.jobs[0].epoch += 1u;   // the group's next run (ALLREDUCE flags)
       __threadfence();
     }
@@ -902,7 +968,7 @@ constexpr int kChainSlots = 8;   // partial-slot ring of a chain, in ops
 
 inline int ntb_of(int M) { return (M + 7) / 8; }
 inline size_t chain_partial_bytes(int M, int G) { return (size_t)kChainSlots * G * 4 * ntb_of(M) * 2 * 32 * 16; }
-inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 1) * 4 + 255) / 256 * 256; }
+inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 2) * 4 + 255) / 256 * 256; }   // run, exit, per op
 
 }  // namespace ma
 }  // namespace w4
@@ -1032,7 +1098,7 @@ extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op* ops, int n_ops
   int mode = 0;
   const int G = chain_ctas(sms);
   if (check_ops(ops, n_ops, M, G, &tiles, &mode) != W4A16_OK) return 0;
-  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 4;
+  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 8;   // counters + flags
 }
 
 extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes,
@@ -1086,12 +1152,24 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
     // completion of every op before it, so the latest conflicting op is enough.
     J.dep_x = -1;
     J.dep_y = -1;
+    J.xf_off = -1;
     for (int i = j - 1; i >= 0 && (J.dep_x < 0 || J.dep_y < 0); --i) {
       if (J.dep_x < 0 && overlaps(y_span(ops[i], M), x_span(o, M))) J.dep_x = i;
       if (J.dep_y < 0 && (overlaps(y_span(ops[i], M), y_span(o, M)) || overlaps(x_span(ops[i], M), y_span(o, M)))) J.dep_y = i;
     }
+    // tile-level RAW dependency: X is a whole-tile column range of the producing GEMM's Y with Y's row stride
+    if (o.kind == W4A16_OP_GEMM && J.dep_x >= 0 && ops[J.dep_x].kind == W4A16_OP_GEMM) {
+      const w4a16_op& d = ops[J.dep_x];
+      const uintptr_t xb = reinterpret_cast<uintptr_t>(o.X), yb = reinterpret_cast<uintptr_t>(d.Y);
+      if (xb >= yb && (xb - yb) % 256 == 0 && ldx_of(o) == d.N && (int)((xb - yb) / 2) + o.K <= d.N)
+      {
+        J.xf_off = jobs[J.dep_x].cnt_off + (int)((xb - yb) / 2) / 128;
+        jobs[J.dep_x].pub_tiles = 1;   // the producing op publishes its tile-ready flags
+      }
+    }
   }
   jobs[0].epoch = epoch;
+  jobs[0].n_tiles = cnt;
   return W4A16_OK;
 }
 
@@ -1109,8 +1187,9 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   const size_t pb = w4::ma::chain_partial_bytes(M, p.G), db = w4::ma::chain_done_bytes(n_ops);
   if (ws_bytes < pb + db) return W4A16_ERR_WORKSPACE;
   p.partials = reinterpret_cast<float*>(ws);
-  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb);
+  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb) + 2;   // after the run number and exit counter
   p.counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb + db);
+  p.flags = nullptr;   // interleaved with the counters (JobInfo)
   p.jobs = reinterpret_cast<const w4::ma::ChainJob*>(dev_plan);
   p.n_jobs = n_ops;
   p.slots = w4::ma::kChainSlots;

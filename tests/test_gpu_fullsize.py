@@ -77,6 +77,17 @@ def _h16(y64):
     return y64.astype(np.float16).view(np.uint16)
 
 
+def _scaled_oracle_weights(st, tids, seed):
+    """Host-regenerated weights times the stack's power-of-two calibration scales (exact), quantised by the oracle."""
+    Wq = {}
+    for (l, name), (tid, K, N) in tids.items():
+        a = st.calib_scale[l][name]
+        assert a == 2.0 ** round(np.log2(a))
+        W = synth.host(seed, tid, synth.WEIGHT, K, N).view(np.float16).astype(np.float32) * np.float32(a)
+        Wq[(l, name)] = oracle.quantize(W.astype(np.float16).view(np.uint16))[:3]
+    return Wq
+
+
 def _oracle_stack(Wq, x_in_u16, layers, K_o, M):
     """The verify forward's data flow (tp.py module docstring) on the ORACLE only, from the host input: each
     GEMM output rounded to fp16 as the GPU stores it; SiLU*mul glue in fp64. Returns the last layer's buffers."""
@@ -105,15 +116,17 @@ def test_verify_stack_against_oracle(dims, layers, chains):
     # (QKV -> O on the query columns -> gate-up -> SiLU*mul -> down -> next layer); buffers hold the last layer.
     from paper_2505_22179_b200 import tp
     d = tp.ModelDims("tiny", hidden=dims[0], ffn=dims[1], n_q=dims[2], n_kv=dims[3], head=128, layers=layers)
-    Wq = {}
+    tids = {}
 
     def make_weight(l, name, K, N, out):
-        synth.gpu(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
-        c, s_, z, _ = oracle.quantize(synth.host(21, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N))
-        Wq[(l, name)] = (c, s_, z)
+        tids[(l, name)] = (synth.tensor_id(l, tp.MATRICES.index(name)), K, N)
+        synth.gpu(21, tids[(l, name)][0], synth.WEIGHT, K, N, out=out)
 
     M = 13
-    st = tp.VerifyStack(d, layers, 16, make_weight)
+    # calibrated (power-of-two weight scales, reproduced on the host below): O(1) activations in every layer, so
+    # the absolute part of the tolerance keeps its meaning through the dependent layers
+    st = tp.VerifyStack(d, layers, 16, make_weight, calibrate=synth.gpu(23, 1, synth.ACT, 8, d.hidden))
+    Wq = _scaled_oracle_weights(st, tids, 21)
     st.use_chains = chains
     synth.gpu(22, 0, synth.ACT, 16, d.hidden, out=st.x_in)
     rng = np.random.default_rng(3)
@@ -159,14 +172,15 @@ def test_verify_stack_tp2_shard_chains_match_op_by_op():
 
 def _tp2_body(dist, tp):
     d = tp.ModelDims("small", hidden=4096, ffn=8192, n_q=32, n_kv=8, head=128, layers=2)
-    Wh = {}
+    tids = {}
 
     def make_weight(l, name, K, N, out):
-        synth.gpu(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N, out=out)
-        Wh[(l, name)] = synth.host(31, synth.tensor_id(l, tp.MATRICES.index(name)), synth.WEIGHT, K, N)
+        tids[(l, name)] = (synth.tensor_id(l, tp.MATRICES.index(name)), K, N)
+        synth.gpu(31, tids[(l, name)][0], synth.WEIGHT, K, N, out=out)
 
     M = 8
-    st = tp.VerifyStack(d, 2, 16, make_weight, tp_size=2, tp_rank=0, group=dist.group.WORLD)
+    st = tp.VerifyStack(d, 2, 16, make_weight, tp_size=2, tp_rank=0, group=dist.group.WORLD,
+                        calibrate=synth.gpu(33, 1, synth.ACT, 8, d.hidden))
     synth.gpu(32, 0, synth.ACT, 16, d.hidden, out=st.x_in)
     assert st.chains(M) is not None and len(st.chains(M)) == 4     # two segments per layer
     outs = {}
@@ -180,7 +194,7 @@ def _tp2_body(dist, tp):
 
     # rank 0 of a 1-process group: the all-reduce is the identity, so the rank's shard stack is the oracle's
     # data flow on the rank-0 shard weights (from the host input)
-    Wq = {(l, n): oracle.quantize(W)[:3] for (l, n), W in Wh.items()}
+    Wq = _scaled_oracle_weights(st, tids, 31)
     ref = _oracle_stack(Wq, synth.host(32, 0, synth.ACT, 16, d.hidden)[:M], 2, st.plan["o"]["K"], M)
     for name, yout in (("qkv", st.y_qkv), ("o", st.y_o), ("down", st.y_down)):
         r = ref[name]
@@ -209,13 +223,7 @@ def test_llama70b_chain_M8_bench_configuration_vs_oracle():
     assert ch is not None and len(ch) == 1 and ch[0].n == 5 * layers
     st.forward(M)
     torch.cuda.synchronize()
-    Wq = {}
-    for (l, name), (tid, K, N) in tids.items():
-        a = st.calib_scale[l][name]
-        assert a == 2.0 ** round(np.log2(a))
-        W = synth.host(51, tid, synth.WEIGHT, K, N).view(np.float16).astype(np.float32) * np.float32(a)
-        Wq[(l, name)] = oracle.quantize(W.astype(np.float16).view(np.uint16))[:3]
-        del W
+    Wq = _scaled_oracle_weights(st, tids, 51)
     ref = _oracle_stack(Wq, synth.host(52, 0, synth.ACT, M, d.hidden), layers, st.plan["o"]["K"], M)
     for name, buf in (("qkv", st.y_qkv), ("o", st.y_o), ("gate_up", st.y_gu), ("act", st.act), ("down", st.y_down)):
         r = ref[name]

@@ -73,3 +73,17 @@ for k, name in enumerate(kinds):
 for k, name in enumerate(kinds):
     d = [np.median(b[:, j, 7] - b[:, j, 0]) / 1e3 for j in range(k, n, 5) if (buf[:G, j, 7] > 0).all()]
     print(f"{name:8s} descriptor load {np.median(d) if d else float('nan'):6.2f} us")
+
+# critical-path view: for each op, T_dep = the last CTA's done-count of the op its activations depend on
+# (the previous op in this forward); per CTA: first stage ready - T_dep, compute, flush+count, done - T_dep
+print("\nper op (layers 2..): percentiles p0/p50/p90/p100 over CTAs, us; T_dep = previous op's last done-count")
+pq = lambda v: "/".join(f"{x:5.1f}" for x in np.percentile(v / 1e3, [0, 50, 90, 100]))
+for k, name in enumerate(kinds):
+    rows = {"ready-Tdep": [], "compute": [], "flush+cnt": [], "done-Tdep": []}
+    for j in range(5 + k, n, 5):
+        Tdep = b[:, j - 1, 3].max()
+        rows["ready-Tdep"].append(b[:, j, 1] - Tdep)
+        rows["compute"].append(b[:, j, 2] - b[:, j, 1])
+        rows["flush+cnt"].append(b[:, j, 3] - b[:, j, 2])
+        rows["done-Tdep"].append(b[:, j, 3] - Tdep)
+    print(f"{name:8s} " + "  ".join(f"{key} {pq(np.concatenate(v))}" for key, v in rows.items()))
