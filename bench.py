@@ -686,7 +686,7 @@ def main():
                 plain += qa + qb
                 h = stack.x_in[:M] if l == 0 else r_d
                 fused += [("gemm", h, L["qkv"], stack.y_qkv[:M]), ("gemm", stack.q_part(M), L["o"], P_o),
-                          ("allreduce", P_o, r_o, g1), ("gemm", r_o, L["gate_up"], stack.y_gu[:M]), qb[1],
+                          ("allreduce", P_o, r_o, g1), ("gemm_silu", r_o, L["gate_up"], stack.act[:M]),
                           ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
             t_ch = {}
             for name, ops in (("plain", plain), ("allreduce", fused)):
@@ -768,7 +768,7 @@ def main():
                     "(stand-in for the excluded norms); N(0,1.15^2) input activations with 4 x16 outlier channels; "
                     "EAGLE-2-shaped draft tree)",
             "config": {"workload": f"{dims.name} W4A16 g128 {args.mode} verify forward: {n_layers} decoder layers "
-                                   f"(QKV -> O -> gate-up -> SiLU*mul -> down -> next layer, each GEMM reading the "
+                                   f"(QKV -> O -> gate-up with SiLU*mul fused -> down -> next layer, each GEMM reading the "
                                    f"previous one's output; attention/norms out of scope) + verify_accept; "
                                    f"BASELINE configs 3-4",
                        "M": args.M, "layers": n_layers, "tp": world, "parallelism": f"tp{world}",

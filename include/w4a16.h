@@ -173,6 +173,11 @@ int w4a16_hadamard(const uint16_t* X, uint16_t* Y, int M, int K, int block, w4a1
  * rank-local shard layout of tp.py), out is fp16 [M][F], out[m][j] = fp16_rne(silu(gate) * up) in fp32.
  * F % 8 == 0, M >= 1. */
 int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream_t stream);
+/* w4a16_silu_mul_blocked — the same glue for a gate-up output whose columns come in blocks: GU[m] holds, for
+ * b = 0 .. F/block - 1, `block` gate columns then the matching `block` up columns; out[m][b*block + i] =
+ * fp16_rne(silu(GU[m][2b*block + i]) * GU[m][(2b+1)*block + i]) in fp32. block = F is w4a16_silu_mul; block = 64
+ * is the layout W4A16_OP_GEMM_SILU fuses. block % 8 == 0, F % block == 0. */
+int w4a16_silu_mul_blocked(const uint16_t* GU, int M, int F, int block, uint16_t* out, w4a16_stream_t stream);
 
 /* ---- Chains: a verify forward's whole sequence of ops in ONE persistent launch ----------------------
  * A verify forward is a long sequence of small W4A16 GEMMs (4 per decoder layer, 320 for Llama-3-70B)
@@ -185,14 +190,19 @@ int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w4a16_stream
  * reduction order: bit-identical results); each SILU_MUL op exactly what w4a16_silu_mul computes.
  * All G CTAs of a chain must be co-resident: do not run other kernels concurrently with a chain on the
  * same device (it is launched as a cooperative kernel). */
-enum { W4A16_OP_GEMM = 0, W4A16_OP_SILU_MUL = 1, W4A16_OP_ALLREDUCE = 2 };
+enum { W4A16_OP_GEMM = 0, W4A16_OP_SILU_MUL = 1, W4A16_OP_ALLREDUCE = 2, W4A16_OP_GEMM_SILU = 3 };
+/* W4A16_OP_GEMM_SILU: the Llama MLP's gate-up GEMM with SiLU*mul fused into its epilogue (family A chains).
+ * The weight's N columns come in 128-column tiles of [64 gate | 64 up] (w4a16_silu_mul_blocked's block = 64
+ * layout); Y is [M][N/2]: Y[m][64 t + i] = fp16_rne(silu(g) * u), g = fp16(G[m][128 t + i]),
+ * u = fp16(G[m][128 t + 64 + i]), G = X . W_hat — exactly w4a16_gemm followed by w4a16_silu_mul_blocked. */
 typedef struct {
-  int kind;            /* W4A16_OP_GEMM, W4A16_OP_SILU_MUL or W4A16_OP_ALLREDUCE */
+  int kind;            /* W4A16_OP_GEMM, W4A16_OP_GEMM_SILU, W4A16_OP_SILU_MUL or W4A16_OP_ALLREDUCE */
   const void* X;       /* GEMM: X [M][K] fp16.  SILU_MUL: GU [M][2N] fp16 ([gate | up] per row).
                         * ALLREDUCE: this rank's partial P [M][N] fp16, inside its symmetric region */
   const void* packed;  /* GEMM: packed weight blob of w4a16_pack (K x N, `mode`).  SILU_MUL: NULL.
                         * ALLREDUCE: HOST pointer to the w4a16_peer_group (read by w4a16_chain_plan only) */
-  void* Y;             /* GEMM: Y [M][N] fp16.  SILU_MUL: out [M][N] fp16.  ALLREDUCE: out [M][N] fp16 */
+  void* Y;             /* GEMM: Y [M][N] fp16.  GEMM_SILU: Y [M][N/2] fp16.  SILU_MUL: out [M][N] fp16.
+                        * ALLREDUCE: out [M][N] fp16 */
   int K, N;            /* GEMM: as w4a16_gemm.  SILU_MUL: K = 2N, N = F (N % 8 == 0).  ALLREDUCE: K = N, N % 8 == 0 */
   int mode;            /* GEMM: W4A16_ASYM or W4A16_SYM; every GEMM of a chain uses the same mode */
   int ldx;             /* GEMM: row stride of X in elements; 0 = K (contiguous), else ldx >= K and ldx % 8 == 0

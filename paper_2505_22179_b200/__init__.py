@@ -9,7 +9,7 @@ from .ops import (  # noqa: F401
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE, W4A16Error,
     W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05_OC,
     w4a16_pack, w4a16_unpack, w4a16_gemm, w4a16_gemm_workspace_bytes, w4a16_workspace_init,
-    verify_accept, w4a16_status_string, w4a16_gemm_family, w4a16_silu_mul,
+    verify_accept, w4a16_status_string, w4a16_gemm_family, w4a16_silu_mul, w4a16_silu_mul_blocked,
     PackedLinear, pack_linear, alloc_workspace, w4a16_packed_bytes, Chain,
     w4a16_lmhead_argmax, w4a16_lmhead_workspace_bytes, alloc_lmhead_workspace,
     w4a16_tree_attention, w4a16_tree_attention_workspace_bytes, w4a16_kv_compact, w4a16_hadamard,

@@ -35,6 +35,7 @@ ABI_SYMBOLS = (
     "w4a16_status_string",
     "w4a16_gemm_family",
     "w4a16_silu_mul",
+    "w4a16_silu_mul_blocked",
     "w4a16_chain_plan_bytes",
     "w4a16_chain_workspace_bytes",
     "w4a16_chain_plan",
@@ -54,7 +55,7 @@ ABI_SYMBOLS = (
     "w4a8_workspace_bytes",
     "w4a8_gemm",
 )
-W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE = 0, 1, 2
+W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE, W4A16_OP_GEMM_SILU = 0, 1, 2, 3
 W4A16_MAX_PEERS = 8
 
 
@@ -95,6 +96,7 @@ def _load():
     lib.w4a16_status_string.restype = ctypes.c_char_p
     lib.w4a16_gemm_family.argtypes = [i32, i32, i32]
     lib.w4a16_silu_mul.argtypes = [vp, i32, i32, vp, vp]
+    lib.w4a16_silu_mul_blocked.argtypes = [vp, i32, i32, i32, vp, vp]
     lib.w4a16_lmhead_workspace_bytes.argtypes = [i32, i32, i32]
     lib.w4a16_lmhead_workspace_bytes.restype = sz
     lib.w4a16_lmhead_argmax.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
@@ -134,7 +136,7 @@ def _load():
     lib.w4a16_chain_run_sms.argtypes = [vp, i32, i32, i32, i32, vp, sz, i32, vp]
     for name in ("w4a16_ipc_alloc", "w4a16_ipc_open", "w4a16_ipc_close", "w4a16_ipc_free", "w4a16_chain_plan_sms",
                  "w4a16_chain_run_sms", "w4a16_chain_plan", "w4a16_chain_run", "w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
-                 "w4a16_gemm_family", "w4a16_silu_mul"):
+                 "w4a16_gemm_family", "w4a16_silu_mul", "w4a16_silu_mul_blocked"):
         getattr(lib, name).restype = i32
     return lib
 

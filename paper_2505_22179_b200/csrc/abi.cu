@@ -9,7 +9,7 @@
 extern "C" int w4a16_launch_pack(const uint16_t*, int, int, int, void*, int32_t*, cudaStream_t);
 extern "C" int w4a16_launch_unpack(const void*, int, int, int, uint16_t*, cudaStream_t);
 extern "C" int w4a16_launch_accept(const int32_t*, const int32_t*, const int32_t*, int, int32_t*, cudaStream_t);
-extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, uint16_t*, cudaStream_t);
+extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, int, uint16_t*, cudaStream_t);
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
@@ -145,7 +145,14 @@ extern "C" int w4a16_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, w
   if (!GU || !out) return W4A16_ERR_ARG;
   if (M < 1 || F < 8 || F % 8 != 0) return W4A16_ERR_SHAPE;
   if (!aligned16(GU) || !aligned16(out)) return W4A16_ERR_ALIGN;
-  return w4a16_launch_silu_mul(GU, M, F, out, (cudaStream_t)stream);
+  return w4a16_launch_silu_mul(GU, M, F, F, out, (cudaStream_t)stream);
+}
+
+extern "C" int w4a16_silu_mul_blocked(const uint16_t* GU, int M, int F, int block, uint16_t* out, w4a16_stream_t stream) {
+  if (!GU || !out) return W4A16_ERR_ARG;
+  if (M < 1 || F < 8 || F % 8 != 0 || block < 8 || block % 8 != 0 || F % block != 0) return W4A16_ERR_SHAPE;
+  if (!aligned16(GU) || !aligned16(out)) return W4A16_ERR_ALIGN;
+  return w4a16_launch_silu_mul(GU, M, F, block, out, (cudaStream_t)stream);
 }
 
 extern "C" size_t w4a16_chain_workspace_bytes(const w4a16_op* ops, int n_ops, int M, int family) {

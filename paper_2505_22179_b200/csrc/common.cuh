@@ -31,6 +31,8 @@ struct alignas(64) ChainJob {
   // at flags[xf_off + g], reached the run number). -1: wait for the whole op dep_x instead.
   int xf_off;
   int pub_tiles;           // 1: publish this op's tile-ready flags (a later op reads its Y tile by tile)
+  int epi;                 // GEMM: 0 = plain Y, 1 = SiLU*mul of [64 gate | 64 up] tiles into Y [M][N/2]
+  int xf_mul;              // producer tiles per activation k-group (1, or 2 when X is a GEMM_SILU output)
   int n_tiles;             // job 0: tiles of all GEMM ops (counters, then as many tile-ready flags, in the workspace)
   // ALLREDUCE (include/w4a16.h): every rank's partial as mapped here (rank order), this rank's ready flag in
   // every rank's flag area, this rank's own `world` ready flags of the op's slot, the group's run counter

@@ -68,12 +68,13 @@ struct Cfg {
   static constexpr int kXBox = kMpad * 128;                       // one 64-k SW128 box (multiple of 1024 B)
   static constexpr int kXUnit = 2 * kXBox;
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
-  static constexpr int kRedSlots = 2 * kGroups - 1;               // partial-sum sets handed to (group 0, kh 0)
-  static constexpr int kRedFloats = kRedSlots * 4 * NTB * 2 * 4 * 32;
-  static constexpr int kSumBytes = kR * 2 * NTB * 4 * 16;         // per stage: {-C, -S} float4 per (unit, kh, tb, c4)
-  static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - 1024) / (kStage + kSumBytes);
+  static constexpr int kRedSlots = kGroups - 1;                   // partial-sum sets handed to group 0
+  static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;
+  static constexpr int kSumBytes = kR * NTB * 4 * 16;             // per stage: {-C, -S} float4 per (unit, tb, c4)
+  static constexpr int kXchBytes = 4 * NTB * 4 * 32 * 4;          // SiLU epilogue: up values of a tile (fp16 in u32)
+  static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / (kStage + kSumBytes);
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + 1024;
+  static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + kXchBytes + 1024;
 };
 
 // A single w4a16_gemm is a one-op list whose fields come from GemmParams and the kernel's tensor-map
@@ -86,7 +87,7 @@ using w4::kOpAllReduce;
 struct GemmParams {
   const uint8_t* packed;
   uint16_t* Y;
-  float* partials;   // [slots][G][4 rq][NTB][2 mt][32 lanes] float4 (a CTA publishes at most its first segment per op)
+  float* partials;   // [slots][G][8 row groups][NTB][32 lanes] float4 (a CTA publishes at most its first segment per op)
   int* counters;     // tile counters: [N/128] (single GEMM) or per op at ChainJob::cnt_off (chain)
   int M, K, N;
   int Gk;            // K / 128 groups per n-tile
@@ -109,14 +110,14 @@ struct JobInfo {
   const CUtensorMap* m1;
   int* counters;
   int* flags;             // this op's tile-ready flags (chain) or nullptr
-  int kind, N, Gk, U, dep_x, dep_y, xf_off, pub_tiles;
+  int kind, N, Gk, U, dep_x, dep_y, xf_off, pub_tiles, epi, xf_mul;
   int cs;                 // counter / flag stride (1: single GEMM; 2: chain, counters and flags interleaved)
 };
 __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
   JobInfo J;
   if (p.jobs == nullptr) {
     J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters; J.flags = nullptr; J.cs = 1;
-    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0;
+    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0; J.epi = 0; J.xf_mul = 1;
   } else {
     const ChainJob* c = p.jobs + j;
     // chain: tile counter and tile-ready flag interleaved per tile (same layout in every chain that shares the
@@ -125,7 +126,7 @@ __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap
     J.flags = J.counters + 1;
     J.cs = 2;
     J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y; J.xf_off = c->xf_off;
-    J.pub_tiles = c->pub_tiles;
+    J.pub_tiles = c->pub_tiles; J.epi = c->epi; J.xf_mul = c->xf_mul;
   }
   return J;
 }
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         int g = u0 % J.Gk;
         bool ok = true;
         for (int jj = 0; jj < nu; ++jj) {
-          ok &= ld_acquire_gpu(&p.counters[2 * (J.xf_off + g) + 1]) > run;
+          for (int i = 0; i < J.xf_mul; ++i) ok &= ld_acquire_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1]) > run;
           if (++g == J.Gk) g = 0;
         }
         return ok;
@@ -457,19 +458,24 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                   mma_16816_nv(d[jj][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
                 }
           if (c4 == 0) {
+            // the consumers own whole units (all 128 k): sum the two k-halves' -C and -S per token
 #pragma unroll
-            for (int jj = 0; jj < NU; ++jj)
+            for (int jj = 0; jj < NU; ++jj) {
+              if (NTB == 1) {   // rows g8 / g8 + 8 = k-half 0 / 1 of token tok_pi(g8)
+                const int m = tok_pi(g8);
+                const uint32_t slot = sb + (((jbase + jj) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
+                sts32f(slot, d[jj][0][0] + d[jj][0][2]);       // -C[m]
+                sts32f(slot + 8, d[jj][0][1] + d[jj][0][3]);   // -S[m]
+              } else {          // pass pz = k-half; rows g8 / g8 + 8 = tokens tok_pi(g8) / 8 + tok_pi(g8)
 #pragma unroll
-              for (int pz = 0; pz < kPasses; ++pz)
-#pragma unroll
-                for (int rh = 0; rh < 2; ++rh) {   // D rows g8 (rh 0) and g8+8 (rh 1)
-                  const int kh = NTB == 1 ? rh : pz;
-                  const int m = NTB == 1 ? tok_pi(g8) : 8 * rh + tok_pi(g8);
-                  // consumer lane c4 holds MMA columns 2c4, 2c4 + 1 = tokens c4, c4 + 4 of the block
-                  const uint32_t slot = sb + ((((jbase + jj) * 2 + kh) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
-                  sts32f(slot, d[jj][pz][2 * rh]);          // -C[m]
-                  sts32f(slot + 8, d[jj][pz][2 * rh + 1]);  // -S[m]
+                for (int rh = 0; rh < 2; ++rh) {
+                  const int m = 8 * rh + tok_pi(g8);
+                  const uint32_t slot = sb + (((jbase + jj) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
+                  sts32f(slot, d[jj][0][2 * rh] + d[jj][kPasses - 1][2 * rh]);
+                  sts32f(slot + 8, d[jj][0][2 * rh + 1] + d[jj][kPasses - 1][2 * rh + 1]);
                 }
+              }
+            }
           }
         };
         if (p.dbg & 32) {
@@ -545,15 +551,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   };
   pdl_wait();   // Y / workspace writes must follow the preceding kernel (returns at once when satisfied)
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
-  const int rq = warp & 3, kh = (warp >> 2) & 1, grp = warp >> 3;   // row quarter, k half, unit group
-  int rows[2][2];                              // tile rows owned by this lane: [m-tile][g / g+8]
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    rows[mt][0] = 32 * rq + 16 * mt + g8;
-    rows[mt][1] = rows[mt][0] + 8;
-  }
+  // warp (grp, r8): tile rows 16 r8 .. 16 r8 + 15 (one m16 MMA tile) and all 128 k of its group's units
+  const int r8 = warp & 7, grp = warp >> 3;
+  const int row0 = 16 * r8 + g8, row1 = row0 + 8;   // this lane's two tile rows (fragment rows g / g + 8)
 
-  float acc[2][NTB][4];
+  float acc[NTB][4];
   int s = 0;
   uint32_t ph = 0;
   const uint32_t ready_base = smem_u32(kScaleInA ? &full_bar[0] : &sums_bar[0]);
@@ -600,61 +602,80 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // Y writes (and this op's partial slot) wait for the earlier ops that read / write the same buffers.
     const int wdep = chain ? max(J.dep_y, job - p.slots) : -1;
     bool y_ready = wdep < 0;
-    float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (4 * NTB * 2 * 32);
+    float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (8 * NTB * 32);
 
     auto flush = [&](int t, int sg0, int sg1) {
       if (!y_ready) {
         if (threadIdx.x == 0) wait_op(p, wdep);   // released to the other warps by the barrier below
         y_ready = true;
       }
-      // 1. combine the k-halves and unit groups: every (grp, kh) != (0, 0) hands its partial sums to
-      //    (0, 0) through shared memory; (0, 0) adds them in fixed slot order
-      const int slot_id = grp * 2 + kh;   // 0 = owner
-      if (slot_id != 0) {
+      // 1. combine the unit groups: group 1 hands its partial sums to group 0 through shared memory
+      if (grp != 0) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-          for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              red[((((slot_id - 1) * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane] = acc[mt][tb][e];
+          for (int e = 0; e < 4; ++e) red[(((grp - 1) * 8 + r8) * NTB + tb) * 128 + e * 32 + lane] = acc[tb][e];
       }
       named_bar_sync(1, kWarps * 32);
-      if (slot_id == 0) {
+      if (grp == 0) {
 #pragma unroll
         for (int sl = 0; sl < C::kRedSlots; ++sl)
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
+          for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[tb][e] += red[((sl * 8 + r8) * NTB + tb) * 128 + e * 32 + lane];
+      }
+      named_bar_sync(1, kWarps * 32);
+      if (grp != 0) return;
+      // 2. the eight group-0 warps own the result
+      const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
+      auto store = [&](float (&v)[NTB][4]) {
+        if (J.epi == 1) {
+          // SiLU*mul epilogue (W4A16_OP_GEMM_SILU): tile rows 0..63 are gate, 64..127 the matching up columns;
+          // the up warps (r8 >= 4) hand their fp16-rounded values to the gate warps through a shared-memory
+          // area of their own (group 1 may already be writing `red` for its next flush), and the gate warps
+          // write Y[m][64 t + row] = fp16(silu(g) * u) — w4a16_silu_mul's arithmetic
+          uint32_t* xch = reinterpret_cast<uint32_t*>(smem + S * (C::kStage + C::kSumBytes) + C::kRedFloats * 4);
+          if (r8 >= 4) {
 #pragma unroll
             for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) acc[mt][tb][e] += red[(((sl * 4 + rq) * 2 + mt) * NTB + tb) * 128 + e * 32 + lane];
-      }
-      named_bar_sync(1, kWarps * 32);
-      if (slot_id != 0) return;
-      // 2. the four kh = 0 warps own the result
-      const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
-      auto store = [&](float (&v)[2][NTB][4]) {
+              for (int e = 0; e < 4; ++e)
+                xch[(((r8 - 4) * NTB + tb) * 4 + e) * 32 + lane] = __half_as_ushort(__float2half_rn(v[tb][e]));
+          }
+          named_bar_sync(2, 8 * 32);
+          if (r8 < 4) {
+            const int Nh = J.N / 2, c0 = t * 64 + row0, c1 = t * 64 + row1;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int n0 = t * kTileN + rows[mt][0], n1 = t * kTileN + rows[mt][1];
+            for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-          for (int tb = 0; tb < NTB; ++tb) {
-            const int m0 = tb * 8 + c4, m1 = m0 + 4;   // MMA columns 2c4, 2c4 + 1 = tokens tok_pi(2c4), tok_pi(2c4 + 1)
-            if (m0 < p.M) {
-              J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][0]));
-              J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][2]));
-            }
-            if (m1 < p.M) {
-              J.Y[(size_t)m1 * J.N + n0] = __half_as_ushort(__float2half_rn(v[mt][tb][1]));
-              J.Y[(size_t)m1 * J.N + n1] = __half_as_ushort(__float2half_rn(v[mt][tb][3]));
-            }
+              for (int e = 0; e < 4; ++e) {
+                const float g = __half2float(__float2half_rn(v[tb][e]));
+                const float u = __half2float(__ushort_as_half((uint16_t)xch[((r8 * NTB + tb) * 4 + e) * 32 + lane]));
+                const int m = tb * 8 + c4 + 4 * (e & 1);
+                if (m < p.M) J.Y[(size_t)m * Nh + ((e >> 1) ? c1 : c0)] = __half_as_ushort(__float2half_rn(g / (1.0f + __expf(-g)) * u));
+              }
+          }
+          named_bar_sync(2, 8 * 32);   // xch is reused by the next flush
+          return;
+        }
+        const int n0 = t * kTileN + row0, n1 = t * kTileN + row1;
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          const int m0 = tb * 8 + c4, m1 = m0 + 4;   // MMA columns 2c4, 2c4 + 1 = tokens tok_pi(2c4), tok_pi(2c4 + 1)
+          if (m0 < p.M) {
+            J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[tb][0]));
+            J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[tb][2]));
+          }
+          if (m1 < p.M) {
+            J.Y[(size_t)m1 * J.N + n0] = __half_as_ushort(__float2half_rn(v[tb][1]));
+            J.Y[(size_t)m1 * J.N + n1] = __half_as_ushort(__float2half_rn(v[tb][3]));
           }
         }
       };
       auto tile_written = [&]() {   // chain: the tile's Y is complete -> its ready flag (tile-level deps)
         if (!chain || !J.pub_tiles) return;
-        named_bar_sync(2, 4 * 32);
+        named_bar_sync(2, 8 * 32);
         if (threadIdx.x == 0) publish(&J.flags[J.cs * t], run_c + 1);
       };
       if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); tile_written(); return; }
@@ -664,14 +685,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       // on (no round trip); the owner acquires the counter, adds the partials in CTA order to its own and
       // writes Y. All G CTAs are co-resident (G = resident capacity), so the owner's wait always completes.
       const int c_first = cta_of_unit(tile_u0, J.U, p.G), c_last = cta_of_unit(tile_u1 - 1, J.U, p.G);
-      auto pidx = [&](int c, int tb, int mt) { return ((((size_t)c * 4 + rq) * NTB + tb) * 2 + mt) * 32 + lane; };
+      auto pidx = [&](int c, int tb) { return (((size_t)c * 8 + r8) * NTB + tb) * 32 + lane; };
       if (cta != c_first) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int tb = 0; tb < NTB; ++tb)
-            __stcg(&part[pidx(cta, tb, mt)], make_float4(acc[mt][tb][0], acc[mt][tb][1], acc[mt][tb][2], acc[mt][tb][3]));
-        named_bar_sync(2, 4 * 32);
+        for (int tb = 0; tb < NTB; ++tb) __stcg(&part[pidx(cta, tb)], make_float4(acc[tb][0], acc[tb][1], acc[tb][2], acc[tb][3]));
+        named_bar_sync(2, 8 * 32);
         if (threadIdx.x == 0) publish(&J.counters[J.cs * t]);
         return;
       }
@@ -682,162 +700,133 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         trace_op(p, job, 5);
         J.counters[J.cs * t] = 0;   // every contributor has arrived: re-arm for the next launch
       }
-      named_bar_sync(2, 4 * 32);
+      named_bar_sync(2, 8 * 32);
       for (int c = c_first + 1; c <= c_last; ++c) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int tb = 0; tb < NTB; ++tb) {
-            const float4 v = __ldcg(&part[pidx(c, tb, mt)]);
-            acc[mt][tb][0] += v.x; acc[mt][tb][1] += v.y; acc[mt][tb][2] += v.z; acc[mt][tb][3] += v.w;
-          }
+        for (int tb = 0; tb < NTB; ++tb) {
+          const float4 v = __ldcg(&part[pidx(c, tb)]);
+          acc[tb][0] += v.x; acc[tb][1] += v.y; acc[tb][2] += v.z; acc[tb][3] += v.w;
+        }
       }
       store(acc);
       tile_written();
     };
 
     // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
-    // dequant + 16 MMAs, then the post-MMA group scale.
+    // dequant + 8 MMAs (one m16 tile x 8 k-steps), then the post-MMA group scale.
     auto process_unit = [&](uint32_t st, uint32_t sb, int j) {
-      const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box kh holds k 64kh..
+      const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box b holds k 64b..
       const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
-      uint4 xr[2][NTB];
+      uint4 xr[4][NTB];                                       // [32-k chunk p][token block]
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc)
+      for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
           const int m = 8 * tb + tok_pi(g8);                    // MMA column g8 carries token tok_pi(g8)
-          const int jx = 4 * cc + c4;                           // chunk pch = 2kh + cc: k 32 pch + 8 c4 .. +7
-          if (W4_MA_EXP & 4) xr[cc][tb] = make_uint4(0x3c003c00u + m, 0x3c003c00u, 0x3c003c00u ^ jx, 0x3c003c00u);
-          else xr[cc][tb] = lds128(xu + kh * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
+          const int jx = 4 * (pc & 1) + c4;                     // chunk pc: k 32 pc + 8 c4 .. +7
+          if (W4_MA_EXP & 4) xr[pc][tb] = make_uint4(0x3c003c00u + m, 0x3c003c00u, 0x3c003c00u ^ jx, 0x3c003c00u);
+          else xr[pc][tb] = lds128(xu + (pc >> 1) * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
-      uint32_t wq[2][2][2];                                     // [cc][mt][row g / g+8]
-      // One ldmatrix.x4 per chunk: matrix q = (mt, hf) is the 8 rows 32rq + 16mt + 8hf + 0..7 of the
-      // chunk, and lane (g8, c4) receives word c4 of row g8 — exactly its code word (conflict-free: the
+      uint32_t wq[4][2];                                      // [chunk][row g / g + 8]
+      // Two ldmatrix.x4: matrix q = (hf = q & 1, chunk 2 pp + (q >> 1)) is the 8 rows 16 r8 + 8 hf + 0..7 of
+      // that chunk, and lane (g8, c4) receives word c4 of row g8 — exactly its code word (conflict-free: the
       // XOR chunk layout spreads the 8 rows over all 32 banks).
       {
-        const int lr = 32 * rq + 8 * (lane >> 3) + (lane & 7);   // lanes 8q..8q+7: rows of matrix q
+        const int lr = 16 * r8 + 8 * ((lane >> 3) & 1) + (lane & 7);
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int pch = 2 * kh + cc;
-          ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[cc][0][0], wq[cc][0][1], wq[cc][1][0], wq[cc][1][1]);
+        for (int pp = 0; pp < 2; ++pp) {
+          const int pch = 2 * pp + (lane >> 4);
+          ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[2 * pp][0], wq[2 * pp][1], wq[2 * pp + 1][0],
+                  wq[2 * pp + 1][1]);
         }
       }
-      float sc[2][2], zrow[2][2];
-      __half2 zp[2][2];
+      float sc[2], zrow[2];
+      __half2 zp[2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int r = rows[mt][hf];
-          if (SYM) {
-            sc[mt][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
-            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
-            zrow[mt][hf] = 8.f;
-          } else if (W4_MA_EXP & 8) {
-            sc[mt][hf] = 0.01f * (r + 1);
-            zrow[mt][hf] = 8.f;
-            zp[mt][hf] = __floats2half2_rn(72.f, 1032.f);
-          } else {
-            const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
-            sc[mt][hf] = __low2float(sz);
-            zrow[mt][hf] = __high2float(sz);
-            zp[mt][hf] = zero_pair(__high2half(sz));
-          }
+      for (int hf = 0; hf < 2; ++hf) {
+        const int r = hf ? row1 : row0;
+        if (SYM) {
+          sc[hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+          zp[hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
+          zrow[hf] = 8.f;
+        } else if (W4_MA_EXP & 8) {
+          sc[hf] = 0.01f * (r + 1);
+          zrow[hf] = 8.f;
+          zp[hf] = __floats2half2_rn(72.f, 1032.f);
+        } else {
+          const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
+          sc[hf] = __low2float(sz);
+          zrow[hf] = __high2float(sz);
+          zp[hf] = zero_pair(__high2half(sz));
         }
+      }
       if constexpr (kScaleInA) {
         // w_hat = fp16((q - z) * s) in the A fragments (exactly the oracle's dequantised weight), accumulated
-        // straight into acc: no per-unit group accumulator (saves 16 registers at NTB = 2).
-        __half2 s2[2][2];
+        // straight into acc: no per-unit group accumulator.
+        __half2 s2[2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int hf = 0; hf < 2; ++hf) s2[hf] = __float2half2_rn(sc[hf]);
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) s2[mt][hf] = __float2half2_rn(sc[mt][hf]);
+        for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc)
+          for (int hs = 0; hs < 2; ++hs) {
+            const uint32_t qa = hs ? wq[pc][0] >> 8 : wq[pc][0];
+            const uint32_t qb = hs ? wq[pc][1] >> 8 : wq[pc][1];
+            const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[0])), s2[0]));
+            const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[1])), s2[1]));
+            const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[0])), s2[0]));
+            const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[1])), s2[1]));
 #pragma unroll
-          for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
-              const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-              const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[mt][0])), s2[mt][0]));
-              const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[mt][1])), s2[mt][1]));
-              const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[mt][0])), s2[mt][0]));
-              const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[mt][1])), s2[mt][1]));
-#pragma unroll
-              for (int tb = 0; tb < NTB; ++tb) {
-                const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-                mma_16816(acc[mt][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
-              }
+            for (int tb = 0; tb < NTB; ++tb) {
+              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
+              mma_16816(acc[tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
             }
+          }
       } else {
         // Post-scale with offset codes: one LOP3 per code pair, no zero-point arithmetic.
         //   lo slots: (w & 0x000F000F) | 0x6400 -> 1024 + q      hi slots: (w & 0x00F000F0) | 0x5400 -> 64 + q
         // so the MMA sums sum_k (off_k + q_k) x_k. The offsets and the zero point come back out as
         //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
-        // with C and S of this unit's k-half supplied by the activation-sum warp and folded into the
-        // initial group accumulator: gacc0 = -C - z S.
+        // with C and S of the unit supplied by the activation-sum warp and folded into the initial group
+        // accumulator: gacc0 = -C - z S.
         float cs[NTB][4];   // {-C[m0], -C[m1], -S[m0], -S[m1]}, m0 = 8tb + c4, m1 = m0 + 4 (activation-sum warp)
 #pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
-          const float4 v = lds128f(sb + (((j * 2 + kh) * NTB + tb) * 4 + c4) * 16);
+          const float4 v = lds128f(sb + ((j * NTB + tb) * 4 + c4) * 16);
           cs[tb][0] = v.x; cs[tb][1] = v.y; cs[tb][2] = v.z; cs[tb][3] = v.w;
         }
-        float zf[2][2];
+        float gacc[NTB][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) zf[mt][hf] = SYM ? 8.f : zrow[mt][hf];
-        // m-tiles innermost when registers allow (NTB = 1): the two accumulation chains alternate, so a
-        // dependent MMA is never issued right behind its predecessor; at NTB = 2 the token blocks alternate.
-        constexpr int kMtGroups = NTB == 1 ? 1 : 2;
-        constexpr int kMtPer = 2 / kMtGroups;
+          for (int e = 0; e < 4; ++e)
+            gacc[tb][e] = (W4_MA_EXP & 1) ? acc[tb][e] : fmaf(SYM ? 8.f : zrow[e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
 #pragma unroll
-        for (int mg = 0; mg < kMtGroups; ++mg) {
-          float gacc[kMtPer][NTB][4];
+        for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
-          for (int mi = 0; mi < kMtPer; ++mi)
-#pragma unroll
-            for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                gacc[mi][tb][e] = (W4_MA_EXP & 1) ? acc[mg * kMtPer + mi][tb][e]
-                                                  : fmaf(zf[mg * kMtPer + mi][e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-              for (int mi = 0; mi < kMtPer; ++mi) {
-                const int mt = mg * kMtPer + mi;
-                const uint32_t qa = hs ? wq[cc][mt][0] >> 8 : wq[cc][mt][0];
-                const uint32_t qb = hs ? wq[cc][mt][1] >> 8 : wq[cc][mt][1];
-                const uint32_t a0 = (W4_MA_EXP & 2) ? qa : lop3_and_or(qa, 0x000F000Fu, 0x64006400u);
-                const uint32_t a1 = (W4_MA_EXP & 2) ? qb : lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
-                const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : lop3_and_or(qa, 0x00F000F0u, 0x54005400u);
-                const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
-#pragma unroll
-                for (int tb = 0; tb < NTB; ++tb) {
-                  const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[cc][tb]);
-                  mma_16816_nv(gacc[mi][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
-                }
-              }
-#pragma unroll
-          for (int mi = 0; mi < kMtPer; ++mi)
+          for (int hs = 0; hs < 2; ++hs) {
+            const uint32_t qa = hs ? wq[pc][0] >> 8 : wq[pc][0];
+            const uint32_t qb = hs ? wq[pc][1] >> 8 : wq[pc][1];
+            const uint32_t a0 = (W4_MA_EXP & 2) ? qa : lop3_and_or(qa, 0x000F000Fu, 0x64006400u);
+            const uint32_t a1 = (W4_MA_EXP & 2) ? qb : lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
+            const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : lop3_and_or(qa, 0x00F000F0u, 0x54005400u);
+            const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
 #pragma unroll
             for (int tb = 0; tb < NTB; ++tb) {
-              const int mt = mg * kMtPer + mi;
-              if (W4_MA_EXP & 1) {
-                acc[mt][tb][0] = gacc[mi][tb][0]; acc[mt][tb][1] = gacc[mi][tb][1];
-                acc[mt][tb][2] = gacc[mi][tb][2]; acc[mt][tb][3] = gacc[mi][tb][3];
-                continue;
-              }
-              acc[mt][tb][0] = fmaf(sc[mt][0], gacc[mi][tb][0], acc[mt][tb][0]);
-              acc[mt][tb][1] = fmaf(sc[mt][0], gacc[mi][tb][1], acc[mt][tb][1]);
-              acc[mt][tb][2] = fmaf(sc[mt][1], gacc[mi][tb][2], acc[mt][tb][2]);
-              acc[mt][tb][3] = fmaf(sc[mt][1], gacc[mi][tb][3], acc[mt][tb][3]);
+              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
+              mma_16816_nv(gacc[tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
             }
+          }
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) {
+          if (W4_MA_EXP & 1) {
+            acc[tb][0] = gacc[tb][0]; acc[tb][1] = gacc[tb][1]; acc[tb][2] = gacc[tb][2]; acc[tb][3] = gacc[tb][3];
+            continue;
+          }
+          acc[tb][0] = fmaf(sc[0], gacc[tb][0], acc[tb][0]);
+          acc[tb][1] = fmaf(sc[0], gacc[tb][1], acc[tb][1]);
+          acc[tb][2] = fmaf(sc[1], gacc[tb][2], acc[tb][2]);
+          acc[tb][3] = fmaf(sc[1], gacc[tb][3], acc[tb][3]);
         }
       }
     };
@@ -852,9 +841,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       boundary = (cur_t + 1) * J.Gk;
       seg_u0 = u;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) acc[mt][tb][0] = acc[mt][tb][1] = acc[mt][tb][2] = acc[mt][tb][3] = 0.f;
+      for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0.f;
     };
     auto stage_begin = [&](int i) {
       if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
@@ -901,8 +888,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     trace_ma(p, 3);
     // This CTA's share of the op is written: count it. Only the four warps that store Y / partials (group 0,
     // k-half 0) take part; the other warps are already streaming the next op.
-    if (chain && grp == 0 && kh == 0) {
-      named_bar_sync(2, 4 * 32);
+    if (chain && grp == 0) {
+      named_bar_sync(2, 8 * 32);
       if (threadIdx.x == 0) publish(&p.done[job]);
     }
     trace_op(p, job, 3);
@@ -1014,14 +1001,16 @@ int chain_family(int M, int family) {
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 struct Span { uintptr_t a, b; };
 bool overlaps(Span x, Span y) { return x.a < y.b && y.a < x.b; }
-int ldx_of(const w4a16_op& o) { return o.kind == W4A16_OP_GEMM && o.ldx > 0 ? o.ldx : o.K; }
+bool is_gemm(int kind) { return kind == W4A16_OP_GEMM || kind == W4A16_OP_GEMM_SILU; }
+int ldx_of(const w4a16_op& o) { return is_gemm(o.kind) && o.ldx > 0 ? o.ldx : o.K; }
+int y_cols(const w4a16_op& o) { return o.kind == W4A16_OP_GEMM_SILU ? o.N / 2 : o.N; }   // Y row stride
 Span x_span(const w4a16_op& o, int M) {   // rows of X with their row stride (gaps between rows included)
   const uintptr_t a = reinterpret_cast<uintptr_t>(o.X);
   return {a, a + ((size_t)(M - 1) * (size_t)ldx_of(o) + (size_t)o.K) * 2};
 }
 Span y_span(const w4a16_op& o, int M) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(o.Y);
-  return {a, a + (size_t)M * (size_t)o.N * 2};
+  return {a, a + (size_t)M * (size_t)y_cols(o) * 2};
 }
 // Validate the ops; on success return the number of tile counters and the common mode.
 int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, int* mode) {
@@ -1034,7 +1023,7 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
     const w4a16_op& o = ops[j];
     if (!o.X || !o.Y) return W4A16_ERR_ARG;
     if (!al16(o.X) || !al16(o.Y)) return W4A16_ERR_ALIGN;
-    if (o.kind == W4A16_OP_GEMM) {
+    if (is_gemm(o.kind)) {
       if (!o.packed || (o.mode != W4A16_ASYM && o.mode != W4A16_SYM)) return W4A16_ERR_ARG;
       if (*mode >= 0 && o.mode != *mode) return W4A16_ERR_ARG;
       *mode = o.mode;
@@ -1119,12 +1108,13 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
     const w4a16_op& o = ops[j];
     w4::ma::ChainJob& J = jobs[j];
     memset(&J, 0, sizeof(J));
-    J.kind = o.kind;
-    J.packed = reinterpret_cast<const uint8_t*>(o.kind == W4A16_OP_GEMM ? o.packed : o.X);
+    J.kind = is_gemm(o.kind) ? W4A16_OP_GEMM : o.kind;
+    J.epi = o.kind == W4A16_OP_GEMM_SILU ? 1 : 0;
+    J.packed = reinterpret_cast<const uint8_t*>(is_gemm(o.kind) ? o.packed : o.X);
     J.Y = reinterpret_cast<uint16_t*>(o.Y);
     J.K = o.K;
     J.N = o.N;
-    if (o.kind == W4A16_OP_GEMM) {
+    if (is_gemm(o.kind)) {
       J.Gk = o.K / 128;
       J.U = (o.N / 128) * J.Gk;
       J.cnt_off = cnt;
@@ -1153,17 +1143,20 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
     J.dep_x = -1;
     J.dep_y = -1;
     J.xf_off = -1;
+    J.xf_mul = 1;
     for (int i = j - 1; i >= 0 && (J.dep_x < 0 || J.dep_y < 0); --i) {
       if (J.dep_x < 0 && overlaps(y_span(ops[i], M), x_span(o, M))) J.dep_x = i;
       if (J.dep_y < 0 && (overlaps(y_span(ops[i], M), y_span(o, M)) || overlaps(x_span(ops[i], M), y_span(o, M)))) J.dep_y = i;
     }
     // tile-level RAW dependency: X is a whole-tile column range of the producing GEMM's Y with Y's row stride
-    if (o.kind == W4A16_OP_GEMM && J.dep_x >= 0 && ops[J.dep_x].kind == W4A16_OP_GEMM) {
+    // (a GEMM_SILU producer writes 64 output columns per tile: 2 tiles per 128-column k-group)
+    if (is_gemm(o.kind) && J.dep_x >= 0 && is_gemm(ops[J.dep_x].kind)) {
       const w4a16_op& d = ops[J.dep_x];
+      const int per_tile = d.kind == W4A16_OP_GEMM_SILU ? 64 : 128, yc = y_cols(d);
       const uintptr_t xb = reinterpret_cast<uintptr_t>(o.X), yb = reinterpret_cast<uintptr_t>(d.Y);
-      if (xb >= yb && (xb - yb) % 256 == 0 && ldx_of(o) == d.N && (int)((xb - yb) / 2) + o.K <= d.N)
-      {
-        J.xf_off = jobs[J.dep_x].cnt_off + (int)((xb - yb) / 2) / 128;
+      if (xb >= yb && (xb - yb) % 256 == 0 && ldx_of(o) == yc && (int)((xb - yb) / 2) + o.K <= yc) {
+        J.xf_mul = 128 / per_tile;
+        J.xf_off = jobs[J.dep_x].cnt_off + (int)((xb - yb) / 2) / per_tile;
         jobs[J.dep_x].pub_tiles = 1;   // the producing op publishes its tile-ready flags
       }
     }

@@ -6,25 +6,27 @@
 
 namespace w4 {
 
-__global__ void __launch_bounds__(256) silu_mul_kernel(const uint16_t* __restrict__ GU, int M, int F,
+__global__ void __launch_bounds__(256) silu_mul_kernel(const uint16_t* __restrict__ GU, int M, int F, int block,
                                                        uint16_t* __restrict__ out) {
   const int vecs = F / 8;  // 8 halves per 16-byte vector
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)M * vecs;
        i += (long long)gridDim.x * blockDim.x) {
     const int m = (int)(i / vecs), v = (int)(i % vecs);
-    const uint4 g = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + (size_t)v * 8);
-    const uint4 u = *reinterpret_cast<const uint4*>(GU + (size_t)m * 2 * F + F + (size_t)v * 8);
+    const int b = (v * 8) / block, o = v * 8 - b * block;   // block b, offset o inside it
+    const uint16_t* row = GU + (size_t)m * 2 * F + (size_t)2 * b * block + o;
+    const uint4 g = *reinterpret_cast<const uint4*>(row);
+    const uint4 u = *reinterpret_cast<const uint4*>(row + block);
     *reinterpret_cast<uint4*>(out + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
   }
 }
 
 }  // namespace w4
 
-extern "C" int w4a16_launch_silu_mul(const uint16_t* GU, int M, int F, uint16_t* out, cudaStream_t stream) {
+extern "C" int w4a16_launch_silu_mul(const uint16_t* GU, int M, int F, int block, uint16_t* out, cudaStream_t stream) {
   const long long work = (long long)M * (F / 8);
   if (work == 0) return W4A16_OK;
   long long blocks = (work + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  w4::silu_mul_kernel<<<(unsigned)blocks, 256, 0, stream>>>(GU, M, F, out);
+  w4::silu_mul_kernel<<<(unsigned)blocks, 256, 0, stream>>>(GU, M, F, block, out);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }

@@ -14,7 +14,7 @@ from ._lib import (  # noqa: F401
     W4A16_ASYM, W4A16_SYM, W4A16_GROUP, W4A16_MAX_M, W4A16_MAX_TREE,
     W4A16_DEV_OK, W4A16_DEV_NONFINITE, W4A16_DEV_BAD_TREE,
     W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05_OC,
-    W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE, W4A16_MAX_PEERS, W4A16Op, W4A16PeerGroup,
+    W4A16_OP_GEMM, W4A16_OP_SILU_MUL, W4A16_OP_ALLREDUCE, W4A16_OP_GEMM_SILU, W4A16_MAX_PEERS, W4A16Op, W4A16PeerGroup,
 )
 
 
@@ -172,6 +172,13 @@ def w4a16_silu_mul(GU, out, stream=None):
                              _stream(stream)), "w4a16_silu_mul")
 
 
+def w4a16_silu_mul_blocked(GU, out, block: int, stream=None):
+    """out [M, F] = silu(gate) * up of GU [M, 2F] laid out in blocks of `block` gate then `block` up columns."""
+    M, F2 = GU.shape
+    check(lib.w4a16_silu_mul_blocked(_ptr(GU, torch.float16, "GU"), M, F2 // 2, int(block), _ptr(out, torch.float16, "out"),
+                                     _stream(stream)), "w4a16_silu_mul_blocked")
+
+
 def w4a16_status_string(status: int) -> str:
     return status_string(status)
 
@@ -208,7 +215,8 @@ def pack_linear(W: torch.Tensor, mode=W4A16_ASYM, dev_status=None, stream=None) 
 class Chain:
     """A sequence of ops run as ONE persistent launch (include/w4a16.h: w4a16_chain_plan / w4a16_chain_run).
 
-    ops: ("gemm", X [M,K] fp16, PackedLinear, Y [M,N] fp16) or ("silu_mul", GU [M,2F] fp16, out [M,F] fp16).
+    ops: ("gemm", X [M,K] fp16, PackedLinear, Y [M,N] fp16), ("gemm_silu", X, PackedLinear, out [M,N/2] fp16)
+    (gate-up with SiLU*mul fused; weight columns in [64 gate | 64 up] tiles) or ("silu_mul", GU [M,2F], out [M,F]).
     The plan (TMA descriptors, dependencies) is encoded once by the library into host memory and copied to
     the device here; the tensors must stay where they are while the chain is in use (references are kept)."""
 
@@ -222,12 +230,13 @@ class Chain:
         arr = (W4A16Op * len(ops))()
         mode = W4A16_ASYM
         for i, op in enumerate(ops):
-            if op[0] == "gemm":
+            if op[0] in ("gemm", "gemm_silu"):
                 _, X, pl, Y = op
-                if X.shape[0] != M or Y.shape[0] != M or X.shape[1] != pl.K or Y.shape[1] != pl.N:
+                ny = pl.N if op[0] == "gemm" else pl.N // 2
+                if X.shape[0] != M or Y.shape[0] != M or X.shape[1] != pl.K or Y.shape[1] != ny:
                     raise W4A16Error(f"chain op {i}: shapes do not match M={M}, K={pl.K}, N={pl.N}")
-                arr[i] = W4A16Op(W4A16_OP_GEMM, _ptr_rows(X, "X"), _ptr(pl.packed, None, "packed"),
-                                 _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode, _ldx(X))
+                arr[i] = W4A16Op(W4A16_OP_GEMM if op[0] == "gemm" else W4A16_OP_GEMM_SILU, _ptr_rows(X, "X"),
+                                 _ptr(pl.packed, None, "packed"), _ptr(Y, torch.float16, "Y"), pl.K, pl.N, pl.mode, _ldx(X))
                 mode = pl.mode
                 self._keep += [X, pl.packed, Y]
             elif op[0] == "allreduce":

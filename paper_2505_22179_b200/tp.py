@@ -3,14 +3,16 @@
 One process per GPU. Megatron-style partition of each Llama decoder layer's linear layers:
   * column-parallel (split N, no communication): QKV (head-aligned: rank r owns q heads
     [r*nq/t, (r+1)*nq/t) and kv heads [r*nkv/t, ...)), gate-up (rank r owns the matching gate AND up
-    columns, stored locally as [gate_r | up_r] so w4a16_silu_mul pairs them);
+    columns, given by make_weight as [gate_r | up_r] and stored interleaved in [64 gate | 64 up] tiles so the
+    gate-up GEMM's epilogue can apply SiLU*mul);
   * row-parallel (split K): O (rank's heads) and down (rank's FFN slice); each rank produces a partial
     Y[M, hidden] that an all-reduce (NCCL over NVLink/NVSwitch, via torch.distributed) sums.
 Data flow of one verify forward (the dependencies of a real decoder stack: the target
 verifies the draft "in one forward pass"):
   h_0 = x_in;  per layer l:  qkv = h_l . W_qkv;  o = qkv[:, :K_o] . W_o  (the attention stub: the rank's query
   columns stand in for the attention output, whose kernel is SURVEY §8(f) f2 and outside the timed stack);
-  [all-reduce];  gu = o . W_gu;  act = silu(gate) * up;  h_{l+1} = act . W_down  [all-reduce].
+  [all-reduce];  act = silu(gate) * up of gu = o . W_gu (fused into the gate-up GEMM's epilogue in chains:
+  the gate-up weight is stored in 128-column tiles of [64 gate | 64 up]);  h_{l+1} = act . W_down  [all-reduce].
 Attention, norms and residual adds are outside the hot path. So every GEMM reads what the previous one
 wrote: QKV -> O -> gate-up -> SiLU*mul -> down -> QKV of the next layer (read-after-write edges, which a
 persistent chain must honour). Because the norms are absent, `calibrate=True` rescales each synthetic weight
@@ -26,7 +28,16 @@ import torch
 import torch.distributed as dist
 
 from .ops import (W4A16_ASYM, Chain, PackedLinear, PeerGroup, W4A16Error, alloc_workspace, pack_linear,
-                  verify_accept, w4a16_peer_flag_bytes, w4a16_silu_mul)
+                  verify_accept, w4a16_peer_flag_bytes, w4a16_silu_mul_blocked)
+
+SILU_BLOCK = 64   # gate-up weight columns are stored in 128-column tiles of [64 gate | 64 up] (W4A16_OP_GEMM_SILU)
+
+
+def interleave_gate_up(W: torch.Tensor) -> torch.Tensor:
+    """[K, 2F] in the logical [gate | up] column order -> [64 gate | 64 up] blocks (the stored layout)."""
+    K, F2 = W.shape
+    F = F2 // 2
+    return W.view(K, 2, F // SILU_BLOCK, SILU_BLOCK).permute(0, 2, 1, 3).reshape(K, F2)
 
 
 @dataclass(frozen=True)
@@ -129,7 +140,9 @@ class VerifyStack:
             for name in MATRICES:
                 s = self.plan[name]
                 W = tmp[: s["K"] * s["N"]].view(s["K"], s["N"])
-                make_weight(l, name, s["K"], s["N"], W)
+                make_weight(l, name, s["K"], s["N"], W)   # logical column order ([gate | up] for gate-up)
+                if name == "gate_up":
+                    W.copy_(interleave_gate_up(W))
                 mats[name] = pack_linear(W, mode=mode, dev_status=self.status)
                 if cal is not None:
                     mats[name] = cal.step(l, name, W, mats[name])
@@ -190,7 +203,7 @@ class VerifyStack:
         """The layer's ops between its all-reduces: [QKV, O] and [gate-up, SiLU*mul, down]; with the fused
         all-reduce each segment ends with its ALLREDUCE op (partial in the peer region -> reduced output)."""
         a = [("gemm", self.layer_input(l, M), L["qkv"], self.y_qkv[:M]), ("gemm", self.q_part(M), L["o"], self.y_o[:M])]
-        b = [("gemm", self.y_o_red[:M], L["gate_up"], self.y_gu[:M]), ("silu_mul", self.y_gu[:M], self.act[:M]),
+        b = [("gemm_silu", self.y_o_red[:M], L["gate_up"], self.act[:M]),   # gate-up with SiLU*mul fused
              ("gemm", self.act[:M], L["down"], self.y_down[:M])]
         if self.fused:
             a.append(("allreduce", self.y_o[:M], self.y_o_red[:M], self.peers))
@@ -246,7 +259,7 @@ class VerifyStack:
                 o_out.copy_(self.y_o[:M])
             self._allreduce(o_out)
             L["gate_up"](o_out, self.y_gu[:M], ws, stream)
-            w4a16_silu_mul(self.y_gu[:M], self.act[:M], stream)
+            w4a16_silu_mul_blocked(self.y_gu[:M], self.act[:M], SILU_BLOCK, stream)
             L["down"](self.act[:M], self.y_down[:M], ws, stream)
             if self.fused:
                 d_out.copy_(self.y_down[:M])
@@ -351,7 +364,7 @@ class _Calibration:
             self.o = y
         elif name == "gate_up":
             self.act = torch.empty(M, st.plan["down"]["K"], dtype=torch.float16, device=st.device)
-            w4a16_silu_mul(y, self.act)
+            w4a16_silu_mul_blocked(y, self.act, SILU_BLOCK)
         else:
             self.h = y
         return pl

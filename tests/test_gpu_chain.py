@@ -149,3 +149,40 @@ def test_chain_rejects_bad_ops():
     sq = w4.pack_linear(synth.gpu(0, 3, synth.WEIGHT, 2048, 2048))
     with pytest.raises(w4.W4A16Error):               # in place (X and Y overlap)
         w4.Chain([("gemm", buf[:M * 2048].view(M, 2048), sq, buf[M * 1024:M * 3072].view(M, 2048))], M)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("M,family", [(1, 0), (8, 0), (13, 2), (16, 0)])
+def test_chain_fused_silu_matches_gemm_then_blocked_silu(M, family):
+    # W4A16_OP_GEMM_SILU (gate-up weight in [64 gate | 64 up] tiles, SiLU*mul in the GEMM epilogue) against
+    # the same gate-up GEMM launched alone followed by w4a16_silu_mul_blocked(block = 64): bit-identical, also
+    # across layers (the down GEMM reads the fused output tile by tile), and act itself against numpy on the
+    # host-side unfused values
+    w4 = _w4()
+    H, F = 2048, 2560
+    mats = _mlp(H, F, layers=2, seed=M + 11)
+    f16 = dict(dtype=torch.float16, device="cuda")
+    x = synth.gpu(8, 5, synth.ACT, M, H)
+    ws = w4.alloc_workspace(M, [(H, 2 * F), (F, H)])
+    gu_e, act_e, y_e = torch.empty((M, 2 * F), **f16), torch.empty((M, F), **f16), torch.empty((M, H), **f16)
+    cur = x
+    for gu, dn in mats:
+        gu(cur, gu_e, ws, family=family)
+        w4.w4a16_silu_mul_blocked(gu_e, act_e, 64)
+        dn(act_e, y_e, ws, family=family)
+        cur = y_e.clone()
+    torch.cuda.synchronize()
+    # blocked SiLU*mul against an fp32 reference of its definition (include/w4a16.h)
+    g = gu_e.float().view(M, F // 64, 2, 64)
+    ref = (g[:, :, 0] / (1 + torch.exp(-g[:, :, 0])) * g[:, :, 1]).reshape(M, F)
+    assert torch.allclose(act_e.float(), ref, rtol=2e-3, atol=1e-3)
+    act_c, y_c, y_mid = torch.empty((M, F), **f16), torch.empty((M, H), **f16), torch.empty((M, H), **f16)
+    (gu0, dn0), (gu1, dn1) = mats
+    ops = [("gemm_silu", x, gu0, act_c), ("gemm", act_c, dn0, y_mid), ("gemm_silu", y_mid, gu1, act_c),
+           ("gemm", act_c, dn1, y_c)]
+    ch = w4.Chain(ops, M, family=family)
+    for rep in range(2):
+        ch()
+        torch.cuda.synchronize()
+        assert np.array_equal(_u16(act_c), _u16(act_e)), rep
+        assert np.array_equal(_u16(y_c), _u16(y_e)), rep

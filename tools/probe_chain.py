@@ -34,11 +34,11 @@ G = int((buf[:, 0, 0] > 0).sum())   # CTAs of this chain
 b = buf[:G, :n, :].astype(np.int64)
 t0 = b[:, 0, 0].min()
 b -= t0
-kinds = ["qkv", "o", "gate_up", "silu", "down"]
+kinds = ["qkv", "o", "gate_up_silu", "down"]
 print(f"{'op':8s} {'span':>7s} {'wait1st':>8s} {'compute':>8s} {'flush':>7s} {'skewStart':>9s} {'skewDone':>8s}  (us, medians over layers)")
 for k, name in enumerate(kinds):
     rows = []
-    for j in range(k, n, 5):
+    for j in range(k, n, len(kinds)):
         s, f1, l, d = b[:, j, 0], b[:, j, 1], b[:, j, 2], b[:, j, 3]
         rows.append([d.max() - s.min(), np.median(f1 - s), np.median(l - f1), np.median(d - l), s.max() - s.min(), d.max() - d.min()])
     r = np.median(np.array(rows), axis=0) / 1e3
@@ -48,7 +48,7 @@ print("total span us:", (max(ends)) / 1e3)
 # per-CTA spread of the compute phase (first stage -> last stage) for each op kind, summed over layers
 for k, name in enumerate(kinds):
     comp = np.zeros(G)
-    for j in range(k, n, 5):
+    for j in range(k, n, len(kinds)):
         comp += (b[:, j, 2] - b[:, j, 1]) / 1e3
     q = np.percentile(comp, [0, 10, 50, 90, 100])
     order = np.argsort(comp)
@@ -57,10 +57,8 @@ for k, name in enumerate(kinds):
 
 # last-segment flush decomposition: owner wait (slots 4 -> 5) and flush end (slot 6) vs loop end (slot 2)
 for k, name in enumerate(kinds):
-    if name == "silu":
-        continue
     ow, fl, dn = [], [], []
-    for j in range(k, n, 5):
+    for j in range(k, n, len(kinds)):
         w = b[:, j, 5] - b[:, j, 4]
         own = (buf[:G, j, 4] > 0) & (buf[:G, j, 5] >= buf[:G, j, 4])
         if own.any():
@@ -71,7 +69,7 @@ for k, name in enumerate(kinds):
 
 # op start -> descriptor loaded (slot 7) vs -> first stage ready (slot 1)
 for k, name in enumerate(kinds):
-    d = [np.median(b[:, j, 7] - b[:, j, 0]) / 1e3 for j in range(k, n, 5) if (buf[:G, j, 7] > 0).all()]
+    d = [np.median(b[:, j, 7] - b[:, j, 0]) / 1e3 for j in range(k, n, len(kinds)) if (buf[:G, j, 7] > 0).all()]
     print(f"{name:8s} descriptor load {np.median(d) if d else float('nan'):6.2f} us")
 
 # critical-path view: for each op, T_dep = the last CTA's done-count of the op its activations depend on
@@ -80,7 +78,7 @@ print("\nper op (layers 2..): percentiles p0/p50/p90/p100 over CTAs, us; T_dep =
 pq = lambda v: "/".join(f"{x:5.1f}" for x in np.percentile(v / 1e3, [0, 50, 90, 100]))
 for k, name in enumerate(kinds):
     rows = {"ready-Tdep": [], "compute": [], "flush+cnt": [], "done-Tdep": []}
-    for j in range(5 + k, n, 5):
+    for j in range(len(kinds) + k, n, len(kinds)):
         Tdep = b[:, j - 1, 3].max()
         rows["ready-Tdep"].append(b[:, j, 1] - Tdep)
         rows["compute"].append(b[:, j, 2] - b[:, j, 1])
