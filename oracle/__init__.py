@@ -37,6 +37,7 @@ def _load():
     L.orc_dequantize.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]; L.orc_dequantize.restype = i32
     L.orc_gemm.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32]; L.orc_gemm.restype = i32
     L.orc_gemm_cols.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32, vp]; L.orc_gemm_cols.restype = i32
+    L.orc_gemm_exact.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32]; L.orc_gemm_exact.restype = i32
     L.orc_packed_bytes.argtypes = [i32, i32, i32]; L.orc_packed_bytes.restype = sz
     L.orc_code_word_offset.argtypes = [i32, i32, i32, i32, i32]; L.orc_code_word_offset.restype = sz
     L.orc_nibble_slot.argtypes = [i32]; L.orc_nibble_slot.restype = i32
@@ -113,6 +114,19 @@ def gemm(X, codes, sc, ze, group=128, mode=ASYM, nthreads=1):
     if L.orc_gemm(_p(X), _p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), M, K, N, group, mode, _p(Y),
                   int(nthreads)) != 0:
         raise ValueError("orc_gemm: bad arguments")
+    return Y
+
+
+def gemm_exact(X, codes, sc, ze, group=128, mode=ASYM, nthreads=1):
+    """fp64 Y[M, N] = X . W with W = (q - z) * s exactly, no fp16 rounding of the weight (reading R22)."""
+    X = _u16(X)
+    codes = _c(codes, np.uint8)
+    K, N = codes.shape
+    M = X.shape[0]
+    Y = np.zeros((M, N), dtype=np.float64)
+    if L.orc_gemm_exact(_p(X), _p(codes), _p(_u16(sc)), _p(None if ze is None else _u16(ze)), M, K, N, group, mode,
+                        _p(Y), int(nthreads)) != 0:
+        raise ValueError("orc_gemm_exact: bad arguments")
     return Y
 
 

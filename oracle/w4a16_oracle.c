@@ -131,6 +131,7 @@ int orc_dequantize(const uint8_t* codes, const uint16_t* scales, const uint16_t*
 typedef struct {
   const uint16_t* X; const uint8_t* codes; const uint16_t* sc; const uint16_t* ze;
   int M, K, N, group, mode;
+  int exact_w;                           /* 1: weight = (q - z) * s exactly (reading R22); 0: fp16_rne of it */
   const int32_t* cols;                   /* column list (NULL: all columns) */
   double* Y; int ystride;                /* Y[m*ystride + j] */
   int j0, j1;                            /* this worker's column positions [j0, j1) */
@@ -143,7 +144,12 @@ static void* gemm_worker(void* p) {
     int n = a->cols ? a->cols[j] : j;
     for (int k = 0; k < a->K; ++k) {
       size_t gi = (size_t)(k / a->group) * a->N + n;
-      wcol[k] = orc_half_to_double(dequant(a->codes[(size_t)k * a->N + n], a->sc[gi], a->ze, gi, a->mode));
+      if (a->exact_w) {   /* (q - z) * s: a 4-bit integer times an fp16 scale, exact in double */
+        double z = a->mode == ORC_SYM ? 8.0 : orc_half_to_double(a->ze[gi]);
+        wcol[k] = ((double)a->codes[(size_t)k * a->N + n] - z) * orc_half_to_double(a->sc[gi]);
+      } else {
+        wcol[k] = orc_half_to_double(dequant(a->codes[(size_t)k * a->N + n], a->sc[gi], a->ze, gi, a->mode));
+      }
     }
     for (int m = 0; m < a->M; ++m) {
       const uint16_t* xr = a->X + (size_t)m * a->K;
@@ -157,7 +163,8 @@ static void* gemm_worker(void* p) {
 }
 
 static int gemm_run(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
-                    int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Y, int nthreads) {
+                    int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Y, int nthreads,
+                    int exact_w) {
   if (!X || !codes || !scales || !Y || M < 0 || !shape_ok(K, N, group)) return -1;
   if (mode != ORC_ASYM && mode != ORC_SYM) return -1;
   if (mode == ORC_ASYM && !zeros) return -1;
@@ -166,7 +173,7 @@ static int gemm_run(const uint16_t* X, const uint8_t* codes, const uint16_t* sca
   gemm_job* jobs = (gemm_job*)calloc((size_t)nthreads, sizeof(gemm_job));
   pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
   for (int t = 0; t < nthreads; ++t) {
-    gemm_job j = {X, codes, scales, zeros, M, K, N, group, mode, cols, Y, ncols,
+    gemm_job j = {X, codes, scales, zeros, M, K, N, group, mode, exact_w, cols, Y, ncols,
                   (int)((long long)ncols * t / nthreads), (int)((long long)ncols * (t + 1) / nthreads)};
     jobs[t] = j;
   }
@@ -179,14 +186,22 @@ static int gemm_run(const uint16_t* X, const uint8_t* codes, const uint16_t* sca
 
 int orc_gemm(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M, int K,
              int N, int group, int mode, double* Y, int nthreads) {
-  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads);
+  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads, 0);
+}
+
+/* The same GEMM on the exact quantised weights (reading R22): W[k][n] = (q - z) * s with no fp16 rounding of
+ * the product — the value the scale-after-sum kernel families compute with (they apply s to fp32 sums of
+ * (q - z) x). Differs from orc_gemm by at most sum_k |x_k| * ulp16(w_hat_k) / 2. */
+int orc_gemm_exact(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
+                   int K, int N, int group, int mode, double* Y, int nthreads) {
+  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, NULL, N, Y, nthreads, 1);
 }
 
 int orc_gemm_cols(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
                   int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols) {
   if (!cols || ncols < 0) return -1;
   for (int j = 0; j < ncols; ++j) if (cols[j] < 0 || cols[j] >= N) return -1;
-  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, cols, ncols, Ycols, 1);
+  return gemm_run(X, codes, scales, zeros, M, K, N, group, mode, cols, ncols, Ycols, 1, 0);
 }
 
 /* ------------------------------------------------------------------------------------------------------

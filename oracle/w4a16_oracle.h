@@ -74,6 +74,9 @@ int orc_gemm(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, co
              int N, int group, int mode, double* Y, int nthreads);
 
 /* Same definition for a list of columns only: Ycols[m*ncols + j] = Y[m][cols[j]]. */
+/* Y = X . W with W[k][n] = (q - z) * s exactly (no fp16 rounding; reading R22: the scale-after-sum families). */
+int orc_gemm_exact(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
+                   int K, int N, int group, int mode, double* Y, int nthreads);
 int orc_gemm_cols(const uint16_t* X, const uint8_t* codes, const uint16_t* scales, const uint16_t* zeros, int M,
                   int K, int N, int group, int mode, const int32_t* cols, int ncols, double* Ycols);
 

@@ -330,6 +330,38 @@ def test_gemm_matches_numpy_float64(mode):
     assert np.array_equal(oracle.gemm_cols(X, qw, sc, ze, cols, mode=mode), Y1[:, cols])
 
 
+@pytest.mark.parametrize("mode", [oracle.ASYM, oracle.SYM])
+def test_gemm_exact_weights_pins(mode):
+    # reading R22: orc_gemm_exact uses the exact quantised weight (q - z) * s. Pinned to (i) one-hot rows = the
+    # exact products (a 4-bit integer times an fp16 scale, exact in double), whose fp16 rounding is the
+    # dequantised weight of orc_dequantize (consistency of the two definitions); (ii) a numpy float64 matmul of
+    # (codes - z) * s built from the codes (library routine); (iii) the definitional gap to orc_gemm is bounded
+    # by sum_k |x_k| ulp16(w_hat_k) / 2
+    K, N, M = 640, 384, 5
+    W = synth.host(13, 2, synth.WEIGHT, K, N)
+    X = synth.host(13, 3, synth.ACT, M, K)
+    qw, sc, ze, st = oracle.quantize(W, mode=mode)
+    z = np.full((K // 128, N), 8.0) if mode == oracle.SYM else ze.view(np.float16).astype(np.float64)
+    s = sc.view(np.float16).astype(np.float64)
+    Wx = (qw.astype(np.float64) - np.repeat(z, 128, axis=0)) * np.repeat(s, 128, axis=0)
+    ks = [0, 1, 7, 127, 128, 300, 639]
+    Xh = np.zeros((len(ks), K), dtype=np.float16)
+    for m, k in enumerate(ks):
+        Xh[m, k] = 1.0
+    Yh = oracle.gemm_exact(Xh, qw, sc, ze, mode=mode)
+    assert np.array_equal(Yh, Wx[ks])
+    Wh = oracle.dequantize(qw, sc, ze, mode=mode).view(np.float16).astype(np.float64)
+    assert np.array_equal(Wx.astype(np.float16).astype(np.float64), Wh)     # one rounding of the exact weight
+    Xd = X.view(np.float16).astype(np.float64)
+    Ye = oracle.gemm_exact(X, qw, sc, ze, mode=mode, nthreads=3)
+    assert np.allclose(Ye, Xd @ Wx, rtol=1e-12, atol=1e-12)
+    Y16 = oracle.gemm(X, qw, sc, ze, mode=mode)
+    ulp = np.spacing(np.abs(Wh).astype(np.float16)).astype(np.float64)      # fp16 ulp of each w_hat
+    bound = np.abs(Xd) @ (ulp / 2)
+    assert np.all(np.abs(Ye - Y16) <= bound * (1 + 1e-9) + 1e-12)
+    assert np.any(Ye != Y16)                                                 # the definitions do differ
+
+
 def test_gemm_transposition_sensitive():
     # a transposed operand (using W_hat[n][k]) or swapped X rows would change this product
     K, N = 256, 256
