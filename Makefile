@@ -48,3 +48,12 @@ clean:
 	rm -rf build $(LIB) $(DIAG_LIB) synth/*.so oracle/*.so
 
 .PHONY: all clean diag
+
+# A/B variant of the mma.sync family (diagnostics): make variant V=<name> VDEFS="-DW4_MA_OC=1" builds
+# libw4a16_<name>.so with gemm_mma.cu compiled under VDEFS; loaded with W4A16_LIB=<name>.
+V ?= ab
+VDEFS ?=
+variant: $(filter-out $(BUILD)/gemm_mma.o,$(OBJS))
+	$(NVCC) $(NVFLAGS) $(VDEFS) -c $(CSRC)/gemm_mma.cu -o $(BUILD)/gemm_mma_$(V).o 2> $(BUILD)/gemm_mma_$(V).ptxas.txt || (cat $(BUILD)/gemm_mma_$(V).ptxas.txt; false)
+	$(NVCC) $(ARCH) -shared -cudart static -o paper_2505_22179_b200/libw4a16_$(V).so $^ $(BUILD)/gemm_mma_$(V).o
+.PHONY: variant

@@ -489,7 +489,7 @@ def main():
                              "family": w4.w4a16_gemm_family(M, s["K"], s["N"])}
             # the other engine (mma.sync <-> tcgen05) on the same launches, for comparison (not part of the step)
             alt = (w4.W4A16_FAMILY_TCGEN05 if kernels[name]["family"] != w4.W4A16_FAMILY_TCGEN05 else
-                   w4.W4A16_FAMILY_MMA_SYNC if M <= 8 else w4.W4A16_FAMILY_MMA_SYNC_S if M <= 16 else None)
+                   w4.W4A16_FAMILY_MMA_SYNC if M <= 16 else None)
             if alt is None:
                 continue
             g2 = torch.cuda.CUDAGraph()

@@ -108,12 +108,13 @@ int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K,
                void* workspace, size_t workspace_bytes, w4a16_stream_t stream);
 
 /* w4a16_gemm_ex — w4a16_gemm with an explicit kernel family: W4A16_FAMILY_AUTO (= w4a16_gemm),
- * W4A16_FAMILY_MMA_SYNC (mma.sync, group scale applied to fp32 group sums; M <= 16, else W4A16_ERR_SHAPE),
- * W4A16_FAMILY_MMA_SYNC_S (mma.sync, scale folded into the dequantised fp16 weights; M <= 16) or
- * W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, exact w_hat in TMEM; any M <= 64) or W4A16_FAMILY_TCGEN05_OC
- * (5th-gen tensor cores, offset codes 1024+q / 64+q in TMEM, per-unit TMEM accumulator, scale and offset
- * correction per group in fp32; any M <= 64). All compute the same definition
- * (within the tolerance above); results are batch-invariant within one family. */
+ * W4A16_FAMILY_MMA_SYNC (mma.sync, exact integer codes (q - z) in the MMA operands, group scale applied to
+ * the fp32 group sums; M <= 16, else W4A16_ERR_SHAPE), W4A16_FAMILY_MMA_SYNC_S (mma.sync, scale folded into
+ * the dequantised fp16 weights w_hat; M <= 16), W4A16_FAMILY_TCGEN05 (5th-gen tensor cores, exact w_hat in
+ * TMEM; any M <= 64) or W4A16_FAMILY_TCGEN05_OC (5th-gen tensor cores, exact (q - z) codes in TMEM, per-unit
+ * TMEM accumulator, group scale applied in fp32; any M <= 64). The families that scale group sums compute
+ * sum_g s_g * sum_k (q - z) x (the exact weight, reading R22), the others sum_k w_hat x; both are within the
+ * tolerance above of the oracle and results are batch-invariant within one family. */
 int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
                   void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);
 
@@ -284,7 +285,7 @@ int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void
 /* Human-readable name of a w4a16_status value. */
 const char* w4a16_status_string(int status);
 
-/* Kernel family w4a16_gemm uses: W4A16_FAMILY_MMA_SYNC for M <= 8, W4A16_FAMILY_MMA_SYNC_S for 9 <= M <= 16,
+/* Kernel family w4a16_gemm uses: W4A16_FAMILY_MMA_SYNC for M <= 16,
  * W4A16_FAMILY_TCGEN05 above. */
 int w4a16_gemm_family(int M, int K, int N);
 

@@ -93,13 +93,11 @@ extern "C" int w4a16_workspace_init(void* workspace, size_t workspace_bytes, w4a
   return cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
-// Family choice: mma.sync with the group scale applied to fp32 group sums for M <= 8,
-// mma.sync with the scale inside the dequantised weights for 9 <= M <= 16 (register-bound variant),
-// tcgen05/TMEM above (MMA cost nearly independent of M).
+// Family choice: mma.sync with exact (q - z) codes and the group scale applied to fp32 group
+// sums for M <= 16, tcgen05/TMEM above (MMA cost nearly independent of M).
 extern "C" int w4a16_gemm_family(int M, int K, int N) {
   (void)K; (void)N;
-  if (M <= 8) return W4A16_FAMILY_MMA_SYNC;
-  if (M <= 16) return W4A16_FAMILY_MMA_SYNC_S;
+  if (M <= 16) return W4A16_FAMILY_MMA_SYNC;
   return W4A16_FAMILY_TCGEN05;
 }
 

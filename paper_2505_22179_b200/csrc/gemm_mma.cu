@@ -42,7 +42,6 @@ constexpr int kTileN = 128, kTileK = 128;
 constexpr int kGroups = W4_MA_GROUPS;              // consumer groups sharing one pipeline (1 CTA per SM at 2)
 constexpr int kWarps = 8 * kGroups;                // per group: 4 row-quarters x 2 k-halves
 constexpr int kProducerWarp = kWarps;
-constexpr int kXsumWarp = kWarps + 1;              // activation sums (offset-code family only)
 #ifndef W4_MA_PUB
 #define W4_MA_PUB 1   // 1: a publisher warp issues the counter increments (fence + red) for the storing warps
 #endif
@@ -50,7 +49,7 @@ constexpr int kXsumWarp = kWarps + 1;              // activation sums (offset-co
 // (~1 us under load); the storing warps hand the increment to this warp through a shared-memory ring and
 // go straight on to the next units.
 template <bool kScaleInA>
-__host__ __device__ constexpr int pub_warp() { return kWarps + (kScaleInA ? 1 : 2); }
+__host__ __device__ constexpr int pub_warp() { return kWarps + 1; }
 template <bool kScaleInA>
 constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0)) * 32; }
 constexpr int kPubSlots = 8;
@@ -70,11 +69,10 @@ struct Cfg {
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
   static constexpr int kRedSlots = kGroups - 1;                   // partial-sum sets handed to group 0
   static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;
-  static constexpr int kSumBytes = kR * NTB * 4 * 16;             // per stage: {-C, -S} float4 per (unit, tb, c4)
   static constexpr int kXchBytes = 4 * NTB * 4 * 32 * 4;          // SiLU epilogue: up values of a tile (fp16 in u32)
-  static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / (kStage + kSumBytes);
+  static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / kStage;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  static constexpr int kSmem = kStages * (kStage + kSumBytes) + kRedFloats * 4 + kXchBytes + 1024;
+  static constexpr int kSmem = kStages * kStage + kRedFloats * 4 + kXchBytes + 1024;
 };
 
 // A single w4a16_gemm is a one-op list whose fields come from GemmParams and the kernel's tensor-map
@@ -180,10 +178,14 @@ __device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
 // MMA column j (fragment group g8 = j) carries token pi(j) of its 8-token block: with it, the 8 lanes of each
 // quarter-warp phase of an activation LDS.128 read rows {r, r + 4}, whose SWIZZLE_128B chunk positions differ
 // in the high bit, instead of rows {r, r + 1}, which collide on the same four bank groups (2-way conflict).
+#ifndef W4_MA_CH
+#define W4_MA_CH 1    // independent MMA accumulator chains per unit in the post-scale family (1 or 2)
+#endif
+constexpr int kCh = W4_MA_CH;
 #ifndef W4_MA_EXP
-#define W4_MA_EXP 0   // cost experiments only (tools/probe_exp.sh; WRONG results): bit0 no per-unit post-scale /
-                      // offset correction, bit1 no LOP3 (raw words as A), bit2 no activation loads, bit3 no
-                      // scale/zero loads
+#define W4_MA_EXP 0   // cost experiments only (make variant VDEFS=-DW4_MA_EXP=..; WRONG results): bit0 no per-unit
+                      // group accumulator / post-scale, bit1 no dequant (raw words as A), bit2 no activation
+                      // loads, bit3 no scale/zero loads
 #endif
 __device__ __forceinline__ int tok_pi(int j) { return (j >> 1) | ((j & 1) << 2); }
 
@@ -288,7 +290,6 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
   __shared__ __align__(8) uint64_t empty_bar[S];
-  __shared__ __align__(8) uint64_t sums_bar[S];   // offset-code family: the stage's activation sums are ready
   __shared__ __align__(8) uint64_t pub_full[kPubSlots], pub_empty[kPubSlots];
   __shared__ int* pub_ptr[kPubSlots];
   __shared__ int pub_val[kPubSlots];   // 0: add 1 (counters); else store this value (tile-ready flags)
@@ -299,10 +300,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_base = smem_u32(smem);
   float* red = reinterpret_cast<float*>(smem + S * C::kStage);
-  const uint32_t sums_base = smem_base + S * C::kStage + C::kRedFloats * 4;   // [S][kSumBytes]
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); mbar_init(&sums_bar[s], 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], kWarps); }
     for (int s = 0; s < kPubSlots; ++s) { mbar_init(&pub_full[s], 1); mbar_init(&pub_empty[s], 1); }
     fence_mbar_init();
     pdl_launch_dependents();   // the next GEMM's CTAs may take SMs as this grid's CTAs retire
@@ -411,87 +411,6 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     return;
   }
 
-  if (!kScaleInA && warp == kXsumWarp) {
-    // ---------------- activation sums (offset-code family) ----------------
-    // Per unit, k-half kh and token m: {-C[m], -S[m]} with C = 1024 sum_lo x + 64 sum_hi x and S = sum x
-    // over the k-half (see process_unit). One MMA per k-step with the activations as the A operand (16
-    // MMA rows = the two k-halves' 8 tokens at NTB = 1, or one k-half's 16 tokens at NTB = 2) and a
-    // constant B (column 0: -1024 on lo slots, -64 on hi slots; column 1: -1): D[row][0] = -C, D[row][1] = -S.
-    // The tensor core sums these products exactly like the consumers' own MMAs, so the offsets cancel to
-    // fp32 rounding. The activation fragments are the consumers' own B fragments, re-read as A.
-    const int g8 = lane >> 2, c4 = lane & 3;
-    const uint32_t b0 = g8 == 0 ? 0xE400E400u : g8 == 1 ? 0xBC00BC00u : 0u;   // lo k slots
-    const uint32_t b1 = g8 == 0 ? 0xD400D400u : g8 == 1 ? 0xBC00BC00u : 0u;   // hi k slots
-    constexpr int kPasses = NTB == 1 ? 1 : 2;   // MMAs per k-step and unit (k-halves at NTB = 2)
-    int s = 0;
-    uint32_t ph = 0;
-    for (int j = 0; j < p.n_jobs; ++j) {
-      const JobInfo J = job_at(p, &xmapR, &xmap1, j);
-      if (J.kind != kOpGemm) continue;
-      const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
-      for (int u0 = u_begin; u0 < u_end; u0 += kR) {
-        const int nu = min(kR, u_end - u0);
-        mbar_wait(&full_bar[s], ph);
-        const uint32_t st = smem_base + s * C::kStage;
-        const uint32_t sb = sums_base + s * C::kSumBytes;
-        auto run = [&](auto nu_c, int jbase) {
-          constexpr int NU = decltype(nu_c)::value;
-          float d[NU][kPasses][4];
-#pragma unroll
-          for (int jj = 0; jj < NU; ++jj)
-#pragma unroll
-            for (int pz = 0; pz < kPasses; ++pz) d[jj][pz][0] = d[jj][pz][1] = d[jj][pz][2] = d[jj][pz][3] = 0.f;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-              for (int jj = 0; jj < NU; ++jj)
-#pragma unroll
-                for (int pz = 0; pz < kPasses; ++pz) {
-                  // A rows g8 / g8+8: (kh 0 / kh 1, token g8) at NTB = 1; (kh = pz, token g8 / 8+g8) at NTB = 2
-                  const int kh0 = NTB == 1 ? 0 : pz, kh1 = NTB == 1 ? 1 : pz;
-                  const int m0 = tok_pi(g8), m1 = NTB == 1 ? m0 : 8 + m0;
-                  const uint32_t xu = st + (jbase + jj) * C::kXUnit + (((4 * cc + c4) ^ tok_pi(g8)) << 4) + 8 * hs;
-                  const uint2 r0 = lds64(xu + kh0 * C::kXBox + m0 * 128);
-                  const uint2 r1 = lds64(xu + kh1 * C::kXBox + m1 * 128);
-                  mma_16816_nv(d[jj][pz], r0.x, r1.x, r0.y, r1.y, b0, b1);
-                }
-          if (c4 == 0) {
-            // the consumers own whole units (all 128 k): sum the two k-halves' -C and -S per token
-#pragma unroll
-            for (int jj = 0; jj < NU; ++jj) {
-              if (NTB == 1) {   // rows g8 / g8 + 8 = k-half 0 / 1 of token tok_pi(g8)
-                const int m = tok_pi(g8);
-                const uint32_t slot = sb + (((jbase + jj) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
-                sts32f(slot, d[jj][0][0] + d[jj][0][2]);       // -C[m]
-                sts32f(slot + 8, d[jj][0][1] + d[jj][0][3]);   // -S[m]
-              } else {          // pass pz = k-half; rows g8 / g8 + 8 = tokens tok_pi(g8) / 8 + tok_pi(g8)
-#pragma unroll
-                for (int rh = 0; rh < 2; ++rh) {
-                  const int m = 8 * rh + tok_pi(g8);
-                  const uint32_t slot = sb + (((jbase + jj) * NTB + (m >> 3)) * 4 + (m & 3)) * 16 + 4 * ((m & 7) >> 2);
-                  sts32f(slot, d[jj][0][2 * rh] + d[jj][kPasses - 1][2 * rh]);
-                  sts32f(slot + 8, d[jj][0][2 * rh + 1] + d[jj][kPasses - 1][2 * rh + 1]);
-                }
-              }
-            }
-          }
-        };
-        if (p.dbg & 32) {
-        } else if (nu == kR) {
-          run(std::integral_constant<int, kR>{}, 0);
-        } else {
-          for (int j0 = 0; j0 < nu; ++j0) run(std::integral_constant<int, 1>{}, j0);   // ragged last stage
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sums_bar[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
-    }
-    return;
-  }
-
   if (W4_MA_PUB && warp == pub_warp<kScaleInA>()) {
     // ---------------- publisher ----------------
     // Requests arrive in order from thread 0 (after a barrier of the threads whose stores they publish):
@@ -558,7 +477,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   float acc[NTB][4];
   int s = 0;
   uint32_t ph = 0;
-  const uint32_t ready_base = smem_u32(kScaleInA ? &full_bar[0] : &sums_bar[0]);
+  const uint32_t ready_base = smem_u32(&full_bar[0]);
   const uint32_t empty_base = smem_u32(&empty_bar[0]);
   const bool skip_compute = W4A16_MMA_DIAG && (p.dbg & 1);   // diagnostics only
 
@@ -635,7 +554,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           // the up warps (r8 >= 4) hand their fp16-rounded values to the gate warps through a shared-memory
           // area of their own (group 1 may already be writing `red` for its next flush), and the gate warps
           // write Y[m][64 t + row] = fp16(silu(g) * u) — w4a16_silu_mul's arithmetic
-          uint32_t* xch = reinterpret_cast<uint32_t*>(smem + S * (C::kStage + C::kSumBytes) + C::kRedFloats * 4);
+          uint32_t* xch = reinterpret_cast<uint32_t*>(smem + S * C::kStage + C::kRedFloats * 4);
           if (r8 >= 4) {
 #pragma unroll
             for (int tb = 0; tb < NTB; ++tb)
@@ -714,7 +633,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
     // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
     // dequant + 8 MMAs (one m16 tile x 8 k-steps), then the post-MMA group scale.
-    auto process_unit = [&](uint32_t st, uint32_t sb, int j) {
+    auto process_unit = [&](uint32_t st, int j) {
       const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box b holds k 64b..
       const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
       uint4 xr[4][NTB];                                       // [32-k chunk p][token block]
@@ -740,7 +659,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                   wq[2 * pp + 1][1]);
         }
       }
-      float sc[2], zrow[2];
+      float sc[2];
       __half2 zp[2];
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -748,15 +667,12 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         if (SYM) {
           sc[hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
           zp[hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
-          zrow[hf] = 8.f;
         } else if (W4_MA_EXP & 8) {
           sc[hf] = 0.01f * (r + 1);
-          zrow[hf] = 8.f;
           zp[hf] = __floats2half2_rn(72.f, 1032.f);
         } else {
           const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
           sc[hf] = __low2float(sz);
-          zrow[hf] = __high2float(sz);
           zp[hf] = zero_pair(__high2half(sz));
         }
       }
@@ -783,50 +699,50 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             }
           }
       } else {
-        // Post-scale with offset codes: one LOP3 per code pair, no zero-point arithmetic.
-        //   lo slots: (w & 0x000F000F) | 0x6400 -> 1024 + q      hi slots: (w & 0x00F000F0) | 0x5400 -> 64 + q
-        // so the MMA sums sum_k (off_k + q_k) x_k. The offsets and the zero point come back out as
-        //   sum_k (q_k - z) x_k = gacc - C[m] - z * S[m],  C = 1024 sum_lo x + 64 sum_hi x,  S = sum x,
-        // with C and S of the unit supplied by the activation-sum warp and folded into the initial group
-        // accumulator: gacc0 = -C - z S.
-        float cs[NTB][4];   // {-C[m0], -C[m1], -S[m0], -S[m1]}, m0 = 8tb + c4, m1 = m0 + 4 (activation-sum warp)
+        // Post-scale with exact codes: the A fragments hold the integers (q - z) (LOP3 +
+        // HSUB2 / HFMA2 per pair, exact in fp16), the MMAs sum sum_k (q_k - z) x_k over the unit's 128 k into
+        // a fresh fp32 group accumulator, and the group scale multiplies that sum once: Y += s * sum. This is
+        // the exact-weight definition (reading R22, orc_gemm_exact); no offsets, so no cancellation whatever
+        // the activation magnitude.
+        // kCh independent accumulator chains per unit (32-k chunks alternate between them): more MMAs in flight
+        float gacc[kCh][NTB][4];
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const float4 v = lds128f(sb + ((j * NTB + tb) * 4 + c4) * 16);
-          cs[tb][0] = v.x; cs[tb][1] = v.y; cs[tb][2] = v.z; cs[tb][3] = v.w;
-        }
-        float gacc[NTB][4];
+        for (int ch = 0; ch < kCh; ++ch)
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb)
+          for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            gacc[tb][e] = (W4_MA_EXP & 1) ? acc[tb][e] : fmaf(SYM ? 8.f : zrow[e >> 1], cs[tb][2 + (e & 1)], cs[tb][e & 1]);
+            for (int e = 0; e < 4; ++e) gacc[ch][tb][e] = (W4_MA_EXP & 1) && ch == 0 ? acc[tb][e] : 0.f;
 #pragma unroll
         for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
           for (int hs = 0; hs < 2; ++hs) {
             const uint32_t qa = hs ? wq[pc][0] >> 8 : wq[pc][0];
             const uint32_t qb = hs ? wq[pc][1] >> 8 : wq[pc][1];
-            const uint32_t a0 = (W4_MA_EXP & 2) ? qa : lop3_and_or(qa, 0x000F000Fu, 0x64006400u);
-            const uint32_t a1 = (W4_MA_EXP & 2) ? qb : lop3_and_or(qb, 0x000F000Fu, 0x64006400u);
-            const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : lop3_and_or(qa, 0x00F000F0u, 0x54005400u);
-            const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : lop3_and_or(qb, 0x00F000F0u, 0x54005400u);
+            const uint32_t a0 = (W4_MA_EXP & 2) ? qa : dq_lo(qa, zp[0]), a1 = (W4_MA_EXP & 2) ? qb : dq_lo(qb, zp[1]);
+            const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : dq_hi(qa, zp[0]);
+            const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : dq_hi(qb, zp[1]);
 #pragma unroll
             for (int tb = 0; tb < NTB; ++tb) {
               const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
-              mma_16816_nv(gacc[tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+              mma_16816_nv(gacc[pc % kCh][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
             }
           }
 #pragma unroll
+        for (int ch = 1; ch < kCh; ++ch)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) gacc[0][tb][e] += gacc[ch][tb][e];
+#pragma unroll
         for (int tb = 0; tb < NTB; ++tb) {
           if (W4_MA_EXP & 1) {
-            acc[tb][0] = gacc[tb][0]; acc[tb][1] = gacc[tb][1]; acc[tb][2] = gacc[tb][2]; acc[tb][3] = gacc[tb][3];
+            acc[tb][0] = gacc[0][tb][0]; acc[tb][1] = gacc[0][tb][1]; acc[tb][2] = gacc[0][tb][2]; acc[tb][3] = gacc[0][tb][3];
             continue;
           }
-          acc[tb][0] = fmaf(sc[0], gacc[tb][0], acc[tb][0]);
-          acc[tb][1] = fmaf(sc[0], gacc[tb][1], acc[tb][1]);
-          acc[tb][2] = fmaf(sc[1], gacc[tb][2], acc[tb][2]);
-          acc[tb][3] = fmaf(sc[1], gacc[tb][3], acc[tb][3]);
+          acc[tb][0] = fmaf(sc[0], gacc[0][tb][0], acc[tb][0]);
+          acc[tb][1] = fmaf(sc[0], gacc[0][tb][1], acc[tb][1]);
+          acc[tb][2] = fmaf(sc[1], gacc[0][tb][2], acc[tb][2]);
+          acc[tb][3] = fmaf(sc[1], gacc[0][tb][3], acc[tb][3]);
         }
       }
     };
@@ -844,7 +760,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0.f;
     };
     auto stage_begin = [&](int i) {
-      if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(kScaleInA ? &full_bar[s] : &sums_bar[s], ph, 32);
+      if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(&full_bar[s], ph, 32);
       else mbar_wait_a(ready_base + 8 * s, ph);
       if (i == 0) { trace_ma(p, 1); trace_op(p, job, 1); }
     };
@@ -860,11 +776,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       {
         const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
         stage_begin(i);
-        const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+        const uint32_t st = smem_base + s * C::kStage;
         // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
         for (int j = 0; j < nu; ++j) {
           if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
-          if ((j >> 1) == grp && !skip_compute) process_unit(st, sb, j);
+          if ((j >> 1) == grp && !skip_compute) process_unit(st, j);
         }
         stage_end();
         ++i;
@@ -873,10 +789,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       const int i_end = min(n_full, (boundary - u_begin) / kR);
       for (; i < i_end; ++i) {
         stage_begin(i);
-        const uint32_t st = smem_base + s * C::kStage, sb = sums_base + s * C::kSumBytes;
+        const uint32_t st = smem_base + s * C::kStage;
         if (!skip_compute) {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) process_unit(st, sb, 2 * grp + j);
+          for (int j = 0; j < 2; ++j) process_unit(st, 2 * grp + j);
         }
         stage_end();
       }
@@ -993,7 +909,7 @@ extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms) {
 // ---- chains (include/w4a16.h) ----
 namespace {
 int chain_family(int M, int family) {
-  if (family == W4A16_FAMILY_AUTO) family = M <= 8 ? W4A16_FAMILY_MMA_SYNC : W4A16_FAMILY_MMA_SYNC_S;
+  if (family == W4A16_FAMILY_AUTO) family = W4A16_FAMILY_MMA_SYNC;
   if (M < 1 || M > 16) return W4A16_ERR_SHAPE;   // chains serve the mma.sync families (M <= 16)
   if (family != W4A16_FAMILY_MMA_SYNC && family != W4A16_FAMILY_MMA_SYNC_S) return W4A16_ERR_ARG;
   return family;
