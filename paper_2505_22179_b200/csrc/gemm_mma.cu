@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         // Post-scale with exact codes: the A fragments hold the integers (q - z) (LOP3 +
         // HSUB2 / HFMA2 per pair, exact in fp16), the MMAs sum sum_k (q_k - z) x_k over the unit's 128 k into
         // a fresh fp32 group accumulator, and the group scale multiplies that sum once: Y += s * sum. This is
-        // the exact-weight definition (reading R22, orc_gemm_exact); no offsets, so no cancellation whatever
+        // the exact-weight definition (reading R22); no offsets, so no cancellation whatever
         // the activation magnitude.
         // kCh independent accumulator chains per unit (32-k chunks alternate between them): more MMAs in flight
         float gacc[kCh][NTB][4];
