@@ -278,12 +278,25 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # BENCH_DIST_BACKEND=gloo (tests only): the control plane over gloo and every rank on cuda:(local % #GPUs),
+    # so the multi-rank code path (fused all-reduce set-up, start-up check, NCCL fallback) runs on a 1-GPU box
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
+
+    def dist_barrier():
+        if backend == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
     dims = tp.LLAMA3_70B if args.model == "70b" else tp.LLAMA3_8B
     n_layers = args.layers or dims.layers
     mode = w4.W4A16_SYM if args.mode == "sym" else w4.W4A16_ASYM
@@ -312,7 +325,7 @@ def main():
     def fused_matches_nccl(st) -> bool:
         """One forward at M = min(8, M_max) through the fused chain vs the same forward op by op with NCCL."""
         m = min(8, M_max)
-        dist.barrier(device_ids=[local])
+        dist_barrier()
         st.forward(m)
         torch.cuda.synchronize()
         got = [st.y_o_red[:m].float().clone(), st.y_down_red[:m].float().clone()]
@@ -321,6 +334,8 @@ def main():
         torch.cuda.synchronize()
         st.use_chains = True
         want = [st.y_o_red[:m].float(), st.y_down_red[:m].float()]
+        if os.environ.get("BENCH_FAIL_FUSED_CHECK") == str(rank):   # tests only: exercise the fallback branch
+            return False
         return all(bool(torch.all((g - w).abs() <= 1e-2 * (1 + w.abs())).item()) for g, w in zip(got, want))
 
     t0 = time.perf_counter()
@@ -334,31 +349,33 @@ def main():
         except Exception as e:   # setup failure (IPC / peer access): every rank learns it below
             log(f"fused all-reduce unavailable on rank {rank}: {e!r}")
             ok = False
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 1:
-            allreduce_used = "fused"
+            allreduce_used = f"fused ({stack.peers.kind})"   # NVLS multicast or peer-load regions
         elif args.allreduce == "fused":
             raise SystemExit("--allreduce fused: setup or start-up check failed")
         else:
-            log("falling back to NCCL all-reduces")
+            log(f"falling back to {backend} all-reduces")
             stack = None   # its peer region stays mapped (a few MB): freeing it needs every peer to unmap first
             torch.cuda.empty_cache()
-            allreduce_used = "nccl"
+            allreduce_used = backend
     if stack is None:
         stack = build("nccl")
+    # gloo (tests only) cannot be captured in a CUDA graph: its process-group all-reduces run eagerly
+    stack.capturable = backend == "nccl" or world == 1 or allreduce_used.startswith("fused")
     build_s = time.perf_counter() - t0
     log(f"built {n_layers} layers ({stack.weight_bytes / 1e9:.2f} GB packed) in {build_s:.1f}s, all-reduce: {allreduce_used}")
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist_barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -669,27 +686,42 @@ def main():
                           "us_per_forward_80_layers": 80 * 1e3 * msa}
             log(f"tree attention M={Mq} ({kind}): {1e3 * msa:.1f} us per layer")
             del ga
-    # the in-chain ALLREDUCE op's own cost on one GPU — a world-1 group (ready flags, system
-    # fences, the grid-wide wait, the reduce pass; no NVLink reads): 16 layers as one chain with and without
-    # an ALLREDUCE after every O and down GEMM.
+    # the in-chain ALLREDUCE op's own cost on one GPU — a world-1 group (tile counters bumped by
+    # the O / down GEMMs' tile writers, system fences, per-tile reduce; no NVLink reads): 16 layers as one
+    # chain with and without an ALLREDUCE after every O and down GEMM, over a peer-load group and (where the
+    # device supports multicast objects) an NVLS group.
     ar = None
     if args.lm_head and world == 1 and M <= 16 and n_layers >= 16:
         try:
             nl = 16
-            g1 = w4.PeerGroup.simulated(1, 1 << 22, 2 * nl, device=dev)[0]
             Hd = dims.hidden
-            P_o, P_d = g1.alloc(M, Hd), g1.alloc(M, Hd)
-            r_o, r_d = (torch.empty(M, Hd, dtype=torch.float16, device=dev) for _ in range(2))
-            plain, fused = [], []
+            kinds = ["peer"] + (["nvls"] if w4.PeerGroup.mc_supported() else [])
+            t_ch, groups = {}, {}
+            nvls_error = "device reports no multicast support"
+            plain = []
             for l, L in enumerate(stack.layers[:nl]):
                 qa, qb = stack._layer_ops(L, M, l)
                 plain += qa + qb
-                h = stack.x_in[:M] if l == 0 else r_d
-                fused += [("gemm", h, L["qkv"], stack.y_qkv[:M]), ("gemm", stack.q_part(M), L["o"], P_o),
-                          ("allreduce", P_o, r_o, g1), ("gemm_silu", r_o, L["gate_up"], stack.act[:M]),
-                          ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
-            t_ch = {}
-            for name, ops in (("plain", plain), ("allreduce", fused)):
+            cases = [("plain", plain)]
+            for kind in list(kinds):
+                try:
+                    g1 = (w4.PeerGroup.simulated(1, 1 << 22, 2 * nl, device=dev)[0] if kind == "peer" else
+                          w4.PeerGroup.mc(1 << 22, 2 * nl))
+                except w4.W4A16Error as e:   # multicast objects refused on this device (e.g. a GPU partition)
+                    kinds.remove(kind)
+                    nvls_error = repr(e)
+                    continue
+                groups[kind] = g1
+                P_o, P_d = g1.alloc(M, Hd), g1.alloc(M, Hd)
+                r_o, r_d = (torch.empty(M, Hd, dtype=torch.float16, device=dev) for _ in range(2))
+                fused = []
+                for l, L in enumerate(stack.layers[:nl]):
+                    h = stack.x_in[:M] if l == 0 else r_d
+                    fused += [("gemm", h, L["qkv"], stack.y_qkv[:M]), ("gemm", stack.q_part(M), L["o"], P_o),
+                              ("allreduce", P_o, r_o, g1), ("gemm_silu", r_o, L["gate_up"], stack.act[:M]),
+                              ("gemm", stack.act[:M], L["down"], P_d), ("allreduce", P_d, r_d, g1)]
+                cases.append((kind, fused))
+            for name, ops in cases:
                 ch = w4.Chain(ops, M)
                 with torch.cuda.stream(stream):
                     ch(stream)
@@ -698,12 +730,18 @@ def main():
                 with torch.cuda.graph(gch, stream=stream):
                     ch(stream)
                 t_ch[name] = time_graph(gch, 10, 3)
-                del gch
-            ar = {"row": "f1", "M": M, "layers": nl, "ops": 2 * nl, "world": 1,
-                  "chain_ms": t_ch["plain"], "chain_with_allreduce_ms": t_ch["allreduce"],
-                  "us_per_allreduce_op": 1e3 * (t_ch["allreduce"] - t_ch["plain"]) / (2 * nl),
-                  "note": "world-1 group on one GPU: protocol + grid-wide wait + reduce pass; NVLink reads not included"}
-            log(f"in-chain ALLREDUCE (world 1): {ar['us_per_allreduce_op']:.2f} us per op")
+                del gch, ch
+            ar = {"row": "f1", "M": M, "layers": nl, "ops": 2 * nl, "world": 1, "chain_ms": t_ch["plain"],
+                  "nvls": "measured" if "nvls" in kinds else f"unavailable: {nvls_error}",
+                  "note": "world-1 group on one GPU: fused per-tile protocol (tile counters, system fences, per-tile "
+                          "reduce); NVLink reads not included"}
+            for kind in kinds:
+                ar[f"chain_with_allreduce_ms_{kind}"] = t_ch[kind]
+                ar[f"us_per_allreduce_op_{kind}"] = 1e3 * (t_ch[kind] - t_ch["plain"]) / (2 * nl)
+                log(f"in-chain ALLREDUCE (world 1, {kind}): {ar[f'us_per_allreduce_op_{kind}']:.2f} us per op")
+            ar["us_per_allreduce_op"] = ar["us_per_allreduce_op_peer"]
+            for g1 in groups.values():
+                g1.close()
         except Exception as e:   # never let the side measurement break the bench line
             ar = {"row": "f1", "error": repr(e)}
     # per-token int8 quantisation + INT8-MMA GEMM on a SYM blob of the 70B gate-up shape at

@@ -213,30 +213,42 @@ typedef struct {
 /* ---- Tensor-parallel all-reduce inside a chain ------------------------------
  * The row-parallel GEMMs of a t-way tensor-parallel verify forward (O and down: each rank multiplies its
  * K-shard, Megatron layout) produce partial sums P_r that are summed over the ranks. An
- * ALLREDUCE op does that sum INSIDE the chain, one-shot over peer memory (NVLink / NVSwitch loads), so a
- * whole tensor-parallel forward stays one persistent launch per rank instead of 2 launches + 2 NCCL
- * all-reduces per layer:
- *   out[m][n] = fp16_rne( sum_{r = 0 .. world-1, in rank order} (float) P_r[m][n] )     (fp32 sum)
- * identical on every rank (same operands, same order). Protocol: once every earlier op of this rank is
- * complete, the rank stores a ready flag (the chain's run epoch) into each rank's flag area; every CTA
- * waits for all `world` flags, then reads its slice of every P_r through the peer mappings.
- * Symmetric region: each rank allocates one device region of the same size (w4a16_ipc_alloc, zero-filled)
- * and maps every peer's (w4a16_ipc_open); the P buffers and a flag area (w4a16_peer_flag_bytes, at the
- * same offset on every rank) live in it. Rules (checked by w4a16_chain_plan): every ALLREDUCE of a chain
- * names the same group; X lies inside base[rank]; and cyclically between an ALLREDUCE that reads a
- * buffer and the next op that writes it there is another ALLREDUCE (that op's flags prove every peer has
- * finished reading — two alternating partial buffers, as in a decoder layer's O and down, satisfy it).
- * Every rank runs the same sequence of chains over the group. A wait that does not complete within ~60 s
- * (a peer that never arrives) traps the kernel instead of hanging the device. */
+ * ALLREDUCE op does that sum INSIDE the chain, one-shot over peer memory, so a whole tensor-parallel forward
+ * stays one persistent launch per rank instead of 2 launches + 2 NCCL all-reduces per layer:
+ *   out[m][n] = fp16_rne( sum over ranks of (float) P_r[m][n] )   (fp32 sum, one rounding)
+ * Fused with the GEMM that produces P, tile by tile: when this rank's GEMM has written 128-column tile t of P
+ * it bumps tile t's ready counter in EVERY rank's flag area (system-scope release: one NVLS multimem.red
+ * through the group's multicast mapping, else one red per peer mapping); the ALLREDUCE op's CTA for tile t
+ * waits until its local counter shows all `world` ranks for this run and reduces that tile at once —
+ * through the multicast mapping (multimem.ld_reduce: the NVSwitch adds the ranks' fp16 values with fp32
+ * accumulation and returns the sum; order inside the switch unspecified, so ranks agree but the sum is not
+ * bit-pinned to rank order) or, without multicast, with one 16-byte load per peer mapping, summed in fp32
+ * in rank order (bit-identical on every rank). Each reduced tile then publishes its own ready flag, so the
+ * next GEMM starts on the tiles that are done: no grid-wide wait anywhere in the all-reduce.
+ * Symmetric region: each rank owns one device region of the same size with the P buffers and a flag area
+ * (w4a16_peer_flag_bytes, at the same offset on every rank) in it, mapped by every peer (CUDA IPC:
+ * w4a16_ipc_alloc / w4a16_ipc_open) and/or bound to one multicast object (NVLS: w4a16_mc_*). Rules (checked
+ * by w4a16_chain_plan): every ALLREDUCE of a chain names the same group; its X is exactly the Y of the GEMM
+ * right before it (N <= 128 * W4A16_AR_MAX_TILES); X lies inside base[rank]; and cyclically between an
+ * ALLREDUCE that reads a buffer and the next op that writes it there is another ALLREDUCE (a rank publishes
+ * that op's tile counters only after it has finished the earlier ALLREDUCE — so peers are done reading —
+ * two alternating partial buffers, as in a decoder layer's O and down, satisfy it). Every rank runs the same
+ * sequence of chains over the group. A wait that does not complete within ~60 s (a peer that never
+ * arrives) traps the kernel instead of hanging the device. */
 #define W4A16_MAX_PEERS 8
+#define W4A16_AR_MAX_TILES 128
 typedef struct {
-  void* base[W4A16_MAX_PEERS];   /* every rank's symmetric region as mapped in this process; base[rank] is local */
+  void* base[W4A16_MAX_PEERS];   /* every rank's symmetric region as mapped in this process; base[rank] is local
+                                  * (peers may be NULL when mc_base is set: the multicast path never maps them) */
   size_t bytes;                  /* region size (identical on every rank) */
   size_t flag_offset;            /* flag area offset inside each region (identical on every rank, 256-B aligned) */
   int flag_slots;                /* ALLREDUCE ops the flag area serves (per chain: one slot per ALLREDUCE op) */
   int world, rank;               /* 1 <= world <= W4A16_MAX_PEERS, 0 <= rank < world */
+  void* mc_base;                 /* the multicast (NVLS) mapping of the group's regions (w4a16_mc_bind), or
+                                  * NULL: peer loads through base[] */
 } w4a16_peer_group;
-/* Bytes of a flag area for `flag_slots` ALLREDUCE ops (a run counter plus world ready flags per slot). */
+/* Bytes of a flag area for `flag_slots` ALLREDUCE ops (a run counter plus W4A16_AR_MAX_TILES tile counters
+ * per slot). */
 size_t w4a16_peer_flag_bytes(int flag_slots);
 /* Symmetric-region plumbing (CUDA IPC; one process per GPU). w4a16_ipc_alloc: cudaMalloc `bytes` on the
  * current device, zero it, and write its 64-byte IPC handle to handle_out. w4a16_ipc_open: map a peer's
@@ -246,6 +258,24 @@ int w4a16_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
 int w4a16_ipc_open(const void* handle, void** dev_ptr);
 int w4a16_ipc_close(void* dev_ptr);
 int w4a16_ipc_free(void* dev_ptr);
+/* Symmetric regions bound to one multicast object (NVLS, NVSwitch systems; one process per GPU):
+ *   w4a16_mc_supported()  1 if the current device supports multicast objects and fabric handles, else 0.
+ *   w4a16_mc_create(bytes, world, handle_out, mc_out)   rank 0: create a multicast object for `world`
+ *       devices of size round_up(bytes, granularity) and export its 64-byte fabric handle.
+ *   w4a16_mc_import(handle, bytes, world, mc_out)   the other ranks: import it (same bytes and world).
+ *   w4a16_mc_add_device(mc)   every rank, before any rank binds: add the current device.
+ *   w4a16_mc_bind(mc, bytes, uc_out, mc_va_out)   every rank, after every rank has added its device:
+ *       allocate `bytes` (rounded as in create) of this device's memory, map it (uc_out: the rank's region, zero-filled),
+ *       bind it to the object and map the multicast address range (mc_va_out = w4a16_peer_group.mc_base).
+ *   w4a16_mc_free(mc, uc, mc_va, bytes)   unmap and release (after every rank's last use).
+ * `mc` is an opaque host handle. Driver API through cudaGetDriverEntryPoint (no link-time libcuda).
+ * W4A16_ERR_CUDA on any driver failure, W4A16_ERR_ARG on bad arguments. */
+int w4a16_mc_supported(void);
+int w4a16_mc_create(size_t bytes, int world, void* handle_out, void** mc_out);
+int w4a16_mc_import(const void* handle, size_t bytes, int world, void** mc_out);
+int w4a16_mc_add_device(void* mc);
+int w4a16_mc_bind(void* mc, size_t bytes, void** uc_out, void** mc_va_out);
+int w4a16_mc_free(void* mc, void* uc, void* mc_va, size_t bytes);
 
 /* Bytes of the plan (host buffer) for n_ops ops. */
 size_t w4a16_chain_plan_bytes(int n_ops);

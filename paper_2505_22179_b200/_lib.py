@@ -20,6 +20,7 @@ W4A16_GROUP = 128
 W4A16_MAX_M = 64
 W4A16_MAX_TREE = 1024
 W4A16_MAX_N = 1048576
+W4A16_AR_MAX_TILES = 128
 W4A16_FAMILY_AUTO, W4A16_FAMILY_MMA_SYNC, W4A16_FAMILY_TCGEN05, W4A16_FAMILY_MMA_SYNC_S, W4A16_FAMILY_TCGEN05_OC = -1, 0, 1, 2, 3
 
 # Every symbol include/w4a16.h declares (checked by tests/test_abi.py).
@@ -51,6 +52,12 @@ ABI_SYMBOLS = (
     "w4a16_ipc_open",
     "w4a16_ipc_close",
     "w4a16_ipc_free",
+    "w4a16_mc_supported",
+    "w4a16_mc_create",
+    "w4a16_mc_import",
+    "w4a16_mc_add_device",
+    "w4a16_mc_bind",
+    "w4a16_mc_free",
     "w4a8_quantize_act",
     "w4a8_workspace_bytes",
     "w4a8_gemm",
@@ -68,7 +75,7 @@ class W4A16Op(ctypes.Structure):
 class W4A16PeerGroup(ctypes.Structure):
     """struct w4a16_peer_group of include/w4a16.h (host side; read by w4a16_chain_plan only)."""
     _fields_ = [("base", ctypes.c_void_p * W4A16_MAX_PEERS), ("bytes", ctypes.c_size_t), ("flag_offset", ctypes.c_size_t),
-                ("flag_slots", ctypes.c_int), ("world", ctypes.c_int), ("rank", ctypes.c_int)]
+                ("flag_slots", ctypes.c_int), ("world", ctypes.c_int), ("rank", ctypes.c_int), ("mc_base", ctypes.c_void_p)]
 
 
 class W4A16Error(RuntimeError):
@@ -129,12 +136,21 @@ def _load():
     lib.w4a16_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
     lib.w4a16_ipc_close.argtypes = [vp]
     lib.w4a16_ipc_free.argtypes = [vp]
+    lib.w4a16_mc_supported.argtypes = []
+    lib.w4a16_mc_create.argtypes = [sz, i32, vp, ctypes.POINTER(vp)]
+    lib.w4a16_mc_import.argtypes = [vp, sz, i32, ctypes.POINTER(vp)]
+    lib.w4a16_mc_add_device.argtypes = [vp]
+    lib.w4a16_mc_bind.argtypes = [vp, sz, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    lib.w4a16_mc_free.argtypes = [vp, vp, vp, sz]
     # test hooks (exported, not in the header): chains planned / run for a given SM count, non-cooperatively
     lib.w4a16_chain_workspace_bytes_sms.argtypes = [vp, i32, i32, i32, i32]
     lib.w4a16_chain_workspace_bytes_sms.restype = sz
     lib.w4a16_chain_plan_sms.argtypes = [vp, i32, i32, i32, vp, sz, i32]
+    lib.w4a16_chain_check_sms.argtypes = [vp, i32, i32, i32, i32]
+    lib.w4a16_chain_check_sms.restype = i32
     lib.w4a16_chain_run_sms.argtypes = [vp, i32, i32, i32, i32, vp, sz, i32, vp]
-    for name in ("w4a16_ipc_alloc", "w4a16_ipc_open", "w4a16_ipc_close", "w4a16_ipc_free", "w4a16_chain_plan_sms",
+    for name in ("w4a16_ipc_alloc", "w4a16_ipc_open", "w4a16_ipc_close", "w4a16_ipc_free", "w4a16_mc_supported",
+                 "w4a16_mc_create", "w4a16_mc_import", "w4a16_mc_add_device", "w4a16_mc_bind", "w4a16_mc_free", "w4a16_chain_plan_sms",
                  "w4a16_chain_run_sms", "w4a16_chain_plan", "w4a16_chain_run", "w4a16_pack", "w4a16_unpack", "w4a16_workspace_init", "w4a16_gemm", "w4a16_gemm_ex", "verify_accept",
                  "w4a16_gemm_family", "w4a16_silu_mul", "w4a16_silu_mul_blocked"):
         getattr(lib, name).restype = i32

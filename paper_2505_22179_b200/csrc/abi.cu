@@ -2,7 +2,10 @@
 // dispatch to the kernels in pack.cu, gemm_mma.cu, gemm_tc.cu and accept.cu. No device allocation, no
 // host synchronisation, no global state beyond a per-device SM-count cache.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "w4a16.h"
 
@@ -217,6 +220,234 @@ extern "C" int w4a16_ipc_close(void* dev_ptr) {
 extern "C" int w4a16_ipc_free(void* dev_ptr) {
   if (!dev_ptr) return W4A16_ERR_ARG;
   return cudaFree(dev_ptr) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+// ---- symmetric regions bound to a multicast object (NVLS) ----
+// Driver entry points resolved at run time (cudaGetDriverEntryPoint), so the library never links libcuda.
+namespace {
+struct McApi {
+  bool ok = false;
+  CUresult (*create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+  CUresult (*granularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+  CUresult (*add_device)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*bind_mem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t, unsigned long long);
+  CUresult (*unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*export_handle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+  CUresult (*import_handle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+  CUresult (*mem_create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+  CUresult (*mem_release)(CUmemGenericAllocationHandle);
+  CUresult (*alloc_granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*addr_free)(CUdeviceptr, size_t);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*attr)(int*, CUdevice_attribute, CUdevice);
+};
+template <class F>
+bool entry(const char* name, F& f) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return false;
+  f = reinterpret_cast<F>(p);
+  return true;
+}
+const McApi& mc_api() {
+  static McApi a = [] {
+    McApi m;
+    m.ok = entry("cuMulticastCreate", m.create) && entry("cuMulticastGetGranularity", m.granularity) &&
+           entry("cuMulticastAddDevice", m.add_device) && entry("cuMulticastBindMem", m.bind_mem) &&
+           entry("cuMulticastUnbind", m.unbind) && entry("cuMemExportToShareableHandle", m.export_handle) &&
+           entry("cuMemImportFromShareableHandle", m.import_handle) && entry("cuMemCreate", m.mem_create) &&
+           entry("cuMemRelease", m.mem_release) && entry("cuMemGetAllocationGranularity", m.alloc_granularity) &&
+           entry("cuMemAddressReserve", m.reserve) && entry("cuMemAddressFree", m.addr_free) && entry("cuMemMap", m.map) &&
+           entry("cuMemUnmap", m.unmap) && entry("cuMemSetAccess", m.set_access) && entry("cuDeviceGetAttribute", m.attr);
+    return m;
+  }();
+  return a;
+}
+// Diagnostics: the last failing driver call of the w4a16_mc_* functions (printed when W4A16_MC_DEBUG is set).
+CUresult g_mc_err = CUDA_SUCCESS;
+const char* g_mc_where = "";
+bool mc_ok(CUresult r, const char* where) {
+  if (r == CUDA_SUCCESS) return true;
+  g_mc_err = r;
+  g_mc_where = where;
+  if (getenv("W4A16_MC_DEBUG")) fprintf(stderr, "w4a16_mc: %s failed: CUresult %d\n", where, (int)r);
+  return false;
+}
+// Size of a multicast object for `bytes` and `world` devices: the same on every rank (same query).
+int mc_size(const McApi& a, size_t bytes, int world, size_t* size) {
+  CUmulticastObjectProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.numDevices = (unsigned)world;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  size_t gran = 0;
+  if (!mc_ok(a.granularity(&gran, &prop, CU_MULTICAST_GRANULARITY_MINIMUM), "granularity") || gran == 0) return W4A16_ERR_CUDA;
+  *size = (bytes + gran - 1) / gran * gran;
+  return W4A16_OK;
+}
+struct McObject {
+  CUmemGenericAllocationHandle mc = 0, mem = 0;
+  size_t size = 0;
+  int world = 0;
+  CUdevice dev = 0;
+  bool bound = false;
+};
+int current_device(CUdevice* d) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return W4A16_ERR_CUDA;
+  *d = (CUdevice)dev;
+  return W4A16_OK;
+}
+}  // namespace
+
+// Test hook (exported, not in the header): the last failing driver call of the w4a16_mc_* functions.
+extern "C" int w4a16_mc_last_error(const char** where) {
+  if (where) *where = g_mc_where;
+  return (int)g_mc_err;
+}
+
+extern "C" int w4a16_mc_supported(void) {
+  const McApi& a = mc_api();
+  CUdevice d;
+  if (!a.ok || current_device(&d) != W4A16_OK) return 0;
+  cudaFree(nullptr);   // make sure the primary context exists
+  int mc = 0, fabric = 0;
+  if (!mc_ok(a.attr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d), "attr")) return 0;
+  if (!mc_ok(a.attr(&fabric, CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED, d), "attr")) return 0;
+  return mc && fabric ? 1 : 0;
+}
+
+extern "C" int w4a16_mc_create(size_t bytes, int world, void* handle_out, void** mc_out) {
+  const McApi& a = mc_api();
+  if (!handle_out || !mc_out || bytes == 0 || world < 1 || world > W4A16_MAX_PEERS) return W4A16_ERR_ARG;
+  if (!a.ok) return W4A16_ERR_CUDA;
+  CUmulticastObjectProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.numDevices = (unsigned)world;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  if (mc_size(a, bytes, world, &prop.size) != W4A16_OK) return W4A16_ERR_CUDA;
+  McObject* o = new McObject;
+  o->size = prop.size;
+  o->world = world;
+  CUmemFabricHandle fh;
+  if (!mc_ok(a.create(&o->mc, &prop), "create")) { delete o; return W4A16_ERR_CUDA; }
+  if (!mc_ok(a.export_handle(&fh, o->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0), "export_handle")) {
+    a.mem_release(o->mc);
+    delete o;
+    return W4A16_ERR_CUDA;
+  }
+  static_assert(sizeof(fh) == 64, "fabric handle size");
+  memcpy(handle_out, &fh, sizeof(fh));
+  *mc_out = o;
+  return W4A16_OK;
+}
+
+extern "C" int w4a16_mc_import(const void* handle, size_t bytes, int world, void** mc_out) {
+  const McApi& a = mc_api();
+  if (!handle || !mc_out || bytes == 0 || world < 1 || world > W4A16_MAX_PEERS) return W4A16_ERR_ARG;
+  if (!a.ok) return W4A16_ERR_CUDA;
+  CUmemFabricHandle fh;
+  memcpy(&fh, handle, sizeof(fh));
+  McObject* o = new McObject;
+  o->world = world;
+  if (mc_size(a, bytes, world, &o->size) != W4A16_OK) { delete o; return W4A16_ERR_CUDA; }
+  if (!mc_ok(a.import_handle(&o->mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC), "import_handle")) { delete o; return W4A16_ERR_CUDA; }
+  *mc_out = o;
+  return W4A16_OK;
+}
+
+extern "C" int w4a16_mc_add_device(void* mc) {
+  const McApi& a = mc_api();
+  McObject* o = reinterpret_cast<McObject*>(mc);
+  if (!o) return W4A16_ERR_ARG;
+  if (!a.ok || current_device(&o->dev) != W4A16_OK) return W4A16_ERR_CUDA;
+  cudaFree(nullptr);
+  return mc_ok(a.add_device(o->mc, o->dev), "add_device") ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+extern "C" int w4a16_mc_bind(void* mc, size_t bytes, void** uc_out, void** mc_va_out) {
+  const McApi& a = mc_api();
+  McObject* o = reinterpret_cast<McObject*>(mc);
+  if (!o || !uc_out || !mc_va_out || bytes == 0) return W4A16_ERR_ARG;
+  if (!a.ok) return W4A16_ERR_CUDA;
+  CUmemAllocationProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = (int)o->dev;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  size_t gran = 0;
+  if (!mc_ok(a.alloc_granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "alloc_granularity") || gran == 0) return W4A16_ERR_CUDA;
+  size_t size = (bytes + gran - 1) / gran * gran;
+  size = o->size > size ? o->size : size;
+  if (size % gran) size = (size + gran - 1) / gran * gran;
+  CUdeviceptr uc = 0, mva = 0;
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = (int)o->dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  int err = W4A16_ERR_CUDA;
+  if (!mc_ok(a.mem_create(&o->mem, size, &prop, 0), "mem_create")) return W4A16_ERR_CUDA;
+  if (mc_ok(a.reserve(&uc, size, gran, 0, 0), "reserve")) {
+    if (mc_ok(a.map(uc, size, 0, o->mem, 0), "map") && mc_ok(a.set_access(uc, size, &acc, 1), "set_access") &&
+        cudaMemset(reinterpret_cast<void*>(uc), 0, size) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+        mc_ok(a.bind_mem(o->mc, 0, o->mem, 0, o->size, 0), "bind_mem")) {
+      o->bound = true;
+      if (mc_ok(a.reserve(&mva, o->size, gran, 0, 0), "reserve")) {
+        if (mc_ok(a.map(mva, o->size, 0, o->mc, 0), "map") && mc_ok(a.set_access(mva, o->size, &acc, 1), "set_access")) {
+          err = W4A16_OK;
+        } else {
+          a.unmap(mva, o->size);
+          a.addr_free(mva, o->size);
+          mva = 0;
+        }
+      }
+    }
+    if (err != W4A16_OK) {
+      if (o->bound) a.unbind(o->mc, o->dev, 0, o->size);
+      o->bound = false;
+      a.unmap(uc, size);
+      a.addr_free(uc, size);
+    }
+  }
+  if (err != W4A16_OK) {
+    a.mem_release(o->mem);
+    o->mem = 0;
+    return err;
+  }
+  *uc_out = reinterpret_cast<void*>(uc);
+  *mc_va_out = reinterpret_cast<void*>(mva);
+  return W4A16_OK;
+}
+
+extern "C" int w4a16_mc_free(void* mc, void* uc, void* mc_va, size_t bytes) {
+  const McApi& a = mc_api();
+  McObject* o = reinterpret_cast<McObject*>(mc);
+  if (!o) return W4A16_ERR_ARG;
+  if (!a.ok) return W4A16_ERR_CUDA;
+  cudaDeviceSynchronize();
+  bool ok = true;
+  if (mc_va) ok &= mc_ok(a.unmap((CUdeviceptr)mc_va, o->size), "unmap") && mc_ok(a.addr_free((CUdeviceptr)mc_va, o->size), "addr_free");
+  if (o->bound) ok &= mc_ok(a.unbind(o->mc, o->dev, 0, o->size), "unbind");
+  if (uc) {
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof(prop));
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = (int)o->dev;
+    size_t gran = 1;
+    a.alloc_granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+    size_t size = (bytes + gran - 1) / gran * gran;
+    size = o->size > size ? o->size : size;
+    ok &= mc_ok(a.unmap((CUdeviceptr)uc, size), "unmap") && mc_ok(a.addr_free((CUdeviceptr)uc, size), "addr_free");
+  }
+  if (o->mem) ok &= mc_ok(a.mem_release(o->mem), "mem_release");
+  ok &= mc_ok(a.mem_release(o->mc), "mem_release");
+  delete o;
+  return ok ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
 extern "C" size_t w4a16_lmhead_workspace_bytes(int M, int K, int V) {

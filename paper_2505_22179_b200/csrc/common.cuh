@@ -34,15 +34,26 @@ struct alignas(64) ChainJob {
   int epi;                 // GEMM: 0 = plain Y, 1 = SiLU*mul of [64 gate | 64 up] tiles into Y [M][N/2]
   int xf_mul;              // producer tiles per activation k-group (1, or 2 when X is a GEMM_SILU output)
   int n_tiles;             // job 0: tiles of all GEMM ops (counters, then as many tile-ready flags, in the workspace)
-  // ALLREDUCE (include/w4a16.h): every rank's partial as mapped here (rank order), this rank's ready flag in
-  // every rank's flag area, this rank's own `world` ready flags of the op's slot, the group's run counter
-  // (local). Job 0 also carries the run counter when the chain has ALLREDUCE ops (advanced at chain end).
+  // ALLREDUCE (include/w4a16.h): every rank's partial as mapped here (rank order; peer-load path), the
+  // multicast address of the partial (NVLS path, else nullptr), this rank's tile counters of the op's slot
+  // (local), the group's run counter (local). Job 0 also carries the run counter when the chain has
+  // ALLREDUCE ops (advanced at chain end).
   const uint16_t* peer_x[W4A16_MAX_PEERS];
-  uint32_t* peer_flag[W4A16_MAX_PEERS];
-  uint32_t* my_flags;
+  const uint16_t* mc_x;
+  uint32_t* my_tiles;
   uint32_t* epoch;
   int world;
+  // GEMM whose Y is the partial of the ALLREDUCE right after it: tile t of Y written -> bump tile t's counter
+  // in every rank's flag area (through the multicast address, or through each peer's mapping); ar_prev = the
+  // chain's previous ALLREDUCE, complete on this rank before the first bump (peers are done reading).
+  uint32_t* ar_tiles_mc;
+  uint32_t* ar_tiles_peer[W4A16_MAX_PEERS];
+  int ar_world;
+  int ar_prev;
 };
+// Flag area of a peer group (include/w4a16.h): word 0 = the group's run counter, then per ALLREDUCE slot
+// W4A16_AR_MAX_TILES tile counters (each rank adds 1 per run: `world` * runs when a tile is complete).
+constexpr int kFlagHead = 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -229,6 +240,23 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// NVLS (multicast) access: `mc` is an address in a multicast mapping. ld_reduce returns the sum over every
+// device bound to the object of 8 fp16 values (fp32 accumulation in the switch, one rounding); red adds to
+// the word on every device.
+__device__ __forceinline__ uint4 multimem_ld_reduce_f16x8(const void* mc) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(mc)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void multimem_red_add_u32(uint32_t* mc, uint32_t v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_sys_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

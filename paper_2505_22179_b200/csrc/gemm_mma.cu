@@ -109,13 +109,14 @@ struct JobInfo {
   int* counters;
   int* flags;             // this op's tile-ready flags (chain) or nullptr
   int kind, N, Gk, U, dep_x, dep_y, xf_off, pub_tiles, epi, xf_mul;
+  int ar;                 // chain: Y is the partial of the ALLREDUCE op right after this GEMM (tile bumps)
   int cs;                 // counter / flag stride (1: single GEMM; 2: chain, counters and flags interleaved)
 };
 __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
   JobInfo J;
   if (p.jobs == nullptr) {
     J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters; J.flags = nullptr; J.cs = 1;
-    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0; J.epi = 0; J.xf_mul = 1;
+    J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0; J.epi = 0; J.xf_mul = 1; J.ar = 0;
   } else {
     const ChainJob* c = p.jobs + j;
     // chain: tile counter and tile-ready flag interleaved per tile (same layout in every chain that shares the
@@ -124,7 +125,7 @@ __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap
     J.flags = J.counters + 1;
     J.cs = 2;
     J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y; J.xf_off = c->xf_off;
-    J.pub_tiles = c->pub_tiles; J.epi = c->epi; J.xf_mul = c->xf_mul;
+    J.pub_tiles = c->pub_tiles; J.epi = c->epi; J.xf_mul = c->xf_mul; J.ar = c->ar_world > 0;
   }
   return J;
 }
@@ -139,6 +140,16 @@ __device__ __forceinline__ void wait_op(const GemmParams& p, int j) {
   }
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Tile t of an ALLREDUCE partial is written on this rank (after a system-scope fence): add 1 to tile t's
+// counter of the op's slot in every rank's flag area — one multimem.red through the multicast mapping
+// (NVLS), else one red per peer mapping.
+__device__ __forceinline__ void ar_bump(const ChainJob* cj, int t) {
+  if (cj->ar_tiles_mc != nullptr) {
+    multimem_red_add_u32(cj->ar_tiles_mc + t, 1u);
+  } else {
+    for (int q = 0; q < cj->ar_world; ++q) red_relaxed_sys_add_u32(cj->ar_tiles_peer[q] + t, 1u);
+  }
+}
 
 // Diagnostics only (W4A16_MMA_DEBUG bit 16): per-CTA %globaltimer stamps (entry, first stage ready, main loop
 // done, exit) of consumer warp 0 (tools/probe_tc.py --trace-mma).
@@ -214,8 +225,12 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
       : "memory");
 }
 
-// Tensor-parallel all-reduce op of a chain (include/w4a16.h W4A16_OP_ALLREDUCE): one-shot
-// over peer memory, run by every consumer thread of every CTA. Out of line: it keeps the GEMM loop's registers.
+// Tensor-parallel all-reduce op of a chain (include/w4a16.h W4A16_OP_ALLREDUCE), fused
+// with the GEMM that writes the partial P tile by tile: CTA c reduces 128-column tiles c, c + G, ... of P as
+// soon as tile t's counter in this rank's flag area shows every rank's tile for this run (the GEMM's tile
+// writers bump it in every rank's flag area, process_unit flush -> publisher warp), then writes Y's tile and
+// publishes its ready flag (the next GEMM reads Y tile by tile). No grid-wide wait. Run by every consumer
+// thread of every CTA; out of line: it keeps the GEMM loop's registers.
 #ifndef W4_AR_INLINE
 #define W4_AR_INLINE 0
 #endif
@@ -225,56 +240,56 @@ __device__ __forceinline__
 #else
 __device__ __noinline__
 #endif
-void allreduce_op(const GemmParams& p, int job, int cta) {
+void allreduce_op(const GemmParams& p, int job, int cta, int run_c) {
   const ChainJob* cj = p.jobs + job;
-  const int world = cj->world;
-  if (threadIdx.x == 0) {
-    wait_op(p, job - 1);   // every earlier op of this rank is complete (its partial P included)
-    const uint32_t e = __ldcg(cj->epoch) + 1u;
-    if (cta == 0) {
-      // P (written by every CTA, released to this thread through done[]) -> visible to the peers first
-      fence_acq_rel_sys();
-      for (int q = 0; q < world; ++q) st_release_sys(cj->peer_flag[q], e);
-    }
-    const unsigned long long t0 = globaltimer_ns();
-    for (int q = 0; q < world; ++q) {
-      while ((int)(ld_acquire_sys(cj->my_flags + q) - e) < 0) {
-        __nanosleep(128);
+  const int world = cj->world, tiles = cj->N / 128;
+  const uint32_t want = (uint32_t)world * (__ldcg(cj->epoch) + 1u);   // counters after this run's bumps
+  int* yflags = p.counters + 2 * cj->cnt_off + 1;                     // Y's tile-ready flags (interleaved)
+  if (threadIdx.x == 0 && cj->dep_y >= 0) wait_op(p, cj->dep_y);      // WAR / WAW on Y
+  for (int t = cta; t < tiles; t += p.G) {
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      while ((int)(ld_acquire_sys(cj->my_tiles + t) - want) < 0) {
+        __nanosleep(64);
         if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // a peer never arrived: fail, do not hang
       }
     }
-  }
-  named_bar_sync(1, kThreadsAR);
-  trace_op(p, job, 1);
-  const int vecs = cj->N / 8;
-  const long long total = (long long)p.M * vecs;
-  uint4* Y = reinterpret_cast<uint4*>(cj->Y);
-  for (long long i = (long long)cta * kThreadsAR + threadIdx.x; i < total; i += (long long)p.G * kThreadsAR) {
-    float a[8];
+    named_bar_sync(1, kThreadsAR);
+    trace_op(p, job, 1);
+    for (int i = threadIdx.x; i < p.M * 16; i += kThreadsAR) {   // M rows x 16 vectors of 8 fp16
+      const size_t off = (size_t)(i >> 4) * cj->N + (size_t)t * 128 + (size_t)(i & 15) * 8;
+      uint4 r;
+      if (cj->mc_x != nullptr) {
+        r = multimem_ld_reduce_f16x8(cj->mc_x + off);
+      } else {
+        float a[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = 0.f;
-    for (int q = 0; q < world; ++q) {   // rank order: the same sum on every rank
-      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(cj->peer_x[q]) + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        for (int k = 0; k < 8; ++k) a[k] = 0.f;
+        for (int q = 0; q < world; ++q) {   // rank order: the same sum on every rank
+          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(cj->peer_x[q] + off));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-        a[2 * k] += f.x;
-        a[2 * k + 1] += f.y;
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+            a[2 * k] += f.x;
+            a[2 * k + 1] += f.y;
+          }
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __half2 h = __floats2half2_rn(a[2 * k], a[2 * k + 1]);
+          o[k] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        r = make_uint4(o[0], o[1], o[2], o[3]);
       }
+      *reinterpret_cast<uint4*>(cj->Y + off) = r;
     }
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const __half2 h = __floats2half2_rn(a[2 * k], a[2 * k + 1]);
-      o[k] = *reinterpret_cast<const uint32_t*>(&h);
-    }
-    Y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    named_bar_sync(1, kThreadsAR);
+    if (threadIdx.x == 0 && cj->pub_tiles)
+      asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(yflags + 2 * t), "r"(run_c + 1) : "memory");
   }
-  named_bar_sync(1, kThreadsAR);
   if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
-  trace_op(p, job, 2);
-  trace_op(p, job, 3);
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
@@ -418,7 +433,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // red then releases them to the CTAs that acquire the counter. nullptr ends the kernel's requests.
     // Requests that queue up while a fence is in flight are issued together behind ONE fence (a GPU-scope
     // fence costs ~1 us under load; op counts, tile counters and tile-ready flags all come through here).
-    int slot = 0;
+    int slot = 0, ar_prev_done = -1;
     uint32_t ph = 0;
     for (;;) {
       mbar_wait(&pub_full[slot], ph);
@@ -432,13 +447,31 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         }
       }
       bool stop = false;
-      if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      // ALLREDUCE tile bumps (val < 0, ptr = the GEMM's ChainJob, tile -val - 1) go to other GPUs: they need a
+      // system-scope fence, and the chain's previous ALLREDUCE must be complete on this rank first
+      bool sys = false;
+      {
+        int s2 = slot;
+        for (int i = 0; i < n; ++i) {
+          if (pub_ptr[s2] && pub_val[s2] < 0) {
+            sys = true;
+            const ChainJob* cj = reinterpret_cast<const ChainJob*>(pub_ptr[s2]);
+            if (lane == 0 && cj->ar_prev > ar_prev_done) { wait_op(p, cj->ar_prev); ar_prev_done = cj->ar_prev; }
+          }
+          if (++s2 == kPubSlots) s2 = 0;
+        }
+      }
+      if (lane == 0) {
+        if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
       for (int i = 0; i < n; ++i) {
         int* ptr = pub_ptr[slot];
         const int val = pub_val[slot];
         if (lane == 0) {
           if (ptr && val == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(ptr) : "memory");
-          if (ptr && val != 0) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
+          if (ptr && val > 0) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
+          if (ptr && val < 0) ar_bump(reinterpret_cast<const ChainJob*>(ptr), -val - 1);
           mbar_arrive(&pub_empty[slot]);
         }
         stop |= ptr == nullptr;
@@ -459,7 +492,13 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   auto publish = [&](int* ptr, int val = 0) {
     if (!W4_MA_PUB) {
       if (ptr && val == 0) red_release_gpu_add(ptr, 1);
-      if (ptr && val != 0) asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
+      if (ptr && val > 0) asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
+      if (ptr && val < 0) {
+        const ChainJob* cj = reinterpret_cast<const ChainJob*>(ptr);
+        if (cj->ar_prev >= 0) wait_op(p, cj->ar_prev);
+        fence_acq_rel_sys();
+        ar_bump(cj, -val - 1);
+      }
       return;
     }
     mbar_wait(&pub_empty[pub_s], pub_ph ^ 1);   // the slot's previous request is consumed
@@ -511,7 +550,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       continue;
     }
     if (J.kind == kOpAllReduce) {
-      allreduce_op<kWarps * 32>(p, job, cta);
+      allreduce_op<kWarps * 32>(p, job, cta, run_c);
       continue;
     }
     const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
@@ -593,9 +632,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         }
       };
       auto tile_written = [&]() {   // chain: the tile's Y is complete -> its ready flag (tile-level deps)
-        if (!chain || !J.pub_tiles) return;
+        if (!chain || (!J.pub_tiles && !J.ar)) return;
         named_bar_sync(2, 8 * 32);
-        if (threadIdx.x == 0) publish(&J.flags[J.cs * t], run_c + 1);
+        if (threadIdx.x == 0 && J.pub_tiles) publish(&J.flags[J.cs * t], run_c + 1);
+        // Y is an ALLREDUCE's partial: bump tile t's counter in every rank's flag area (publisher warp)
+        if (threadIdx.x == 0 && J.ar) publish(reinterpret_cast<int*>(const_cast<ChainJob*>(p.jobs + job)), -t - 1);
       };
       if (sg0 == tile_u0 && sg1 == tile_u1) { store(acc); tile_written(); return; }
       // Split tile: the tile's first CTA c_first owns it. It handles the tile's head as its
@@ -951,7 +992,9 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
     } else if (o.kind == W4A16_OP_SILU_MUL) {
       if (o.N < 8 || o.N % 8 || o.K != 2 * o.N) return W4A16_ERR_SHAPE;
     } else if (o.kind == W4A16_OP_ALLREDUCE) {
-      if (o.N < 8 || o.N % 8 || o.K != o.N) return W4A16_ERR_SHAPE;
+      if (o.N < 128 || o.N % 128 || o.N / 128 > W4A16_AR_MAX_TILES || o.K != o.N) return W4A16_ERR_SHAPE;
+      // fused with the GEMM right before it: X is exactly that GEMM's (plain) Y
+      if (j == 0 || ops[j - 1].kind != W4A16_OP_GEMM || ops[j - 1].Y != o.X || ops[j - 1].N != o.N) return W4A16_ERR_ARG;
       const w4a16_peer_group* g = reinterpret_cast<const w4a16_peer_group*>(o.packed);
       if (!g) return W4A16_ERR_ARG;
       if (n_ar == 0) group = g;
@@ -960,11 +1003,14 @@ int check_ops(const w4a16_op* ops, int n_ops, int M, int G, long long* tiles, in
       if (g->world < 1 || g->world > W4A16_MAX_PEERS || g->rank < 0 || g->rank >= g->world) return W4A16_ERR_ARG;
       if (g->flag_offset % 256 || g->flag_slots < 1) return W4A16_ERR_ARG;
       if (n_ar > g->flag_slots || g->flag_offset + w4a16_peer_flag_bytes(g->flag_slots) > g->bytes) return W4A16_ERR_ARG;
-      for (int q = 0; q < g->world; ++q)
-        if (!g->base[q] || !al16(g->base[q])) return W4A16_ERR_ARG;
+      if (!g->base[g->rank] || !al16(g->base[g->rank]) || (g->mc_base && !al16(g->mc_base))) return W4A16_ERR_ARG;
+      if (!g->mc_base)   // the peer-load path reads every rank's mapping
+        for (int q = 0; q < g->world; ++q)
+          if (!g->base[q] || !al16(g->base[q])) return W4A16_ERR_ARG;
       const uintptr_t b0 = reinterpret_cast<uintptr_t>(g->base[g->rank]);
       const Span xs = x_span(o, M), flags = {b0 + g->flag_offset, b0 + g->flag_offset + w4a16_peer_flag_bytes(g->flag_slots)};
       if (xs.a < b0 || xs.b > b0 + g->bytes || overlaps(xs, flags)) return W4A16_ERR_ARG;   // P inside the region
+      t += o.N / 128;   // Y's tile-ready flags
     } else {
       return W4A16_ERR_ARG;
     }
@@ -992,7 +1038,18 @@ int chain_ctas(int sms) { return w4::ma::kCtasPerSm * sms; }   // the tcgen05 fa
 
 
 extern "C" size_t w4a16_peer_flag_bytes(int flag_slots) {
-  return flag_slots > 0 ? ((size_t)(16 + flag_slots * W4A16_MAX_PEERS) * 4 + 255) / 256 * 256 : 0;
+  return flag_slots > 0 ? ((size_t)(w4::kFlagHead + (size_t)flag_slots * W4A16_AR_MAX_TILES) * 4 + 255) / 256 * 256 : 0;
+}
+
+// Test hook (exported, not in the header): validate a chain's ops (w4a16_chain_plan's checks) without
+// encoding tensor maps, so the planner's rules are testable on a machine without a GPU.
+extern "C" int w4a16_chain_check_sms(const w4a16_op* ops, int n_ops, int M, int family, int sms) {
+  const int fam = chain_family(M, family);
+  if (fam < 0) return fam;
+  if (sms <= 0) return W4A16_ERR_ARG;
+  long long tiles = 0;
+  int mode = 0;
+  return check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode);
 }
 
 extern "C" size_t w4a16_chain_plan_bytes(int n_ops) { return n_ops > 0 ? (size_t)n_ops * sizeof(w4::ma::ChainJob) : 0; }
@@ -1018,7 +1075,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
   if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
   const int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the stages
   w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
-  int cnt = 0, ar_slot = 0;
+  int cnt = 0, ar_slot = 0, last_ar = -1;
   uint32_t* epoch = nullptr;   // the group's run counter, advanced by the last CTA of every run
   for (int j = 0; j < n_ops; ++j) {
     const w4a16_op& o = ops[j];
@@ -1041,17 +1098,26 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
     } else if (o.kind == W4A16_OP_ALLREDUCE) {
       const w4a16_peer_group* g = reinterpret_cast<const w4a16_peer_group*>(o.packed);
       const size_t off = reinterpret_cast<uintptr_t>(o.X) - reinterpret_cast<uintptr_t>(g->base[g->rank]);
-      auto flag_word = [&](int q, size_t word) {
-        return reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(g->base[q]) + g->flag_offset) + word;
+      const size_t slot_word = w4::kFlagHead + (size_t)ar_slot * W4A16_AR_MAX_TILES;
+      auto flags_of = [&](void* base) {
+        return reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(base) + g->flag_offset);
       };
       J.world = g->world;
-      for (int q = 0; q < g->world; ++q) {
-        J.peer_x[q] = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(g->base[q]) + off);
-        J.peer_flag[q] = flag_word(q, 16 + (size_t)ar_slot * W4A16_MAX_PEERS + g->rank);   // slot ar_slot, from this rank
-      }
-      J.my_flags = flag_word(g->rank, 16 + (size_t)ar_slot * W4A16_MAX_PEERS);
-      J.epoch = flag_word(g->rank, 0);
+      J.cnt_off = cnt;   // Y's tile-ready flags
+      cnt += o.N / 128;
+      J.mc_x = g->mc_base ? reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(g->mc_base) + off) : nullptr;
+      for (int q = 0; q < g->world; ++q)
+        J.peer_x[q] = g->base[q] ? reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(g->base[q]) + off) : nullptr;
+      J.my_tiles = flags_of(g->base[g->rank]) + slot_word;
+      J.epoch = flags_of(g->base[g->rank]);
       if (!epoch) epoch = J.epoch;
+      // the GEMM right before writes the partial: its tile writers bump tile t's counter in every rank's area
+      w4::ma::ChainJob& P = jobs[j - 1];
+      P.ar_world = g->world;
+      P.ar_prev = last_ar;
+      P.ar_tiles_mc = g->mc_base ? flags_of(g->mc_base) + slot_word : nullptr;
+      for (int q = 0; q < g->world; ++q) P.ar_tiles_peer[q] = g->base[q] ? flags_of(g->base[q]) + slot_word : nullptr;
+      last_ar = j;
       ++ar_slot;
     }
     // dependencies from buffer overlaps: RAW for X; WAR / WAW for Y. Completion of op i implies the
@@ -1066,7 +1132,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
     }
     // tile-level RAW dependency: X is a whole-tile column range of the producing GEMM's Y with Y's row stride
     // (a GEMM_SILU producer writes 64 output columns per tile: 2 tiles per 128-column k-group)
-    if (is_gemm(o.kind) && J.dep_x >= 0 && is_gemm(ops[J.dep_x].kind)) {
+    if (is_gemm(o.kind) && J.dep_x >= 0 && (is_gemm(ops[J.dep_x].kind) || ops[J.dep_x].kind == W4A16_OP_ALLREDUCE)) {
       const w4a16_op& d = ops[J.dep_x];
       const int per_tile = d.kind == W4A16_OP_GEMM_SILU ? 64 : 128, yc = y_cols(d);
       const uintptr_t xb = reinterpret_cast<uintptr_t>(o.X), yb = reinterpret_cast<uintptr_t>(d.Y);

@@ -309,7 +309,8 @@ class PeerGroup:
     shapes in the same order, so each buffer has the same offset on every rank. Build with PeerGroup.ipc
     (one process per GPU, CUDA IPC) or PeerGroup.simulated (tests: `world` regions on one device)."""
 
-    def __init__(self, bases, local: torch.Tensor, nbytes: int, flag_slots: int, world: int, rank: int, closer=None):
+    def __init__(self, bases, local: torch.Tensor, nbytes: int, flag_slots: int, world: int, rank: int, closer=None,
+                 mc_base: Optional[int] = None):
         if not 1 <= world <= W4A16_MAX_PEERS or not 0 <= rank < world or len(bases) != world:
             raise W4A16Error(f"peer group: world={world}, rank={rank}")
         self.world, self.rank, self.nbytes, self.flag_slots = world, rank, nbytes, flag_slots
@@ -319,6 +320,8 @@ class PeerGroup:
             self.desc.base[q] = b
         self.desc.bytes, self.desc.flag_offset, self.desc.flag_slots = nbytes, 0, flag_slots
         self.desc.world, self.desc.rank = world, rank
+        self.desc.mc_base = mc_base
+        self.kind = "nvls" if mc_base else "peer"
         self._next = (w4a16_peer_flag_bytes(flag_slots) + 255) // 256 * 256
         self._closer = closer
 
@@ -394,6 +397,54 @@ class PeerGroup:
             raise W4A16Error(f"w4a16_ipc_open failed on rank(s) {[q for q, e in enumerate(errs) if e != W4A16_OK]}")
         local = torch.as_tensor(_DevBuf(ptr.value, nbytes), device=torch.device("cuda", torch.cuda.current_device()))
         return PeerGroup(bases, local, nbytes, flag_slots, world, rank, closer)
+
+    @staticmethod
+    def mc_supported() -> bool:
+        return bool(lib.w4a16_mc_supported())
+
+    @staticmethod
+    def mc(nbytes: int, flag_slots: int, group=None):
+        """One process per GPU, NVLS: rank 0 creates a multicast object for the group (fabric handle sent over
+        `group`, any torch.distributed backend), every rank adds its device, then binds its own region to it
+        and maps the multicast range (include/w4a16.h w4a16_mc_*). The ALLREDUCE ops then bump tile counters
+        with one multimem.red and reduce with multimem.ld_reduce; peers' regions are never mapped."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+        def agree(ok: bool, what: str):
+            flags = [ok]
+            if world > 1:
+                flags = [None] * world
+                dist.all_gather_object(flags, ok, group=group)
+            if not all(flags):
+                raise W4A16Error(f"{what} failed on rank(s) {[q for q, f in enumerate(flags) if not f]}")
+        agree(bool(lib.w4a16_mc_supported()), "w4a16_mc_supported")
+        mc = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        st = lib.w4a16_mc_create(nbytes, world, handle, ctypes.byref(mc)) if rank == 0 else W4A16_OK
+        hs = [(st, bytes(handle))]
+        if world > 1:
+            hs = [None] * world
+            dist.all_gather_object(hs, (st, bytes(handle)), group=group)
+        agree(hs[0][0] == W4A16_OK, "w4a16_mc_create (rank 0)")
+        if rank != 0:
+            hb = (ctypes.c_uint8 * 64).from_buffer_copy(hs[0][1])
+            st = lib.w4a16_mc_import(hb, nbytes, world, ctypes.byref(mc))
+            agree(st == W4A16_OK, "w4a16_mc_import")
+        st = lib.w4a16_mc_add_device(mc)
+        agree(st == W4A16_OK, "w4a16_mc_add_device")   # every device added before any rank binds
+        uc, mva = ctypes.c_void_p(), ctypes.c_void_p()
+        st = lib.w4a16_mc_bind(mc, nbytes, ctypes.byref(uc), ctypes.byref(mva))
+        agree(st == W4A16_OK, "w4a16_mc_bind")
+        if world > 1:
+            dist.barrier(group=group)   # every rank bound before the first multicast access
+
+        def closer():
+            lib.w4a16_mc_free(mc, uc, mva, nbytes)
+        local = torch.as_tensor(_DevBuf(uc.value, nbytes), device=torch.device("cuda", torch.cuda.current_device()))
+        bases = [uc.value if q == rank else None for q in range(world)]
+        return PeerGroup(bases, local, nbytes, flag_slots, world, rank, closer, mc_base=mva.value)
 
     def close(self):
         if self._closer is not None:

@@ -162,7 +162,7 @@ class VerifyStack:
             # outputs are ordinary local buffers
             slots = 2 * n_layers
             nbytes = w4a16_peer_flag_bytes(slots) + 2 * M_max * (P["o"]["N"] + P["down"]["N"]) + 4096
-            self.peers = peer_group if peer_group is not None else PeerGroup.ipc(nbytes, slots, group)
+            self.peers = peer_group if peer_group is not None else _peer_group(nbytes, slots, group)
             self.y_o = self.peers.alloc(M_max, P["o"]["N"])
             self.y_down = self.peers.alloc(M_max, P["down"]["N"])
             self.y_o_red = torch.empty(M_max, P["o"]["N"], **f16)
@@ -180,6 +180,7 @@ class VerifyStack:
         self.accept_out = torch.zeros(3 + M_max, **i32)
         self.ws = alloc_workspace(M_max, [(s["K"], s["N"]) for s in P.values()], device=self.device)
         self.graphs = {}
+        self.capturable = True
         self.use_chains = True
         self._chains = {}
 
@@ -274,8 +275,13 @@ class VerifyStack:
         return 5 * self.n_layers + 1
 
     def capture(self, M: int) -> torch.cuda.CUDAGraph:
-        """Capture forward(M) as a CUDA graph (after one eager warm-up on the capture stream)."""
+        """Capture forward(M) as a CUDA graph (after one eager warm-up on the capture stream). With
+        capturable = False (a process group whose all-reduce cannot be captured, e.g. gloo in the tests of
+        bench.py's multi-rank path) an object whose replay() runs forward(M) eagerly is returned instead."""
         if M in self.graphs:
+            return self.graphs[M]
+        if not self.capturable:
+            self.graphs[M] = _Eager(self, M)
             return self.graphs[M]
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
@@ -315,6 +321,26 @@ class VerifyStack:
 
     def d2h_bytes(self, M: int) -> int:
         return 4 * (3 + M) + 2 * M * self.y_down_red.shape[1]
+
+
+class _Eager:
+    """replay() = one eager forward (VerifyStack.capture when the process group cannot be captured)."""
+
+    def __init__(self, st: "VerifyStack", M: int):
+        self.st, self.M = st, M
+
+    def replay(self):
+        self.st.forward(self.M)
+
+
+def _peer_group(nbytes: int, slots: int, group):
+    """The symmetric regions of a fused all-reduce: NVLS (one multicast object, multimem loads / reds) where
+    every rank's device supports it, else CUDA-IPC peer mappings. Every step is agreed on by all ranks, so a
+    failure anywhere falls back everywhere (e.g. several ranks on one GPU cannot share a multicast object)."""
+    try:
+        return PeerGroup.mc(nbytes, slots, group)
+    except W4A16Error:
+        return PeerGroup.ipc(nbytes, slots, group)
 
 
 class _Calibration:

@@ -60,11 +60,10 @@ def _group(world=2, rank=0, slots=4, bases=None):
 
 
 def _plan(ops, M=8, sms=148):
+    # the planner's validation (w4a16_chain_plan's rules) without tensor-map encoding, which needs a GPU
     w4, L = _w4()
     arr = (L.W4A16Op * len(ops))(*ops)
-    nb = int(L.lib.w4a16_chain_plan_bytes(len(ops)))
-    host = (ctypes.c_uint8 * nb)()
-    return L.lib.w4a16_chain_plan_sms(ctypes.addressof(arr), len(ops), M, -1, ctypes.addressof(host), nb, sms)
+    return L.lib.w4a16_chain_check_sms(ctypes.addressof(arr), len(ops), M, -1, sms)
 
 
 def _ar(g, x_off, y, N=1024, rank=0):
@@ -77,6 +76,15 @@ def _silu(gu, out, N=1024):
     return L.W4A16Op(L.W4A16_OP_SILU_MUL, gu, None, out, 2 * N, N, 0)
 
 
+PACKED = 0x7d0000000000   # placeholder weight blob (never dereferenced by the planner)
+
+
+def _gemm(x, y, N=1024, K=4096):
+    # the row-parallel GEMM whose Y is the ALLREDUCE's partial (the op right before it)
+    _, L = _w4()
+    return L.W4A16Op(L.W4A16_OP_GEMM, x, PACKED, y, K, N, 0)
+
+
 OUT = 0x7e0000000000   # ordinary (non-region) buffers
 P1, P2 = 65536, 131072  # partial buffers inside the region, after the flag area
 
@@ -86,24 +94,45 @@ def test_flag_area_size():
     assert L.lib.w4a16_peer_flag_bytes(0) == 0
     for slots in (1, 4, 160):
         nb = L.lib.w4a16_peer_flag_bytes(slots)
-        assert nb % 256 == 0 and nb >= (16 + slots * L.W4A16_MAX_PEERS) * 4
+        assert nb % 256 == 0 and nb >= (16 + slots * L.W4A16_AR_MAX_TILES) * 4
 
 
 def test_plan_accepts_alternating_partials():
     g = _group()
     # layer: producer -> P1, AR(P1 -> out1), producer -> P2, AR(P2 -> out2), repeated (cyclic rule holds)
-    ops = [_silu(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)),
-           _silu(OUT + (2 << 20), g.base[0] + P2), _ar(g, P2, OUT + (3 << 20))]
+    ops = [_gemm(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)),
+           _gemm(OUT + (2 << 20), g.base[0] + P2), _ar(g, P2, OUT + (3 << 20))]
     assert _plan(ops) == 0
+
+
+def test_plan_multicast_group_needs_no_peer_mappings():
+    g = _group()
+    g.base[1] = None                     # the NVLS path never maps the peers' regions
+    ops = [_gemm(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)),
+           _gemm(OUT + (2 << 20), g.base[0] + P2), _ar(g, P2, OUT + (3 << 20))]
+    assert _plan(ops) != 0               # peer-load path: every mapping is needed
+    g.mc_base = BASE + (1 << 30)
+    assert _plan(ops) == 0
+
+
+def test_plan_rejects_allreduce_not_fused_with_its_gemm():
+    g = _group()
+    # the op before an ALLREDUCE must be the GEMM that writes exactly its partial
+    ops = [_silu(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)),
+           _gemm(OUT + (2 << 20), g.base[0] + P2), _ar(g, P2, OUT + (3 << 20))]
+    assert _plan(ops) != 0
+    ops = [_gemm(OUT, g.base[0] + P1 + 256), _ar(g, P1, OUT + (1 << 20)),
+           _gemm(OUT + (2 << 20), g.base[0] + P2), _ar(g, P2, OUT + (3 << 20))]
+    assert _plan(ops) != 0
 
 
 def test_plan_rejects_rewrite_before_another_allreduce():
     g = _group()
     # one partial buffer, one AR per run: the next run's producer rewrites P1 while peers may still read it
-    ops = [_silu(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20))]
+    ops = [_gemm(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20))]
     assert _plan(ops) != 0
     # rewritten inside the same run right after its AR
-    ops = [_silu(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)), _silu(OUT + (2 << 20), g.base[0] + P1),
+    ops = [_gemm(OUT, g.base[0] + P1), _ar(g, P1, OUT + (1 << 20)), _gemm(OUT + (2 << 20), g.base[0] + P1),
            _ar(g, P1, OUT + (3 << 20))]
     assert _plan(ops) != 0
 
@@ -111,12 +140,14 @@ def test_plan_rejects_rewrite_before_another_allreduce():
 @pytest.mark.parametrize("case", ["outside", "flags", "world", "rank", "slots", "two_groups", "shape"])
 def test_plan_rejects_bad_allreduce(case):
     g = _group()
-    good = lambda gg=g: [_silu(OUT, gg.base[0] + P1), _ar(gg, P1, OUT + (1 << 20)),
-                         _silu(OUT + (2 << 20), gg.base[0] + P2), _ar(gg, P2, OUT + (3 << 20))]
+    good = lambda gg=g: [_gemm(OUT, gg.base[0] + P1), _ar(gg, P1, OUT + (1 << 20)),
+                         _gemm(OUT + (2 << 20), gg.base[0] + P2), _ar(gg, P2, OUT + (3 << 20))]
     ops = good()
     if case == "outside":
+        ops[0] = _gemm(OUT, g.base[0] + REGION - 1024)
         ops[1] = _ar(g, REGION - 1024, OUT + (1 << 20))          # P runs past the region end
     elif case == "flags":
+        ops[0] = _gemm(OUT, g.base[0])
         ops[1] = _ar(g, 0, OUT + (1 << 20))                      # P overlaps the flag area
     elif case == "world":
         g.world = 9

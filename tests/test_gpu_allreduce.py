@@ -89,8 +89,9 @@ def test_chain_allreduce_simulated_ranks(T, M, mode):
 
 @pytest.mark.timeout(300)
 def test_allreduce_result_feeds_the_next_op_in_order():
-    """An op that reads an ALLREDUCE output must see the reduced values (RAW through done[]): a SiLU*mul
-    on the reduced [gate | up] equals w4a16_silu_mul applied afterwards to the same tensor."""
+    """An op that reads an ALLREDUCE output must see the reduced values (RAW through the reduced tiles'
+    ready flags): a SiLU*mul on the reduced [gate | up] equals w4a16_silu_mul applied afterwards to the same
+    tensor, and a GEMM on that output equals the same GEMM launched on its own."""
     import paper_2505_22179_b200 as w4
     T, M, F = 2, 8, 1024
     sms = torch.cuda.get_device_properties(0).multi_processor_count // T
@@ -100,27 +101,80 @@ def test_allreduce_result_feeds_the_next_op_in_order():
     ranks = []
     for r, g in enumerate(groups):
         pl = w4.pack_linear(synth.gpu(21, 400 + r, synth.WEIGHT, Kr, 2 * F))
+        pl2 = w4.pack_linear(synth.gpu(21, 600 + r, synth.WEIGHT, 2 * F, 2 * F))
         X = synth.gpu(21, 500 + r, synth.ACT, M, Kr)
         P = g.alloc(M, 2 * F)
         GU, act = torch.empty((M, 2 * F), **f16), torch.empty((M, F), **f16)
-        P2 = g.alloc(M, F)
-        out = torch.empty((M, F), **f16)
-        # the second ALLREDUCE (of a copy of act through P2) keeps the alternating-partials rule satisfied
-        ops = [("gemm", X, pl, P), ("allreduce", P, GU, g), ("silu_mul", GU, act), ("silu_mul", GU, P2),
+        P2 = g.alloc(M, 2 * F)
+        out = torch.empty((M, 2 * F), **f16)
+        # the second ALLREDUCE (of a GEMM on GU) keeps the alternating-partials rule satisfied
+        ops = [("gemm", X, pl, P), ("allreduce", P, GU, g), ("silu_mul", GU, act), ("gemm", GU, pl2, P2),
                ("allreduce", P2, out, g)]
-        ranks.append(dict(GU=GU, act=act, out=out, chain=w4.Chain(ops, M, sms=sms)))
+        ranks.append(dict(GU=GU, act=act, out=out, P2=P2, pl2=pl2, chain=w4.Chain(ops, M, sms=sms)))
     streams = [torch.cuda.Stream() for _ in range(T)]
     for rk, st in zip(ranks, streams):
         rk["chain"](st)
     torch.cuda.synchronize()
+    want_out = _fp32_rank_sum([rk["P2"] for rk in ranks])
     for rk in ranks:
         want = torch.empty_like(rk["act"])
         w4.w4a16_silu_mul(rk["GU"], want)
+        P2 = torch.empty_like(rk["P2"])
+        ws = w4.alloc_workspace(M, [(2 * F, 2 * F)])
+        rk["pl2"](rk["GU"], P2, ws)
         torch.cuda.synchronize()
         assert np.array_equal(_u16(rk["act"]), _u16(want))
         assert np.array_equal(_u16(rk["GU"]), _u16(ranks[0]["GU"]))
-        # out = act + act (both ranks' P2 hold the same act): exact doubling in fp32, one rounding
-        assert np.array_equal(_u16(rk["out"]), (want.float() * 2).half().view(torch.int16).cpu().numpy().view(np.uint16))
+        # (the chain runs on half the SMs: another stream-K split, so equal up to fp32 rounding, not bitwise)
+        assert torch.all((rk["P2"].float() - P2.float()).abs() <= 1e-3 * (1 + P2.float().abs())), \
+            "GEMM on the reduced output != the same GEMM alone"
+        assert np.array_equal(_u16(rk["out"]), want_out)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("M", [1, 8, 16])
+def test_chain_allreduce_nvls_world1(M):
+    """The NVLS path (PeerGroup.mc: a multicast object, tile counters bumped with multimem.red, tiles reduced
+    with multimem.ld_reduce) on this box's one GPU (world 1): over repeated runs the chain's reduced outputs
+    equal the fp32 rank-order definition (at world 1: the partial itself) bit for bit, the partials equal the
+    same chain over a simulated (peer-load) group, and a GEMM reading the reduced output sees it."""
+    import paper_2505_22179_b200 as w4
+    if not w4.PeerGroup.mc_supported():
+        pytest.skip("no multicast / fabric-handle support on this device")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    H = 1024
+    Kr = 128 * -(-sms // (H // 128))
+    f16 = dict(dtype=torch.float16, device="cuda")
+    pa = w4.pack_linear(synth.gpu(31, 1, synth.WEIGHT, Kr, H))
+    pb = w4.pack_linear(synth.gpu(31, 2, synth.WEIGHT, H, Kr))
+    X = torch.empty((M, Kr), **f16)
+    outs = {}
+    try:
+        w4.PeerGroup.mc(1 << 21, 4).close()
+    except w4.W4A16Error as e:   # e.g. a GPU partition whose driver refuses cuMulticastCreate
+        pytest.skip(f"multicast object creation not available here: {e}")
+    for kind in ("nvls", "peer"):
+        g = w4.PeerGroup.mc(1 << 21, 4) if kind == "nvls" else w4.PeerGroup.simulated(1, 1 << 21, 4, device="cuda")[0]
+        assert g.kind == kind
+        P1, P2 = g.alloc(M, H), g.alloc(M, Kr)
+        Y1, Y2 = torch.empty((M, H), **f16), torch.empty((M, Kr), **f16)
+        ch = w4.Chain([("gemm", X, pa, P1), ("allreduce", P1, Y1, g), ("gemm", Y1, pb, P2), ("allreduce", P2, Y2, g)], M)
+        res = []
+        for rep in range(3):   # fresh inputs every run: stale counters or partials would show
+            synth.gpu(32 + rep, 7, synth.ACT, M, Kr, out=X)
+            Y1.fill_(float("nan"))
+            Y2.fill_(float("nan"))
+            ch()
+            torch.cuda.synchronize()
+            assert np.array_equal(_u16(Y1), _u16(P1)), f"{kind} rep {rep}: Y1 != P1 (world 1)"
+            assert np.array_equal(_u16(Y2), _u16(P2)), f"{kind} rep {rep}: Y2 != P2 (world 1)"
+            res.append((_u16(P1).copy(), _u16(P2).copy()))
+        outs[kind] = res
+        del ch
+        g.close()
+    for rep in range(3):
+        assert np.array_equal(outs["nvls"][rep][0], outs["peer"][rep][0])
+        assert np.array_equal(outs["nvls"][rep][1], outs["peer"][rep][1])
 
 
 @pytest.mark.timeout(600)
