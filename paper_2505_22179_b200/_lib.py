@@ -136,6 +136,8 @@ def _load():
     lib.w4a16_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
     lib.w4a16_ipc_close.argtypes = [vp]
     lib.w4a16_ipc_free.argtypes = [vp]
+    if not hasattr(lib, "w4a16_mc_supported") and os.environ.get("W4A16_LIB"):
+        return lib   # an older A/B build without the NVLS functions
     lib.w4a16_mc_supported.argtypes = []
     lib.w4a16_mc_create.argtypes = [sz, i32, vp, ctypes.POINTER(vp)]
     lib.w4a16_mc_import.argtypes = [vp, sz, i32, ctypes.POINTER(vp)]

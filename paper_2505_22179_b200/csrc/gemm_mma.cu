@@ -43,8 +43,9 @@ constexpr int kGroups = W4_MA_GROUPS;              // consumer groups sharing on
 constexpr int kWarps = 8 * kGroups;                // per group: 4 row-quarters x 2 k-halves
 constexpr int kProducerWarp = kWarps;
 #ifndef W4_MA_PUB
-#define W4_MA_PUB 1   // 1: a publisher warp issues the counter increments (fence + red) for the storing warps
+#define W4_MA_PUB 1   // a publisher warp issues the counter increments (fence + red) for the storing warps
 #endif
+static_assert(W4_MA_PUB == 1, "the chain protocol and ALLREDUCE ops run on the publisher warp");
 // Publisher warp (W4_MA_PUB): the release of a tile / op counter costs the issuing thread a GPU-scope fence
 // (~1 us under load); the storing warps hand the increment to this warp through a shared-memory ring and
 // go straight on to the next units.
@@ -53,7 +54,11 @@ __host__ __device__ constexpr int pub_warp() { return kWarps + 1; }
 template <bool kScaleInA>
 constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0)) * 32; }
 constexpr int kPubSlots = 8;
+constexpr int kPubAllReduce = -0x40000000;   // publisher request: run ALLREDUCE op (ptr = its ChainJob)
 constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
+#ifndef W4_MA_RT
+#define W4_MA_RT 1   // 16-row MMA tiles per consumer warp at M <= 8 (2: 4 warps per unit; measured slower)
+#endif
 #ifndef W4_MA_CTAS
 #define W4_MA_CTAS 2
 #endif
@@ -67,8 +72,15 @@ struct Cfg {
   static constexpr int kXBox = kMpad * 128;                       // one 64-k SW128 box (multiple of 1024 B)
   static constexpr int kXUnit = 2 * kXBox;
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
-  static constexpr int kRedSlots = kGroups - 1;                   // partial-sum sets handed to group 0
-  static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;
+  // consumer geometry (the kWarps = 16 consumer warps): kRT 16-row MMA tiles per warp, kGW warps per unit
+  // group, kNG groups, kUPG units per group and stage (W4_MA_RT: row tiles per warp at NTB = 1)
+  static constexpr int kRT = NTB == 1 ? W4_MA_RT : 1;
+  static constexpr int kGW = 8 / kRT;
+  static constexpr int kNG = kWarps / kGW;
+  static constexpr int kUPG = kR / kNG;
+  static_assert(kUPG * kNG == kR && kGW * kRT == 8, "consumer geometry");
+  static constexpr int kRedSlots = kNG == 4 ? 2 : 1;               // group sums combined through shared memory
+  static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;   // [slot][row tile][tb][e][lane]
   static constexpr int kXchBytes = 4 * NTB * 4 * 32 * 4;          // SiLU epilogue: up values of a tile (fp16 in u32)
   static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / kStage;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
@@ -189,10 +201,6 @@ __device__ __forceinline__ void trace_ma(const GemmParams& p, int ev) {
 // MMA column j (fragment group g8 = j) carries token pi(j) of its 8-token block: with it, the 8 lanes of each
 // quarter-warp phase of an activation LDS.128 read rows {r, r + 4}, whose SWIZZLE_128B chunk positions differ
 // in the high bit, instead of rows {r, r + 1}, which collide on the same four bank groups (2-way conflict).
-#ifndef W4_MA_CH
-#define W4_MA_CH 1    // independent MMA accumulator chains per unit in the post-scale family (1 or 2)
-#endif
-constexpr int kCh = W4_MA_CH;
 #ifndef W4_MA_EXP
 #define W4_MA_EXP 0   // cost experiments only (make variant VDEFS=-DW4_MA_EXP=..; WRONG results): bit0 no per-unit
                       // group accumulator / post-scale, bit1 no dequant (raw words as A), bit2 no activation
@@ -226,37 +234,30 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
 }
 
 // Tensor-parallel all-reduce op of a chain (include/w4a16.h W4A16_OP_ALLREDUCE), fused
-// with the GEMM that writes the partial P tile by tile: CTA c reduces 128-column tiles c, c + G, ... of P as
-// soon as tile t's counter in this rank's flag area shows every rank's tile for this run (the GEMM's tile
-// writers bump it in every rank's flag area, process_unit flush -> publisher warp), then writes Y's tile and
-// publishes its ready flag (the next GEMM reads Y tile by tile). No grid-wide wait. Run by every consumer
-// thread of every CTA; out of line: it keeps the GEMM loop's registers.
-#ifndef W4_AR_INLINE
-#define W4_AR_INLINE 0
-#endif
-template <int kThreadsAR>
-#if W4_AR_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-void allreduce_op(const GemmParams& p, int job, int cta, int run_c) {
+// with the GEMM that writes the partial P tile by tile and run by the PUBLISHER warp of each CTA in the
+// background: when the consumers reach the op they post one request and go straight on to the next GEMM
+// (whose activation loads wait for the reduced tiles' ready flags). CTA c reduces 128-column tiles c, c + G,
+// ... of P as soon as tile t's counter in this rank's flag area shows every rank's tile for this run (the
+// GEMM's tile writers bump it in every rank's flag area, also through the publisher), writes Y's tile and
+// publishes its ready flag. No grid-wide wait, and no all-reduce code in the consumers' loop (a call there
+// cost ~5% of the chain, measured). Requests are served in order, so the CTA's own bumps precede it.
+__device__ __forceinline__ void allreduce_tiles(const GemmParams& p, int job, int cta, int lane) {
   const ChainJob* cj = p.jobs + job;
   const int world = cj->world, tiles = cj->N / 128;
+  const int run = __ldcg(&p.done[-2]);
   const uint32_t want = (uint32_t)world * (__ldcg(cj->epoch) + 1u);   // counters after this run's bumps
   int* yflags = p.counters + 2 * cj->cnt_off + 1;                     // Y's tile-ready flags (interleaved)
-  if (threadIdx.x == 0 && cj->dep_y >= 0) wait_op(p, cj->dep_y);      // WAR / WAW on Y
+  if (lane == 0 && cj->dep_y >= 0) wait_op(p, cj->dep_y);            // WAR / WAW on Y
   for (int t = cta; t < tiles; t += p.G) {
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       const unsigned long long t0 = globaltimer_ns();
       while ((int)(ld_acquire_sys(cj->my_tiles + t) - want) < 0) {
         __nanosleep(64);
         if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // a peer never arrived: fail, do not hang
       }
     }
-    named_bar_sync(1, kThreadsAR);
-    trace_op(p, job, 1);
-    for (int i = threadIdx.x; i < p.M * 16; i += kThreadsAR) {   // M rows x 16 vectors of 8 fp16
+    __syncwarp();
+    for (int i = lane; i < p.M * 16; i += 32) {   // M rows x 16 vectors of 8 fp16
       const size_t off = (size_t)(i >> 4) * cj->N + (size_t)t * 128 + (size_t)(i & 15) * 8;
       uint4 r;
       if (cj->mc_x != nullptr) {
@@ -285,11 +286,12 @@ void allreduce_op(const GemmParams& p, int job, int cta, int run_c) {
       }
       *reinterpret_cast<uint4*>(cj->Y + off) = r;
     }
-    named_bar_sync(1, kThreadsAR);
-    if (threadIdx.x == 0 && cj->pub_tiles)
-      asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(yflags + 2 * t), "r"(run_c + 1) : "memory");
+    __syncwarp();
+    if (lane == 0 && cj->pub_tiles)
+      asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(yflags + 2 * t), "r"(run + 1) : "memory");
   }
-  if (threadIdx.x == 0) red_release_gpu_add(&p.done[job], 1);
+  __syncwarp();
+  if (lane == 0) red_release_gpu_add(&p.done[job], 1);
 }
 
 template <int NTB, bool SYM, bool kScaleInA>
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       {
         int s2 = slot;
         for (int i = 0; i < n; ++i) {
-          if (pub_ptr[s2] && pub_val[s2] < 0) {
+          if (pub_ptr[s2] && pub_val[s2] < 0 && pub_val[s2] != kPubAllReduce) {
             sys = true;
             const ChainJob* cj = reinterpret_cast<const ChainJob*>(pub_ptr[s2]);
             if (lane == 0 && cj->ar_prev > ar_prev_done) { wait_op(p, cj->ar_prev); ar_prev_done = cj->ar_prev; }
@@ -468,7 +470,12 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       for (int i = 0; i < n; ++i) {
         int* ptr = pub_ptr[slot];
         const int val = pub_val[slot];
-        if (lane == 0) {
+        if (ptr && val == kPubAllReduce) {
+          // the whole warp reduces this CTA's tiles of the ALLREDUCE op (requests before it are published)
+          const int job = (int)(reinterpret_cast<const ChainJob*>(ptr) - p.jobs);
+          if (lane == 0) mbar_arrive(&pub_empty[slot]);
+          allreduce_tiles(p, job, cta, lane);
+        } else if (lane == 0) {
           if (ptr && val == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(ptr) : "memory");
           if (ptr && val > 0) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
           if (ptr && val < 0) ar_bump(reinterpret_cast<const ChainJob*>(ptr), -val - 1);
@@ -490,17 +497,6 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   uint32_t pub_ph = 0;
   // thread 0 only, after a barrier of the threads whose global stores the increment releases
   auto publish = [&](int* ptr, int val = 0) {
-    if (!W4_MA_PUB) {
-      if (ptr && val == 0) red_release_gpu_add(ptr, 1);
-      if (ptr && val > 0) asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(val) : "memory");
-      if (ptr && val < 0) {
-        const ChainJob* cj = reinterpret_cast<const ChainJob*>(ptr);
-        if (cj->ar_prev >= 0) wait_op(p, cj->ar_prev);
-        fence_acq_rel_sys();
-        ar_bump(cj, -val - 1);
-      }
-      return;
-    }
     mbar_wait(&pub_empty[pub_s], pub_ph ^ 1);   // the slot's previous request is consumed
     pub_ptr[pub_s] = ptr;
     pub_val[pub_s] = val;
@@ -509,11 +505,14 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   };
   pdl_wait();   // Y / workspace writes must follow the preceding kernel (returns at once when satisfied)
   const int g8 = lane >> 2, c4 = lane & 3;   // mma fragment coordinates
-  // warp (grp, r8): tile rows 16 r8 .. 16 r8 + 15 (one m16 MMA tile) and all 128 k of its group's units
-  const int r8 = warp & 7, grp = warp >> 3;
-  const int row0 = 16 * r8 + g8, row1 = row0 + 8;   // this lane's two tile rows (fragment rows g / g + 8)
+  // Unit groups: kNG groups of kGW warps; group grp computes kUPG units of every kR-unit stage
+  // (units kUPG grp ..), warp wg of the group owns the kRT 16-row MMA tiles rt = kRT wg .. kRT wg + kRT - 1
+  // (tile rows 16 rt .. 16 rt + 15) and all 128 k of those units. At NTB = 1 a warp owns two row tiles: the
+  // activation fragments it loads feed twice the MMAs, and the two row tiles are independent MMA chains.
+  constexpr int kRT = C::kRT, kGW = C::kGW, kNG = C::kNG, kUPG = C::kUPG;
+  const int wg = warp % kGW, grp = warp / kGW;
 
-  float acc[NTB][4];
+  float acc[kRT][NTB][4];
   int s = 0;
   uint32_t ph = 0;
   const uint32_t ready_base = smem_u32(&full_bar[0]);
@@ -549,8 +548,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       trace_op(p, job, 3);
       continue;
     }
-    if (J.kind == kOpAllReduce) {
-      allreduce_op<kWarps * 32>(p, job, cta, run_c);
+    if (J.kind == kOpAllReduce) {   // run by this CTA's publisher warp (allreduce_tiles)
+      if (threadIdx.x == 0) publish(reinterpret_cast<int*>(const_cast<ChainJob*>(p.jobs + job)), kPubAllReduce);
       continue;
     }
     const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
@@ -567,73 +566,97 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         if (threadIdx.x == 0) wait_op(p, wdep);   // released to the other warps by the barrier below
         y_ready = true;
       }
-      // 1. combine the unit groups: group 1 hands its partial sums to group 0 through shared memory
-      if (grp != 0) {
+      // 1. combine the unit groups through shared memory, in a fixed order: ((g0 + g1) + (g2 + g3))
+      auto red_put = [&](int slot) {
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) red[(((grp - 1) * 8 + r8) * NTB + tb) * 128 + e * 32 + lane] = acc[tb][e];
-      }
-      named_bar_sync(1, kWarps * 32);
-      if (grp == 0) {
-#pragma unroll
-        for (int sl = 0; sl < C::kRedSlots; ++sl)
+        for (int i = 0; i < kRT; ++i)
 #pragma unroll
           for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[tb][e] += red[((sl * 8 + r8) * NTB + tb) * 128 + e * 32 + lane];
+            for (int e = 0; e < 4; ++e) red[(((slot * 8 + kRT * wg + i) * NTB + tb) * 4 + e) * 32 + lane] = acc[i][tb][e];
+      };
+      auto red_add = [&](int slot) {
+#pragma unroll
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][tb][e] += red[(((slot * 8 + kRT * wg + i) * NTB + tb) * 4 + e) * 32 + lane];
+      };
+      if (kNG == 2) {
+        if (grp == 1) red_put(0);
+        named_bar_sync(1, kWarps * 32);
+        if (grp == 0) red_add(0);
+      } else {
+        if (grp & 1) red_put(grp >> 1);   // g1 -> slot 0, g3 -> slot 1
+        named_bar_sync(1, kWarps * 32);
+        if (!(grp & 1)) red_add(grp >> 1);   // g0 += g1, g2 += g3
+        named_bar_sync(1, kWarps * 32);
+        if (grp == 2) red_put(0);
+        named_bar_sync(1, kWarps * 32);
+        if (grp == 0) red_add(0);
       }
       named_bar_sync(1, kWarps * 32);
       if (grp != 0) return;
-      // 2. the eight group-0 warps own the result
+      // 2. the group-0 warps own the result
       const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
-      auto store = [&](float (&v)[NTB][4]) {
+      auto store = [&](float (&v)[kRT][NTB][4]) {
         if (J.epi == 1) {
-          // SiLU*mul epilogue (W4A16_OP_GEMM_SILU): tile rows 0..63 are gate, 64..127 the matching up columns;
-          // the up warps (r8 >= 4) hand their fp16-rounded values to the gate warps through a shared-memory
-          // area of their own (group 1 may already be writing `red` for its next flush), and the gate warps
-          // write Y[m][64 t + row] = fp16(silu(g) * u) — w4a16_silu_mul's arithmetic
+          // SiLU*mul epilogue (W4A16_OP_GEMM_SILU): tile rows 0..63 (row tiles 0..3) are gate, 64..127 the
+          // matching up columns; the up warps hand their fp16-rounded values to the gate warps through a
+          // shared-memory area of their own (the other groups may already be writing `red` for their next
+          // flush), and the gate warps write Y[m][64 t + row] = fp16(silu(g) * u) — w4a16_silu_mul's arithmetic
           uint32_t* xch = reinterpret_cast<uint32_t*>(smem + S * C::kStage + C::kRedFloats * 4);
-          if (r8 >= 4) {
+          const bool up = wg >= kGW / 2;
+          if (up) {
 #pragma unroll
-            for (int tb = 0; tb < NTB; ++tb)
+            for (int i = 0; i < kRT; ++i)
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                xch[(((r8 - 4) * NTB + tb) * 4 + e) * 32 + lane] = __half_as_ushort(__float2half_rn(v[tb][e]));
+              for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  xch[(((kRT * wg + i - 4) * NTB + tb) * 4 + e) * 32 + lane] = __half_as_ushort(__float2half_rn(v[i][tb][e]));
           }
-          named_bar_sync(2, 8 * 32);
-          if (r8 < 4) {
-            const int Nh = J.N / 2, c0 = t * 64 + row0, c1 = t * 64 + row1;
+          named_bar_sync(2, kGW * 32);
+          if (!up) {
+            const int Nh = J.N / 2;
 #pragma unroll
-            for (int tb = 0; tb < NTB; ++tb)
+            for (int i = 0; i < kRT; ++i) {
+              const int rt = kRT * wg + i, c0 = t * 64 + 16 * rt + g8, c1 = c0 + 8;
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float g = __half2float(__float2half_rn(v[tb][e]));
-                const float u = __half2float(__ushort_as_half((uint16_t)xch[((r8 * NTB + tb) * 4 + e) * 32 + lane]));
-                const int m = tb * 8 + c4 + 4 * (e & 1);
-                if (m < p.M) J.Y[(size_t)m * Nh + ((e >> 1) ? c1 : c0)] = __half_as_ushort(__float2half_rn(g / (1.0f + __expf(-g)) * u));
-              }
+              for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float g = __half2float(__float2half_rn(v[i][tb][e]));
+                  const float u = __half2float(__ushort_as_half((uint16_t)xch[((rt * NTB + tb) * 4 + e) * 32 + lane]));
+                  const int m = tb * 8 + c4 + 4 * (e & 1);
+                  if (m < p.M) J.Y[(size_t)m * Nh + ((e >> 1) ? c1 : c0)] = __half_as_ushort(__float2half_rn(g / (1.0f + __expf(-g)) * u));
+                }
+            }
           }
-          named_bar_sync(2, 8 * 32);   // xch is reused by the next flush
+          named_bar_sync(2, kGW * 32);   // xch is reused by the next flush
           return;
         }
-        const int n0 = t * kTileN + row0, n1 = t * kTileN + row1;
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const int m0 = tb * 8 + c4, m1 = m0 + 4;   // MMA columns 2c4, 2c4 + 1 = tokens tok_pi(2c4), tok_pi(2c4 + 1)
-          if (m0 < p.M) {
-            J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[tb][0]));
-            J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[tb][2]));
-          }
-          if (m1 < p.M) {
-            J.Y[(size_t)m1 * J.N + n0] = __half_as_ushort(__float2half_rn(v[tb][1]));
-            J.Y[(size_t)m1 * J.N + n1] = __half_as_ushort(__float2half_rn(v[tb][3]));
+        for (int i = 0; i < kRT; ++i) {
+          const int n0 = t * kTileN + 16 * (kRT * wg + i) + g8, n1 = n0 + 8;
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const int m0 = tb * 8 + c4, m1 = m0 + 4;   // MMA columns 2c4, 2c4 + 1 = tokens tok_pi(2c4), tok_pi(2c4 + 1)
+            if (m0 < p.M) {
+              J.Y[(size_t)m0 * J.N + n0] = __half_as_ushort(__float2half_rn(v[i][tb][0]));
+              J.Y[(size_t)m0 * J.N + n1] = __half_as_ushort(__float2half_rn(v[i][tb][2]));
+            }
+            if (m1 < p.M) {
+              J.Y[(size_t)m1 * J.N + n0] = __half_as_ushort(__float2half_rn(v[i][tb][1]));
+              J.Y[(size_t)m1 * J.N + n1] = __half_as_ushort(__float2half_rn(v[i][tb][3]));
+            }
           }
         }
       };
       auto tile_written = [&]() {   // chain: the tile's Y is complete -> its ready flag (tile-level deps)
         if (!chain || (!J.pub_tiles && !J.ar)) return;
-        named_bar_sync(2, 8 * 32);
+        named_bar_sync(2, kGW * 32);
         if (threadIdx.x == 0 && J.pub_tiles) publish(&J.flags[J.cs * t], run_c + 1);
         // Y is an ALLREDUCE's partial: bump tile t's counter in every rank's flag area (publisher warp)
         if (threadIdx.x == 0 && J.ar) publish(reinterpret_cast<int*>(const_cast<ChainJob*>(p.jobs + job)), -t - 1);
@@ -645,11 +668,14 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       // on (no round trip); the owner acquires the counter, adds the partials in CTA order to its own and
       // writes Y. All G CTAs are co-resident (G = resident capacity), so the owner's wait always completes.
       const int c_first = cta_of_unit(tile_u0, J.U, p.G), c_last = cta_of_unit(tile_u1 - 1, J.U, p.G);
-      auto pidx = [&](int c, int tb) { return (((size_t)c * 8 + r8) * NTB + tb) * 32 + lane; };
+      auto pidx = [&](int c, int rt, int tb) { return (((size_t)c * 8 + rt) * NTB + tb) * 32 + lane; };
       if (cta != c_first) {
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) __stcg(&part[pidx(cta, tb)], make_float4(acc[tb][0], acc[tb][1], acc[tb][2], acc[tb][3]));
-        named_bar_sync(2, 8 * 32);
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb)
+            __stcg(&part[pidx(cta, kRT * wg + i, tb)], make_float4(acc[i][tb][0], acc[i][tb][1], acc[i][tb][2], acc[i][tb][3]));
+        named_bar_sync(2, kGW * 32);
         if (threadIdx.x == 0) publish(&J.counters[J.cs * t]);
         return;
       }
@@ -660,20 +686,22 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         trace_op(p, job, 5);
         J.counters[J.cs * t] = 0;   // every contributor has arrived: re-arm for the next launch
       }
-      named_bar_sync(2, 8 * 32);
+      named_bar_sync(2, kGW * 32);
       for (int c = c_first + 1; c <= c_last; ++c) {
 #pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          const float4 v = __ldcg(&part[pidx(c, tb)]);
-          acc[tb][0] += v.x; acc[tb][1] += v.y; acc[tb][2] += v.z; acc[tb][3] += v.w;
-        }
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const float4 v = __ldcg(&part[pidx(c, kRT * wg + i, tb)]);
+            acc[i][tb][0] += v.x; acc[i][tb][1] += v.y; acc[i][tb][2] += v.z; acc[i][tb][3] += v.w;
+          }
       }
       store(acc);
       tile_written();
     };
 
     // One unit: all shared-memory loads first (activation fragments, code words, scale/zero pairs), then
-    // dequant + 8 MMAs (one m16 tile x 8 k-steps), then the post-MMA group scale.
+    // dequant + 8 MMAs per row tile (one m16 tile x 8 k-steps), then the post-MMA group scale.
     auto process_unit = [&](uint32_t st, int j) {
       const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box b holds k 64b..
       const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
@@ -687,104 +715,106 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           if (W4_MA_EXP & 4) xr[pc][tb] = make_uint4(0x3c003c00u + m, 0x3c003c00u, 0x3c003c00u ^ jx, 0x3c003c00u);
           else xr[pc][tb] = lds128(xu + (pc >> 1) * C::kXBox + m * 128 + ((jx ^ (m & 7)) << 4));
         }
-      uint32_t wq[4][2];                                      // [chunk][row g / g + 8]
-      // Two ldmatrix.x4: matrix q = (hf = q & 1, chunk 2 pp + (q >> 1)) is the 8 rows 16 r8 + 8 hf + 0..7 of
-      // that chunk, and lane (g8, c4) receives word c4 of row g8 — exactly its code word (conflict-free: the
-      // XOR chunk layout spreads the 8 rows over all 32 banks).
-      {
-        const int lr = 16 * r8 + 8 * ((lane >> 3) & 1) + (lane & 7);
+      uint32_t wq[kRT][4][2];                                 // [row tile][chunk][row g / g + 8]
+      float sc[kRT][2];
+      __half2 zp[kRT][2];
+#pragma unroll
+      for (int i = 0; i < kRT; ++i) {
+        const int rt = kRT * wg + i;
+        // Two ldmatrix.x4: matrix q = (hf = q & 1, chunk 2 pp + (q >> 1)) is the 8 rows 16 rt + 8 hf + 0..7 of
+        // that chunk, and lane (g8, c4) receives word c4 of row g8 — exactly its code word (conflict-free: the
+        // XOR chunk layout spreads the 8 rows over all 32 banks).
+        const int lr = 16 * rt + 8 * ((lane >> 3) & 1) + (lane & 7);
 #pragma unroll
         for (int pp = 0; pp < 2; ++pp) {
           const int pch = 2 * pp + (lane >> 4);
-          ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[2 * pp][0], wq[2 * pp][1], wq[2 * pp + 1][0],
-                  wq[2 * pp + 1][1]);
+          ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[i][2 * pp][0], wq[i][2 * pp][1], wq[i][2 * pp + 1][0],
+                  wq[i][2 * pp + 1][1]);
         }
-      }
-      float sc[2];
-      __half2 zp[2];
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        const int r = hf ? row1 : row0;
-        if (SYM) {
-          sc[hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
-          zp[hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
-        } else if (W4_MA_EXP & 8) {
-          sc[hf] = 0.01f * (r + 1);
-          zp[hf] = __floats2half2_rn(72.f, 1032.f);
-        } else {
-          const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
-          sc[hf] = __low2float(sz);
-          zp[hf] = zero_pair(__high2half(sz));
+        for (int hf = 0; hf < 2; ++hf) {
+          const int r = 16 * rt + g8 + 8 * hf;
+          if (SYM) {
+            sc[i][hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * r)));
+            zp[i][hf] = __floats2half2_rn(72.f, 1032.f);   // z = 8
+          } else if (W4_MA_EXP & 8) {
+            sc[i][hf] = 0.01f * (r + 1);
+            zp[i][hf] = __floats2half2_rn(72.f, 1032.f);
+          } else {
+            const __half2 sz = u2h2(lds32(ub + 8192 + 4 * r));   // {s, z}
+            sc[i][hf] = __low2float(sz);
+            zp[i][hf] = zero_pair(__high2half(sz));
+          }
         }
       }
       if constexpr (kScaleInA) {
         // w_hat = fp16((q - z) * s) in the A fragments (exactly the oracle's dequantised weight), accumulated
         // straight into acc: no per-unit group accumulator.
-        __half2 s2[2];
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) s2[hf] = __float2half2_rn(sc[hf]);
+        for (int i = 0; i < kRT; ++i) {
+          __half2 s2[2];
 #pragma unroll
-        for (int pc = 0; pc < 4; ++pc)
+          for (int hf = 0; hf < 2; ++hf) s2[hf] = __float2half2_rn(sc[i][hf]);
 #pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {
-            const uint32_t qa = hs ? wq[pc][0] >> 8 : wq[pc][0];
-            const uint32_t qb = hs ? wq[pc][1] >> 8 : wq[pc][1];
-            const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[0])), s2[0]));
-            const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[1])), s2[1]));
-            const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[0])), s2[0]));
-            const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[1])), s2[1]));
+          for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) {
-              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
-              mma_16816(acc[tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            for (int hs = 0; hs < 2; ++hs) {
+              const uint32_t qa = hs ? wq[i][pc][0] >> 8 : wq[i][pc][0];
+              const uint32_t qb = hs ? wq[i][pc][1] >> 8 : wq[i][pc][1];
+              const uint32_t a0 = h22u(__hmul2(u2h2(dq_lo(qa, zp[i][0])), s2[0]));
+              const uint32_t a1 = h22u(__hmul2(u2h2(dq_lo(qb, zp[i][1])), s2[1]));
+              const uint32_t a2 = h22u(__hmul2(u2h2(dq_hi(qa, zp[i][0])), s2[0]));
+              const uint32_t a3 = h22u(__hmul2(u2h2(dq_hi(qb, zp[i][1])), s2[1]));
+#pragma unroll
+              for (int tb = 0; tb < NTB; ++tb) {
+                const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
+                mma_16816(acc[i][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+              }
             }
-          }
+        }
       } else {
         // Post-scale with exact codes: the A fragments hold the integers (q - z) (LOP3 +
         // HSUB2 / HFMA2 per pair, exact in fp16), the MMAs sum sum_k (q_k - z) x_k over the unit's 128 k into
-        // a fresh fp32 group accumulator, and the group scale multiplies that sum once: Y += s * sum. This is
-        // the exact-weight definition (reading R22); no offsets, so no cancellation whatever
-        // the activation magnitude.
-        // kCh independent accumulator chains per unit (32-k chunks alternate between them): more MMAs in flight
-        float gacc[kCh][NTB][4];
+        // a fresh fp32 group accumulator per row tile (independent MMA chains), and the group scale multiplies
+        // that sum once: Y += s * sum. This is the exact-weight definition (reading R22); no offsets, so no
+        // cancellation whatever the activation magnitude.
+        float gacc[kRT][NTB][4];
 #pragma unroll
-        for (int ch = 0; ch < kCh; ++ch)
+        for (int i = 0; i < kRT; ++i)
 #pragma unroll
           for (int tb = 0; tb < NTB; ++tb)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) gacc[ch][tb][e] = (W4_MA_EXP & 1) && ch == 0 ? acc[tb][e] : 0.f;
+            for (int e = 0; e < 4; ++e) gacc[i][tb][e] = (W4_MA_EXP & 1) ? acc[i][tb][e] : 0.f;
 #pragma unroll
         for (int pc = 0; pc < 4; ++pc)
 #pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {
-            const uint32_t qa = hs ? wq[pc][0] >> 8 : wq[pc][0];
-            const uint32_t qb = hs ? wq[pc][1] >> 8 : wq[pc][1];
-            const uint32_t a0 = (W4_MA_EXP & 2) ? qa : dq_lo(qa, zp[0]), a1 = (W4_MA_EXP & 2) ? qb : dq_lo(qb, zp[1]);
-            const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : dq_hi(qa, zp[0]);
-            const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : dq_hi(qb, zp[1]);
+          for (int hs = 0; hs < 2; ++hs)
 #pragma unroll
-            for (int tb = 0; tb < NTB; ++tb) {
-              const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
-              mma_16816_nv(gacc[pc % kCh][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+            for (int i = 0; i < kRT; ++i) {
+              const uint32_t qa = hs ? wq[i][pc][0] >> 8 : wq[i][pc][0];
+              const uint32_t qb = hs ? wq[i][pc][1] >> 8 : wq[i][pc][1];
+              const uint32_t a0 = (W4_MA_EXP & 2) ? qa : dq_lo(qa, zp[i][0]), a1 = (W4_MA_EXP & 2) ? qb : dq_lo(qb, zp[i][1]);
+              const uint32_t a2 = (W4_MA_EXP & 2) ? qa ^ 0x10001u : dq_hi(qa, zp[i][0]);
+              const uint32_t a3 = (W4_MA_EXP & 2) ? qb ^ 0x10001u : dq_hi(qb, zp[i][1]);
+#pragma unroll
+              for (int tb = 0; tb < NTB; ++tb) {
+                const uint32_t* xv = reinterpret_cast<const uint32_t*>(&xr[pc][tb]);
+                mma_16816_nv(gacc[i][tb], a0, a1, a2, a3, xv[2 * hs], xv[2 * hs + 1]);
+              }
             }
+#pragma unroll
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            if (W4_MA_EXP & 1) {
+              acc[i][tb][0] = gacc[i][tb][0]; acc[i][tb][1] = gacc[i][tb][1]; acc[i][tb][2] = gacc[i][tb][2]; acc[i][tb][3] = gacc[i][tb][3];
+              continue;
+            }
+            acc[i][tb][0] = fmaf(sc[i][0], gacc[i][tb][0], acc[i][tb][0]);
+            acc[i][tb][1] = fmaf(sc[i][0], gacc[i][tb][1], acc[i][tb][1]);
+            acc[i][tb][2] = fmaf(sc[i][1], gacc[i][tb][2], acc[i][tb][2]);
+            acc[i][tb][3] = fmaf(sc[i][1], gacc[i][tb][3], acc[i][tb][3]);
           }
-#pragma unroll
-        for (int ch = 1; ch < kCh; ++ch)
-#pragma unroll
-          for (int tb = 0; tb < NTB; ++tb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) gacc[0][tb][e] += gacc[ch][tb][e];
-#pragma unroll
-        for (int tb = 0; tb < NTB; ++tb) {
-          if (W4_MA_EXP & 1) {
-            acc[tb][0] = gacc[0][tb][0]; acc[tb][1] = gacc[0][tb][1]; acc[tb][2] = gacc[0][tb][2]; acc[tb][3] = gacc[0][tb][3];
-            continue;
-          }
-          acc[tb][0] = fmaf(sc[0], gacc[0][tb][0], acc[tb][0]);
-          acc[tb][1] = fmaf(sc[0], gacc[0][tb][1], acc[tb][1]);
-          acc[tb][2] = fmaf(sc[1], gacc[0][tb][2], acc[tb][2]);
-          acc[tb][3] = fmaf(sc[1], gacc[0][tb][3], acc[tb][3]);
-        }
       }
     };
     auto begin_segment = [&](int u) {
@@ -798,7 +828,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       boundary = (cur_t + 1) * J.Gk;
       seg_u0 = u;
 #pragma unroll
-      for (int tb = 0; tb < NTB; ++tb) acc[tb][0] = acc[tb][1] = acc[tb][2] = acc[tb][3] = 0.f;
+      for (int i = 0; i < kRT; ++i)
+#pragma unroll
+        for (int tb = 0; tb < NTB; ++tb) acc[i][tb][0] = acc[i][tb][1] = acc[i][tb][2] = acc[i][tb][3] = 0.f;
     };
     auto stage_begin = [&](int i) {
       if (W4A16_MMA_DIAG && (p.dbg & 4)) mbar_wait_backoff(&full_bar[s], ph, 32);
@@ -821,7 +853,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
         for (int j = 0; j < nu; ++j) {
           if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
-          if ((j >> 1) == grp && !skip_compute) process_unit(st, j);
+          if (j / kUPG == grp && !skip_compute) process_unit(st, j);
         }
         stage_end();
         ++i;
@@ -833,7 +865,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         const uint32_t st = smem_base + s * C::kStage;
         if (!skip_compute) {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) process_unit(st, 2 * grp + j);
+          for (int j = 0; j < kUPG; ++j) process_unit(st, kUPG * grp + j);
         }
         stage_end();
       }
@@ -843,10 +875,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     if (cur_t >= 0) flush(cur_t, seg_u0, u_end);
     trace_op(p, job, 6);
     trace_ma(p, 3);
-    // This CTA's share of the op is written: count it. Only the four warps that store Y / partials (group 0,
-    // k-half 0) take part; the other warps are already streaming the next op.
+    // This CTA's share of the op is written: count it. Only the warps that store Y / partials (group 0) take
+    // part; the other warps are already streaming the next op.
     if (chain && grp == 0) {
-      named_bar_sync(2, 8 * 32);
+      named_bar_sync(2, kGW * 32);
       if (threadIdx.x == 0) publish(&p.done[job]);
     }
     trace_op(p, job, 3);
