@@ -56,6 +56,9 @@ constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0
 constexpr int kPubSlots = 8;
 constexpr int kPubAllReduce = -0x40000000;   // publisher request: run ALLREDUCE op (ptr = its ChainJob)
 constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
+#ifndef W4_POLL_ACQ
+#define W4_POLL_ACQ 0   // A/B only: poll tile flags with one acquire load each (round 1-2 behaviour)
+#endif
 #ifndef W4_MA_RT
 #define W4_MA_RT 1   // 16-row MMA tiles per consumer warp at M <= 8 (2: 4 warps per unit; measured slower)
 #endif
@@ -175,6 +178,8 @@ __device__ unsigned long long g_trace_ma[kTraceCtas][8];
 constexpr int kOpTraceCtas = 296, kOpTraceOps = 512;
 #if W4A16_MMA_DIAG
 __device__ unsigned long long g_op_trace[kOpTraceCtas][kOpTraceOps][8];
+// producer side: when the activation load of the op's first stage of this CTA was issued
+__device__ unsigned long long g_prod_trace[kOpTraceCtas][kOpTraceOps];
 #endif
 __device__ __forceinline__ void trace_op(const GemmParams& p, int job, int ev) {
 #if W4A16_MMA_DIAG
@@ -354,13 +359,18 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       const int run = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile flags)
       // Tile-level dependency: the stage's activation k-groups are complete once the producing op's tiles
       // xf_off + g are written in this run (their flags reached run + 1).
+      // The flags are polled with relaxed loads, all in flight at once (an acquire per flag would serialise
+      // them: one L2 round trip each, several us per poll); one acquire fence once all are set.
       auto tiles_ready = [&](const JobInfo& J, int u0, int nu) {
         int g = u0 % J.Gk;
         bool ok = true;
         for (int jj = 0; jj < nu; ++jj) {
-          for (int i = 0; i < J.xf_mul; ++i) ok &= ld_acquire_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1]) > run;
+          for (int i = 0; i < J.xf_mul; ++i)
+            ok &= (W4_POLL_ACQ ? ld_acquire_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1])
+                               : ld_relaxed_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1])) > run;
           if (++g == J.Gk) g = 0;
         }
+        if (ok) fence_acquire_gpu();
         return ok;
       };
       auto drain = [&](bool block) {   // issue queued activation loads whose producers are done
@@ -372,7 +382,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
           const JobInfo J = job_at(p, &xmapR, &xmap1, q_j[q_head]);
           if (J.dep_x > ok_upto) {
-            if (ld_acquire_gpu(&p.done[J.dep_x]) >= p.G) {
+            if ((W4_POLL_ACQ ? ld_acquire_gpu(&p.done[J.dep_x]) : ld_relaxed_gpu(&p.done[J.dep_x])) >= p.G) {
+              if (!W4_POLL_ACQ) fence_acquire_gpu();
               ok_upto = J.dep_x;   // the whole producing op is complete: no more per-tile checks
             } else if (J.xf_off >= 0) {
               if (!tiles_ready(J, q_u0[q_head], q_nu[q_head])) {
@@ -390,6 +401,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             }
             fence_proxy_async_global();   // generic-proxy stores of other CTAs -> this TMA (async proxy) read
           }
+#if W4A16_MMA_DIAG
+          if ((p.dbg & 64) && cta < kOpTraceCtas && q_j[q_head] < kOpTraceOps && g_prod_trace[cta][q_j[q_head]] == 0)
+            g_prod_trace[cta][q_j[q_head]] = globaltimer_ns();
+#endif
           issue_x(q_s[q_head], J, q_u0[q_head], q_nu[q_head]);
           q_head = (q_head + 1) & 7;
           --q_n;
@@ -955,6 +970,20 @@ extern "C" int w4a16_debug_op_trace(void* host, size_t bytes) {
                  cudaSuccess ? 0 : -5;
 #else
   (void)host; (void)bytes;
+  return -1;
+#endif
+}
+
+extern "C" int w4a16_debug_prod_trace(void* host, size_t bytes, int clear) {
+#if W4A16_MMA_DIAG
+  if (clear) {
+    static unsigned long long zero[w4::ma::kOpTraceCtas][w4::ma::kOpTraceOps];
+    return cudaMemcpyToSymbol(w4::ma::g_prod_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -5;
+  }
+  return cudaMemcpyFromSymbol(host, w4::ma::g_prod_trace, bytes < sizeof(w4::ma::g_prod_trace) ? bytes : sizeof(w4::ma::g_prod_trace)) ==
+                 cudaSuccess ? 0 : -5;
+#else
+  (void)host; (void)bytes; (void)clear;
   return -1;
 #endif
 }

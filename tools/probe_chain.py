@@ -23,6 +23,9 @@ for _ in range(3):
     ch()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+lib.w4a16_debug_prod_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+lib.w4a16_debug_prod_trace(None, 0, 1)
+torch.cuda.synchronize()
 e0.record(); ch(); e1.record(); torch.cuda.synchronize()
 print(f"chain {a.layers} layers M={a.M}: {e0.elapsed_time(e1) * 1e3:.1f} us")
 G, NOPS = 296, 512
@@ -34,6 +37,10 @@ G = int((buf[:, 0, 0] > 0).sum())   # CTAs of this chain
 b = buf[:G, :n, :].astype(np.int64)
 t0 = b[:, 0, 0].min()
 b -= t0
+pt = np.zeros((296, 512), dtype=np.uint64)
+lib.w4a16_debug_prod_trace(pt.ctypes.data, pt.nbytes, 0)
+pt_ok = pt[:G, :n] > 0
+pt = pt[:G, :n].astype(np.int64) - t0
 kinds = ["qkv", "o", "gate_up_silu", "down"]
 print(f"{'op':8s} {'span':>7s} {'wait1st':>8s} {'compute':>8s} {'flush':>7s} {'skewStart':>9s} {'skewDone':>8s}  (us, medians over layers)")
 for k, name in enumerate(kinds):
@@ -85,3 +92,17 @@ for k, name in enumerate(kinds):
         rows["flush+cnt"].append(b[:, j, 3] - b[:, j, 2])
         rows["done-Tdep"].append(b[:, j, 3] - Tdep)
     print(f"{name:8s} " + "  ".join(f"{key} {pq(np.concatenate(v))}" for key, v in rows.items()))
+
+# producer: activation load of the op's first stage issued (after its tile dependencies) vs consumers' first
+# stage ready: the activation TMA's latency behind the weight stream
+print("\nfirst stage of each op (layers 2..), p10/p50/p90 over CTAs, us: act issue - T_dep, ready - act issue")
+for k, name in enumerate(kinds):
+    a1, a2 = [], []
+    for l in range(1, n // 4):
+        j = 4 * l + k
+        Tdep = b[:, j - 1, 3].max()
+        ok = pt_ok[:, j]
+        a1 += list((pt[ok, j] - Tdep) / 1e3)
+        a2 += list((b[ok, j, 1] - pt[ok, j]) / 1e3)
+    q = lambda v: "/".join(f"{x:5.2f}" for x in np.percentile(v, [10, 50, 90])) if v else "-"
+    print(f"{name:12s} issue-Tdep {q(a1)}   ready-issue {q(a2)}")
