@@ -554,7 +554,8 @@ def main():
                         "note": "achieved = weight bytes/launch / avg launch time over 80 back-to-back launches (CUDA "
                                 "graph, CUDA events on the launching stream)"}
             fam_tag = ("famB" if gate["family"] == w4.W4A16_FAMILY_TCGEN05 else "famA") + f"_gateup_M{M}"
-        ncu_path = os.path.join(ROOT, "profiles", f"r01_ncu_{fam_tag}.json")
+        ncu_path = next((q for q in (os.path.join(ROOT, "profiles", f"r{r:02d}_ncu_{fam_tag}.json") for r in (2, 1))
+                         if os.path.exists(q)), "")   # the newest round's committed capture
         if os.path.exists(ncu_path):   # committed ncu --set full capture of this kernel at this M
             try:
                 with open(ncu_path) as f:
