@@ -11,7 +11,7 @@ BENCH_WATCHDOG=800 timeout 1000 python bench.py > $OUT/bench_$TAG.json 2> $OUT/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --layers 4 --steps 3 --warmup 3 --sweep "" --sym-sweep "" --no-cpu-baseline --no-kernels --no-lm-head > $OUT/bench_ncu_$TAG.log 2>&1; echo "ncu list rc=$?"
 # full capture of the dominant kernel: the persistent chain (8-layer stack, headline M=8)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a16_mma -s 1 -c 1 -f -o $OUT/prof_chain_$TAG \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a16_mma -s 70 -c 1 -f -o $OUT/prof_chain_$TAG \
     python bench.py --layers 8 --steps 1 --warmup 3 --sweep "" --sym-sweep "" --no-cpu-baseline --no-kernels --no-lm-head > $OUT/ncu_chain_$TAG.log 2>&1; echo "ncu chain rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a16_mma -s 3 -c 1 -f -o $OUT/prof_famA_$TAG \
     python tools/probe_fam.py --shapes gate_up --M 8 --families 0 --bytes 6e8 --reps 1 > $OUT/ncu_famA_$TAG.log 2>&1; echo "ncu famA rc=$?"
