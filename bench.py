@@ -775,7 +775,7 @@ def main():
             Xqa = torch.empty(M, Ka, dtype=torch.int8, device=dev)
             sxa = torch.empty(M, dtype=torch.float32, device=dev)
             xsa = torch.empty(M, Ka // 128, dtype=torch.int32, device=dev)
-            wsa8 = torch.empty(w4.w4a8_workspace_bytes(M, Ka, Na), dtype=torch.uint8, device=dev)
+            wsa8 = torch.zeros(w4.w4a8_workspace_bytes(M, Ka, Na), dtype=torch.uint8, device=dev)
             Ya = torch.empty(M, Na, dtype=torch.float16, device=dev)
             with torch.cuda.stream(stream):
                 w4.w4a8_quantize_act(Xa, Xqa, sxa, xsa, stream=stream)

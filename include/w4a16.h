@@ -15,6 +15,10 @@
  *     alignment, workspace, launch failure).  Problems only visible on the device are written to a
  *     caller-provided device status word (w4a16_dev_status values).
  *   - Thread safety: calls are re-entrant; concurrent calls must not share output or workspace buffers.
+ *   - Residency: the family-A GEMMs (w4a16_gemm at M <= 16, w4a8_gemm at M <= 16) launch one CTA per SM and a
+ *     split tile's owner CTA waits for the other CTAs of its tile, so they assume the whole grid becomes
+ *     resident: another kernel that occupies SMs indefinitely (a spinning persistent kernel on a concurrent
+ *     stream) can delay them until it yields. Ordinary concurrent kernels only delay them.
  *
  * Shapes (GEMM convention of BASELINE.json): Y[M,N] = X[M,K] · W[K,N]; K = in-features, N = out-features.
  * Requirements: group == 128, K % 128 == 0, N % 128 == 0, 1 <= M <= 64 for the GEMM.
@@ -304,8 +308,10 @@ int w4a16_chain_run(const void* dev_plan, int n_ops, int M, int mode, int family
  *   all device pointers; Xq 16-byte aligned, sx and xsum 4-byte aligned (else W4A16_ERR_ALIGN).
  * w4a8_gemm: Y[m][n] = fp16_rne(sx[m] * sum_g s[g][n] * (sum_{k in g} Xq[m][k] * q[k][n] - 8 * xsum[m][g]))
  *   on the SYM (z = 8) blob of w4a16_pack (K x N, group 128): int32-exact group sums (INT8 MMA), fp32 group
- *   scaling in k order, per-split partials summed in split order (deterministic). workspace: at least
- *   w4a8_workspace_bytes(M, K, N) bytes (scratch; no initialisation needed). Xq, packed and workspace
+ *   scaling in k order, per-split partials summed in split order (deterministic). M <= 16 runs on the family-A
+ *   pipeline (int8 codes (q - 8) * 16, mma m16n8k32 s8, stream-K; xsum unused), larger M on a k-split kernel
+ *   that applies the -8 * xsum correction. workspace: at least w4a8_workspace_bytes(M, K, N) bytes, zeroed
+ *   once (w4a16_workspace_init) before its first use; every call leaves it zeroed. Xq, packed and workspace
  *   16-byte aligned (16-byte copies), sx and xsum 4-byte aligned, else W4A16_ERR_ALIGN. */
 int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, w4a16_stream_t stream);
 size_t w4a8_workspace_bytes(int M, int K, int N);

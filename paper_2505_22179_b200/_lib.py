@@ -150,6 +150,8 @@ def _load():
     lib.w4a16_chain_plan_sms.argtypes = [vp, i32, i32, i32, vp, sz, i32]
     lib.w4a16_chain_check_sms.argtypes = [vp, i32, i32, i32, i32]
     lib.w4a16_chain_check_sms.restype = i32
+    lib.w4a8_gemm_ex.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, sz, i32, vp]
+    lib.w4a8_gemm_ex.restype = i32
     lib.w4a16_chain_run_sms.argtypes = [vp, i32, i32, i32, i32, vp, sz, i32, vp]
     for name in ("w4a16_ipc_alloc", "w4a16_ipc_open", "w4a16_ipc_close", "w4a16_ipc_free", "w4a16_mc_supported",
                  "w4a16_mc_create", "w4a16_mc_import", "w4a16_mc_add_device", "w4a16_mc_bind", "w4a16_mc_free", "w4a16_chain_plan_sms",

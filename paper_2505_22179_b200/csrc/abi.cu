@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "w4a16.h"
+#include "common.cuh"
 
 extern "C" int w4a16_launch_pack(const uint16_t*, int, int, int, void*, int32_t*, cudaStream_t);
 extern "C" int w4a16_launch_unpack(const void*, int, int, int, uint16_t*, cudaStream_t);
@@ -31,6 +32,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op*, int, int, int, void*, size_
 extern "C" int w4a16_launch_chain_mma(const void*, int, int, int, int, void*, size_t, int, int, cudaStream_t);
 extern "C" size_t w4a8_workspace_bytes_sms(int, int, int, int);
 extern "C" int w4a8_launch_quantize(const uint16_t*, int, int, int8_t*, float*, int32_t*, cudaStream_t);
+extern "C" int w4a8_launch_gemm_mma(const int8_t*, const float*, const void*, uint16_t*, int, int, int, void*, int, cudaStream_t);
 extern "C" int w4a8_launch_gemm(const int8_t*, const float*, const int32_t*, const void*, uint16_t*, int, int, int, void*, int,
                                 cudaStream_t);
 extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
@@ -534,22 +536,47 @@ extern "C" int w4a8_quantize_act(const uint16_t* X, int M, int K, int8_t* Xq, fl
 }
 
 extern "C" size_t w4a8_workspace_bytes(int M, int K, int N) {
-  if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128) return 0;
+  if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128 || N > W4A16_MAX_N) return 0;
   const int sms = num_sms_of_current_device();
-  return sms > 0 ? w4a8_workspace_bytes_sms(M, K, N, sms) : 0;
+  if (sms <= 0) return 0;
+  // the k-split kernel's partials start after the family-A tile counters, so one workspace serves both paths
+  const size_t a = w4::kCounterBytes + w4a8_workspace_bytes_sms(M, K, N, sms), b = M <= 16 ? w4a16_mma_workspace_bytes(M, K, N, sms) : 0;
+  return a > b ? a : b;
 }
 
-extern "C" int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K, int N,
-                         void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+namespace {
+// impl: 0 = auto (the family-A pipeline for M <= 16, the round-1 INT8 kernel above), 1 = family-A pipeline,
+// 2 = round-1 kernel
+int w4a8_gemm_impl(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K,
+                   int N, void* workspace, size_t workspace_bytes, int impl, cudaStream_t stream) {
   if (!Xq || !sx || !xsum || !packed || !Y || !workspace) return W4A16_ERR_ARG;
   if (M < 1 || M > W4A16_MAX_M || K < 128 || K % 128 || N < 128 || N % 128 || N > W4A16_MAX_N) return W4A16_ERR_SHAPE;
-  // the GEMM streams Xq and the blob with 16-byte cp.async copies: a smaller alignment would fault on the device
+  // the GEMMs stream Xq and the blob with 16-byte copies: a smaller alignment would fault on the device
   if ((reinterpret_cast<uintptr_t>(Xq) & 15u) || (reinterpret_cast<uintptr_t>(packed) & 15u) || (reinterpret_cast<uintptr_t>(Y) & 1u) ||
       (reinterpret_cast<uintptr_t>(workspace) & 15u) || (reinterpret_cast<uintptr_t>(sx) & 3u) ||
       (reinterpret_cast<uintptr_t>(xsum) & 3u))
     return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
   if (sms <= 0) return W4A16_ERR_CUDA;
-  if (workspace_bytes < w4a8_workspace_bytes_sms(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-  return w4a8_launch_gemm(Xq, sx, xsum, packed, Y, M, K, N, workspace, sms, (cudaStream_t)stream);
+  if (impl == 0) impl = M <= 16 ? 1 : 2;
+  if (impl == 1) {
+    if (M > 16) return W4A16_ERR_SHAPE;
+    if (workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+    return w4a8_launch_gemm_mma(Xq, sx, packed, Y, M, K, N, workspace, sms, stream);
+  }
+  if (workspace_bytes < w4::kCounterBytes + w4a8_workspace_bytes_sms(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
+  return w4a8_launch_gemm(Xq, sx, xsum, packed, Y, M, K, N, reinterpret_cast<uint8_t*>(workspace) + w4::kCounterBytes, sms,
+                          stream);
+}
+}  // namespace
+
+extern "C" int w4a8_gemm(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K, int N,
+                         void* workspace, size_t workspace_bytes, w4a16_stream_t stream) {
+  return w4a8_gemm_impl(Xq, sx, xsum, packed, Y, M, K, N, workspace, workspace_bytes, 0, (cudaStream_t)stream);
+}
+
+// Test hook (exported, not in the header): w4a8_gemm with an explicit implementation (see w4a8_gemm_impl).
+extern "C" int w4a8_gemm_ex(const int8_t* Xq, const float* sx, const int32_t* xsum, const void* packed, uint16_t* Y, int M, int K,
+                            int N, void* workspace, size_t workspace_bytes, int impl, w4a16_stream_t stream) {
+  return w4a8_gemm_impl(Xq, sx, xsum, packed, Y, M, K, N, workspace, workspace_bytes, impl, (cudaStream_t)stream);
 }

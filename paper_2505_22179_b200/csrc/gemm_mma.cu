@@ -68,12 +68,13 @@ constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 
 constexpr int kCtasPerSm = kGroups >= 2 ? 1 : W4_MA_CTAS;   // resident CTAs per SM
 constexpr int kSmemBudget = kCtasPerSm == 1 ? 227 * 1024 - 512 : (kCtasPerSm == 2 ? 112 : 74) * 1024;   // 512 B static
 
-template <int NTB, bool SYM>
+template <int NTB, bool SYM, bool kA8 = false>
 struct Cfg {
   static constexpr int kMpad = 8 * NTB;                           // token rows per TMA box
   static constexpr int kTB = SYM ? 8448 : 8704;
-  static constexpr int kXBox = kMpad * 128;                       // one 64-k SW128 box (multiple of 1024 B)
-  static constexpr int kXUnit = 2 * kXBox;
+  static constexpr int kXBox = kMpad * 128;                       // one SW128 box: 64 fp16 k (or 128 int8 k) x kMpad rows
+  static constexpr int kBPU = kA8 ? 1 : 2;                        // activation boxes per unit (128 k)
+  static constexpr int kXUnit = kBPU * kXBox;
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
   // consumer geometry (the kWarps = 16 consumer warps): kRT 16-row MMA tiles per warp, kGW warps per unit
   // group, kNG groups, kUPG units per group and stage (W4_MA_RT: row tiles per warp at NTB = 1)
@@ -114,6 +115,7 @@ struct GemmParams {
   int* flags;             // chain: tile-ready flags (one per tile of every GEMM op, at the op's cnt_off): the run
                           // number + 1 of the last run that wrote the tile's Y (run number at done[n_jobs + 1])
   int slots;              // chain: partial-slot ring length in ops (1 for a single GEMM)
+  const float* sx;        // W4A8 (kA8): per-token activation scales [M]
 };
 
 struct JobInfo {
@@ -231,6 +233,24 @@ __device__ __forceinline__ uint16_t lds16(uint32_t addr) {
 __device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
 }
+// W4A8 (kA8): int8 MMA m16n8k32 with signed operands. The 4-bit codes become int8 (q - 8) * 16 with one
+// LOP3 per 4 codes: a code's nibble moved to the top of its byte and its bit 3 flipped is (q - 8) * 16 as a
+// two's-complement byte (q ^ 8 read as a signed 4-bit number is q - 8). lo8: the low nibbles of the word's
+// bytes (code slots 0, 2, 4, 6 = logical k 0, 4, 1, 5 of the word's 8 k), hi8: the high nibbles (k 2, 6, 3, 7).
+__device__ __forceinline__ uint32_t a8_lo(uint32_t w) { return ((w << 4) & 0xF0F0F0F0u) ^ 0x80808080u; }
+__device__ __forceinline__ uint32_t a8_hi(uint32_t w) { return (w & 0xF0F0F0F0u) ^ 0x80808080u; }
+__device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ void mma_s8_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                             uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
@@ -299,11 +319,11 @@ __device__ __forceinline__ void allreduce_tiles(const GemmParams& p, int job, in
   if (lane == 0) red_release_gpu_add(&p.done[job], 1);
 }
 
-template <int NTB, bool SYM, bool kScaleInA>
+template <int NTB, bool SYM, bool kScaleInA, bool kA8>
 __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a16_mma_kernel(const __grid_constant__ CUtensorMap xmapR,
                                                                       const __grid_constant__ CUtensorMap xmap1,
                                                                       const GemmParams p) {
-  using C = Cfg<NTB, SYM>;
+  using C = Cfg<NTB, SYM, kA8>;
   constexpr int S = C::kStages;
   static_assert(S <= 8, "producer queue holds at most 8 stages");
   // kScaleInA (family W4A16_FAMILY_MMA_SYNC_S): scale inside the A fragments instead of a per-unit group
@@ -351,9 +371,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         const int g0 = u0 % J.Gk;
         const uint32_t st = smem_base + s * C::kStage;
         if (nu == kR && g0 + kR <= J.Gk) {
-          tma_3d(st, J.mR, 0, 0, 2 * g0, &full_bar[s]);
+          tma_3d(st, J.mR, 0, 0, C::kBPU * g0, &full_bar[s]);
         } else {
-          for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, 2 * ((u0 + jj) % J.Gk), &full_bar[s]);
+          for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, C::kBPU * ((u0 + jj) % J.Gk), &full_bar[s]);
         }
       };
       const int run = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile flags)
@@ -652,6 +672,18 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           named_bar_sync(2, kGW * 32);   // xch is reused by the next flush
           return;
         }
+        if constexpr (kA8) {   // the token scale (and the 1/16 of the (q - 8) * 16 codes), once per tile sum
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const int m0 = tb * 8 + c4, m1 = m0 + 4;
+            const float s0 = m0 < p.M ? __ldg(p.sx + m0) * 0.0625f : 0.f, s1 = m1 < p.M ? __ldg(p.sx + m1) * 0.0625f : 0.f;
+#pragma unroll
+            for (int i = 0; i < kRT; ++i) {
+              v[i][tb][0] *= s0; v[i][tb][2] *= s0;
+              v[i][tb][1] *= s1; v[i][tb][3] *= s1;
+            }
+          }
+        }
 #pragma unroll
         for (int i = 0; i < kRT; ++i) {
           const int n0 = t * kTileN + 16 * (kRT * wg + i) + g8, n1 = n0 + 8;
@@ -720,6 +752,55 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     auto process_unit = [&](uint32_t st, int j) {
       const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box b holds k 64b..
       const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
+      if constexpr (kA8) {
+        // W4A8 (include/w4a16.h w4a8_gemm; reading R21): int8 activations (one 128-k SW128 box), int8 codes
+        // (q - 8) * 16, exact int32 group sums from mma m16n8k32, then the fp32 group scale; the token scale
+        // sx[m] / 16 is applied to the tile sum at the store. One MMA per 32-k chunk and row tile.
+        uint2 xb[4][NTB];   // [32-k chunk][token block]: the 8 int8 activations k = 32 pc + 8 c4 .. +7
+#pragma unroll
+        for (int pc = 0; pc < 4; ++pc)
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) {
+            const int m = 8 * tb + tok_pi(g8);
+            const int ch = 2 * pc + (c4 >> 1);                    // 16-byte chunk of the 128-byte row
+            xb[pc][tb] = lds64(xu + m * 128 + ((ch ^ (m & 7)) << 4) + (c4 & 1) * 8);
+          }
+#pragma unroll
+        for (int i = 0; i < kRT; ++i) {
+          const int rt = kRT * wg + i;
+          uint32_t wq[4][2];
+          const int lr = 16 * rt + 8 * ((lane >> 3) & 1) + (lane & 7);
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            const int pch = 2 * pp + (lane >> 4);
+            ldsm_x4(ub + lr * 64 + ((pch ^ ((lr >> 1) & 3)) << 4), wq[2 * pp][0], wq[2 * pp][1], wq[2 * pp + 1][0],
+                    wq[2 * pp + 1][1]);
+          }
+          float sc[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) sc[hf] = __half2float(__ushort_as_half(lds16(ub + 8192 + 2 * (16 * rt + g8 + 8 * hf))));
+          int iacc[NTB][4];
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb) iacc[tb][0] = iacc[tb][1] = iacc[tb][2] = iacc[tb][3] = 0;
+#pragma unroll
+          for (int pc = 0; pc < 4; ++pc) {
+            const uint32_t a0 = a8_lo(wq[pc][0]), a1 = a8_lo(wq[pc][1]), a2 = a8_hi(wq[pc][0]), a3 = a8_hi(wq[pc][1]);
+#pragma unroll
+            for (int tb = 0; tb < NTB; ++tb) {
+              // B bytes in the A fragments' k order: MMA k 4 c4 + j <-> lo byte j (word k 0, 4, 1, 5), MMA k
+              // 16 + 4 c4 + j <-> hi byte j (word k 2, 6, 3, 7)
+              const uint32_t b0 = prmt_b32(xb[pc][tb].x, xb[pc][tb].y, 0x5140u);
+              const uint32_t b1 = prmt_b32(xb[pc][tb].x, xb[pc][tb].y, 0x7362u);
+              mma_s8_16832(iacc[tb], a0, a1, a2, a3, b0, b1);
+            }
+          }
+#pragma unroll
+          for (int tb = 0; tb < NTB; ++tb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][tb][e] = fmaf(sc[e >> 1], (float)iacc[tb][e], acc[i][tb][e]);
+        }
+        return;
+      }
       uint4 xr[4][NTB];                                       // [32-k chunk p][token block]
 #pragma unroll
       for (int pc = 0; pc < 4; ++pc)
@@ -922,11 +1003,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
 template <int NTB, bool SYM, bool kScaleInA>
 static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream) {
-  using C = Cfg<NTB, SYM>;
+  using C = Cfg<NTB, SYM, false>;
   CUtensorMap mapR, map1;
   if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * kR)) return e;
   if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
-  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
+  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA, false>;
   static unsigned long long attr_set = 0;
   if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
   return launch_pdl(kern, dim3(p.G), dim3(threads_for<kScaleInA>()), C::kSmem, stream, mapR, map1, p) == cudaSuccess ? W4A16_OK
@@ -935,8 +1016,8 @@ static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream)
 
 template <int NTB, bool SYM, bool kScaleInA>
 static int launch_chain_t(const GemmParams& p, bool cooperative, cudaStream_t stream) {
-  using C = Cfg<NTB, SYM>;
-  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA>;
+  using C = Cfg<NTB, SYM, false>;
+  auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA, false>;
   static unsigned long long attr_set = 0;
   if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
   CUtensorMap unused;
@@ -953,6 +1034,31 @@ static int launch_chain_t(const GemmParams& p, bool cooperative, cudaStream_t st
   cfg.attrs = attr;
   cfg.numAttrs = cooperative ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, unused, unused, p) == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+}
+
+// W4A8 on the family-A pipeline (SYM blob, int8 activations Xq [M][K] viewed as (128 k, M rows, K/128 boxes)).
+template <int NTB>
+static int launch_a8_t(const int8_t* Xq, const GemmParams& p, cudaStream_t stream) {
+  using C = Cfg<NTB, true, true>;
+  auto enc = get_encode();
+  if (!enc) return W4A16_ERR_CUDA;
+  CUtensorMap maps[2];
+  const int depth[2] = {kR, 1};
+  for (int i = 0; i < 2; ++i) {
+    const cuuint64_t dims[3] = {128, (cuuint64_t)p.M, (cuuint64_t)(p.K / 128)};
+    const cuuint64_t strides[2] = {(cuuint64_t)p.K, 128};
+    const cuuint32_t box[3] = {128, (cuuint32_t)C::kMpad, (cuuint32_t)depth[i]};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(Xq), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return W4A16_ERR_CUDA;
+  }
+  auto kern = gemm_w4a16_mma_kernel<NTB, true, false, true>;
+  static unsigned long long attr_set = 0;
+  if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
+  return launch_pdl(kern, dim3(p.G), dim3(threads_for<false>()), C::kSmem, stream, maps[0], maps[1], p) == cudaSuccess
+             ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
 constexpr int kChainSlots = 8;   // partial-slot ring of a chain, in ops
@@ -1242,6 +1348,29 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
       return sym ? w4::ma::launch_chain_t<2, true, false>(p, cooperative != 0, stream) : w4::ma::launch_chain_t<2, false, false>(p, cooperative != 0, stream);
     default:
       return W4A16_ERR_SHAPE;
+  }
+}
+
+// W4A8 GEMM on the family-A pipeline (include/w4a16.h w4a8_gemm; M <= 16). Workspace: w4a16_mma_workspace_bytes.
+extern "C" int w4a8_launch_gemm_mma(const int8_t* Xq, const float* sx, const void* packed, uint16_t* Y, int M, int K, int N,
+                                    void* ws, int num_sms, cudaStream_t stream) {
+  w4::ma::GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.packed = reinterpret_cast<const uint8_t*>(packed);
+  p.Y = Y;
+  p.M = M; p.K = K; p.N = N;
+  p.Gk = K / w4::ma::kTileK;
+  p.U = (N / w4::ma::kTileN) * p.Gk;
+  p.G = w4a16_mma_plan_ctas(K, N, num_sms);
+  p.counters = reinterpret_cast<int*>(ws);
+  p.partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + w4::kCounterBytes);
+  p.n_jobs = 1;
+  p.slots = 1;
+  p.sx = sx;
+  switch ((M + 7) / 8) {
+    case 1: return w4::ma::launch_a8_t<1>(Xq, p, stream);
+    case 2: return w4::ma::launch_a8_t<2>(Xq, p, stream);
+    default: return W4A16_ERR_SHAPE;
   }
 }
 

@@ -22,37 +22,79 @@ constexpr int kTB = 8448;       // SYM unit bytes (8192 codes + 128 fp16 scales)
 constexpr int kWarps = 8;       // 16 output columns (tile rows) each
 
 // ---- activation quantisation: one CTA per token row ----
-__global__ void __launch_bounds__(256) quant_kernel(const __half* __restrict__ X, int K, int8_t* __restrict__ Xq,
+// One CTA per token row, kQT threads, one pass over the row: every thread keeps its 8-value chunks (16-byte
+// loads) in registers, the row's amax is reduced through shared memory, then each chunk is quantised and a
+// 128-k group's sum (16 consecutive chunks = 16 lanes) is reduced with shuffles. The GEMM that follows is
+// launched with programmatic dependent launch: this kernel lets it start at once, so its weight stream
+// overlaps the quantisation (the GEMM waits for this grid before it reads Xq).
+constexpr int kQT = 512;
+constexpr int kQChunks = 8;   // 8-value chunks per thread kept in registers: K <= kQT * 8 * kQChunks = 32768
+__global__ void __launch_bounds__(kQT) quant_kernel(const __half* __restrict__ X, int K, int8_t* __restrict__ Xq,
                                                     float* __restrict__ sx, int32_t* __restrict__ xsum) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int m = blockIdx.x;
-  const __half* xr = X + (size_t)m * K;
-  __shared__ float s_red[8];
+  const uint4* xr = reinterpret_cast<const uint4*>(X + (size_t)m * K);
+  const int nc = K / 8;   // 8-value chunks in the row
+  __shared__ float s_red[kQT / 32];
+  uint4 v[kQChunks];
   float amax = 0.f;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) amax = fmaxf(amax, fabsf(__half2float(xr[k])));
+#pragma unroll
+  for (int j = 0; j < kQChunks; ++j) {
+    const int c = threadIdx.x + j * kQT;
+    v[j] = c < nc ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+    const __half2* h = reinterpret_cast<const __half2*>(&v[j]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(h[e]);
+      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+  }
   for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
   __syncthreads();
   amax = s_red[0];
-  for (int w = 1; w < 8; ++w) amax = fmaxf(amax, s_red[w]);
+#pragma unroll
+  for (int w = 1; w < kQT / 32; ++w) amax = fmaxf(amax, s_red[w]);
   const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
   if (threadIdx.x == 0) sx[m] = __fdiv_rn(amax, 127.f);
-  // groups of 128: each warp takes whole groups, 4 values per lane
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int g = warp; g < K / kTile; g += 8) {
-    int sum = 0;
-    char4 q4;
-    int8_t q[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float v = rintf(__fmul_rn(__half2float(xr[g * kTile + lane * 4 + j]), inv));
-      v = fminf(fmaxf(v, -127.f), 127.f);
-      q[j] = (int8_t)(int)v;
-      sum += q[j];
+  for (int j = 0; j < kQChunks; ++j) {
+    const int c = threadIdx.x + j * kQT;   // chunks 16 g .. 16 g + 15 of group g sit on 16 consecutive lanes
+    if (j * kQT >= nc) break;
+    const __half2* h = reinterpret_cast<const __half2*>(&v[j]);
+    int8_t q[8];
+    int sum = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(h[e]);
+      float a = fminf(fmaxf(rintf(__fmul_rn(f.x, inv)), -127.f), 127.f);
+      float b = fminf(fmaxf(rintf(__fmul_rn(f.y, inv)), -127.f), 127.f);
+      q[2 * e] = (int8_t)(int)a;
+      q[2 * e + 1] = (int8_t)(int)b;
+      sum += q[2 * e] + q[2 * e + 1];
     }
-    q4.x = q[0]; q4.y = q[1]; q4.z = q[2]; q4.w = q[3];
-    *reinterpret_cast<char4*>(Xq + (size_t)m * K + g * kTile + lane * 4) = q4;
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) xsum[(size_t)m * (K / kTile) + g] = sum;
+    if (c < nc) *reinterpret_cast<int2*>(Xq + (size_t)m * K + (size_t)c * 8) = *reinterpret_cast<const int2*>(q);
+    for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);   // 16-lane halves = one group
+    if (c < nc && (threadIdx.x & 15) == 0) xsum[(size_t)m * (K / kTile) + c / 16] = sum;
+  }
+  for (int c0 = kQChunks * kQT; c0 < nc; c0 += kQT) {   // K > 32768: second pass from memory (warp-uniform loop)
+    const int c = c0 + threadIdx.x;
+    const uint4 w = c < nc ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+    const __half2* h = reinterpret_cast<const __half2*>(&w);
+    int8_t q[8];
+    int sum = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(h[e]);
+      float a = fminf(fmaxf(rintf(__fmul_rn(f.x, inv)), -127.f), 127.f);
+      float b = fminf(fmaxf(rintf(__fmul_rn(f.y, inv)), -127.f), 127.f);
+      q[2 * e] = (int8_t)(int)a;
+      q[2 * e + 1] = (int8_t)(int)b;
+      sum += q[2 * e] + q[2 * e + 1];
+    }
+    if (c < nc) *reinterpret_cast<int2*>(Xq + (size_t)m * K + (size_t)c * 8) = *reinterpret_cast<const int2*>(q);
+    for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (c < nc && (threadIdx.x & 15) == 0) xsum[(size_t)m * (K / kTile) + c / 16] = sum;
   }
 }
 
@@ -232,7 +274,7 @@ extern "C" size_t w4a8_workspace_bytes_sms(int M, int K, int N, int num_sms) {
 }
 
 extern "C" int w4a8_launch_quantize(const uint16_t* X, int M, int K, int8_t* Xq, float* sx, int32_t* xsum, cudaStream_t stream) {
-  w4::a8::quant_kernel<<<M, 256, 0, stream>>>(reinterpret_cast<const __half*>(X), K, Xq, sx, xsum);
+  w4::a8::quant_kernel<<<M, w4::a8::kQT, 0, stream>>>(reinterpret_cast<const __half*>(X), K, Xq, sx, xsum);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
 

@@ -468,12 +468,16 @@ def w4a8_workspace_bytes(M: int, K: int, N: int) -> int:
     return int(lib.w4a8_workspace_bytes(M, K, N))
 
 
-def w4a8_gemm(Xq, sx, xsum, packed, Y, workspace, stream=None):
-    """Y [M, N] fp16 = W4A8 GEMM of the quantised activations with a SYM w4a16_pack blob (K x N)."""
+def w4a8_gemm(Xq, sx, xsum, packed, Y, workspace, stream=None, impl: int = 0):
+    """Y [M, N] fp16 = W4A8 GEMM of the quantised activations with a SYM w4a16_pack blob (K x N).
+    impl (tests / A-B only, the w4a8_gemm_ex hook): 0 = auto, 1 = family-A pipeline (M <= 16), 2 = round-1 kernel."""
     M, K = Xq.shape
     N = Y.shape[1]
     if Xq.dtype != torch.int8 or Y.shape[0] != M:
         raise W4A16Error("w4a8_gemm: shapes / dtypes")
-    check(lib.w4a8_gemm(Xq.data_ptr(), sx.data_ptr(), xsum.data_ptr(), _ptr(packed, None, "packed"),
-                        _ptr(Y, torch.float16, "Y"), M, K, N, workspace.data_ptr(),
-                        workspace.numel() * workspace.element_size(), _stream(stream)), "w4a8_gemm")
+    args = (Xq.data_ptr(), sx.data_ptr(), xsum.data_ptr(), _ptr(packed, None, "packed"), _ptr(Y, torch.float16, "Y"), M, K, N,
+            workspace.data_ptr(), workspace.numel() * workspace.element_size())
+    if impl == 0:
+        check(lib.w4a8_gemm(*args, _stream(stream)), "w4a8_gemm")
+    else:
+        check(lib.w4a8_gemm_ex(*args, int(impl), _stream(stream)), "w4a8_gemm_ex")

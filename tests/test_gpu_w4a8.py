@@ -45,18 +45,22 @@ def test_act_quant_bit_exact(M, K):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("impl", [0, 1, 2])
 @pytest.mark.parametrize("M", [1, 5, 8, 16, 33, 64])
 @pytest.mark.parametrize("K,N", [(1024, 1280), (4096, 2560)])
-def test_w4a8_gemm_vs_oracle(M, K, N):
+def test_w4a8_gemm_vs_oracle(M, K, N, impl):
+    # impl: 0 = auto, 1 = the family-A pipeline (M <= 16: int8 codes (q - 8) * 16, mma m16n8k32 s8), 2 = round 1
+    if impl == 1 and M > 16:
+        pytest.skip("the family-A W4A8 path serves M <= 16")
     w4 = _w4()
     W = synth.host(42, K + N, synth.WEIGHT, K, N)
     Wd = torch.from_numpy(W.view(np.int16)).cuda().view(torch.float16)
     pl = w4.pack_linear(Wd, mode=w4.W4A16_SYM)
     X = synth.gpu(43, M + K, synth.ACT, M, K)
     Xq, sx, xs = _quant_gpu(X)
-    ws = torch.empty(w4.w4a8_workspace_bytes(M, K, N), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(w4.w4a8_workspace_bytes(M, K, N), dtype=torch.uint8, device="cuda")
     Y = torch.full((M, N), float("nan"), dtype=torch.float16, device="cuda")
-    w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y, ws)
+    w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y, ws, impl=impl)
     torch.cuda.synchronize()
     # the oracle quantises the HOST activations itself; the GPU's codes / scales / group sums must equal them
     # bit for bit, and only the oracle's own values feed the oracle GEMM
@@ -71,7 +75,7 @@ def test_w4a8_gemm_vs_oracle(M, K, N):
     assert np.all(np.abs(y - ref) <= 1e-3 * (1 + np.abs(ref))), np.abs(y - ref).max()
     # deterministic: a second run gives the same bits
     Y2 = torch.empty_like(Y)
-    w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y2, ws)
+    w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y2, ws, impl=impl)
     torch.cuda.synchronize()
     assert torch.equal(Y.view(torch.int16), Y2.view(torch.int16))
 

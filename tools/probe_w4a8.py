@@ -18,15 +18,19 @@ for M in [int(x) for x in a.Ms.split(",")]:
     Xq = torch.empty(M, a.K, dtype=torch.int8, device="cuda")
     sx = torch.empty(M, dtype=torch.float32, device="cuda")
     xs = torch.empty(M, a.K // 128, dtype=torch.int32, device="cuda")
-    ws = torch.empty(w4.w4a8_workspace_bytes(M, a.K, a.N), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(w4.w4a8_workspace_bytes(M, a.K, a.N), dtype=torch.uint8, device="cuda")
     Y = torch.empty(M, a.N, dtype=torch.float16, device="cuda")
     ws16 = w4.alloc_workspace(M, [(a.K, a.N)])
     res = {}
-    for name in ("w4a8", "w4a16"):
+    for name in ("w4a8", "w4a8_famA", "w4a8_r1", "w4a8_gemm_only", "w4a16"):
+        if name == "w4a8_famA" and M > 16:
+            continue
         def step():
-            if name == "w4a8":
-                w4.w4a8_quantize_act(X, Xq, sx, xs, stream=s)
-                w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y, ws, stream=s)
+            if name.startswith("w4a8"):
+                impl = {"w4a8": 0, "w4a8_famA": 1, "w4a8_r1": 2, "w4a8_gemm_only": 0}[name]
+                if name != "w4a8_gemm_only":
+                    w4.w4a8_quantize_act(X, Xq, sx, xs, stream=s)
+                w4.w4a8_gemm(Xq, sx, xs, pl.packed, Y, ws, stream=s, impl=impl)
             else:
                 pl(X, Y, ws16, stream=s)
         with torch.cuda.stream(s):
@@ -46,4 +50,4 @@ for M in [int(x) for x in a.Ms.split(",")]:
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / 50
         res[name] = us
-    print(f"M={M} K={a.K} N={a.N}: W4A8 {res['w4a8']:.1f} us ({wb / res['w4a8'] / 1e6:.2f} TB/s) | W4A16 {res['w4a16']:.1f} us ({wb / res['w4a16'] / 1e6:.2f} TB/s)")
+    print(f"M={M} K={a.K} N={a.N}: " + " | ".join(f"{k} {v:.1f} us ({wb / v / 1e6:.2f} TB/s)" for k, v in res.items()))
