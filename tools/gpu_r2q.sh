@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_tree_attn.py -q -x --timeout 200 2>&1 | tail -3
+for M in 8 61; do timeout 120 python tools/probe_attn.py --M $M; done
