@@ -26,4 +26,17 @@ e0.record()
 for _ in range(20):
     w4.w4a16_tree_attention(Q, K, V, par, O, ws)
 e1.record(); torch.cuda.synchronize()
-print(json.dumps({"M": a.M, "L": a.L, "us": e0.elapsed_time(e1) * 1e3 / 20}))
+eager = e0.elapsed_time(e1) * 1e3 / 20
+s = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    for _ in range(20):
+        w4.w4a16_tree_attention(Q, K, V, par, O, ws, stream=s)
+with torch.cuda.stream(s):
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(s); g.replay(); e1.record(s)
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / 20
+kv = 2 * (a.L + a.M) * a.Hkv * D * 2
+print(json.dumps({"M": a.M, "L": a.L, "us_eager": eager, "us_graph": us, "kv_GBps": kv / us / 1e3}))
