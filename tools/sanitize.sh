@@ -18,5 +18,5 @@ for tool in racecheck synccheck memcheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_chain.py tests/test_gpu_allreduce.py -x -q \
       -k "independent or (simulated_ranks and 1-8-0)" > $OUT/sanitize_chain_$tool.log 2>&1; echo "chain $tool rc=$?"; grep -E "ERROR SUMMARY|passed" $OUT/sanitize_chain_$tool.log | tail -2
 done
-timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_w4a8.py -x -q \
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_w4a8.py -x -q -k "1024 or quant" \
     > $OUT/sanitize_w4a8.log 2>&1; echo "w4a8 memcheck rc=$?"; grep -E "ERROR SUMMARY|passed" $OUT/sanitize_w4a8.log | tail -2
