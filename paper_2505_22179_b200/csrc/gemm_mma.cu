@@ -2,28 +2,31 @@
 //
 //   Y[M,N] = X[M,K] · W_hat[K,N]   with W_hat = (q - z) * s per group of 128 k (include/w4a16.h)
 //
-// Design. At M <= 16 the tensor work per weight is small enough for the legacy mma.sync
-// pipe (~550 TFLOP/s measured on B200), and keeping dequant + MMA inside each warp's registers avoids the
-// TMEM traffic and cross-warp hand-offs of the tcgen05 family.
+// Design. At M <= 16 the tensor work per weight is small enough for the legacy
+// mma.sync pipe (~540 TFLOP/s measured on B200), and keeping dequant + MMA inside each warp's registers avoids
+// the TMEM traffic and cross-warp hand-offs of the tcgen05 families.
 //  * Work unit = one 128x128 (n x k) weight tile (8704 / 8448 contiguous bytes of the packed blob: codes,
 //    scales, zeros). Units are numbered in blob order, so a CTA's range is one contiguous byte range.
-//  * Stream-K: CTA c of G = 2 x SMs owns units [c*U/G, (c+1)*U/G) — a (K, N, SM-count)-only plan.
-//  * Warp 8 (producer) streams stages of 2 units with ONE bulk copy each (the TMA engine costs ~100+
-//    cycles per issued copy), plus the units' activation slices with a 3-D TMA (SWIZZLE_128B, rows >= M
-//    zero-filled), into a 4-deep shared-memory ring.
-//  * Warps 0..7 = 4 row-quarters x 2 k-halves: warp (rq, kh) owns tile rows 32rq..32rq+31 (two m16 MMA
-//    tiles) and k = 64kh..64kh+63 of every unit, so each activation fragment is reused by 2 MMA row tiles
-//    and only 2 warps read each activation byte (the v1 layout re-read X 8x and was L1-bound).
-//    A lane reads one 32-bit word (8 consecutive k of one row) per row and chunk — conflict-free thanks to
-//    the XOR chunk permutation of the layout — dequantises it to EXACT (q - z) fp16 with LOP3 +
-//    HSUB2/HFMA2, and issues mma.sync m16n8k16 with weights as the MMA-M operand ("swap AB"; tokens are
-//    MMA-N). Inside each 32-k chunk a k-permutation lets one lane's 8 consecutive k feed two MMA k-steps,
-//    with the activations read as one 16-byte vector per token block.
-//  * The group scale is applied after the MMA to the fp32 group sum: Y += s * sum_k X (q - z), keeping the
-//    dequant at 9 integer/fp16 instructions per 8 weights (no HMUL2).
-//  * Tile boundary: the two k-half warps combine through shared memory; a tile split across CTAs goes to
-//    the fp32 workspace and the last CTA to arrive (atomic counter per tile) sums the partials in CTA order
-//    (fixed, hence deterministic) and writes fp16 Y, re-zeroing the counter.
+//  * Stream-K: CTA c of G = #SMs (one CTA per SM) owns units [c*U/G, (c+1)*U/G) — a (K, N, SM-count)-only plan.
+//  * Warp 16 (producer) streams stages of 4 units with ONE bulk copy each (the TMA engine costs ~100+ cycles
+//    per issued copy), plus the units' activation slices with a 3-D TMA (SWIZZLE_128B, rows >= M
+//    zero-filled), into a ring of up to 8 stages (as many as fit in shared memory); activation loads wait in
+//    a queue for their producing op's tile-ready flags (chains), weights never wait.
+//  * Warps 0..15 (consumers) = 2 groups x 8 warps; group g takes units 2g, 2g+1 of every stage; warp w of a
+//    group owns tile rows 16w..16w+15 (one m16 MMA tile) and all 128 k of its units. A lane reads one 32-bit
+//    word (8 consecutive k of one row) per row and chunk with ldmatrix — conflict-free thanks to the XOR
+//    chunk permutation of the layout — dequantises it to EXACT (q - z) fp16 with LOP3 + HSUB2/HFMA2, and
+//    issues mma.sync m16n8k16 with weights as the MMA-M operand ("swap AB"; tokens are MMA-N). Inside each
+//    32-k chunk a k-permutation lets one lane's 8 consecutive k feed two MMA k-steps, with the activations
+//    read as one 16-byte vector per token block.
+//  * The group scale is applied after the MMA to the fp32 group sum: Y += s * sum_k X (q - z) (the exact
+//    weight, reading R22).
+//  * Tile boundary: group 1 hands its sums to group 0 through shared memory; a tile split across CTAs is
+//    owned by its first CTA, which handles the tile's head as its LAST segment: the others store fp32
+//    partials and bump the tile counter, the owner sums them in CTA order (deterministic) and writes Y.
+//  * Warp 17 (publisher) issues every GPU- or system-scope release (tile counters, tile-ready flags, op
+//    counts, ALLREDUCE tile bumps) behind one fence per batch and runs the chain's ALLREDUCE ops.
+//  * W4A8 (kA8): the same pipeline with int8 activations and int8 codes (q - 8) * 16 on mma m16n8k32.
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>

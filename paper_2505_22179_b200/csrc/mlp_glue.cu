@@ -26,7 +26,12 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t* GU, int M, int F, int block
   const long long work = (long long)M * (F / 8);
   if (work == 0) return W4A16_OK;
   long long blocks = (work + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  static int sms = 0;   // grid-stride loop: at most 8 blocks of 256 per SM of this device
+  if (sms <= 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
   w4::silu_mul_kernel<<<(unsigned)blocks, 256, 0, stream>>>(GU, M, F, block, out);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }

@@ -8,7 +8,8 @@
 // w4a16_tree_attention: split-KV flash attention on the tensor cores (mma.sync m16n8k16, fp32 softmax).
 //  * CTA = (kv head g, block of 64 query rows, KV split). Query row r of head group g is (token m = r / G,
 //    head g*G + r % G), G = Hq / Hkv: the G query heads that share a kv head (GQA) share every K/V load.
-//  * 4 warps x 16 query rows. Per 64-position KV chunk (cp.async, double-buffered, XOR-swizzled rows):
+//  * 4 warps x 16 query rows. Per 64-position KV chunk (cp.async into one buffer — three CTAs per SM hide
+//    the latency better than double-buffering, measured —, XOR-swizzled rows):
 //    S = Q K^T (ldmatrix + mma), the mask (prefix visible; tree row L + j visible iff j is an ancestor of m
 //    or m itself: a 64-bit ancestor mask per token), online softmax in fp32 (exp2), O += P V (P from the S
 //    registers, V through ldmatrix.trans).
