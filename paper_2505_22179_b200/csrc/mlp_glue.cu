@@ -2,12 +2,17 @@
 // a Llama MLP in the verify forward. GU[m] = [gate_0..gate_{F-1} | up_0..up_{F-1}] (the
 // rank-local gate-up shard), out[m][j] = fp16_rne(silu(gate_j) * up_j), computed in fp32.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "w4a16.h"
 
 namespace w4 {
 
 __global__ void __launch_bounds__(256) silu_mul_kernel(const uint16_t* __restrict__ GU, int M, int F, int block,
                                                        uint16_t* __restrict__ out) {
+  // programmatic dependent launch: the next GEMM may start streaming its weights now (it waits for this
+  // grid before it reads `out`); GU comes from the previous kernel, so wait for it before reading
+  pdl_launch_dependents();
+  pdl_wait();
   const int vecs = F / 8;  // 8 halves per 16-byte vector
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)M * vecs;
        i += (long long)gridDim.x * blockDim.x) {
@@ -32,6 +37,6 @@ extern "C" int w4a16_launch_silu_mul(const uint16_t* GU, int M, int F, int block
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
   }
   if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
-  w4::silu_mul_kernel<<<(unsigned)blocks, 256, 0, stream>>>(GU, M, F, block, out);
-  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+  return w4::launch_pdl(w4::silu_mul_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, GU, M, F, block, out) == cudaSuccess
+             ? W4A16_OK : W4A16_ERR_CUDA;
 }
