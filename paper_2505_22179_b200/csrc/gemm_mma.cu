@@ -58,7 +58,10 @@ template <bool kScaleInA>
 constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0)) * 32; }
 constexpr int kPubSlots = 8;
 constexpr int kPubAllReduce = -0x40000000;   // publisher request: run ALLREDUCE op (ptr = its ChainJob)
-constexpr int kR = 2 * kGroups;                    // units per pipeline stage: 2 per group
+#ifndef W4_MA_UPG
+#define W4_MA_UPG 2   // units per consumer group and pipeline stage
+#endif
+constexpr int kR = W4_MA_UPG * kGroups;            // units per pipeline stage
 #ifndef W4_POLL_ACQ
 #define W4_POLL_ACQ 0   // A/B only: poll tile flags with one acquire load each (round 1-2 behaviour)
 #endif
@@ -90,7 +93,7 @@ struct Cfg {
   static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;   // [slot][row tile][tb][e][lane]
   static constexpr int kXchBytes = 4 * NTB * 4 * 32 * 4;          // SiLU epilogue: up values of a tile (fp16 in u32)
   static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / kStage;
-  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
   static constexpr int kSmem = kStages * kStage + kRedFloats * 4 + kXchBytes + 1024;
 };
 
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
                                                                       const GemmParams p) {
   using C = Cfg<NTB, SYM, kA8>;
   constexpr int S = C::kStages;
-  static_assert(S <= 8, "producer queue holds at most 8 stages");
+  static_assert(S <= 16, "producer queue holds at most 16 stages");
   // kScaleInA (family W4A16_FAMILY_MMA_SYNC_S): scale inside the A fragments instead of a per-unit group
   // accumulator — fewer registers (NTB = 2 runs at the 96-register cap of 18 warps/SM), 4 more HMUL2 per
   // word. Post-scale (family W4A16_FAMILY_MMA_SYNC) is faster when registers allow (NTB = 1).
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
       }
       const uint64_t pol = policy_evict_first();
-      int q_s[8], q_j[8], q_u0[8], q_nu[8];   // stages whose activations are not issued yet (FIFO)
+      int q_s[16], q_j[16], q_u0[16], q_nu[16];   // stages whose activations are not issued yet (FIFO)
       int q_head = 0, q_n = 0, ok_upto = -1;
       bool pdl_done = chain;                 // a chain is not launched with PDL
       auto issue_x = [&](int s, const JobInfo& J, int u0, int nu) {
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             g_prod_trace[cta][q_j[q_head]] = globaltimer_ns();
 #endif
           issue_x(q_s[q_head], J, q_u0[q_head], q_nu[q_head]);
-          q_head = (q_head + 1) & 7;
+          q_head = (q_head + 1) & 15;
           --q_n;
         }
       };
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
           mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
           bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
-          const int e = (q_head + q_n) & 7;
+          const int e = (q_head + q_n) & 15;
           q_s[e] = s; q_j[e] = j; q_u0[e] = u0; q_nu[e] = nu;
           ++q_n;
           drain(false);
