@@ -58,10 +58,17 @@ template <bool kScaleInA>
 constexpr int threads_for() { return (pub_warp<kScaleInA>() + (W4_MA_PUB ? 1 : 0)) * 32; }
 constexpr int kPubSlots = 8;
 constexpr int kPubAllReduce = -0x40000000;   // publisher request: run ALLREDUCE op (ptr = its ChainJob)
-#ifndef W4_MA_UPG
-#define W4_MA_UPG 2   // units per consumer group and pipeline stage
+// Units per consumer group and pipeline stage. It must be the same for every token-block class: the group
+// split of a stage's units fixes the fp32 summation order, and results are batch-invariant over M = 1..16.
+// (3 at M <= 8 alone: gate-up 54.3 -> 52.1 us and the chain -1.6 %, but M = 16 is faster with 2 and
+// splitting the classes broke the invariance; an M-independent pairing with 3 was slower — DESIGN.md §5.1.)
+#ifndef W4_MA_UPG1
+#define W4_MA_UPG1 2
 #endif
-constexpr int kR = W4_MA_UPG * kGroups;            // units per pipeline stage
+#ifndef W4_MA_UPG2
+#define W4_MA_UPG2 W4_MA_UPG1
+#endif
+__host__ __device__ constexpr int kR_for(int ntb) { return (ntb == 1 ? W4_MA_UPG1 : W4_MA_UPG2) * kGroups; }
 #ifndef W4_POLL_ACQ
 #define W4_POLL_ACQ 0   // A/B only: poll tile flags with one acquire load each (round 1-2 behaviour)
 #endif
@@ -81,6 +88,7 @@ struct Cfg {
   static constexpr int kXBox = kMpad * 128;                       // one SW128 box: 64 fp16 k (or 128 int8 k) x kMpad rows
   static constexpr int kBPU = kA8 ? 1 : 2;                        // activation boxes per unit (128 k)
   static constexpr int kXUnit = kBPU * kXBox;
+  static constexpr int kR = kR_for(NTB);                          // units per pipeline stage
   static constexpr int kStage = (kR * (kXUnit + kTB) + 1023) / 1024 * 1024;
   // consumer geometry (the kWarps = 16 consumer warps): kRT 16-row MMA tiles per warp, kGW warps per unit
   // group, kNG groups, kUPG units per group and stage (W4_MA_RT: row tiles per warp at NTB = 1)
@@ -376,7 +384,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       auto issue_x = [&](int s, const JobInfo& J, int u0, int nu) {
         const int g0 = u0 % J.Gk;
         const uint32_t st = smem_base + s * C::kStage;
-        if (nu == kR && g0 + kR <= J.Gk) {
+        if (nu == C::kR && g0 + C::kR <= J.Gk) {
           tma_3d(st, J.mR, 0, 0, C::kBPU * g0, &full_bar[s]);
         } else {
           for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, C::kBPU * ((u0 + jj) % J.Gk), &full_bar[s]);
@@ -442,8 +450,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         const JobInfo J = job_at(p, &xmapR, &xmap1, j);
         if (J.kind != kOpGemm) continue;
         const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
-        for (int u0 = u_begin; u0 < u_end; u0 += kR) {
-          const int nu = min(kR, u_end - u0);
+        for (int u0 = u_begin; u0 < u_end; u0 += C::kR) {
+          const int nu = min(C::kR, u_end - u0);
           if (issued >= S) {   // slot s must be released by the consumers first
             if (!pdl_done) drain(true);
             while (!mbar_test_wait(&empty_bar[s], ph ^ 1)) drain(false);
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             continue;
           }
           mbar_expect_tx(&full_bar[s], nu * (C::kXUnit + C::kTB));
-          bulk_g2s(smem + s * C::kStage + kR * C::kXUnit, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
+          bulk_g2s(smem + s * C::kStage + C::kR * C::kXUnit, J.packed + (size_t)u0 * C::kTB, nu * C::kTB, &full_bar[s], pol);
           const int e = (q_head + q_n) & 15;
           q_s[e] = s; q_j[e] = j; q_u0[e] = u0; q_nu[e] = nu;
           ++q_n;
@@ -594,7 +602,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       continue;
     }
     const int u_begin = unit_begin(cta, J.U, p.G), u_end = unit_begin(cta + 1, J.U, p.G);
-    const int n_stages = (u_end - u_begin + kR - 1) / kR;
+    const int n_stages = (u_end - u_begin + C::kR - 1) / C::kR;
     int cur_t = -1, seg_u0 = u_begin, boundary = 0;
     bool first_segment = true;
     // Y writes (and this op's partial slot) wait for the earlier ops that read / write the same buffers.
@@ -757,7 +765,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // dequant + 8 MMAs per row tile (one m16 tile x 8 k-steps), then the post-MMA group scale.
     auto process_unit = [&](uint32_t st, int j) {
       const uint32_t xu = st + j * C::kXUnit;                 // activations of this unit: box b holds k 64b..
-      const uint32_t ub = st + kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
+      const uint32_t ub = st + C::kR * C::kXUnit + j * C::kTB;   // packed tile of this unit
       if constexpr (kA8) {
         // W4A8 (include/w4a16.h w4a8_gemm; reading R21): int8 activations (one 128-k SW128 box), int8 codes
         // (q - 8) * 16, exact int32 group sums from mma m16n8k32, then the fp32 group scale; the token scale
@@ -944,24 +952,28 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
       if (lane == 0) mbar_arrive_a(empty_base + 8 * s);
       if (++s == S) { s = 0; ph ^= 1; }
     };
-    const int n_full = (u_end - u_begin) / kR;   // stages holding kR units
+    const int n_full = (u_end - u_begin) / C::kR;   // stages holding C::kR units
+    // The consumer group of unit u (offset j in its stage): j / kUPG. The stage size must not depend on M, so
+    // each group's units — hence the fp32 summation order — depend on the plan (K, N, SMs) only (batch
+    // invariance over M = 1..16).
+    auto group_of = [&](int u) { return ((u - u_begin) % C::kR) / kUPG; };
     int i = 0;
     while (i < n_stages) {
       // a stage that starts a segment, crosses a tile boundary or is the ragged last one
       {
-        const int u0 = u_begin + i * kR, nu = min(kR, u_end - u0);
+        const int u0 = u_begin + i * C::kR, nu = min(C::kR, u_end - u0);
         stage_begin(i);
         const uint32_t st = smem_base + s * C::kStage;
         // every warp walks the stage's units in order (tile flushes are joint); each group computes its own
         for (int j = 0; j < nu; ++j) {
           if (u0 + j == boundary || cur_t < 0) begin_segment(u0 + j);
-          if (j / kUPG == grp && !skip_compute) process_unit(st, j);
+          if (group_of(u0 + j) == grp && !skip_compute) process_unit(st, j);
         }
         stage_end();
         ++i;
       }
       // then the run of full stages inside the current tile: no per-stage bookkeeping
-      const int i_end = min(n_full, (boundary - u_begin) / kR);
+      const int i_end = min(n_full, (boundary - u_begin) / C::kR);
       for (; i < i_end; ++i) {
         stage_begin(i);
         const uint32_t st = smem_base + s * C::kStage;
@@ -1011,7 +1023,7 @@ template <int NTB, bool SYM, bool kScaleInA>
 static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream) {
   using C = Cfg<NTB, SYM, false>;
   CUtensorMap mapR, map1;
-  if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * kR)) return e;
+  if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * C::kR)) return e;
   if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
   auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA, false>;
   static unsigned long long attr_set = 0;
@@ -1049,7 +1061,7 @@ static int launch_a8_t(const int8_t* Xq, const GemmParams& p, cudaStream_t strea
   auto enc = get_encode();
   if (!enc) return W4A16_ERR_CUDA;
   CUtensorMap maps[2];
-  const int depth[2] = {kR, 1};
+  const int depth[2] = {C::kR, 1};
   for (int i = 0; i < 2; ++i) {
     const cuuint64_t dims[3] = {128, (cuuint64_t)p.M, (cuuint64_t)(p.K / 128)};
     const cuuint64_t strides[2] = {(cuuint64_t)p.K, 128};
@@ -1246,7 +1258,7 @@ extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int f
   long long tiles = 0;
   int mode = 0;
   if (int e = check_ops(ops, n_ops, M, chain_ctas(sms), &tiles, &mode)) return e;
-  const int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR;   // activation boxes of the stages
+  const int mpad = 8 * w4::ma::ntb_of(M), depth = 2 * w4::ma::kR_for(w4::ma::ntb_of(M));   // activation boxes of the stages
   w4::ma::ChainJob* jobs = reinterpret_cast<w4::ma::ChainJob*>(plan);
   int cnt = 0, ar_slot = 0, last_ar = -1;
   uint32_t* epoch = nullptr;   // the group's run counter, advanced by the last CTA of every run
