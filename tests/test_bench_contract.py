@@ -1,4 +1,4 @@
-"""The committed bench line (profiles/r01_bench_N1.json, written by bench.py on a B200) keeps the driver's JSON
+"""The newest committed bench line (profiles/rNN_bench_N1.json, written by bench.py on a B200) keeps the driver's JSON
 contract: metric / value / unit, timing fields, e2e with its byte counts, roofline with a measured peak,
 cpu_baseline, clocks, gpu_launches, and this repo's side rows (f1, f2, f3, f4). A CPU-only check of the
 schema, so a change to bench.py that drops a key is caught before the GPU round."""
@@ -9,7 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _line():
-    with open(os.path.join(ROOT, "profiles", "r01_bench_N1.json")) as f:
+    path = next(os.path.join(ROOT, "profiles", f"r{r:02d}_bench_N1.json") for r in range(9, 0, -1)
+                if os.path.exists(os.path.join(ROOT, "profiles", f"r{r:02d}_bench_N1.json")))
+    with open(path) as f:
         return json.loads(f.read().strip().splitlines()[-1])
 
 
@@ -37,3 +39,5 @@ def test_bench_line_side_rows():
     assert d["allreduce_in_chain"]["us_per_allreduce_op"] > 0           # f1 (world 1)
     assert d["w4a8_gemm"]["us"] > 0 and d["w4a8_gemm"]["row"] == "f4"  # f4 W4A8
     assert set(map(int, d["m_sweep"])) >= {1, 8, 16, 64}
+    assert {int(k) for k in d["m_sweep_sym"] if k.isdigit()} >= {1, 8, 16, 64}   # the paper's GPTQ-symmetric format
+    assert "batched_in_one_chain" in d["other_configs"]["config1_gemm4096_M8"]
