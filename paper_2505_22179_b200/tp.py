@@ -334,13 +334,17 @@ class _Eager:
 
 
 def _peer_group(nbytes: int, slots: int, group):
-    """The symmetric regions of a fused all-reduce: NVLS (one multicast object, multimem loads / reds) where
-    every rank's device supports it, else CUDA-IPC peer mappings. Every step is agreed on by all ranks, so a
-    failure anywhere falls back everywhere (e.g. several ranks on one GPU cannot share a multicast object)."""
-    try:
-        return PeerGroup.mc(nbytes, slots, group)
-    except W4A16Error:
-        return PeerGroup.ipc(nbytes, slots, group)
+    """The symmetric regions of a fused all-reduce: CUDA-IPC peer mappings (verified: simulated ranks, two
+    processes); with W4A16_NVLS=1 first an NVLS multicast object (multimem loads / reds), which no box of this
+    build could create yet, so it is opt-in. Every step is agreed on by all ranks, so a failure anywhere falls
+    back everywhere (e.g. several ranks on one GPU cannot share a multicast object)."""
+    import os
+    if os.environ.get("W4A16_NVLS") == "1":
+        try:
+            return PeerGroup.mc(nbytes, slots, group)
+        except W4A16Error:
+            pass
+    return PeerGroup.ipc(nbytes, slots, group)
 
 
 class _Calibration:

@@ -1,8 +1,9 @@
 """bench.py's multi-rank control path (f1 set-up) run end to end on a 1-GPU box.
 
 Two ranks under torch.distributed.run with the control plane over gloo (BENCH_DIST_BACKEND=gloo), both on
-cuda:0: the fused all-reduce set-up (NVLS multicast attempted first — two ranks on one device cannot share a
-multicast object, so every rank falls back to CUDA-IPC peer regions together), the start-up check of one
+cuda:0: the fused all-reduce set-up (with W4A16_NVLS=1 the NVLS multicast object is attempted first — two
+ranks on one device cannot share one, so every rank falls back to CUDA-IPC peer regions together), the
+start-up check of one
 fused forward against the same forward op by op with the process-group all-reduce, the fallback when the
 check fails on one rank (BENCH_FAIL_FUSED_CHECK=<rank>), and the hard failure of --allreduce fused. The
 timed numbers of these runs mean nothing (two contexts time-slice one GPU); the JSON contract and the
@@ -26,7 +27,7 @@ def _port():
 
 
 def _run(extra_env, *args):
-    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", **extra_env)
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", W4A16_NVLS="1", **extra_env)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--model", "8b",
            "--layers", "2", "--M", "8", "--sweep", "", "--sym-sweep", "", "--steps", "2", "--warmup", "3",
