@@ -28,9 +28,12 @@ constexpr int kRowsBlk = 64;        // query rows per CTA
 constexpr int kKv = 64;             // KV positions per chunk
 constexpr int kThreads = 128;       // 4 warps x 16 rows
 constexpr int kTileBytes = 64 * kD * 2;   // 16 KB: 64 rows x 256 B
-constexpr int kNbPart = 1;      // K/V buffers of the partials path (3 CTAs per SM)
-constexpr int kNbCl = 3;        // K/V ring of the cluster path (2 chunks in flight; 2 CTAs per SM)
-constexpr int kMaxCluster = 16; // KV splits per cluster (non-portable size above 8)
+#ifndef W4_TA_BUFS
+#define W4_TA_BUFS 1
+#endif
+constexpr int kKvBufs = W4_TA_BUFS;       // K/V chunk buffers: 2 = double-buffered, 1 = more CTAs per SM
+constexpr int kSmem = kTileBytes * (1 + 2 * kKvBufs) + 64 * 8 + 64 * 4 + 1024;   // Q, (K, V) x bufs, masks, parents
+constexpr int kCtasPerSmEst = kKvBufs == 2 ? 2 : 3;
 
 struct Params {
   const uint16_t* Q;
@@ -62,39 +65,12 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t& r0, uint32_t& r1
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
 }
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) { return h22u(__floats2half2_rn(a, b)); }
-// Distributed shared memory: the same shared-memory offset in cluster CTA `rank`.
-__device__ __forceinline__ uint32_t dsmem_addr(uint32_t a, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float ld_dsmem_f32(uint32_t a, int rank) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(a, rank)) : "memory");
-  return v;
-}
-__device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t a, int rank) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(dsmem_addr(a, rank)) : "memory");
-  return v;
-}
 
-template <int NB>
-constexpr int smem_for() { return kTileBytes * (1 + 2 * NB) + 64 * 8 + 64 * 4 + 2 * 64 * 4 + 1024; }
-
-// NB: K/V chunk buffers, a ring (NB - 1 chunks in flight while one is computed; NB = 1: load, wait, compute).
-// kCl: the KV splits of one (query block, kv head) form a thread-block cluster and merge through distributed
-// shared memory (no partials in global memory, no second kernel); else each split writes fp32 partials for
-// tree_attn_combine.
-template <int NB, bool kCl>
-__global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p, uint16_t* __restrict__ Oout) {
+__global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_u32(smem), sK0 = sQ + kTileBytes, sV0 = sQ + (1 + NB) * kTileBytes;
-  unsigned long long* anc = reinterpret_cast<unsigned long long*>(smem + (1 + 2 * NB) * kTileBytes);
-  float* sm_m = reinterpret_cast<float*>(anc + 64 + 32);   // after anc[64] and the parents (int[64])
-  float* sm_l = sm_m + 64;
+  const uint32_t sQ = smem_u32(smem), sK0 = sQ + kTileBytes, sV0 = sQ + (1 + kKvBufs) * kTileBytes;
+  unsigned long long* anc = reinterpret_cast<unsigned long long*>(smem + (1 + 2 * kKvBufs) * kTileBytes);
   const int split = blockIdx.x, qb = blockIdx.y, g = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, c4 = lane & 3;
   const int P = p.L + p.M;
@@ -134,13 +110,8 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p, uin
       cp_async16(sV0 + buf * kTileBytes + tile_off(r, c), p.V + off, ok);
     }
   };
-  // ring prologue: chunks 0 .. NB-2 in flight (the Q tile rides in the first group)
-  const int nch = ch1 - ch0;
-#pragma unroll
-  for (int i = 0; i < NB - 1; ++i) {
-    if (i < nch) load_kv(ch0 + i, i);
-    cp_async_commit();
-  }
+  if (kKvBufs == 2 && ch0 < ch1) load_kv(ch0, 0);
+  cp_async_commit();
 
   // this lane's two query rows (g8, g8 + 8 of the warp's 16) and their tokens
   const int r_lo = qb * kRowsBlk + 16 * warp + g8, r_hi = r_lo + 8;
@@ -151,10 +122,16 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p, uin
   float mx[2] = {-INFINITY, -INFINITY}, sum[2] = {0.f, 0.f};
 
   for (int ch = ch0; ch < ch1; ++ch) {
-    const int i = ch - ch0, buf = i % NB;
-    if (i + NB - 1 < nch) load_kv(ch + NB - 1, (i + NB - 1) % NB);   // refills the buffer of chunk i - 1
-    cp_async_commit();
-    asm volatile("cp.async.wait_group %0;" ::"n"(NB - 1) : "memory");   // chunk i (and Q) has landed
+    const int buf = kKvBufs == 2 ? (ch - ch0) & 1 : 0;
+    if (kKvBufs == 2) {
+      if (ch + 1 < ch1) load_kv(ch + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait1();
+    } else {
+      load_kv(ch, 0);
+      cp_async_commit();
+      cp_async_wait0();
+    }
     __syncthreads();
     const uint32_t sK = sK0 + buf * kTileBytes, sV = sV0 + buf * kTileBytes;
     // S = Q K^T: 16 rows x 64 positions per warp
@@ -226,80 +203,25 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p, uin
     __syncthreads();   // the buffer is refilled by the next iteration's load
   }
   cp_async_wait0();
-  // row sums across the 4 lanes of a row
+  // row sums across the 4 lanes of a row, then the split's partial results
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     sum[h] += __shfl_xor_sync(0xffffffffu, sum[h], 1);
     sum[h] += __shfl_xor_sync(0xffffffffu, sum[h], 2);
   }
+  const int Rpad = p.qblocks * kRowsBlk;
+  const size_t base = ((size_t)split * p.Hkv + g) * Rpad;
   const int rl = qb * kRowsBlk + 16 * warp + g8;
-  if constexpr (kCl) {
-    // Merge the S splits of this (query block, kv head) inside the cluster (CTA rank = split):
-    //   m* = max_s m_s, w_s = 2^(m_s - m*) / sum_t 2^(m_t - m*) l_t, O = sum_s w_s O_s (s in order).
-    // 1. publish this split's row maxima / sums; 2. every CTA scales its own O_s by w_s into its shared
-    // memory (the K/V ring is free now); 3. CTA c sums rows c, c + S, ... over all S CTAs' shared memory.
-    const int S = p.splits;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = rl + 8 * h;
+    float* op = p.o_part + (base + r) * kD;
+#pragma unroll
+    for (int n = 0; n < 16; ++n)
+      *reinterpret_cast<float2*>(op + 8 * n + 2 * c4) = make_float2(o[n][2 * h], o[n][2 * h + 1]);
     if (c4 == 0) {
-      sm_m[16 * warp + g8] = mx[0]; sm_m[16 * warp + g8 + 8] = mx[1];
-      sm_l[16 * warp + g8] = sum[0]; sm_l[16 * warp + g8 + 8] = sum[1];
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    float w[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = 16 * warp + g8 + 8 * h;
-      const uint32_t am = smem_u32(sm_m + row), al = smem_u32(sm_l + row);
-      float mstar = -INFINITY;
-      for (int t = 0; t < S; ++t) mstar = fmaxf(mstar, ld_dsmem_f32(am, t));
-      float den = 0.f;
-      for (int t = 0; t < S; ++t) {
-        const float mt = ld_dsmem_f32(am, t);
-        if (mt != -INFINITY) den += exp2f(mt - mstar) * ld_dsmem_f32(al, t);
-      }
-      w[h] = (mx[h] == -INFINITY || den == 0.f) ? 0.f : exp2f(mx[h] - mstar) / den;
-    }
-    float* sO = reinterpret_cast<float*>(smem + kTileBytes);   // [64 rows][128] fp32 over the K/V ring
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float* orow = sO + (16 * warp + g8 + 8 * h) * kD;
-#pragma unroll
-      for (int n = 0; n < 16; ++n)
-        *reinterpret_cast<float2*>(orow + 8 * n + 2 * c4) = make_float2(o[n][2 * h] * w[h], o[n][2 * h + 1] * w[h]);
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    // 32 threads per row (float4 over the 128 dims), 4 rows per pass
-    const uint32_t sO_u = smem_u32(sO);
-    for (int row = split * 4 + (tid >> 5); row < kRowsBlk; row += 4 * S) {
-      const int rr = qb * kRowsBlk + row;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int t = 0; t < S; ++t) {
-        const float4 v = ld_dsmem_f32x4(sO_u + (row * kD + 4 * lane) * 4, t);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      if (rr < p.R) {
-        const int m = rr / p.G, h = g * p.G + rr % p.G;
-        uint2 out;
-        out.x = pack_h2(acc.x, acc.y);
-        out.y = pack_h2(acc.z, acc.w);
-        *reinterpret_cast<uint2*>(Oout + ((size_t)m * p.Hq + h) * kD + 4 * lane) = out;
-      }
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");   // keep smem alive
-  } else {
-    // the split's partial results for tree_attn_combine
-    const int Rpad = p.qblocks * kRowsBlk;
-    const size_t base = ((size_t)split * p.Hkv + g) * Rpad;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = rl + 8 * h;
-      float* op = p.o_part + (base + r) * kD;
-#pragma unroll
-      for (int n = 0; n < 16; ++n)
-        *reinterpret_cast<float2*>(op + 8 * n + 2 * c4) = make_float2(o[n][2 * h], o[n][2 * h + 1]);
-      if (c4 == 0) {
-        p.m_part[base + r] = mx[h];
-        p.l_part[base + r] = sum[h];
-      }
+      p.m_part[base + r] = mx[h];
+      p.l_part[base + r] = sum[h];
     }
   }
 }
@@ -363,27 +285,15 @@ __global__ void kv_compact_kernel(uint16_t* K, uint16_t* V, int L, int row_vec, 
 }  // namespace w4
 
 namespace {
-constexpr int kCtasPerSmPart = 3;
-// Partials path (fallback): splits fill kCtasPerSmPart CTAs per SM, at least two chunks per split.
 void plan_splits(int M, int L, int Hq, int Hkv, int sms, int* qblocks, int* splits, int* cps) {
   const int G = Hq / Hkv, R = M * G;
   *qblocks = (R + w4::ta::kRowsBlk - 1) / w4::ta::kRowsBlk;
   const int chunks = (L + M + w4::ta::kKv - 1) / w4::ta::kKv;
-  int s = (kCtasPerSmPart * sms + Hkv * *qblocks - 1) / (Hkv * *qblocks);
+  int s = (w4::ta::kCtasPerSmEst * sms + Hkv * *qblocks - 1) / (Hkv * *qblocks);
   const int max_s = (chunks + 1) / 2;   // at least two chunks per split where there are two (fewer partials to merge)
   s = s < 1 ? 1 : s > max_s ? max_s : s;
   *cps = (chunks + s - 1) / s;
   *splits = (chunks + *cps - 1) / *cps;
-}
-// Cluster path: S <= kMaxCluster splits per (query block, kv head), the grid within 2 CTAs per SM.
-void plan_cluster(int M, int L, int Hq, int Hkv, int sms, int* qblocks, int* splits, int* cps) {
-  const int G = Hq / Hkv, R = M * G;
-  *qblocks = (R + w4::ta::kRowsBlk - 1) / w4::ta::kRowsBlk;
-  const int chunks = (L + M + w4::ta::kKv - 1) / w4::ta::kKv, heads = Hkv * *qblocks, slots = 2 * sms;
-  int c = (chunks + w4::ta::kMaxCluster - 1) / w4::ta::kMaxCluster;
-  while (c < chunks && heads * ((chunks + c - 1) / c) > slots) ++c;
-  *cps = c;
-  *splits = (chunks + c - 1) / c;
 }
 }  // namespace
 
@@ -400,48 +310,15 @@ extern "C" int w4a16_launch_tree_attention(const uint16_t* Q, const uint16_t* K,
   w4::ta::Params p;
   p.Q = Q; p.K = K; p.V = V; p.parents = parents;
   p.M = M; p.L = L; p.Hq = Hq; p.Hkv = Hkv; p.G = Hq / Hkv; p.R = M * p.G;
-  p.scale_log2 = 1.4426950408889634f / sqrtf((float)w4::ta::kD);
-  // 1. one kernel: the KV splits of each (query block, kv head) in a thread-block cluster, merged through
-  //    distributed shared memory
-  static int cl_ok = -1;   // per process: cluster launch of this shape family works (else the partials path)
-  if (cl_ok != 0) {
-    plan_cluster(M, L, Hq, Hkv, sms, &p.qblocks, &p.splits, &p.chunks_per_split);
-    auto kern = w4::ta::tree_attn_kernel<w4::ta::kNbCl, true>;
-    constexpr int smem = w4::ta::smem_for<w4::ta::kNbCl>();
-    static unsigned long long attr = 0;
-    static bool np = false;
-    if (!np) np = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-    if (w4::ensure_smem_attr(kern, smem, attr)) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(p.splits, p.qblocks, Hkv);
-      cfg.blockDim = dim3(w4::ta::kThreads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = stream;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = p.splits;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, kern, p, O) == cudaSuccess) {
-        cl_ok = 1;
-        return W4A16_OK;
-      }
-      cudaGetLastError();   // clear the launch error; fall back for good
-    }
-    cl_ok = 0;
-  }
-  // 2. fallback: fp32 partials per split, merged by tree_attn_combine
   plan_splits(M, L, Hq, Hkv, sms, &p.qblocks, &p.splits, &p.chunks_per_split);
   const size_t rows = (size_t)p.splits * Hkv * p.qblocks * w4::ta::kRowsBlk;
   p.o_part = reinterpret_cast<float*>(ws);
   p.m_part = p.o_part + rows * w4::ta::kD;
   p.l_part = p.m_part + rows;
-  auto kern = w4::ta::tree_attn_kernel<w4::ta::kNbPart, false>;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)w4::ta::kD);
   static unsigned long long attr = 0;
-  if (!w4::ensure_smem_attr(kern, w4::ta::smem_for<w4::ta::kNbPart>(), attr)) return W4A16_ERR_CUDA;
-  kern<<<dim3(p.splits, p.qblocks, Hkv), w4::ta::kThreads, w4::ta::smem_for<w4::ta::kNbPart>(), stream>>>(p, O);
+  if (!w4::ensure_smem_attr(w4::ta::tree_attn_kernel, w4::ta::kSmem, attr)) return W4A16_ERR_CUDA;
+  w4::ta::tree_attn_kernel<<<dim3(p.splits, p.qblocks, Hkv), w4::ta::kThreads, w4::ta::kSmem, stream>>>(p);
   w4::ta::tree_attn_combine<<<dim3((p.R + 7) / 8, Hkv), 256, 0, stream>>>(p, O);
   return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
 }
