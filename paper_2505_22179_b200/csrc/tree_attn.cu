@@ -67,6 +67,7 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t& r0, uint32_t& r1
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) { return h22u(__floats2half2_rn(a, b)); }
 
 __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the merge kernel may launch and wait
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sQ = smem_u32(smem), sK0 = sQ + kTileBytes, sV0 = sQ + (1 + kKvBufs) * kTileBytes;
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) tree_attn_kernel(const Params p) {
 // Merge the splits: O = sum_s 2^(m_s - m*) O_s / sum_s 2^(m_s - m*) l_s, fp16 out. One warp per query row
 // (lanes over the 128 head dims as float4), 8 rows per block.
 __global__ void __launch_bounds__(256) tree_attn_combine(const Params p, uint16_t* __restrict__ O) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // launched with PDL: the split partials are complete
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * 8 + warp, g = blockIdx.y;
   if (r >= p.R) return;
@@ -240,19 +242,20 @@ __global__ void __launch_bounds__(256) tree_attn_combine(const Params p, uint16_
   for (int off = 16; off > 0; off >>= 1) mstar = fmaxf(mstar, __shfl_xor_sync(0xffffffffu, mstar, off));
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
   float den = 0.f;
-  for (int sp0 = 0; sp0 < p.splits; sp0 += 4) {   // four splits' loads in flight at a time
-    float ms[4], l[4];
-    float4 v[4];
+  constexpr int kB = 9;    // splits' loads in flight at a time (one or two L2 round trips for the usual splits)
+  for (int sp0 = 0; sp0 < p.splits; sp0 += kB) {
+    float ms[kB], l[kB];
+    float4 v[kB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int sp = min(sp0 + u, p.splits - 1);
-      const size_t i = ((size_t)sp * p.Hkv + g) * Rpad + r;
-      ms[u] = sp0 + u < p.splits ? __ldcg(&p.m_part[i]) : -INFINITY;
-      l[u] = __ldcg(&p.l_part[i]);
-      v[u] = __ldcg(reinterpret_cast<const float4*>(p.o_part + i * kD) + lane);
+    for (int u = 0; u < kB; ++u) {
+      const bool in = sp0 + u < p.splits;   // no loads past the last split
+      const size_t i = ((size_t)(in ? sp0 + u : 0) * p.Hkv + g) * Rpad + r;
+      ms[u] = in ? __ldcg(&p.m_part[i]) : -INFINITY;
+      l[u] = in ? __ldcg(&p.l_part[i]) : 0.f;
+      v[u] = in ? __ldcg(reinterpret_cast<const float4*>(p.o_part + i * kD) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kB; ++u) {
       if (ms[u] == -INFINITY) continue;
       const float w = exp2f(ms[u] - mstar);
       num.x += w * v[u].x; num.y += w * v[u].y; num.z += w * v[u].z; num.w += w * v[u].w;
@@ -319,8 +322,9 @@ extern "C" int w4a16_launch_tree_attention(const uint16_t* Q, const uint16_t* K,
   static unsigned long long attr = 0;
   if (!w4::ensure_smem_attr(w4::ta::tree_attn_kernel, w4::ta::kSmem, attr)) return W4A16_ERR_CUDA;
   w4::ta::tree_attn_kernel<<<dim3(p.splits, p.qblocks, Hkv), w4::ta::kThreads, w4::ta::kSmem, stream>>>(p);
-  w4::ta::tree_attn_combine<<<dim3((p.R + 7) / 8, Hkv), 256, 0, stream>>>(p, O);
-  return cudaGetLastError() == cudaSuccess ? W4A16_OK : W4A16_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return W4A16_ERR_CUDA;
+  return w4::launch_pdl(w4::ta::tree_attn_combine, dim3((p.R + 7) / 8, Hkv), dim3(256), 0, stream, p, O) == cudaSuccess
+             ? W4A16_OK : W4A16_ERR_CUDA;
 }
 
 extern "C" int w4a16_launch_kv_compact(uint16_t* K, uint16_t* V, int L, int Hkv, int D, const int32_t* accept_out,
