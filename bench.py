@@ -488,7 +488,7 @@ def main():
         P = stack.plan
         for name in tp.MATRICES:
             s = P[name]
-            xin = {"qkv": stack.x_in, "o": stack.x_o, "gate_up": stack.y_o_red, "down": stack.act}[name][:M]
+            xin = {"qkv": stack.x_in[:M], "o": stack.q_part(M), "gate_up": stack.y_o_red[:M], "down": stack.act[:M]}[name]
             yout = {"qkv": stack.y_qkv, "o": stack.y_o, "gate_up": stack.y_gu, "down": stack.y_down}[name][:M]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):

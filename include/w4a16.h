@@ -122,6 +122,13 @@ int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K,
 int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,
                   void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);
 
+/* w4a16_gemm_strided — w4a16_gemm_ex whose X rows are ldx elements apart (row m at X + m * ldx), e.g. the
+ * attention-output slice of a fused QKV projection read in place. ldx >= K and ldx % 8 == 0 (rows stay
+ * 16-byte aligned), else W4A16_ERR_ARG; ldx = K is w4a16_gemm_ex. Only elements [m][0, K) are read; the
+ * result is bitwise the one w4a16_gemm_ex gives for the same rows stored contiguously. */
+int w4a16_gemm_strided(const uint16_t* X, int ldx, const void* packed, uint16_t* Y, int M, int K, int N, int group,
+                       int mode, void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream);
+
 /* verify_accept — greedy acceptance of a draft tree against the target's argmax (rule per
  * S:289/S:298, reading R9).  n nodes, node 0 = root (the last committed token, row 0 of the verify
  * forward), parents[0] = -1, 0 <= parents[i] < i.  target_argmax[i] = target's greedy token after node i.

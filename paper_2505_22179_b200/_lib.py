@@ -32,6 +32,7 @@ ABI_SYMBOLS = (
     "w4a16_workspace_init",
     "w4a16_gemm",
     "w4a16_gemm_ex",
+    "w4a16_gemm_strided",
     "verify_accept",
     "w4a16_status_string",
     "w4a16_gemm_family",
@@ -98,6 +99,9 @@ def _load():
     lib.w4a16_workspace_init.argtypes = [vp, sz, vp]
     lib.w4a16_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, vp]
     lib.w4a16_gemm_ex.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp, sz, i32, vp]
+    if hasattr(lib, "w4a16_gemm_strided"):
+        lib.w4a16_gemm_strided.argtypes = [vp, i32, vp, vp, i32, i32, i32, i32, i32, vp, sz, i32, vp]
+        lib.w4a16_gemm_strided.restype = i32
     lib.verify_accept.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.w4a16_status_string.argtypes = [i32]
     lib.w4a16_status_string.restype = ctypes.c_char_p

@@ -16,9 +16,9 @@ extern "C" int w4a16_launch_accept(const int32_t*, const int32_t*, const int32_t
 extern "C" int w4a16_launch_silu_mul(const uint16_t*, int, int, int, uint16_t*, cudaStream_t);
 extern "C" size_t w4a16_mma_workspace_bytes(int M, int K, int N, int num_sms);
 extern "C" size_t w4a16_tc_workspace_bytes(int M, int K, int N, int num_sms);
-extern "C" int w4a16_launch_gemm_tc(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_gemm_tc(const uint16_t*, int, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 extern "C" size_t w4a16_tp_workspace_bytes(int M, int K, int N, int num_sms);
-extern "C" int w4a16_launch_gemm_tp(const uint16_t*, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
+extern "C" int w4a16_launch_gemm_tp(const uint16_t*, int, const void*, uint16_t*, int, int, int, int, void*, int, cudaStream_t);
 extern "C" size_t w4a16_lmhead_workspace_bytes_sms(int num_sms);
 extern "C" int w4a16_launch_hadamard(const uint16_t*, uint16_t*, int, int, int, cudaStream_t);
 extern "C" size_t w4a16_tree_attention_workspace_bytes_sms(int M, int L, int Hq, int Hkv, int sms);
@@ -35,7 +35,7 @@ extern "C" int w4a8_launch_quantize(const uint16_t*, int, int, int8_t*, float*, 
 extern "C" int w4a8_launch_gemm_mma(const int8_t*, const float*, const void*, uint16_t*, int, int, int, void*, int, cudaStream_t);
 extern "C" int w4a8_launch_gemm(const int8_t*, const float*, const int32_t*, const void*, uint16_t*, int, int, int, void*, int,
                                 cudaStream_t);
-extern "C" int w4a16_launch_gemm_mma(const uint16_t*, const void*, uint16_t*, int, int, int, int, bool, void*, int,
+extern "C" int w4a16_launch_gemm_mma(const uint16_t*, int, const void*, uint16_t*, int, int, int, int, bool, void*, int,
                                      cudaStream_t);
 
 namespace {
@@ -106,10 +106,12 @@ extern "C" int w4a16_gemm_family(int M, int K, int N) {
   return W4A16_FAMILY_TCGEN05;
 }
 
-extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group,
-                             int mode, void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream) {
+extern "C" int w4a16_gemm_strided(const uint16_t* X, int ldx, const void* packed, uint16_t* Y, int M, int K, int N,
+                                  int group, int mode, void* workspace, size_t workspace_bytes, int family,
+                                  w4a16_stream_t stream) {
   if (!X || !packed || !Y || !mode_ok(mode)) return W4A16_ERR_ARG;
   if (int e = check_kn(K, N, group)) return e;
+  if (ldx < K || ldx % 8) return W4A16_ERR_ARG;
   if (M < 1 || M > W4A16_MAX_M) return W4A16_ERR_SHAPE;
   if (!aligned16(X) || !aligned16(packed) || !aligned16(Y) || !aligned16(workspace)) return W4A16_ERR_ALIGN;
   const int sms = num_sms_of_current_device();
@@ -118,18 +120,23 @@ extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y,
   if (family == W4A16_FAMILY_MMA_SYNC || family == W4A16_FAMILY_MMA_SYNC_S) {
     if (M > 16) return W4A16_ERR_SHAPE;
     if (!workspace || workspace_bytes < w4a16_mma_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_mma(X, packed, Y, M, K, N, mode, family == W4A16_FAMILY_MMA_SYNC_S, workspace, sms,
+    return w4a16_launch_gemm_mma(X, ldx, packed, Y, M, K, N, mode, family == W4A16_FAMILY_MMA_SYNC_S, workspace, sms,
                                  (cudaStream_t)stream);
   }
   if (family == W4A16_FAMILY_TCGEN05) {
     if (!workspace || workspace_bytes < w4a16_tc_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_tc(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+    return w4a16_launch_gemm_tc(X, ldx, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
   }
   if (family == W4A16_FAMILY_TCGEN05_OC) {
     if (!workspace || workspace_bytes < w4a16_tp_workspace_bytes(M, K, N, sms)) return W4A16_ERR_WORKSPACE;
-    return w4a16_launch_gemm_tp(X, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
+    return w4a16_launch_gemm_tp(X, ldx, packed, Y, M, K, N, mode, workspace, sms, (cudaStream_t)stream);
   }
   return W4A16_ERR_ARG;
+}
+
+extern "C" int w4a16_gemm_ex(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group,
+                             int mode, void* workspace, size_t workspace_bytes, int family, w4a16_stream_t stream) {
+  return w4a16_gemm_strided(X, K, packed, Y, M, K, N, group, mode, workspace, workspace_bytes, family, stream);
 }
 
 extern "C" int w4a16_gemm(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int group, int mode,

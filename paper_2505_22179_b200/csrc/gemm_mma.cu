@@ -130,6 +130,7 @@ struct GemmParams {
                           // number + 1 of the last run that wrote the tile's Y (run number at done[n_jobs + 1])
   int slots;              // chain: partial-slot ring length in ops (1 for a single GEMM)
   const float* sx;        // W4A8 (kA8): per-token activation scales [M]
+  int ldx;                // host only: X row stride in elements (0 = K), read when the X tensor maps are encoded
 };
 
 struct JobInfo {
@@ -1023,8 +1024,8 @@ template <int NTB, bool SYM, bool kScaleInA>
 static int launch_t(const uint16_t* X, const GemmParams& p, cudaStream_t stream) {
   using C = Cfg<NTB, SYM, false>;
   CUtensorMap mapR, map1;
-  if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * C::kR)) return e;
-  if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2)) return e;
+  if (int e = encode_x_sw128(&mapR, X, p.M, p.K, C::kMpad, 2 * C::kR, p.ldx)) return e;
+  if (int e = encode_x_sw128(&map1, X, p.M, p.K, C::kMpad, 2, p.ldx)) return e;
   auto kern = gemm_w4a16_mma_kernel<NTB, SYM, kScaleInA, false>;
   static unsigned long long attr_set = 0;
   if (!ensure_smem_attr(kern, C::kSmem, attr_set)) return W4A16_ERR_CUDA;
@@ -1392,9 +1393,11 @@ extern "C" int w4a8_launch_gemm_mma(const int8_t* Xq, const float* sx, const voi
   }
 }
 
-extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
-                                     bool scale_in_a, void* ws, int num_sms, cudaStream_t stream) {
+extern "C" int w4a16_launch_gemm_mma(const uint16_t* X, int ldx, const void* packed, uint16_t* Y, int M, int K, int N,
+                                     int mode, bool scale_in_a, void* ws, int num_sms, cudaStream_t stream) {
   w4::ma::GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.ldx = ldx;
   p.packed = reinterpret_cast<const uint8_t*>(packed);
   p.Y = Y;
   p.M = M; p.K = K; p.N = N;

@@ -23,6 +23,7 @@
 //  * epilogue (after the stage's A hand-off): tcgen05.ld of the accumulator (thread = row), fp16 store of
 //    Y, or — for a tile split across CTAs — fp32 partial + ordered last-arriver reduction (as family A).
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -82,6 +83,7 @@ struct Params {
   float* partials;   // [2G][MPAD][128] fp32
   int* counters;     // [W4A16_MAX_N/128], shared by every shape (fixed offset)
   int M, K, N, Gk, U, G;
+  int ldx;           // host only: X row stride in elements (0 = K), read when the X tensor maps are encoded
   int dbg;           // diagnostics only (W4A16_TC_DEBUG): bit0 skip MMA, bit1 skip dequant, bit2 skip X TMA
 };
 
@@ -445,8 +447,8 @@ template <int MPAD, bool SYM>
 int launch(const uint16_t* X, const Params& p, cudaStream_t stream) {
   using C = Cfg<MPAD, SYM>;
   CUtensorMap mapR, map1;
-  if (int e = w4::encode_x_sw128(&mapR, X, p.M, p.K, MPAD, 2 * C::kR)) return e;
-  if (int e = w4::encode_x_sw128(&map1, X, p.M, p.K, MPAD, 2)) return e;
+  if (int e = w4::encode_x_sw128(&mapR, X, p.M, p.K, MPAD, 2 * C::kR, p.ldx)) return e;
+  if (int e = w4::encode_x_sw128(&map1, X, p.M, p.K, MPAD, 2, p.ldx)) return e;
   auto kern = gemm_w4a16_tc_kernel<MPAD, SYM>;
   static unsigned long long attr = 0;
   if (!w4::ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
@@ -473,9 +475,11 @@ extern "C" int w4a16_debug_trace(void* host, size_t bytes) {
                  cudaSuccess ? 0 : -5;
 }
 
-extern "C" int w4a16_launch_gemm_tc(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
-                                    void* ws, int num_sms, cudaStream_t stream) {
+extern "C" int w4a16_launch_gemm_tc(const uint16_t* X, int ldx, const void* packed, uint16_t* Y, int M, int K, int N,
+                                    int mode, void* ws, int num_sms, cudaStream_t stream) {
   w4::tc::Params p;
+  memset(&p, 0, sizeof(p));
+  p.ldx = ldx;
   p.packed = reinterpret_cast<const uint8_t*>(packed);
   p.Y = Y;
   p.M = M; p.K = K; p.N = N;

@@ -85,6 +85,7 @@ struct Params {
   float* partials;      // [slots][2G][MPAD][128] fp32 split-tile partials
   int* counters;        // tile counters: fixed region (single GEMM) or per op at ChainJob::cnt_off (chain)
   int M, K, N, Gk, U, G;
+  int ldx;              // host only: X row stride in elements (0 = K), read when the X tensor maps are encoded
   const ChainJob* jobs; // chain op table (device) or nullptr: a single GEMM
   int n_jobs;
   int* done;            // chain: [n_jobs] CTAs that finished each op, then the exit counter
@@ -548,8 +549,8 @@ template <int MPAD, bool SYM>
 int launch(const uint16_t* X, const Params& p, cudaStream_t stream) {
   using C = Cfg<MPAD>;
   CUtensorMap map1, mapS;
-  if (int e = encode_x_sw128(&map1, X, p.M, p.K, MPAD, 2)) return e;
-  if (int e = encode_x_sw128(&mapS, X, p.M, p.K, MPAD, 2 * C::kRW)) return e;
+  if (int e = encode_x_sw128(&map1, X, p.M, p.K, MPAD, 2, p.ldx)) return e;
+  if (int e = encode_x_sw128(&mapS, X, p.M, p.K, MPAD, 2 * C::kRW, p.ldx)) return e;
   auto kern = gemm_w4a16_tp_kernel<MPAD, SYM>;
   static unsigned long long attr = 0;
   if (!ensure_smem_attr(kern, C::kSmem, attr)) return W4A16_ERR_CUDA;
@@ -603,10 +604,11 @@ extern "C" size_t w4a16_tp_workspace_bytes(int M, int K, int N, int num_sms) {
   return w4::kCounterBytes + (size_t)2 * w4a16_tp_plan_ctas(K, N, num_sms) * w4::tp::mpad_of(M) * w4::tp::kTileN * 4;
 }
 
-extern "C" int w4a16_launch_gemm_tp(const uint16_t* X, const void* packed, uint16_t* Y, int M, int K, int N, int mode,
-                                    void* ws, int num_sms, cudaStream_t stream) {
+extern "C" int w4a16_launch_gemm_tp(const uint16_t* X, int ldx, const void* packed, uint16_t* Y, int M, int K, int N,
+                                    int mode, void* ws, int num_sms, cudaStream_t stream) {
   w4::tp::Params p;
   memset(&p, 0, sizeof(p));
+  p.ldx = ldx;
   p.packed = reinterpret_cast<const uint8_t*>(packed);
   p.Y = Y;
   p.M = M; p.K = K; p.N = N;

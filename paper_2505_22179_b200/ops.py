@@ -91,14 +91,19 @@ def alloc_workspace(M_max: int, shapes, device=None) -> torch.Tensor:
 
 
 def w4a16_gemm(X, packed, Y, workspace, mode=W4A16_ASYM, group=W4A16_GROUP, stream=None, family=W4A16_FAMILY_AUTO):
-    """Y = X . W_hat through w4a16_gemm (family AUTO) or w4a16_gemm_ex (explicit family)."""
+    """Y = X . W_hat through w4a16_gemm (family AUTO) or w4a16_gemm_ex (explicit family); an X whose rows are
+    strided (a column slice of a wider buffer) goes through w4a16_gemm_strided and is read in place."""
     M, K = X.shape
     N = Y.shape[1]
     if Y.shape[0] != M:
         raise W4A16Error("Y must be [M, N]")
-    args = (_ptr(X, torch.float16, "X"), _ptr(packed, None, "packed"), _ptr(Y, torch.float16, "Y"), M, K, N, group,
+    ldx = _ldx(X)
+    xp = _ptr_rows(X, "X") if ldx else _ptr(X, torch.float16, "X")
+    args = (xp, _ptr(packed, None, "packed"), _ptr(Y, torch.float16, "Y"), M, K, N, group,
             mode, _ptr(workspace, None, "workspace"), workspace.numel() * workspace.element_size())
-    if family == W4A16_FAMILY_AUTO:
+    if ldx:
+        st = lib.w4a16_gemm_strided(args[0], ldx, *args[1:], family, _stream(stream))
+    elif family == W4A16_FAMILY_AUTO:
         st = lib.w4a16_gemm(*args, _stream(stream))
     else:
         st = lib.w4a16_gemm_ex(*args, family, _stream(stream))

@@ -154,7 +154,6 @@ class VerifyStack:
         # the forward's input hidden state (caller fills) and per-layer scratch outputs (module docstring)
         self.x_in = torch.zeros(M_max, P["qkv"]["K"], **f16)
         self.y_qkv = torch.zeros(M_max, P["qkv"]["N"], **f16)
-        self.x_o = torch.zeros(M_max, P["o"]["K"], **f16)   # op-by-op path only: contiguous copy of qkv[:, :K_o]
         self.y_gu = torch.empty(M_max, P["gate_up"]["N"], **f16)
         self.act = torch.empty(M_max, P["down"]["K"], **f16)
         if self.fused:
@@ -254,8 +253,7 @@ class VerifyStack:
         o_out, d_out = (self.y_o_red[:M], self.y_down_red[:M]) if self.fused else (self.y_o[:M], self.y_down[:M])
         for l, L in enumerate(self.layers):
             L["qkv"](self.layer_input(l, M), self.y_qkv[:M], ws, stream)
-            self.x_o[:M].copy_(self.q_part(M))   # single GEMMs take contiguous X (chains read the strided view)
-            L["o"](self.x_o[:M], self.y_o[:M], ws, stream)
+            L["o"](self.q_part(M), self.y_o[:M], ws, stream)   # the strided query view, read in place
             if self.fused:
                 o_out.copy_(self.y_o[:M])
             self._allreduce(o_out)

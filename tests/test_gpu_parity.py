@@ -309,6 +309,36 @@ def test_gemm_writes_only_its_output():
     del Y, big, Yv, w4
 
 
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("M", [1, 9, 16, 37])
+def test_gemm_strided_x_equals_contiguous(M, family):
+    # w4a16_gemm_strided: X as a column slice of a wider buffer (NaN in the columns it must not read)
+    # gives bitwise the contiguous result, which is within tolerance of the oracle
+    if family in (0, 2) and M > 16:
+        pytest.skip("the mma.sync families serve M <= 16")
+    w4 = _lib()
+    P = problem(1024, 512, seed=6)
+    X = synth.host(3, 18, synth.ACT, M, 1024)
+    Xc = torch.from_numpy(X.view(np.int16)).cuda().view(torch.float16)
+    wide = torch.full((M, 1024 + 264), float("nan"), dtype=torch.float16, device="cuda")
+    wide[:, :1024] = Xc
+    Xs = wide[:, :1024]
+    assert M == 1 or not Xs.is_contiguous()
+    Yc = torch.empty((M, 512), dtype=torch.float16, device="cuda")
+    Ys = torch.empty((M, 512), dtype=torch.float16, device="cuda")
+    P.pl(Xc, Yc, P.ws, family=family)
+    P.pl(Xs, Ys, P.ws, family=family)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np_u16(Ys), to_np_u16(Yc))
+    assert_gemm_close(Ys, P.ref(X), f"strided M={M} family={family}")
+    # bad strides are rejected: ldx < K, ldx % 8 != 0
+    packed, ws = P.pl.packed.data_ptr(), P.ws.data_ptr()
+    for ldx in (1016, 1028):
+        st = w4._lib.lib.w4a16_gemm_strided(wide.data_ptr(), ldx, packed, Ys.data_ptr(), M, 1024, 512, 128, P.pl.mode,
+                                            ws, P.ws.numel(), family, None)
+        assert st == -1   # W4A16_ERR_ARG
+
+
 def test_gemm_workspace_too_small_is_rejected():
     w4 = _lib()
     P = problem(4096, 4096)

@@ -39,7 +39,7 @@ for M in [int(x) for x in a.Ms.split(",")]:
     for L in st.layers:
         qa, qb = st._layer_ops(L, M)
         plain += qa + qb
-        fused += [qa[0], ("gemm", st.x_o[:M], L["o"], P_o[:M]), ("allreduce", P_o[:M], red_o[:M], g),
+        fused += [qa[0], ("gemm", st.q_part(M), L["o"], P_o[:M]), ("allreduce", P_o[:M], red_o[:M], g),
                   qb[0], qb[1], ("gemm", st.act[:M], L["down"], P_d[:M]), ("allreduce", P_d[:M], red_d[:M], g)]
     t0 = timed(w4.Chain(plain, M))
     t1 = timed(w4.Chain(fused, M))
