@@ -688,7 +688,7 @@ def main():
                 _, pa = synth.eagle_tree(np.random.default_rng(args.seed), Mq - 1, 6)
                 par_a = torch.tensor(pa, dtype=torch.int32, device=dev)
             Oa = torch.empty(Mq, Hq, D, dtype=torch.float16, device=dev)
-            wsa = torch.empty(w4.w4a16_tree_attention_workspace_bytes(Mq, Lctx, Hq, Hkv, D), dtype=torch.uint8, device=dev)
+            wsa = torch.zeros(w4.w4a16_tree_attention_workspace_bytes(Mq, Lctx, Hq, Hkv, D), dtype=torch.uint8, device=dev)
             acc_a = torch.zeros(3 + Mq, dtype=torch.int32, device=dev)
             with torch.cuda.stream(stream):
                 w4.w4a16_tree_attention(Qa, Ka, Va, par_a, Oa, wsa, stream=stream)

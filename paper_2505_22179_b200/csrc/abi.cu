@@ -480,7 +480,7 @@ extern "C" int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int 
 
 namespace {
 int check_attn(int M, int L, int Hq, int Hkv, int D) {
-  if (M < 1 || M > W4A16_MAX_M || L < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || D != 128) return W4A16_ERR_SHAPE;
+  if (M < 1 || M > W4A16_MAX_M || L < 0 || Hq < 1 || Hq > 512 || Hkv < 1 || Hq % Hkv || D != 128) return W4A16_ERR_SHAPE;
   return W4A16_OK;
 }
 }  // namespace

@@ -32,7 +32,7 @@ def _gpu_attn(Q, K, V, par):
     Lt, Hkv, _ = K.shape
     Qd, Kd, Vd = _t(Q), _t(K), _t(V)
     O = torch.full((M, Hq, D), float("nan"), dtype=torch.float16, device="cuda")
-    ws = torch.empty(w4.w4a16_tree_attention_workspace_bytes(M, Lt - M, Hq, Hkv, D), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(w4.w4a16_tree_attention_workspace_bytes(M, Lt - M, Hq, Hkv, D), dtype=torch.uint8, device="cuda")
     w4.w4a16_tree_attention(Qd, Kd, Vd, _t(np.asarray(par, dtype=np.int32)), O, ws)
     torch.cuda.synchronize()
     return O.float().cpu().numpy().astype(np.float64)
@@ -60,6 +60,29 @@ def test_tree_attention_vs_oracle(M, L, Hq, Hkv, kind):
     got = _gpu_attn(Q, K, V, par)
     err = np.abs(got - ref)
     assert np.all(err <= TOL * (1 + np.abs(ref))), f"max err {err.max():.3g}"
+
+
+def test_tree_attention_bench_config_and_workspace_reuse():
+    # the bench's configuration (70B head layout, L = 2048, M = 8 and 61: many splits merged in-kernel), then a
+    # small problem (one split, no merge) and the big one again on the SAME workspace: the split-merge counters
+    # in its header must come back to zero after every call (include/w4a16.h)
+    w4 = _w4()
+    Hq, Hkv, D = 64, 8, 128
+    cases = [(8, 2048), (61, 2048), (3, 20), (8, 2048)]
+    nbytes = max(w4.w4a16_tree_attention_workspace_bytes(M, L, Hq, Hkv, D) for M, L in cases)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    for M, L in cases:
+        Q, K, V = _inputs(M + 7 * L, M, L, Hq, Hkv)
+        _, par = synth.eagle_tree(np.random.default_rng(M), M - 1, 6)
+        par = np.asarray(par, dtype=np.int32)
+        O = torch.full((M, Hq, D), float("nan"), dtype=torch.float16, device="cuda")
+        w4.w4a16_tree_attention(_t(Q), _t(K), _t(V), _t(par), O, ws)
+        torch.cuda.synchronize()
+        got = O.float().cpu().numpy().astype(np.float64)
+        ref = oracle.tree_attention(Q, K, V, par)
+        err = np.abs(got - ref)
+        assert np.all(err <= TOL * (1 + np.abs(ref))), f"M={M} L={L}: max err {err.max():.3g}"
+        assert int(ws[:16384].view(torch.int32)[0::8].abs().sum()) == 0, "split-merge counters not re-armed"
 
 
 def test_tree_attention_masks_non_ancestors_exactly():

@@ -1,0 +1,6 @@
+OUT=gpurun_out; mkdir -p $OUT
+for rep in 1 2; do
+for lib in "" pf4 pf8 pf16; do
+  W4A16_LIB="$lib" timeout 120 python tools/chain_time.py --layers 16 --reps 15 --Ms 1,8,16 2>&1 | grep median
+done; done > $OUT/ab_s3c.log 2>&1
+cat $OUT/ab_s3c.log
