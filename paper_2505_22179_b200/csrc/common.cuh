@@ -231,7 +231,10 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Acquire-only fence (SASS: CCTL.IVALL, no MEMBAR): after relaxed polls that observed a release, orders the later
+// reads. fence.acq_rel.gpu would add a MEMBAR.ALL.GPU, which in a thread with bulk copies in flight cost ~3.5 %
+// of the chain (measured with the fence removed).
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
