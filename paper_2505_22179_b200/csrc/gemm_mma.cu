@@ -72,6 +72,15 @@ __host__ __device__ constexpr int kR_for(int ntb) { return (ntb == 1 ? W4_MA_UPG
 #ifndef W4_POLL_ACQ
 #define W4_POLL_ACQ 0   // A/B only: poll tile flags with one acquire load each (round 1-2 behaviour)
 #endif
+#ifndef W4_MA_CNTREL
+#define W4_MA_CNTREL 1   // split-tile counters released by the storing thread instead of the publisher warp
+#endif
+#ifndef W4_MA_DONEREL
+#define W4_MA_DONEREL 1   // op counts released by the storing thread instead of the publisher warp
+#endif
+#ifndef W4_MA_WPRE
+#define W4_MA_WPRE 1   // consumers: load the WAR op count at the op start (-0.8 % at M = 8)
+#endif
 #ifndef W4_MA_FLAGREL
 #define W4_MA_FLAGREL 1   // tile-ready flags released by the storing thread (st.release.gpu) instead of the publisher warp (+0.5 %)
 #endif
@@ -612,11 +621,17 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // Y writes (and this op's partial slot) wait for the earlier ops that read / write the same buffers.
     const int wdep = chain ? max(J.dep_y, job - p.slots) : -1;
     bool y_ready = wdep < 0;
+    // the WAR / WAW op count is loaded now and looked at by the first flush (its L2 round trip hides under the
+    // op's stages instead of stalling the flush)
+    const int wdep_v = (W4_MA_WPRE && threadIdx.x == 0 && wdep >= 0) ? ld_relaxed_gpu(&p.done[wdep]) : 0;
     float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (8 * NTB * 32);
 
     auto flush = [&](int t, int sg0, int sg1) {
       if (!y_ready) {
-        if (threadIdx.x == 0) wait_op(p, wdep);   // released to the other warps by the barrier below
+        if (threadIdx.x == 0) {   // released to the other warps by the barrier below
+          if (W4_MA_WPRE && wdep_v >= p.G) fence_acquire_gpu();
+          else wait_op(p, wdep);
+        }
         y_ready = true;
       }
       // 1. combine the unit groups through shared memory, in a fixed order: ((g0 + g1) + (g2 + g3))
@@ -746,7 +761,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int tb = 0; tb < NTB; ++tb)
             __stcg(&part[pidx(cta, kRT * wg + i, tb)], make_float4(acc[i][tb][0], acc[i][tb][1], acc[i][tb][2], acc[i][tb][3]));
         named_bar_sync(2, kGW * 32);
-        if (threadIdx.x == 0) publish(&J.counters[J.cs * t]);
+        if (threadIdx.x == 0) {
+          if (W4_MA_CNTREL) red_release_gpu_add(&J.counters[J.cs * t], 1);   // the owner is waiting: no queue
+          else publish(&J.counters[J.cs * t]);
+        }
         return;
       }
       if (threadIdx.x == 0) {
@@ -1002,7 +1020,10 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // part; the other warps are already streaming the next op.
     if (chain && grp == 0) {
       named_bar_sync(2, kGW * 32);
-      if (threadIdx.x == 0) publish(&p.done[job]);
+      if (threadIdx.x == 0) {
+        if (W4_MA_DONEREL) red_release_gpu_add(&p.done[job], 1);
+        else publish(&p.done[job]);
+      }
     }
     trace_op(p, job, 3);
   }
