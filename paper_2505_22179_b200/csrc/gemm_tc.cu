@@ -356,13 +356,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       const int slot = 2 * blockIdx.x + (seg_index == 0 ? 0 : 1);
 #pragma unroll
       for (int i = 0; i < kCols; ++i) __stcg(&p.partials[((size_t)slot * MPAD + m0 + i) * kTileN + row], acc[i]);
-      __threadfence();
+      // one acq_rel atomic by thread 0 after the CTA barrier releases every warp's partial stores and, for the
+      // last arriver, acquires the others' (one fence per segment instead of a MEMBAR.SC in each of 16 warps)
       named_bar_sync(1, kDqWarps * 32);
       const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
-      if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[t], 1) == c_last - c_first);
+      if (threadIdx.x == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&p.counters[t]) : "memory");
+        s_last = old == c_last - c_first;
+      }
       named_bar_sync(1, kDqWarps * 32);
       if (!s_last) return;
-      __threadfence();
 #pragma unroll
       for (int i = 0; i < kCols; ++i) acc[i] = 0.f;
       for (int c = c_first; c <= c_last; ++c) {
