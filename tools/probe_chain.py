@@ -106,3 +106,19 @@ for k, name in enumerate(kinds):
         a2 += list((b[ok, j, 1] - pt[ok, j]) / 1e3)
     q = lambda v: "/".join(f"{x:5.2f}" for x in np.percentile(v, [10, 50, 90])) if v else "-"
     print(f"{name:12s} issue-Tdep {q(a1)}   ready-issue {q(a2)}")
+
+# compute time vs the CTA's number of tile segments in the op (stream-K ranges of (K, N, G) only)
+print("\ncompute per op (us, median over layers 2..) by the CTA's tile segments in the op")
+shapes = {"qkv": (8192, 10240), "o": (8192, 8192), "gate_up_silu": (8192, 57344), "down": (28672, 8192)}
+for k, name in enumerate(kinds):
+    K, N = shapes[name]
+    Gk, U = K // 128, (N // 128) * (K // 128)
+    ub = [(c * U) // G for c in range(G + 1)]
+    nseg = np.array([len({u // Gk for u in (ub[c], ub[c + 1] - 1)}) if ub[c + 1] - 1 - ub[c] < Gk else
+                     (ub[c + 1] - 1) // Gk - ub[c] // Gk + 1 for c in range(G)])
+    comp = np.median(np.stack([(b[:, j, 2] - b[:, j, 1]) / 1e3 for j in range(4 + k, n, 4)]), axis=0)
+    out = []
+    for sgs in sorted(set(nseg.tolist())):
+        sel = nseg == sgs
+        out.append(f"{sgs} seg: n={sel.sum():3d} median {np.median(comp[sel]):6.2f} p90 {np.percentile(comp[sel], 90):6.2f}")
+    print(f"{name:12s} " + " | ".join(out))
