@@ -21,3 +21,7 @@ for k in chain famA famB; do
   ncu -i $OUT/prof_${k}_$TAG.ncu-rep --page raw --csv > $OUT/raw_${k}_$TAG.csv 2>/dev/null
   ncu -i $OUT/prof_${k}_$TAG.ncu-rep --page source --csv --print-source sass > $OUT/src_${k}_$TAG.csv 2>/dev/null
 done
+# f2: the tree-attention kernel at the bench's configuration (M = 8, L = 2048, 70B heads)
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:tree_attn -s 3 -c 1 -f -o $OUT/prof_attn_$TAG \
+    python tools/probe_attn.py --M 8 --L 2048 > $OUT/ncu_attn_$TAG.log 2>&1; echo "ncu attn rc=$?"
+ncu -i $OUT/prof_attn_$TAG.ncu-rep --page raw --csv > $OUT/raw_attn_$TAG.csv 2>/dev/null
