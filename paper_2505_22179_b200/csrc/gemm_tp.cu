@@ -67,14 +67,19 @@ struct Cfg {
   static constexpr int kNAcc = kNAccFit > 8 ? 8 : kNAccFit;       // per-step accumulators (kS x MPAD columns)
   static constexpr int kXBox = MPAD * 128;                        // one 64-k SW128 box of MPAD token rows
   static constexpr int kXUnit = 2 * kXBox;                        // a unit's 128 k
-  static constexpr int kStage = kRW * (kXUnit + 8704);            // [kRW activation slices][kRW packed units]
+  // Weights and activations live in SEPARATE rings: a weight stage is released as soon as the dequant warps
+  // have read it (its HBM refill starts at once), an activation stage when the MMAs that read it complete.
+  static constexpr int kStage = kRW * 8704;                        // kRW packed units
+  static constexpr int kXStage = kRW * kXUnit;                     // their activation slices
   static constexpr int kAux = kNAcc * kS * 128 * 4;               // the scale s per unit row, per accumulator slot
-  static constexpr int kSW0 = (kSmemBudget - kAux) / kStage;
-  static constexpr int kSW = kSW0 > 8 ? 8 : kSW0;                 // stages
-  static constexpr int kSmem = kSW * kStage + kAux + 1024;
+  static constexpr int kSW0 = (kSmemBudget - kAux - 3 * kXStage) / kStage;
+  static constexpr int kSW = kSW0 > 8 ? 8 : kSW0;                 // weight stages
+  static constexpr int kSX0 = (kSmemBudget - 1024 - kAux - kSW * kStage) / kXStage;   // (static smem, alignment)
+  static constexpr int kSX = kSX0 > 8 ? 8 : kSX0;                 // activation stages
+  static constexpr int kSmem = kSW * kStage + kSX * kXStage + kAux + 1024;
   // instruction descriptor: D f32 (bit 4), A/B f16, K-major both, N = MPAD (bits 17-22: N >> 3), M = 128 (bits 24-28: M >> 4)
   static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(MPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  static_assert(kSW >= 3, "weight ring too shallow");
+  static_assert(kSW >= 3 && kSX >= 2, "rings too shallow");
   static_assert(kNAcc >= 2, "accumulator ring too shallow");
   static_assert(kRW % kS == 0, "stages hold whole steps");
 };
@@ -141,28 +146,31 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
     gemm_w4a16_tp_kernel(const __grid_constant__ CUtensorMap xmap1, const __grid_constant__ CUtensorMap xmapS,
                          const Params p) {
   using C = Cfg<MPAD>;
-  constexpr int SW = C::kSW, NA = C::kNA, NACC = C::kNAcc, kRW = C::kRW;
+  constexpr int SW = C::kSW, SX = C::kSX, NA = C::kNA, NACC = C::kNAcc, kRW = C::kRW;
   constexpr int TB = SYM ? 8448 : 8704;
   // barriers: wfull/wempty [SW], afull/aempty [NA], accfull/accempty/sfull [NACC]
-  __shared__ __align__(8) uint64_t bars[2 * SW + 2 * NA + 3 * NACC];
+  __shared__ __align__(8) uint64_t bars[2 * SW + 2 * SX + 2 * NA + 3 * NACC];
   __shared__ uint32_t s_tmem;
   __shared__ int s_last;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t w_base = smem_u32(smem);
-  const uint32_t s_base = w_base + SW * C::kStage;            // [NACC][kS][128] fp32 scale per unit row
+  const uint32_t x_base = w_base + SW * C::kStage;            // activation ring
+  const uint32_t s_base = x_base + SX * C::kXStage;           // [NACC][kS][128] fp32 scale per unit row
   const uint32_t b0 = smem_u32(&bars[0]);
   const uint32_t WFULL = b0, WEMPTY = WFULL + 8 * SW;
   const uint32_t AFULL = WEMPTY + 8 * SW, AEMPTY = AFULL + 8 * NA, ACCFULL = AEMPTY + 8 * NA;
   const uint32_t ACCEMPTY = ACCFULL + 8 * NACC, SFULL = ACCEMPTY + 8 * NACC;
+  const uint32_t XFULL = SFULL + 8 * NACC, XEMPTY = XFULL + 8 * SX;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const bool chain = p.jobs != nullptr;
 
   if (threadIdx.x == 0) {
-    // a stage is released by the dequant warps (weights read) and the MMA warp's commit (activations read)
-    for (int i = 0; i < SW; ++i) { tcx::mbar_init_a(WFULL + 8 * i, 1); tcx::mbar_init_a(WEMPTY + 8 * i, kDq + 1); }
+    // a weight stage is released by the dequant warps (read), an activation stage by the MMA warp's commit
+    for (int i = 0; i < SW; ++i) { tcx::mbar_init_a(WFULL + 8 * i, 1); tcx::mbar_init_a(WEMPTY + 8 * i, kDq); }
+    for (int i = 0; i < SX; ++i) { tcx::mbar_init_a(XFULL + 8 * i, 1); tcx::mbar_init_a(XEMPTY + 8 * i, 1); }
     for (int i = 0; i < NA; ++i) { tcx::mbar_init_a(AFULL + 8 * i, 8); tcx::mbar_init_a(AEMPTY + 8 * i, 1); }
     for (int i = 0; i < NACC; ++i) {
       tcx::mbar_init_a(ACCFULL + 8 * i, 1);
@@ -189,8 +197,9 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap1)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapS)) : "memory");
       }
-      int q_s[8], q_j[8], q_u0[8], q_nu[8];
-      int q_head = 0, q_n = 0, ok_upto = -1, n_w = 0;
+      int q_j[16], q_u0[16], q_nu[16];   // stages whose activation loads are not issued yet (FIFO)
+      int q_head = 0, q_n = 0, ok_upto = -1, n_w = 0, x_issued = 0;
+      Ring x{0, 0};
       bool pdl_done = chain;
       auto drain = [&](bool block) {   // issue queued activation loads whose producers are done
         while (q_n > 0) {
@@ -208,8 +217,13 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
             ok_upto = J.dep_x;
             fence_proxy_async_global();   // generic-proxy stores of other CTAs -> this TMA (async proxy) read
           }
-          const int st = q_s[q_head], u0 = q_u0[q_head], nu = q_nu[q_head];
-          const uint32_t dst = w_base + st * C::kStage, bar = WFULL + 8 * st;
+          const int u0 = q_u0[q_head], nu = q_nu[q_head];
+          if (x_issued >= SX && !mbar_try_wait(reinterpret_cast<uint64_t*>(__cvta_shared_to_generic(XEMPTY + 8 * x.i)), x.ph ^ 1)) {
+            if (!block) return;
+            tcx::wait(XEMPTY + 8 * x.i, x.ph ^ 1);   // the MMAs that read this activation slot are complete
+          }
+          const uint32_t dst = x_base + x.i * C::kXStage, bar = XFULL + 8 * x.i;
+          tcx::expect_tx_a(bar, (p.dbg & 4) ? 0 : nu * C::kXUnit);
           const int g = u0 % J.Gk;
           if (p.dbg & 4) {
           } else if (nu == kRW && g + kRW <= J.Gk) {
@@ -219,8 +233,10 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
               tcx::tma_3d(dst + jj * C::kXUnit, J.xmap1, 0, 0, 2 * gg, bar);
           }
           trace(p, 0, q_u0[q_head] - unit_begin(cta, J.U, p.G));
-          q_head = (q_head + 1) & 7;
+          q_head = (q_head + 1) & 15;
           --q_n;
+          ++x_issued;
+          x.next(SX);
         }
       };
       Ring w{0, 0};
@@ -241,11 +257,11 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
           }
           trace(p, 1, n_w);
           n_w += nu;
-          tcx::expect_tx_a(WFULL + 8 * w.i, nu * TB + ((p.dbg & 4) ? 0 : nu * C::kXUnit));
-          tcx::bulk_g2s_a(w_base + w.i * C::kStage + kRW * C::kXUnit, J.packed + (size_t)u0 * TB, nu * TB,
-                          WFULL + 8 * w.i, pol);
-          const int e = (q_head + q_n) & 7;
-          q_s[e] = w.i; q_j[e] = j; q_u0[e] = u0; q_nu[e] = nu;
+          tcx::expect_tx_a(WFULL + 8 * w.i, nu * TB);
+          tcx::bulk_g2s_a(w_base + w.i * C::kStage, J.packed + (size_t)u0 * TB, nu * TB, WFULL + 8 * w.i, pol);
+          if (q_n == 16) drain(true);
+          const int e = (q_head + q_n) & 15;
+          q_j[e] = j; q_u0[e] = u0; q_nu[e] = nu;
           ++q_n;
           drain(false);
           ++issued;
@@ -256,7 +272,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
     }
   } else if (warp == C::kMmaW) {
     // ---------------- MMA issuer: per step 8 x tcgen05.mma (K = 16) per unit, each unit its own accumulator --
-    Ring w{0, 0}, a{0, 0}, acc{0, 0};
+    Ring x{0, 0}, a{0, 0}, acc{0, 0};
     int n_u = 0;
     const uint32_t desc_hi = (uint32_t)(tcx::kDescSW128 >> 32);
     for (int j = 0; j < p.n_jobs; ++j) {
@@ -265,12 +281,12 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
       const int ub = unit_begin(cta, J.U, p.G), ue = unit_begin(cta + 1, J.U, p.G);
       for (int u0 = ub; u0 < ue; u0 += kRW) {
         const int nw = min(kRW, ue - u0);
-        tcx::wait(WFULL + 8 * w.i, w.ph);
-        const uint32_t xs = w_base + w.i * C::kStage;
+        tcx::wait(XFULL + 8 * x.i, x.ph);
+        const uint32_t xs = x_base + x.i * C::kXStage;
         for (int j0 = 0; j0 < nw; j0 += kS) {
           const int nu = min(kS, nw - j0);
           if (p.dbg & 16) {   // diagnostics: stream only (stage released as soon as it lands)
-            if (tcx::elect_one() && j0 + kS >= nw) tcx::commit(WEMPTY + 8 * w.i);
+            if (tcx::elect_one() && j0 + kS >= nw) tcx::commit(XEMPTY + 8 * x.i);
             __syncwarp();
             continue;
           }
@@ -291,7 +307,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
             }
             tcx::commit(AEMPTY + 8 * a.i);
             tcx::commit(ACCFULL + 8 * acc.i);
-            if (j0 + kS >= nw) tcx::commit(WEMPTY + 8 * w.i);   // the stage's activations are read
+            if (j0 + kS >= nw) tcx::commit(XEMPTY + 8 * x.i);   // the stage's activations are read
           }
           __syncwarp();
           if (lane == 0) trace(p, 6, n_u);
@@ -299,7 +315,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
           a.next(NA);
           acc.next(NACC);
         }
-        w.next(SW);
+        x.next(SX);
       }
     }
   } else if (warp < kDq) {
@@ -319,7 +335,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
         const int nw = min(kRW, ue - u0);
         tcx::wait(WFULL + 8 * w.i, w.ph);
         if (lane == 0 && q == 0 && h == 0) trace(p, 2 + grp, n_u);
-        const uint32_t st = w_base + w.i * C::kStage + kRW * C::kXUnit;   // the stage's packed units
+        const uint32_t st = w_base + w.i * C::kStage;   // the stage's packed units
         for (int j0 = 0; j0 < nw; j0 += kS) {
           const int nu = min(kS, nw - j0);
           if (parity == grp && !(p.dbg & 16)) {
