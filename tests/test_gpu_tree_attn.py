@@ -154,3 +154,28 @@ def test_tree_attention_malformed_parents_do_not_hang():
         Vx = np.concatenate([V[:L], V[L + x:L + x + 1]])
         ref = oracle.tree_attention(Q[x:x + 1], Kx, Vx, np.array([-1], dtype=np.int32))
         assert np.all(np.abs(got[x:x + 1] - ref) <= TOL * (1 + np.abs(ref))), x
+
+
+def test_tree_attention_cuda_graph_replays():
+    # the bench replays the cooperative launch inside a CUDA graph: every replay must leave the split-merge
+    # counters re-armed and give the same (bit-identical) output as an eager call
+    w4 = _w4()
+    M, L, Hq, Hkv, D = 8, 2048, 64, 8, 128
+    Q, K, V = _inputs(4242, M, L, Hq, Hkv)
+    _, par = synth.eagle_tree(np.random.default_rng(5), M - 1, 6)
+    Qd, Kd, Vd, pd = _t(Q), _t(K), _t(V), _t(np.asarray(par, dtype=np.int32))
+    ws = torch.zeros(w4.w4a16_tree_attention_workspace_bytes(M, L, Hq, Hkv, D), dtype=torch.uint8, device="cuda")
+    O_eager = torch.empty(M, Hq, D, dtype=torch.float16, device="cuda")
+    w4.w4a16_tree_attention(Qd, Kd, Vd, pd, O_eager, ws)
+    O = torch.full((M, Hq, D), float("nan"), dtype=torch.float16, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        w4.w4a16_tree_attention(Qd, Kd, Vd, pd, O, ws, stream=s)
+    for _ in range(3):
+        O.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(O.view(torch.int16), O_eager.view(torch.int16))
+        assert int(ws[:16384].view(torch.int32)[0::8].abs().sum()) == 0
