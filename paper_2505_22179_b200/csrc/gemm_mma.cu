@@ -35,10 +35,22 @@
 #include "tma_host.cuh"
 #include "w4a16.h"
 
+// Chain tile counters and tile-ready flags: tile t of an op at ints [kCS (cnt_off + t)] (counter) and
+// [kCS (cnt_off + t) + kFO] (flag)
+#ifndef W4_MA_CSTRIDE
+#define W4_MA_CSTRIDE 64   // 256 B per tile, counter and flag on separate 128-B lines (-4.2 % vs packed 8 B at M = 8)
+#endif
+#ifndef W4_MA_FOFF
+#define W4_MA_FOFF 32
+#endif
+
 namespace w4 {
 namespace ma {
 
 constexpr int kTileN = 128, kTileK = 128;
+constexpr int kCS = W4_MA_CSTRIDE, kFO = W4_MA_FOFF;
+constexpr int kDSMax = 32;   // op counts: op j at done[ds j] (GemmParams::ds); exit counter done[-kDSMax] and run
+                              // number done[-2 kDSMax] at fixed places: chains of every M that share a workspace share them
 #ifndef W4_MA_GROUPS
 #define W4_MA_GROUPS 2
 #endif
@@ -136,7 +148,10 @@ struct GemmParams {
   int dbg;           // diagnostics only (W4A16_MMA_DEBUG, W4A16_MMA_DIAG builds): bit0 skip compute, bit1 skip loads, bit2 backoff waits, bit4 trace
   const ChainJob* jobs;   // chain: the op table (device); nullptr: single GEMM
   int n_jobs;             // 1 for a single GEMM
-  int* done;              // chain: [n_jobs] CTAs that finished each op; done[-2] = run number, done[-1] = exit counter
+  int* done;              // chain: [n_jobs] CTAs that finished each op (stride ds); done[-2 kDSMax] = run number,
+                          // done[-kDSMax] = exit counter
+  int ds;                 // chain: op-count stride in ints (32 = one 128-B line each at M <= 8: -1.9 %; 1 at
+                          // M = 9..16, where the spread layout measured +2 %)
                           // (fixed offsets: chains that share a workspace share them)
   int* flags;             // chain: tile-ready flags (one per tile of every GEMM op, at the op's cnt_off): the run
                           // number + 1 of the last run that wrote the tile's Y (run number at done[n_jobs + 1])
@@ -165,9 +180,9 @@ __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap
     const ChainJob* c = p.jobs + j;
     // chain: tile counter and tile-ready flag interleaved per tile (same layout in every chain that shares the
     // workspace, so one chain's flags never land on another's counters)
-    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + 2 * c->cnt_off;
-    J.flags = J.counters + 1;
-    J.cs = 2;
+    J.packed = c->packed; J.Y = c->Y; J.mR = &c->xmapR; J.m1 = &c->xmap1; J.counters = p.counters + kCS * c->cnt_off;
+    J.flags = J.counters + kFO;
+    J.cs = kCS;
     J.kind = c->kind; J.N = c->N; J.Gk = c->Gk; J.U = c->U; J.dep_x = c->dep_x; J.dep_y = c->dep_y; J.xf_off = c->xf_off;
     J.pub_tiles = c->pub_tiles; J.epi = c->epi; J.xf_mul = c->xf_mul; J.ar = c->ar_world > 0;
   }
@@ -178,7 +193,7 @@ __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap
 __device__ __forceinline__ void wait_op(const GemmParams& p, int j) {
   if (j < 0) return;
   const unsigned long long t0 = globaltimer_ns();
-  while (ld_acquire_gpu(&p.done[j]) < p.G) {
+  while (ld_acquire_gpu(&p.done[p.ds * j]) < p.G) {
     __nanosleep(64);
     if (globaltimer_ns() - t0 > 60000000000ull) __trap();   // never hang the device on a protocol bug
   }
@@ -296,9 +311,9 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
 __device__ __forceinline__ void allreduce_tiles(const GemmParams& p, int job, int cta, int lane) {
   const ChainJob* cj = p.jobs + job;
   const int world = cj->world, tiles = cj->N / 128;
-  const int run = __ldcg(&p.done[-2]);
+  const int run = __ldcg(&p.done[-2 * kDSMax]);
   const uint32_t want = (uint32_t)world * (__ldcg(cj->epoch) + 1u);   // counters after this run's bumps
-  int* yflags = p.counters + 2 * cj->cnt_off + 1;                     // Y's tile-ready flags (interleaved)
+  int* yflags = p.counters + kCS * cj->cnt_off + kFO;                 // Y's tile-ready flags (interleaved)
   if (lane == 0 && cj->dep_y >= 0) wait_op(p, cj->dep_y);            // WAR / WAW on Y
   for (int t = cta; t < tiles; t += p.G) {
     if (lane == 0) {
@@ -340,10 +355,10 @@ __device__ __forceinline__ void allreduce_tiles(const GemmParams& p, int job, in
     }
     __syncwarp();
     if (lane == 0 && cj->pub_tiles)
-      asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(yflags + 2 * t), "r"(run + 1) : "memory");
+      asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(yflags + kCS * t), "r"(run + 1) : "memory");
   }
   __syncwarp();
-  if (lane == 0) red_release_gpu_add(&p.done[job], 1);
+  if (lane == 0) red_release_gpu_add(&p.done[p.ds * job], 1);
 }
 
 template <int NTB, bool SYM, bool kScaleInA, bool kA8>
@@ -403,7 +418,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int jj = 0; jj < nu; ++jj) tma_3d(st + jj * C::kXUnit, J.m1, 0, 0, C::kBPU * ((u0 + jj) % J.Gk), &full_bar[s]);
         }
       };
-      const int run = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile flags)
+      const int run = chain ? __ldcg(&p.done[-2 * kDSMax]) : 0;   // this launch's run number (tile flags)
       // Tile-level dependency: the stage's activation k-groups are complete once the producing op's tiles
       // xf_off + g are written in this run (their flags reached run + 1).
       // The flags are polled with relaxed loads, all in flight at once (an acquire per flag would serialise
@@ -413,8 +428,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         bool ok = true;
         for (int jj = 0; jj < nu; ++jj) {
           for (int i = 0; i < J.xf_mul; ++i)
-            ok &= (W4_POLL_ACQ ? ld_acquire_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1])
-                               : ld_relaxed_gpu(&p.counters[2 * (J.xf_off + J.xf_mul * g + i) + 1])) > run;
+            ok &= (W4_POLL_ACQ ? ld_acquire_gpu(&p.counters[kCS * (J.xf_off + J.xf_mul * g + i) + kFO])
+                               : ld_relaxed_gpu(&p.counters[kCS * (J.xf_off + J.xf_mul * g + i) + kFO])) > run;
           if (++g == J.Gk) g = 0;
         }
         if (ok) fence_acquire_gpu();
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           }
           const JobInfo J = job_at(p, &xmapR, &xmap1, q_j[q_head]);
           if (J.dep_x > ok_upto) {
-            if ((W4_POLL_ACQ ? ld_acquire_gpu(&p.done[J.dep_x]) : ld_relaxed_gpu(&p.done[J.dep_x])) >= p.G) {
+            if ((W4_POLL_ACQ ? ld_acquire_gpu(&p.done[p.ds * J.dep_x]) : ld_relaxed_gpu(&p.done[p.ds * J.dep_x])) >= p.G) {
               if (!W4_POLL_ACQ) fence_acquire_gpu();
               ok_upto = J.dep_x;   // the whole producing op is complete: no more per-tile checks
             } else if (J.xf_off >= 0) {
@@ -554,7 +569,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
 
   // ---------------- consumers ----------------
   trace_ma(p, 0);
-  const int run_c = chain ? __ldcg(&p.done[-2]) : 0;   // this launch's run number (tile-ready flags)
+  const int run_c = chain ? __ldcg(&p.done[-2 * kDSMax]) : 0;   // this launch's run number (tile-ready flags)
   int pub_s = 0;
   uint32_t pub_ph = 0;
   // thread 0 only, after a barrier of the threads whose global stores the increment releases
@@ -605,7 +620,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         *reinterpret_cast<uint4*>(J.Y + (size_t)m * F + (size_t)v * 8) = silu_mul_vec(g, u);
       }
       named_bar_sync(1, kWarps * 32);
-      if (threadIdx.x == 0) publish(&p.done[job]);
+      if (threadIdx.x == 0) publish(&p.done[p.ds * job]);
       trace_op(p, job, 2);
       trace_op(p, job, 3);
       continue;
@@ -623,7 +638,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     bool y_ready = wdep < 0;
     // the WAR / WAW op count is loaded now and looked at by the first flush (its L2 round trip hides under the
     // op's stages instead of stalling the flush)
-    const int wdep_v = (W4_MA_WPRE && threadIdx.x == 0 && wdep >= 0) ? ld_relaxed_gpu(&p.done[wdep]) : 0;
+    const int wdep_v = (W4_MA_WPRE && threadIdx.x == 0 && wdep >= 0) ? ld_relaxed_gpu(&p.done[p.ds * wdep]) : 0;
     float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (8 * NTB * 32);
 
     auto flush = [&](int t, int sg0, int sg1) {
@@ -1022,8 +1037,8 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     if (chain && grp == 0) {
       named_bar_sync(2, kGW * 32);
       if (threadIdx.x == 0) {
-        if (W4_MA_DONEREL) red_release_gpu_add(&p.done[job], 1);
-        else publish(&p.done[job]);
+        if (W4_MA_DONEREL) red_release_gpu_add(&p.done[p.ds * job], 1);
+        else publish(&p.done[p.ds * job]);
       }
     }
     trace_op(p, job, 3);
@@ -1039,11 +1054,11 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     // The last CTA out re-arms the op counters for the next run of the chain (every CTA has finished
     // every access to them once it has counted itself out; the fences order its op counts first).
     __threadfence();
-    if (atomicAdd(&p.done[-1], 1) == p.G - 1) {
+    if (atomicAdd(&p.done[-kDSMax], 1) == p.G - 1) {
       __threadfence();
-      for (int j = 0; j < p.n_jobs; ++j) p.done[j] = 0;
-      p.done[-1] = 0;
-      p.done[-2] += 1;   // the next run's number (tile-ready flags hold run + 1)
+      for (int j = 0; j < p.n_jobs; ++j) p.done[p.ds * j] = 0;
+      p.done[-kDSMax] = 0;
+      p.done[-2 * kDSMax] += 1;   // the next run's number (tile-ready flags hold run + 1)
       if (p.jobs[0].epoch != nullptr) *p.jobs[0].epoch += 1u;   // the group's next run (ALLREDUCE flags)
       __threadfence();
     }
@@ -1114,7 +1129,7 @@ constexpr int kChainSlots = 8;   // partial-slot ring of a chain, in ops
 
 inline int ntb_of(int M) { return (M + 7) / 8; }
 inline size_t chain_partial_bytes(int M, int G) { return (size_t)kChainSlots * G * 4 * ntb_of(M) * 2 * 32 * 16; }
-inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 2) * 4 + 255) / 256 * 256; }   // run, exit, per op
+inline size_t chain_done_bytes(int n_ops) { return ((size_t)(n_ops + 2) * kDSMax * 4 + 255) / 256 * 256; }   // run, exit, per op
 
 }  // namespace ma
 }  // namespace w4
@@ -1276,7 +1291,7 @@ extern "C" size_t w4a16_chain_workspace_bytes_sms(const w4a16_op* ops, int n_ops
   int mode = 0;
   const int G = chain_ctas(sms);
   if (check_ops(ops, n_ops, M, G, &tiles, &mode) != W4A16_OK) return 0;
-  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * 8;   // counters + flags
+  return w4::ma::chain_partial_bytes(M, G) + w4::ma::chain_done_bytes(n_ops) + (size_t)tiles * w4::ma::kCS * 4;   // counters + flags
 }
 
 extern "C" int w4a16_chain_plan_sms(const w4a16_op* ops, int n_ops, int M, int family, void* plan, size_t plan_bytes,
@@ -1378,7 +1393,8 @@ extern "C" int w4a16_launch_chain_mma(const void* dev_plan, int n_ops, int M, in
   const size_t pb = w4::ma::chain_partial_bytes(M, p.G), db = w4::ma::chain_done_bytes(n_ops);
   if (ws_bytes < pb + db) return W4A16_ERR_WORKSPACE;
   p.partials = reinterpret_cast<float*>(ws);
-  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb) + 2;   // after the run number and exit counter
+  p.ds = w4::ma::ntb_of(M) == 1 ? w4::ma::kDSMax : 1;
+  p.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb) + 2 * w4::ma::kDSMax;   // after the run number and exit counter
   p.counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + pb + db);
   p.flags = nullptr;   // interleaved with the counters (JobInfo)
   p.jobs = reinterpret_cast<const w4::ma::ChainJob*>(dev_plan);
