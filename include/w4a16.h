@@ -94,7 +94,7 @@ int w4a16_pack(const uint16_t* W, int K, int N, int group, int mode, void* packe
 int w4a16_unpack(const void* packed, int K, int N, int group, int mode, uint16_t* W_hat, w4a16_stream_t stream);
 
 /* Workspace bytes w4a16_gemm needs for this shape. Layout: a fixed region of W4A16_MAX_N / 128 int32 tile
- * counters (32 KiB, the same offset for every shape) followed by the fp32 split-K partials of this shape.
+ * counters, one per 128-byte line (1 MiB, the same offset for every shape) followed by the fp32 split-K partials of this shape.
  * Before its first use the workspace must be zero-filled (w4a16_workspace_init); every w4a16_gemm leaves
  * the counters zeroed again, so one workspace, sized by the maximum over the shapes it serves, can be
  * shared by any sequence of calls of any shapes on one stream. Returns 0 on bad shape. */

@@ -12,7 +12,10 @@ namespace w4 {
 
 // GEMM workspace: a fixed region of tile counters (same offset for every shape, so GEMMs of different N
 // can share one workspace), then the fp32 split-K partials (include/w4a16.h).
-constexpr size_t kCounterBytes = (size_t)(W4A16_MAX_N / 128) * 4;
+// Single-GEMM tile counters: one per 128-byte line (counters of neighbouring tiles on one line serialise the
+// CTAs' atomics; the chain's sync words showed 4 % from spreading them)
+constexpr int kCounterStride = 32;
+constexpr size_t kCounterBytes = (size_t)(W4A16_MAX_N / 128) * 4 * kCounterStride;
 
 // One op of a chain: the device copy of a w4a16_chain_plan entry (include/w4a16.h), shared by both GEMM
 // families (the activation tensor maps are encoded for the family the plan was made for).

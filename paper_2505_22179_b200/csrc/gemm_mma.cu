@@ -174,7 +174,7 @@ struct JobInfo {
 __device__ __forceinline__ JobInfo job_at(const GemmParams& p, const CUtensorMap* mR, const CUtensorMap* m1, int j) {
   JobInfo J;
   if (p.jobs == nullptr) {
-    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters; J.flags = nullptr; J.cs = 1;
+    J.packed = p.packed; J.Y = p.Y; J.mR = mR; J.m1 = m1; J.counters = p.counters; J.flags = nullptr; J.cs = w4::kCounterStride;
     J.kind = kOpGemm; J.N = p.N; J.Gk = p.Gk; J.U = p.U; J.dep_x = -1; J.dep_y = -1; J.xf_off = -1; J.pub_tiles = 0; J.epi = 0; J.xf_mul = 1; J.ar = 0;
   } else {
     const ChainJob* c = p.jobs + j;

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
       const int c_first = cta_of_unit(tile_u0, p.U, p.G), c_last = cta_of_unit(tile_u1 - 1, p.U, p.G);
       if (threadIdx.x == 0) {
         int old;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&p.counters[t]) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&p.counters[kCounterStride * t]) : "memory");
         s_last = old == c_last - c_first;
       }
       named_bar_sync(1, kDqWarps * 32);
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_w4a16_tc_kernel(const __grid
 #pragma unroll
       for (int i = 0; i < kCols; ++i)
         if (m0 + i < p.M) p.Y[(size_t)(m0 + i) * p.N + n] = __half_as_ushort(__float2half_rn(acc[i]));
-      if (threadIdx.x == 0) p.counters[t] = 0;
+      if (threadIdx.x == 0) p.counters[kCounterStride * t] = 0;
     };
 
     int pend_t[kAU], pend_u0[kAU], pend_u1[kAU], pend_idx[kAU];

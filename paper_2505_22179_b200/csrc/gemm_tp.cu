@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
               named_bar_sync(1, kEpiThreads);
               if (epi0) {
                 __threadfence();
-                s_last = atomicAdd(&J.counters[t], 1) == c_last - c_first;
+                s_last = atomicAdd(&J.counters[kCounterStride * t], 1) == c_last - c_first;
               }
               named_bar_sync(1, kEpiThreads);
               if (s_last) {
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(Cfg<MPAD>::kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < kCols; ++c)
                   if (col0 + c < p.M) J.Y[(size_t)(col0 + c) * J.N + n] = __half_as_ushort(__float2half_rn(r[c]));
-                if (epi0) J.counters[t] = 0;   // every contributor has arrived: re-arm for the next launch / run
+                if (epi0) J.counters[kCounterStride * t] = 0;   // every contributor has arrived: re-arm for the next launch / run
               }
             }
             ++nseg;
