@@ -160,7 +160,7 @@ int w4a16_lmhead_argmax(const uint16_t* H, const uint16_t* W_lm, int M, int K, i
  * parents[i] < i; verify_accept reports malformed trees). O[m][h] = softmax_j(q.k_j / sqrt(D)) . v_j over the
  * visible rows j, kv head h / (Hq / Hkv) (GQA); fp32 scores / softmax / accumulation, fp16 probabilities and
  * output. D == 128, 1 <= M <= 64, Hq % Hkv == 0, Hq <= 512, L >= 0. workspace:
- * w4a16_tree_attention_workspace_bytes(); its first 16384 bytes (the split-merge counters) must be zero before
+ * w4a16_tree_attention_workspace_bytes(); its first 65536 bytes (the split-merge counters) must be zero before
  * the first call, and every call leaves them zero. One cooperative launch: the CTAs of a call must all be
  * resident (the splits are merged inside the kernel).
  * A row m whose ancestry walk meets a parent outside [-1, m) (a malformed tree) sees the prefix and itself

@@ -44,8 +44,8 @@ constexpr int kTileBytes = 64 * kD * 2;   // 16 KB: 64 rows x 256 B, as two SW12
 constexpr int kKvBufs = 4;                // K/V chunk ring
 constexpr int kSmem = kTileBytes * (1 + 2 * kKvBufs) + 64 * 8 + 64 * 4 + 1024;   // Q, (K, V) x bufs, masks, parents
 constexpr int kCtasPerSmEst = 1;
-constexpr int kHeaderBytes = 16384;       // workspace header: per (kv head, row block) {count, generation, pad}
-constexpr int kMaxGroups = kHeaderBytes / 32;
+constexpr int kHeaderBytes = 65536;       // workspace header: per (kv head, row block) {count, generation} on its own
+constexpr int kMaxGroups = kHeaderBytes / 128;   // 128-byte line (the splits' atomics of neighbouring groups do not meet)
 
 struct Params {
   const uint16_t* Q;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(const __grid_con
   // meet the other splits of this (kv head, row block): sense-reversing counter (the count returns to 0)
   __syncthreads();
   if (tid == 0) {
-    int* cnt = p.bar + 8 * (g * p.qblocks + qb);
+    int* cnt = p.bar + 32 * (g * p.qblocks + qb);
     int* gen = cnt + 1;
     const int g0 = ld_relaxed_gpu(gen);
     int arrived;
