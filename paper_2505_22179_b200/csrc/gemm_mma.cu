@@ -10,7 +10,7 @@
 //  * Stream-K: CTA c of G = #SMs (one CTA per SM) owns units [c*U/G, (c+1)*U/G) — a (K, N, SM-count)-only plan.
 //  * Warp 16 (producer) streams stages of 4 units with ONE bulk copy each (the TMA engine costs ~100+ cycles
 //    per issued copy), plus the units' activation slices with a 3-D TMA (SWIZZLE_128B, rows >= M
-//    zero-filled), into a ring of up to 8 stages (as many as fit in shared memory); activation loads wait in
+//    zero-filled), into a ring of up to 12 stages (as many as fit in shared memory); activation loads wait in
 //    a queue for their producing op's tile-ready flags (chains), weights never wait.
 //  * Warps 0..15 (consumers) = 2 groups x 8 warps; group g takes units 2g, 2g+1 of every stage; warp w of a
 //    group owns tile rows 16w..16w+15 (one m16 MMA tile) and all 128 k of its units. A lane reads one 32-bit
@@ -24,8 +24,11 @@
 //  * Tile boundary: group 1 hands its sums to group 0 through shared memory; a tile split across CTAs is
 //    owned by its first CTA, which handles the tile's head as its LAST segment: the others store fp32
 //    partials and bump the tile counter, the owner sums them in CTA order (deterministic) and writes Y.
-//  * Warp 17 (publisher) issues every GPU- or system-scope release (tile counters, tile-ready flags, op
-//    counts, ALLREDUCE tile bumps) behind one fence per batch and runs the chain's ALLREDUCE ops.
+//  * Releases: tile-ready flags, split-tile counters (M <= 8) and op counts are released by the storing
+//    thread right after its group's barrier; warp 17 (publisher) releases the rest (split-tile counters at
+//    M = 9..16, ALLREDUCE tile bumps, SiLU-op counts) behind one fence per batch and runs the chain's
+//    ALLREDUCE ops. The producer acquires what it polled with an acquire-only fence (no MEMBAR behind its
+//    bulk copies). Counters, flags and op counts sit on their own 128-byte lines.
 //  * W4A8 (kA8): the same pipeline with int8 activations and int8 codes (q - 8) * 16 on mma m16n8k32.
 #include <cstdlib>
 #include <cstring>
