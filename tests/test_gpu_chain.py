@@ -186,3 +186,41 @@ def test_chain_fused_silu_matches_gemm_then_blocked_silu(M, family):
         torch.cuda.synchronize()
         assert np.array_equal(_u16(act_c), _u16(act_e)), rep
         assert np.array_equal(_u16(y_c), _u16(y_e)), rep
+
+
+@pytest.mark.timeout(300)
+def test_chains_of_different_M_share_one_workspace():
+    # chains at M <= 8 and M = 9..16 lay their op counts out with different strides but keep the run number and
+    # exit counter at fixed offsets (gemm_mma.cu kDSMax), so chains of any M may share one workspace: run them
+    # alternately on one workspace and compare each run with the op-by-op launches, bit for bit
+    w4 = _w4()
+    H, F = 2048, 2560
+    mats = _mlp(H, F, layers=2, seed=77)
+    f16 = dict(dtype=torch.float16, device="cuda")
+    cases = {}
+    for M in (8, 16):
+        x = synth.gpu(7, 50 + M, synth.ACT, M, H)
+        bufs_e = [torch.empty((M, 2 * F), **f16), torch.empty((M, F), **f16), torch.empty((M, H), **f16)]
+        bufs_c = [torch.empty((M, 2 * F), **f16), torch.empty((M, F), **f16), torch.empty((M, H), **f16)]
+        ws = w4.alloc_workspace(M, [(H, 2 * F), (F, H)])
+        _run_eager(_mlp_ops(mats, x.clone(), *bufs_e), 0, ws)
+        cases[M] = (x.clone(), bufs_e, bufs_c)
+    shared = None
+    chains = {}
+    for M in (8, 16):
+        x_c, _, bufs_c = cases[M]
+        probe = w4.Chain(_mlp_ops(mats, x_c, *bufs_c), M)
+        if shared is None or probe.ws.numel() > shared.numel():
+            shared = torch.zeros(max(probe.ws.numel(), 0 if shared is None else shared.numel()), dtype=torch.uint8, device="cuda")
+    for M in (8, 16):
+        x_c, _, bufs_c = cases[M]
+        chains[M] = w4.Chain(_mlp_ops(mats, x_c, *bufs_c), M, workspace=shared)
+    for rep in range(3):
+        for M in (8, 16, 16, 8):
+            _, bufs_e, bufs_c = cases[M]
+            for b in bufs_c:
+                b.fill_(float("nan"))
+            chains[M]()
+            torch.cuda.synchronize()
+            for a, b in zip(bufs_e, bufs_c):
+                assert np.array_equal(_u16(a), _u16(b)), (rep, M)
