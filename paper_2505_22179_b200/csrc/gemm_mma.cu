@@ -96,6 +96,9 @@ __host__ __device__ constexpr int kR_for(int ntb) { return (ntb == 1 ? W4_MA_UPG
 #ifndef W4_MA_WPRE
 #define W4_MA_WPRE 1   // consumers: load the WAR op count at the op start (-0.8 % at M = 8)
 #endif
+#ifndef W4_MA_MAXST
+#define W4_MA_MAXST 12   // ring stages cap (as many as fit up to this)
+#endif
 #ifndef W4_MA_FLAGREL
 #define W4_MA_FLAGREL 1   // tile-ready flags released by the storing thread (st.release.gpu) instead of the publisher warp (+0.5 %)
 #endif
@@ -128,7 +131,7 @@ struct Cfg {
   static constexpr int kRedFloats = kRedSlots * 8 * NTB * 4 * 32;   // [slot][row tile][tb][e][lane]
   static constexpr int kXchBytes = 4 * NTB * 4 * 32 * 4;          // SiLU epilogue: up values of a tile (fp16 in u32)
   static constexpr int kStagesFit = (kSmemBudget - kRedFloats * 4 - kXchBytes - 1024) / kStage;
-  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
+  static constexpr int kStages = kStagesFit > W4_MA_MAXST ? W4_MA_MAXST : kStagesFit;
   static constexpr int kSmem = kStages * kStage + kRedFloats * 4 + kXchBytes + 1024;
 };
 

@@ -1,0 +1,3 @@
+for rep in 1 2; do for lib in "" st4 st3; do
+  W4A16_LIB="$lib" timeout 120 python tools/chain_time.py --layers 16 --reps 15 --Ms 1,8,16 2>&1 | grep median
+done; done
