@@ -99,6 +99,9 @@ __host__ __device__ constexpr int kR_for(int ntb) { return (ntb == 1 ? W4_MA_UPG
 #ifndef W4_MA_MAXST
 #define W4_MA_MAXST 12   // ring stages cap (as many as fit up to this)
 #endif
+#ifndef W4_MA_ROT
+#define W4_MA_ROT 1   // M <= 8: the two consumer groups take turns owning a flush (combine, store, publish; -0.6 %)
+#endif
 #ifndef W4_MA_FLAGREL
 #define W4_MA_FLAGREL 1   // tile-ready flags released by the storing thread (st.release.gpu) instead of the publisher warp (+0.5 %)
 #endif
@@ -111,6 +114,8 @@ __host__ __device__ constexpr int kR_for(int ntb) { return (ntb == 1 ? W4_MA_UPG
 constexpr int kCtasPerSm = kGroups >= 2 ? 1 : W4_MA_CTAS;   // resident CTAs per SM
 constexpr int kSmemBudget = kCtasPerSm == 1 ? 227 * 1024 - 512 : (kCtasPerSm == 2 ? 112 : 74) * 1024;   // 512 B static
 
+static_assert(!W4_MA_ROT || (W4_MA_CNTREL && W4_MA_DONEREL && W4_MA_FLAGREL),
+              "a rotating flush owner must not use the publisher ring (thread 0's)");
 template <int NTB, bool SYM, bool kA8 = false>
 struct Cfg {
   static constexpr int kMpad = 8 * NTB;                           // token rows per TMA box
@@ -596,6 +601,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
   const int wg = warp % kGW, grp = warp / kGW;
 
   float acc[kRT][NTB][4];
+  int n_fl = 0, last_og = 0;   // flushes so far; the group that owned the last one (W4_MA_ROT)
   int s = 0;
   uint32_t ph = 0;
   const uint32_t ready_base = smem_u32(&full_bar[0]);
@@ -644,12 +650,18 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     bool y_ready = wdep < 0;
     // the WAR / WAW op count is loaded now and looked at by the first flush (its L2 round trip hides under the
     // op's stages instead of stalling the flush)
-    const int wdep_v = (W4_MA_WPRE && threadIdx.x == 0 && wdep >= 0) ? ld_relaxed_gpu(&p.done[p.ds * wdep]) : 0;
+    const int wdep_v = (W4_MA_WPRE && threadIdx.x % (kGW * 32) == 0 && wdep >= 0) ? ld_relaxed_gpu(&p.done[p.ds * wdep]) : 0;
     float4* part = reinterpret_cast<float4*>(p.partials) + (size_t)(job % p.slots) * p.G * (8 * NTB * 32);
 
     auto flush = [&](int t, int sg0, int sg1) {
+      // the group that combines, stores and publishes this tile: alternates flush by flush (W4_MA_ROT), so
+      // the epilogue work is shared between the groups (a + b == b + a: the result is bit-identical)
+      const int og = (W4_MA_ROT && kNG == 2 && NTB == 1 && !J.ar) ? (n_fl & 1) : 0;
+      const int lead = og * kGW * 32;
+      ++n_fl;
+      last_og = og;
       if (!y_ready) {
-        if (threadIdx.x == 0) {   // released to the other warps by the barrier below
+        if (threadIdx.x == lead) {   // released to the other warps by the barrier below
           if (W4_MA_WPRE && wdep_v >= p.G) fence_acquire_gpu();
           else wait_op(p, wdep);
         }
@@ -673,9 +685,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
             for (int e = 0; e < 4; ++e) acc[i][tb][e] += red[(((slot * 8 + kRT * wg + i) * NTB + tb) * 4 + e) * 32 + lane];
       };
       if (kNG == 2) {
-        if (grp == 1) red_put(0);
+        if (grp != og) red_put(0);
         named_bar_sync(1, kWarps * 32);
-        if (grp == 0) red_add(0);
+        if (grp == og) red_add(0);
       } else {
         if (grp & 1) red_put(grp >> 1);   // g1 -> slot 0, g3 -> slot 1
         named_bar_sync(1, kWarps * 32);
@@ -686,7 +698,7 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         if (grp == 0) red_add(0);
       }
       named_bar_sync(1, kWarps * 32);
-      if (grp != 0) return;
+      if (grp != og) return;
       // 2. the group-0 warps own the result
       const int tile_u0 = t * J.Gk, tile_u1 = tile_u0 + J.Gk;
       auto store = [&](float (&v)[kRT][NTB][4]) {
@@ -759,9 +771,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
         if (!chain || (!J.pub_tiles && !J.ar)) return;
         named_bar_sync(2, kGW * 32);
         if (W4_MA_FLAGREL) {   // the tile-ready flag released by this thread (no queue behind the publisher's fences)
-          if (threadIdx.x == 0 && J.pub_tiles)
+          if (threadIdx.x == lead && J.pub_tiles)
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(&J.flags[J.cs * t]), "r"(run_c + 1) : "memory");
-        } else if (threadIdx.x == 0 && J.pub_tiles) {
+        } else if (threadIdx.x == lead && J.pub_tiles) {
           publish(&J.flags[J.cs * t], run_c + 1);
         }
         // Y is an ALLREDUCE's partial: bump tile t's counter in every rank's flag area (publisher warp)
@@ -782,14 +794,14 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
           for (int tb = 0; tb < NTB; ++tb)
             __stcg(&part[pidx(cta, kRT * wg + i, tb)], make_float4(acc[i][tb][0], acc[i][tb][1], acc[i][tb][2], acc[i][tb][3]));
         named_bar_sync(2, kGW * 32);
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == lead) {
           // direct at M <= 8 (-0.6 %); at M = 9..16 the publisher's queue is 1 % faster (measured)
           if (W4_MA_CNTREL && NTB == 1) red_release_gpu_add(&J.counters[J.cs * t], 1);
           else publish(&J.counters[J.cs * t]);
         }
         return;
       }
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == lead) {
         const int want = c_last - c_first;
         trace_op(p, job, 4);
         while (ld_acquire_gpu(&J.counters[J.cs * t]) != want) __nanosleep(32);
@@ -1040,9 +1052,9 @@ __global__ void __launch_bounds__(threads_for<kScaleInA>(), kCtasPerSm) gemm_w4a
     trace_ma(p, 3);
     // This CTA's share of the op is written: count it. Only the warps that store Y / partials (group 0) take
     // part; the other warps are already streaming the next op.
-    if (chain && grp == 0) {
+    if (chain && grp == last_og) {   // the group of the op's last flush has seen every earlier flush's stores
       named_bar_sync(2, kGW * 32);
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == last_og * kGW * 32) {
         if (W4_MA_DONEREL) red_release_gpu_add(&p.done[p.ds * job], 1);
         else publish(&p.done[p.ds * job]);
       }
